@@ -1,0 +1,150 @@
+// Shared device-side types of the onmt B200 library (kernels + runtime).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace onmt {
+
+constexpr int kKMax = 16;     // ONMT_K_MAX
+constexpr int kBK = 64;       // K block (64 bf16 = 128 B = one swizzle row)
+constexpr int kTileM = 128;   // weight rows per tcgen05 tile (TMEM lanes)
+constexpr int kVTile = 128;   // vocabulary rows per generator partial
+
+// Destination of an activation operand: either fp32 [rows_pad x k_pad] (fp32 models,
+// SIMT GEMM) or two bf16 planes hi/lo [2 x rows_pad x k_pad] (bf16 models, tcgen05
+// GEMM; x = hi + lo with hi = bf16(x), lo = bf16(x - hi); DESIGN.md §6 H4).
+struct XOut {
+  float* f32;
+  __nv_bfloat16* hl;
+  int rows_pad;
+  int k_pad;
+};
+
+__device__ __forceinline__ void store_x(const XOut& x, int r, int c, float v) {
+  size_t i = (size_t)r * x.k_pad + c;
+  if (x.hl) {
+    __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    float lo = v - __bfloat162float(hi);
+    x.hl[i] = hi;
+    x.hl[(size_t)x.rows_pad * x.k_pad + i] = __float2bfloat16_rn(lo);
+  } else {
+    x.f32[i] = v;
+  }
+}
+
+// Early-exit control: every decode-step kernel returns at once when all B sentences
+// have stopped (n_done written by the beam merge kernel).
+struct StepCtl {
+  const int* n_done;
+  int B;
+};
+__device__ __forceinline__ bool all_done(const StepCtl& c) {
+  return c.n_done != nullptr && *(volatile const int*)c.n_done >= c.B;
+}
+
+// (z desc, id asc) ordering used by every top-k in the library (R13).
+__device__ __forceinline__ bool better(float za, int ia, float zb, int ib) {
+  return za > zb || (za == zb && ia < ib);
+}
+
+// Generator partial outputs per (vocabulary tile, row): running max and sum of
+// exp(z - max) over the tile, and the tile's top-k (z, id) in (z desc, id asc) order.
+struct GenOut {
+  float2* ms;      // [n_vt][rows_pad]
+  float* tz;       // [n_vt][rows_pad][K]
+  int* ti;         // [n_vt][rows_pad][K]
+  const float* bias;  // [V]
+  int V;
+  int K;
+  int rows_valid;
+  int rows_pad;
+};
+
+// Scan one tile column (n <= 128 logits of one row): online max / sum-exp plus an
+// unrolled register top-KMAX insertion (ids scanned in increasing order).
+template <int KMAX>
+__device__ __forceinline__ void scan_tile_column(const float* vals, int stride, int vbase, const GenOut& g,
+                                                 float& mx, float& sm, float (&tz)[KMAX], int (&ti)[KMAX]) {
+  mx = -INFINITY;
+  sm = 0.f;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) { tz[i] = -INFINITY; ti[i] = 0x7fffffff; }
+  int n = g.V - vbase;
+  if (n > kVTile) n = kVTile;
+  for (int v = 0; v < n; ++v) {
+    const int id = vbase + v;
+    const float z = vals[v * stride] + g.bias[id];
+    if (z > mx) {
+      sm = sm * expf(mx - z) + 1.f;
+      mx = z;
+    } else {
+      sm += expf(z - mx);
+    }
+    if (better(z, id, tz[KMAX - 1], ti[KMAX - 1])) {
+      float cz = z;
+      int ci = id;
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) {
+        if (better(cz, ci, tz[i], ti[i])) {
+          float tzz = tz[i]; int tii = ti[i];
+          tz[i] = cz; ti[i] = ci;
+          cz = tzz; ci = tii;
+        }
+      }
+    }
+  }
+}
+
+template <int KMAX>
+__device__ __forceinline__ void write_gen_partial(const GenOut& g, int vt, int r, float mx, float sm,
+                                                  const float (&tz)[KMAX], const int (&ti)[KMAX]) {
+  g.ms[(size_t)vt * g.rows_pad + r] = make_float2(mx, sm);
+  size_t base = ((size_t)vt * g.rows_pad + r) * g.K;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    if (i < g.K) { g.tz[base + i] = tz[i]; g.ti[base + i] = ti[i]; }
+  }
+}
+
+
+// Destinations of a decoder cell's h output (operand buffers and column offsets).
+struct CellDst {
+  XOut x[2];
+  int col[2];
+  int n;
+};
+
+// Device beam state (DESIGN.md §5 layout); histories are [max_len][B*K].
+struct BeamState {
+  double* cum;        // [B*K] cumulative raw log-prob of live slots
+  int* live;          // [B*K]
+  int* y;             // [B*K] token fed at the next step
+  int* prow;          // [B*K] row (b*K + parent slot) whose state slot r continues
+  int* done;          // [B]
+  int* n_done;        // [1]
+  int* best_t;        // [B] banked best entry: step (1-based), 0 = none
+  int* best_r;        // [B]
+  double* best_raw;   // [B]
+  double* best_norm;  // [B]
+  int* hist_parent;   // [max_len][B*K]
+  int* hist_token;    // [max_len][B*K]
+  float* hist_logp;   // [max_len][B*K]
+  double* sel_score;  // [max_len][B*K] (trace)
+  int* sel_parent;    // [max_len][B*K] (trace; -1 = none)
+};
+
+// Operands of the parent gather (A5).
+struct GatherArgs {
+  const float* emb_tgt;
+  int E, H, L;
+  const float* htilde;
+  const float* h;      // [L][rows_pad][H]
+  const float* c;      // [L][rows_pad][H]
+  float* cg;           // [L][rows_pad][H]
+  int rows_pad;
+  XOut x[8];           // x[0] = layer-0 operand; x[l] = layer-l operand
+};
+
+}  // namespace onmt

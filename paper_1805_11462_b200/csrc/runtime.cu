@@ -1,0 +1,1011 @@
+// Host runtime + C-ABI of the onmt B200 library (include/onmt.h).
+//
+//   loader      MNMT parse -> config inference -> bf16 rounding -> gate-row interleave
+//               (row 4j+g holds gate g of unit j) -> padded device matrices + TMA maps
+//   encoder     A1 gather, A2 hoisted input projection (tcgen05), A3 recurrence
+//               (per step: recurrent GEMM + fused cell), A4 memory bank + init states
+//   decoder     per step: gates GEMM + cell per layer, q GEMM, attention, W_out GEMM +
+//               tanh, fused generator/log-softmax/top-k, beam merge, parent gather -
+//               all enqueued on one stream, no host round-trip per step (optionally
+//               replayed as a CUDA graph)
+//   C-ABI       argument validation, status codes, thread-local error string
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/onmt.h"
+#include "common.cuh"
+
+namespace onmt {
+// kernels / launchers defined in the other translation units
+cudaError_t tc_gemm_partial(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
+                            int n_valid, int k_blocks, int splits, float* out, StepCtl ctl, cudaStream_t st);
+cudaError_t tc_gemm_gen(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
+                        int k_blocks, const GenOut& g, StepCtl ctl, cudaStream_t st);
+cudaError_t simt_gemm_partial(const void* W, bool w_bf16, int m_pad, int k_pad, const float* X, int n_rows_pad,
+                              int n_valid, int splits, float* out, StepCtl ctl, cudaStream_t st);
+int simt_effective_splits(int k_pad, int splits);
+cudaError_t simt_gen_partials(const float* logits, int v_pad, const GenOut& g, StepCtl ctl, cudaStream_t st);
+
+void launch_embed_gather(const float* emb, int E, const int* ids, const int* lens, int B, int S_max, XOut x,
+                         cudaStream_t st);
+void launch_enc_cell(const float* Z, int z_ld, const float* P, int splits, int p_rows_pad, int p_ld,
+                     const float* bias, int Hd, int B, const int* lens, int S_max, int t, int backward, float* h_st,
+                     float* c_st, int st_ld, XOut xrec, XOut xnext, int next_col, float* mem, int mem_ld,
+                     int mem_col, cudaStream_t st);
+void launch_dec_cell(const float* P, int splits, int p_rows_pad, int p_ld, const float* bias, const float* cg,
+                     float* c_out, float* h_out, int H, int R, CellDst dst, StepCtl ctl, cudaStream_t st);
+cudaError_t launch_attention(const float* Pq, int splits, int p_rows_pad, int p_ld, const float* htop,
+                             const float* mem, const int* lens, int B, int S_max, int H, int K, XOut xo,
+                             const int* done, StepCtl ctl, cudaStream_t st);
+void launch_attn_out(const float* P, int splits, int p_rows_pad, int p_ld, float* htilde, int H, int R, XOut xg,
+                     StepCtl ctl, cudaStream_t st);
+void launch_init_decode(const BeamState& bs, int B, int K, const float* enc_h, const float* enc_c, int L, int H,
+                        float* dec_h, float* dec_c, int dec_rows_pad, float* htilde, cudaStream_t st);
+void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepCtl ctl, cudaStream_t st);
+void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int B, int K, int t,
+                       int max_len, float alpha, const BeamState& bs, StepCtl ctl, cudaStream_t st);
+void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
+                     float* tlogp, cudaStream_t st);
+void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int R, int K,
+                       float* lse, float* oz, int* oi, cudaStream_t st);
+
+static thread_local std::string g_err;
+
+struct Error {
+  onmt_status s;
+  std::string msg;
+};
+#define ONMT_CUDA(call)                                                                              \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess)                                                                           \
+      throw Error{e_ == cudaErrorMemoryAllocation ? ONMT_E_OOM : ONMT_E_CUDA,                        \
+                  std::string(#call) + ": " + cudaGetErrorString(e_)};                               \
+  } while (0)
+
+static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// ------------------------------------------------------------------ TMA descriptors
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_t get_encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    ONMT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw Error{ONMT_E_CUDA, "cuTensorMapEncodeTiled not available"};
+    fn = (PFN_encodeTiled_t)p;
+  }
+  return fn;
+}
+// bf16 [rows x k_pad] row-major, box {64 (=128 B), box_rows}, 128-byte swizzle.
+static CUtensorMap make_tmap(const void* base, int k_pad, int rows, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)k_pad, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)k_pad * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error{ONMT_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  return m;
+}
+
+// ------------------------------------------------------------------ device buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    ONMT_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+static float bf16_round_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+// GEMM weight operand: [m_pad x k_pad] (bf16 for bf16 models, fp32 otherwise).
+struct Mat {
+  int m = 0, k = 0, m_pad = 0, k_pad = 0;
+  bool bf16 = false;
+  DevBuf w;
+  CUtensorMap tmap;
+  void upload(const std::vector<float>& host, int m_, int k_, bool bf) {  // host already padded
+    m = m_; k = k_; m_pad = round_up(m_, kTileM); k_pad = round_up(k_, kBK); bf16 = bf;
+    if (bf) {
+      std::vector<__nv_bfloat16> hb(host.size());
+      for (size_t i = 0; i < host.size(); ++i) hb[i] = __float2bfloat16_rn(host[i]);
+      w.ensure(hb.size() * 2);
+      ONMT_CUDA(cudaMemcpy(w.p, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice));
+      tmap = make_tmap(w.p, k_pad, m_pad, kTileM);
+    } else {
+      w.ensure(host.size() * 4);
+      ONMT_CUDA(cudaMemcpy(w.p, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
+    }
+  }
+};
+
+struct RowPlan {
+  int rows_pad, n_group;
+};
+static RowPlan plan_rows(int n) {
+  int p = round_up(std::max(n, 1), 16);
+  if (p <= 256) return {p, p};
+  int g = (p + 255) / 256;
+  int grp = round_up((p + g - 1) / g, 16);
+  return {grp * g, grp};
+}
+
+// Activation operand [rows_pad x k_pad]: fp32 copy and (bf16 models) hi/lo planes.
+struct Act {
+  int rows = 0, rows_pad = 0, n_group = 0, k = 0, k_pad = 0;
+  bool bf16 = false;
+  DevBuf f32, hl;
+  CUtensorMap tmap;
+  void ensure(int rows_, int k_, bool bf) {
+    RowPlan rp = plan_rows(rows_);
+    int kp = round_up(k_, kBK);
+    if (rp.rows_pad == rows_pad && kp == k_pad && bf == bf16 && f32.p) { rows = rows_; return; }
+    rows = rows_; rows_pad = rp.rows_pad; n_group = rp.n_group; k = k_; k_pad = kp; bf16 = bf;
+    f32.ensure((size_t)rows_pad * k_pad * 4);
+    ONMT_CUDA(cudaMemset(f32.p, 0, (size_t)rows_pad * k_pad * 4));
+    if (bf) {
+      hl.ensure((size_t)2 * rows_pad * k_pad * 2);
+      ONMT_CUDA(cudaMemset(hl.p, 0, (size_t)2 * rows_pad * k_pad * 2));
+      tmap = make_tmap(hl.p, k_pad, 2 * rows_pad, n_group);
+    }
+  }
+  XOut xo(bool use_tc) const {
+    XOut x;
+    x.f32 = use_tc ? nullptr : f32.as<float>();
+    x.hl = use_tc ? hl.as<__nv_bfloat16>() : nullptr;
+    x.rows_pad = rows_pad;
+    x.k_pad = k_pad;
+    return x;
+  }
+};
+
+struct EventPairs {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  size_t used = 0;
+  double acc_ms = 0;
+  int64_t count = 0;
+  ~EventPairs() {
+    for (auto& p : pool) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+  }
+  std::pair<cudaEvent_t, cudaEvent_t> next() {
+    if (used == pool.size()) {
+      cudaEvent_t a, b;
+      ONMT_CUDA(cudaEventCreate(&a));
+      ONMT_CUDA(cudaEventCreate(&b));
+      pool.push_back({a, b});
+    }
+    return pool[used++];
+  }
+  void drain() {
+    for (size_t i = 0; i < used; ++i) {
+      float ms = 0;
+      ONMT_CUDA(cudaEventElapsedTime(&ms, pool[i].first, pool[i].second));
+      acc_ms += ms;
+      ++count;
+    }
+    used = 0;
+  }
+};
+
+}  // namespace onmt
+
+using namespace onmt;
+
+struct onmt_model {
+  int device = 0;
+  onmt_precision prec = ONMT_PREC_FP32;
+  int L = 0, E = 0, H = 0, Hd = 0, Vs = 0, Vt = 0, D = 1;
+  bool bidir = false, general = false;
+  bool use_tc = false;       // tcgen05 GEMM backend (bf16 models)
+  bool profile = false;
+  bool use_graph = false;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  int64_t launches = 0;
+
+  // weights
+  DevBuf emb_src, emb_tgt;                   // fp32 [V x E]
+  std::vector<std::unique_ptr<Mat>> enc_wih, enc_whh;  // [l*D + d]
+  std::vector<std::unique_ptr<DevBuf>> enc_bias;
+  std::vector<std::unique_ptr<Mat>> dec_w;
+  std::vector<std::unique_ptr<DevBuf>> dec_bias;
+  Mat attn_win, attn_wout, gen_w;
+  DevBuf gen_b;
+
+  // encoder workspace
+  DevBuf d_ids, d_lens;
+  Act enc_in0, enc_mid[2], enc_rec[2];
+  DevBuf enc_z[2], enc_p, mem, enc_h, enc_c;
+  // decoder workspace
+  std::vector<std::unique_ptr<Act>> xdec;    // [L]
+  Act xq, xo, xg;
+  DevBuf dec_p, st_h, st_c, st_cg, htilde, logits;
+  DevBuf g_ms, g_tz, g_ti;
+  DevBuf b_cum, b_live, b_y, b_prow, b_done, b_ndone, b_bt, b_br, b_braw, b_bnorm;
+  DevBuf h_par, h_tok, h_lp, s_score, s_par;
+  DevBuf o_hyps, o_lens, o_scores, o_raw, o_tlogp;
+
+  EventPairs ev_gen, ev_step, ev_enc;
+
+  ~onmt_model() {
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+};
+
+namespace onmt {
+
+static void count(onmt_model* m, int n = 1) { m->launches += n; }
+
+static int auto_splits(onmt_model* m, const Mat& W, int n_groups) {
+  int ctas = (W.m_pad / kTileM) * n_groups;
+  int s = std::max(1, m->num_sms / std::max(ctas, 1));
+  int kb = W.k_pad / kBK;
+  return std::min(std::min(s, kb), 16);
+}
+
+// P[split][n][m] partial sums of W * X^T; returns the number of splits written.
+static int gemm(onmt_model* m, const Mat& W, const Act& X, int n_valid, int splits, float* out, StepCtl ctl) {
+  if (W.k_pad != X.k_pad) throw Error{ONMT_E_INVALID_ARG, "internal: K mismatch"};
+  if (splits <= 0) splits = auto_splits(m, W, X.rows_pad / X.n_group);
+  if (m->use_tc) {
+    int kb = W.k_pad / kBK;
+    int kbps = (kb + splits - 1) / splits;
+    int eff = (kb + kbps - 1) / kbps;
+    ONMT_CUDA(tc_gemm_partial(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, n_valid, kb, eff, out, ctl, m->stream));
+    count(m);
+    return eff;
+  }
+  int eff = simt_effective_splits(W.k_pad, splits);
+  ONMT_CUDA(simt_gemm_partial(W.w.p, W.bf16, W.m_pad, W.k_pad, X.f32.as<float>(), X.rows_pad, n_valid, eff, out, ctl,
+                              m->stream));
+  count(m);
+  return eff;
+}
+
+static void gen(onmt_model* m, const Act& X, const GenOut& g, StepCtl ctl) {
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (m->profile) { ev = m->ev_gen.next(); ONMT_CUDA(cudaEventRecord(ev.first, m->stream)); }
+  if (m->use_tc) {
+    ONMT_CUDA(tc_gemm_gen(m->gen_w.tmap, X.tmap, m->gen_w.m_pad, X.rows_pad, X.n_group, m->gen_w.k_pad / kBK, g, ctl,
+                          m->stream));
+    count(m);
+  } else {
+    m->logits.ensure((size_t)X.rows_pad * m->gen_w.m_pad * 4);
+    ONMT_CUDA(simt_gemm_partial(m->gen_w.w.p, m->gen_w.bf16, m->gen_w.m_pad, m->gen_w.k_pad, X.f32.as<float>(),
+                                X.rows_pad, g.rows_valid, 1, m->logits.as<float>(), ctl, m->stream));
+    ONMT_CUDA(simt_gen_partials(m->logits.as<float>(), m->gen_w.m_pad, g, ctl, m->stream));
+    count(m, 2);
+  }
+  if (m->profile) ONMT_CUDA(cudaEventRecord(ev.second, m->stream));
+}
+
+// ------------------------------------------------------------------ loader
+struct HostTensor {
+  std::vector<uint64_t> dims;
+  std::vector<float> v;
+};
+
+static std::map<std::string, HostTensor> read_mnmt(const char* path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw Error{ONMT_E_IO, std::string("cannot open ") + path};
+  std::vector<char> data((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  size_t off = 0;
+  auto need = [&](size_t n) {
+    if (off + n > data.size()) throw Error{ONMT_E_FORMAT, "truncated MNMT file"};
+  };
+  auto u32 = [&]() { need(4); uint32_t v; std::memcpy(&v, data.data() + off, 4); off += 4; return v; };
+  auto u64 = [&]() { need(8); uint64_t v; std::memcpy(&v, data.data() + off, 8); off += 8; return v; };
+  need(4);
+  if (std::memcmp(data.data(), "MNMT", 4) != 0) throw Error{ONMT_E_FORMAT, "bad magic"};
+  off = 4;
+  if (u32() != 1) throw Error{ONMT_E_FORMAT, "unsupported MNMT version"};
+  std::map<std::string, HostTensor> out;
+  while (off < data.size()) {
+    uint32_t nlen = u32();
+    need(nlen);
+    std::string name(data.data() + off, nlen);
+    off += nlen;
+    uint32_t rank = u32();
+    if (rank > 8) throw Error{ONMT_E_FORMAT, "rank too large for " + name};
+    HostTensor t;
+    uint64_t n = 1;
+    for (uint32_t i = 0; i < rank; ++i) { t.dims.push_back(u64()); n *= t.dims.back(); }
+    if (u32() != 0) throw Error{ONMT_E_FORMAT, "unsupported dtype tag for " + name};
+    need(n * 4);
+    t.v.resize(n);
+    std::memcpy(t.v.data(), data.data() + off, n * 4);
+    off += n * 4;
+    if (out.count(name)) throw Error{ONMT_E_FORMAT, "duplicate tensor " + name};
+    out[name] = std::move(t);
+  }
+  return out;
+}
+
+static const HostTensor& get(std::map<std::string, HostTensor>& t, const std::string& n, std::vector<uint64_t> dims,
+                             std::vector<std::string>& seen) {
+  auto it = t.find(n);
+  if (it == t.end()) throw Error{ONMT_E_FORMAT, "missing tensor " + n};
+  if (it->second.dims != dims) throw Error{ONMT_E_FORMAT, "bad shape for " + n};
+  seen.push_back(n);
+  return it->second;
+}
+
+// Interleaved gate rows: row 4j+g <- row g*Hn+j of the concatenation [A | B] (columns).
+static std::vector<float> gate_interleave(const HostTensor& A, const HostTensor* Bm, int Hn, int& K) {
+  int ka = (int)A.dims[1], kb = Bm ? (int)Bm->dims[1] : 0;
+  K = ka + kb;
+  int mp = round_up(4 * Hn, kTileM), kp = round_up(K, kBK);
+  std::vector<float> h((size_t)mp * kp, 0.f);
+  for (int g = 0; g < 4; ++g)
+    for (int j = 0; j < Hn; ++j) {
+      float* dst = h.data() + (size_t)(4 * j + g) * kp;
+      const float* a = A.v.data() + (size_t)(g * Hn + j) * ka;
+      std::copy(a, a + ka, dst);
+      if (Bm) {
+        const float* b = Bm->v.data() + (size_t)(g * Hn + j) * kb;
+        std::copy(b, b + kb, dst + ka);
+      }
+    }
+  return h;
+}
+static std::vector<float> gate_bias(const HostTensor& bi, const HostTensor& bh, int Hn) {
+  std::vector<float> b(4 * Hn);
+  for (int g = 0; g < 4; ++g)
+    for (int j = 0; j < Hn; ++j) b[4 * j + g] = bi.v[g * Hn + j] + bh.v[g * Hn + j];
+  return b;
+}
+static std::vector<float> plain_pad(const HostTensor& A) {
+  int mm = (int)A.dims[0], kk = (int)A.dims[1];
+  int mp = round_up(mm, kTileM), kp = round_up(kk, kBK);
+  std::vector<float> h((size_t)mp * kp, 0.f);
+  for (int i = 0; i < mm; ++i) std::copy(A.v.data() + (size_t)i * kk, A.v.data() + (size_t)(i + 1) * kk, h.data() + (size_t)i * kp);
+  return h;
+}
+static void upload_f32(DevBuf& d, const std::vector<float>& h) {
+  d.ensure(h.size() * 4);
+  ONMT_CUDA(cudaMemcpy(d.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+}
+
+static void load_model(onmt_model* m, const char* path) {
+  auto t = read_mnmt(path);
+  auto has = [&](const std::string& n) { return t.count(n) > 0; };
+  if (!has("enc.emb") || !has("dec.emb") || !has("dec.l0.w_hh") || !has("enc.l0.fwd.w_hh") || !has("gen.w"))
+    throw Error{ONMT_E_FORMAT, "missing core tensors"};
+  if (t["enc.emb"].dims.size() != 2 || t["dec.l0.w_hh"].dims.size() != 2 || t["enc.l0.fwd.w_hh"].dims.size() != 2 ||
+      t["gen.w"].dims.size() != 2)
+    throw Error{ONMT_E_FORMAT, "bad rank"};
+  m->Vs = (int)t["enc.emb"].dims[0];
+  m->E = (int)t["enc.emb"].dims[1];
+  m->H = (int)t["dec.l0.w_hh"].dims[1];
+  m->Hd = (int)t["enc.l0.fwd.w_hh"].dims[1];
+  m->Vt = (int)t["gen.w"].dims[0];
+  m->bidir = has("enc.l0.bwd.w_ih");
+  m->D = m->bidir ? 2 : 1;
+  m->general = has("attn.w_in");
+  m->L = 0;
+  while (has("dec.l" + std::to_string(m->L) + ".w_ih")) ++m->L;
+  if (m->L < 1 || m->L > 8) throw Error{ONMT_E_FORMAT, "decoder layer count must be 1..8"};
+  if (m->Hd * m->D != m->H) throw Error{ONMT_E_FORMAT, "encoder width [fwd;bwd] must equal decoder width"};
+  if (m->Vt < ONMT_K_MAX || m->Vs < 1) throw Error{ONMT_E_FORMAT, "vocabulary too small"};
+  const bool bf = m->prec == ONMT_PREC_BF16;
+  if (bf)
+    for (auto& kv : t)
+      for (auto& x : kv.second.v) x = bf16_round_host(x);
+  std::vector<std::string> seen;
+  const uint64_t E = m->E, H = m->H, Hd = m->Hd, Vs = m->Vs, Vt = m->Vt;
+  const auto& es = get(t, "enc.emb", {Vs, E}, seen);
+  upload_f32(m->emb_src, es.v);
+  const char* dn[2] = {"fwd", "bwd"};
+  for (int l = 0; l < m->L; ++l)
+    for (int d = 0; d < m->D; ++d) {
+      std::string p = "enc.l" + std::to_string(l) + "." + dn[d] + ".";
+      uint64_t in = l == 0 ? E : (uint64_t)m->D * Hd;
+      const auto& wih = get(t, p + "w_ih", {4 * Hd, in}, seen);
+      const auto& whh = get(t, p + "w_hh", {4 * Hd, Hd}, seen);
+      const auto& bih = get(t, p + "b_ih", {4 * Hd}, seen);
+      const auto& bhh = get(t, p + "b_hh", {4 * Hd}, seen);
+      int K;
+      auto a = std::make_unique<Mat>();
+      a->upload(gate_interleave(wih, nullptr, (int)Hd, K), 4 * (int)Hd, K, bf);
+      auto b = std::make_unique<Mat>();
+      b->upload(gate_interleave(whh, nullptr, (int)Hd, K), 4 * (int)Hd, K, bf);
+      auto bb = std::make_unique<DevBuf>();
+      upload_f32(*bb, gate_bias(bih, bhh, (int)Hd));
+      m->enc_wih.push_back(std::move(a));
+      m->enc_whh.push_back(std::move(b));
+      m->enc_bias.push_back(std::move(bb));
+    }
+  const auto& et = get(t, "dec.emb", {Vt, E}, seen);
+  upload_f32(m->emb_tgt, et.v);
+  for (int l = 0; l < m->L; ++l) {
+    std::string p = "dec.l" + std::to_string(l) + ".";
+    uint64_t in = l == 0 ? E + H : H;
+    const auto& wih = get(t, p + "w_ih", {4 * H, in}, seen);
+    const auto& whh = get(t, p + "w_hh", {4 * H, H}, seen);
+    const auto& bih = get(t, p + "b_ih", {4 * H}, seen);
+    const auto& bhh = get(t, p + "b_hh", {4 * H}, seen);
+    int K;
+    auto w = std::make_unique<Mat>();
+    w->upload(gate_interleave(wih, &whh, (int)H, K), 4 * (int)H, K, bf);
+    auto bb = std::make_unique<DevBuf>();
+    upload_f32(*bb, gate_bias(bih, bhh, (int)H));
+    m->dec_w.push_back(std::move(w));
+    m->dec_bias.push_back(std::move(bb));
+  }
+  if (m->general) {
+    const auto& wi = get(t, "attn.w_in", {H, H}, seen);
+    m->attn_win.upload(plain_pad(wi), (int)H, (int)H, bf);
+  }
+  const auto& wo = get(t, "attn.w_out", {H, 2 * H}, seen);
+  m->attn_wout.upload(plain_pad(wo), (int)H, 2 * (int)H, bf);
+  const auto& gw = get(t, "gen.w", {Vt, H}, seen);
+  m->gen_w.upload(plain_pad(gw), (int)Vt, (int)H, bf);
+  const auto& gb = get(t, "gen.b", {Vt}, seen);
+  upload_f32(m->gen_b, gb.v);
+  if (seen.size() != t.size()) throw Error{ONMT_E_FORMAT, "unexpected extra tensors in file"};
+  ONMT_CUDA(cudaDeviceSynchronize());
+}
+
+// ------------------------------------------------------------------ encoder
+static void run_encoder(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max) {
+  const bool bf = m->use_tc;
+  const int rows = B * S_max, H = m->H, Hd = m->Hd, D = m->D;
+  StepCtl none{nullptr, 0};
+  m->enc_in0.ensure(rows, m->E, m->prec == ONMT_PREC_BF16);
+  if (m->L > 1) { m->enc_mid[0].ensure(rows, H, m->prec == ONMT_PREC_BF16); m->enc_mid[1].ensure(rows, H, m->prec == ONMT_PREC_BF16); }
+  for (int d = 0; d < D; ++d) m->enc_rec[d].ensure(B, Hd, m->prec == ONMT_PREC_BF16);
+  const int zrows = std::max(m->enc_in0.rows_pad, m->L > 1 ? m->enc_mid[0].rows_pad : 0);
+  const int zld = m->enc_wih[0]->m_pad;
+  for (int d = 0; d < D; ++d) m->enc_z[d].ensure((size_t)zrows * zld * 4);
+  m->enc_p.ensure((size_t)16 * m->enc_rec[0].rows_pad * m->enc_whh[0]->m_pad * 4);
+  m->mem.ensure((size_t)rows * H * 4);
+  m->enc_h.ensure((size_t)m->L * B * H * 4);
+  m->enc_c.ensure((size_t)m->L * B * H * 4);
+  ONMT_CUDA(cudaMemsetAsync(m->mem.p, 0, (size_t)rows * H * 4, m->stream));
+
+  launch_embed_gather(m->emb_src.as<float>(), m->E, d_ids, d_lens, B, S_max, m->enc_in0.xo(bf), m->stream);
+  count(m);
+  const Act* xin = &m->enc_in0;
+  for (int l = 0; l < m->L; ++l) {
+    const Act* xnext = l + 1 < m->L ? &m->enc_mid[l % 2] : nullptr;
+    for (int d = 0; d < D; ++d)
+      gemm(m, *m->enc_wih[l * D + d], *xin, rows, 1, m->enc_z[d].as<float>(), none);
+    for (int t = 0; t < S_max; ++t)
+      for (int d = 0; d < D; ++d) {
+        const Mat& whh = *m->enc_whh[l * D + d];
+        int splits = 0;
+        const float* P = nullptr;
+        if (t > 0) {
+          splits = gemm(m, whh, m->enc_rec[d], B, 0, m->enc_p.as<float>(), none);
+          P = m->enc_p.as<float>();
+        }
+        XOut xn{};
+        if (xnext) xn = xnext->xo(bf);
+        launch_enc_cell(m->enc_z[d].as<float>(), zld, P, splits, m->enc_rec[d].rows_pad, whh.m_pad,
+                        m->enc_bias[l * D + d]->as<float>(), Hd, B, d_lens, S_max, t, d == 1,
+                        m->enc_h.as<float>() + (size_t)l * B * H + d * Hd,
+                        m->enc_c.as<float>() + (size_t)l * B * H + d * Hd, H, m->enc_rec[d].xo(bf), xn, d * Hd,
+                        l + 1 == m->L ? m->mem.as<float>() : nullptr, H, d * Hd, m->stream);
+        count(m);
+      }
+    xin = xnext;
+  }
+  ONMT_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ decoder
+struct DecodeOut {
+  int* hyps;
+  int* lens;
+  float* scores;
+  float* raw;
+  float* tlogp;
+};
+
+static BeamState beam_state(onmt_model* m, bool trace) {
+  BeamState bs;
+  bs.cum = m->b_cum.as<double>();
+  bs.live = m->b_live.as<int>();
+  bs.y = m->b_y.as<int>();
+  bs.prow = m->b_prow.as<int>();
+  bs.done = m->b_done.as<int>();
+  bs.n_done = m->b_ndone.as<int>();
+  bs.best_t = m->b_bt.as<int>();
+  bs.best_r = m->b_br.as<int>();
+  bs.best_raw = m->b_braw.as<double>();
+  bs.best_norm = m->b_bnorm.as<double>();
+  bs.hist_parent = m->h_par.as<int>();
+  bs.hist_token = m->h_tok.as<int>();
+  bs.hist_logp = m->h_lp.as<float>();
+  bs.sel_score = trace ? m->s_score.as<double>() : nullptr;
+  bs.sel_parent = trace ? m->s_par.as<int>() : nullptr;
+  return bs;
+}
+
+static void run_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int K, int max_len, float alpha,
+                        bool trace, const DecodeOut& out) {
+  const bool bf = m->use_tc, bfm = m->prec == ONMT_PREC_BF16;
+  const int R = B * K, H = m->H, E = m->E, L = m->L;
+  while ((int)m->xdec.size() < L) m->xdec.push_back(std::make_unique<Act>());
+  m->xdec[0]->ensure(R, E + 2 * H, bfm);
+  for (int l = 1; l < L; ++l) m->xdec[l]->ensure(R, 2 * H, bfm);
+  if (m->general) m->xq.ensure(R, H, bfm);
+  m->xo.ensure(R, 2 * H, bfm);
+  m->xg.ensure(R, H, bfm);
+  const int rp = m->xg.rows_pad;
+  size_t pm = (size_t)m->dec_w[0]->m_pad;
+  m->dec_p.ensure((size_t)16 * rp * pm * 4);
+  m->st_h.ensure((size_t)L * rp * H * 4);
+  m->st_c.ensure((size_t)L * rp * H * 4);
+  m->st_cg.ensure((size_t)L * rp * H * 4);
+  m->htilde.ensure((size_t)rp * H * 4);
+  const int n_vt = (m->Vt + kVTile - 1) / kVTile;
+  m->g_ms.ensure((size_t)n_vt * rp * 8);
+  m->g_tz.ensure((size_t)n_vt * rp * K * 4);
+  m->g_ti.ensure((size_t)n_vt * rp * K * 4);
+  m->b_cum.ensure((size_t)R * 8);
+  m->b_live.ensure((size_t)R * 4);
+  m->b_y.ensure((size_t)R * 4);
+  m->b_prow.ensure((size_t)R * 4);
+  m->b_done.ensure((size_t)B * 4);
+  m->b_ndone.ensure(4);
+  m->b_bt.ensure((size_t)B * 4);
+  m->b_br.ensure((size_t)B * 4);
+  m->b_braw.ensure((size_t)B * 8);
+  m->b_bnorm.ensure((size_t)B * 8);
+  m->h_par.ensure((size_t)max_len * R * 4);
+  m->h_tok.ensure((size_t)max_len * R * 4);
+  m->h_lp.ensure((size_t)max_len * R * 4);
+  if (trace) {
+    m->s_score.ensure((size_t)max_len * R * 8);
+    m->s_par.ensure((size_t)max_len * R * 4);
+    ONMT_CUDA(cudaMemsetAsync(m->s_par.p, 0xff, (size_t)max_len * R * 4, m->stream));
+    ONMT_CUDA(cudaMemsetAsync(m->h_tok.p, 0, (size_t)max_len * R * 4, m->stream));
+    std::vector<double> ninf((size_t)max_len * R, -INFINITY);
+    ONMT_CUDA(cudaMemcpyAsync(m->s_score.p, ninf.data(), ninf.size() * 8, cudaMemcpyHostToDevice, m->stream));
+    ONMT_CUDA(cudaStreamSynchronize(m->stream));
+  }
+  BeamState bs = beam_state(m, trace);
+  float* hh = m->st_h.as<float>();
+  float* cc = m->st_c.as<float>();
+  float* cg = m->st_cg.as<float>();
+  launch_init_decode(bs, B, K, m->enc_h.as<float>(), m->enc_c.as<float>(), L, H, hh, cc, rp, m->htilde.as<float>(),
+                     m->stream);
+  count(m);
+  StepCtl ctl{bs.n_done, B};
+  GatherArgs ga{};
+  ga.emb_tgt = m->emb_tgt.as<float>();
+  ga.E = E; ga.H = H; ga.L = L;
+  ga.htilde = m->htilde.as<float>();
+  ga.h = hh; ga.c = cc; ga.cg = cg; ga.rows_pad = rp;
+  for (int l = 0; l < L; ++l) ga.x[l] = m->xdec[l]->xo(bf);
+  launch_gather(bs, ga, R, K, StepCtl{nullptr, 0}, m->stream);
+  count(m);
+  GenOut g;
+  g.ms = m->g_ms.as<float2>();
+  g.tz = m->g_tz.as<float>();
+  g.ti = m->g_ti.as<int>();
+  g.bias = m->gen_b.as<float>();
+  g.V = m->Vt;
+  g.K = K;
+  g.rows_valid = R;
+  g.rows_pad = rp;
+  float* P = m->dec_p.as<float>();
+  for (int t = 1; t <= max_len; ++t) {
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    if (m->profile) { ev = m->ev_step.next(); ONMT_CUDA(cudaEventRecord(ev.first, m->stream)); }
+    for (int l = 0; l < L; ++l) {
+      const Mat& W = *m->dec_w[l];
+      int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
+      CellDst dst{};
+      if (l + 1 < L) {
+        dst.x[0] = m->xdec[l + 1]->xo(bf); dst.col[0] = 0; dst.n = 1;
+      } else {
+        dst.x[0] = m->xo.xo(bf); dst.col[0] = H; dst.n = 1;
+        if (m->general) { dst.x[1] = m->xq.xo(bf); dst.col[1] = 0; dst.n = 2; }
+      }
+      launch_dec_cell(P, s, m->xdec[l]->rows_pad, W.m_pad, m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H,
+                      cc + (size_t)l * rp * H, hh + (size_t)l * rp * H, H, R, dst, ctl, m->stream);
+      count(m);
+    }
+    const float* htop = hh + (size_t)(L - 1) * rp * H;
+    if (m->general) {
+      int s = gemm(m, m->attn_win, m->xq, R, 0, P, ctl);
+      ONMT_CUDA(launch_attention(P, s, m->xq.rows_pad, m->attn_win.m_pad, nullptr, m->mem.as<float>(), d_lens, B,
+                                 S_max, H, K, m->xo.xo(bf), bs.done, ctl, m->stream));
+    } else {
+      ONMT_CUDA(launch_attention(nullptr, 0, 0, 0, htop, m->mem.as<float>(), d_lens, B, S_max, H, K, m->xo.xo(bf),
+                                 bs.done, ctl, m->stream));
+    }
+    count(m);
+    {
+      int s = gemm(m, m->attn_wout, m->xo, R, 0, P, ctl);
+      launch_attn_out(P, s, m->xo.rows_pad, m->attn_wout.m_pad, m->htilde.as<float>(), H, R, m->xg.xo(bf), ctl,
+                      m->stream);
+      count(m);
+    }
+    gen(m, m->xg, g, ctl);
+    launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, B, K, t, max_len, alpha, bs, ctl, m->stream);
+    count(m);
+    if (t < max_len) { launch_gather(bs, ga, R, K, ctl, m->stream); count(m); }
+    if (m->profile) ONMT_CUDA(cudaEventRecord(ev.second, m->stream));
+  }
+  launch_finalize(bs, B, K, max_len, out.hyps, out.lens, out.scores, out.raw, out.tlogp, m->stream);
+  count(m);
+  ONMT_CUDA(cudaGetLastError());
+}
+
+}  // namespace onmt
+
+// ====================================================================== C-ABI
+#define ONMT_API_BEGIN try {
+#define ONMT_API_END                              \
+  }                                               \
+  catch (const Error& e) {                        \
+    g_err = e.msg;                                \
+    return e.s;                                   \
+  }                                               \
+  catch (const std::bad_alloc&) {                 \
+    g_err = "host out of memory";                 \
+    return ONMT_E_OOM;                            \
+  }                                               \
+  catch (const std::exception& e) {               \
+    g_err = e.what();                             \
+    return ONMT_E_INVALID_ARG;                    \
+  }
+
+static onmt_status fail(onmt_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+extern "C" {
+
+const char* onmt_last_error(void) { return g_err.c_str(); }
+
+onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision prec, onmt_model** out) {
+  if (out) *out = nullptr;
+  if (!path || !out) return fail(ONMT_E_INVALID_ARG, "null path or out");
+  if (prec != ONMT_PREC_FP32 && prec != ONMT_PREC_BF16) return fail(ONMT_E_INVALID_ARG, "bad precision");
+  g_err.clear();
+  ONMT_API_BEGIN
+  int ndev = 0;
+  ONMT_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(ONMT_E_INVALID_ARG, "bad device index");
+  ONMT_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  ONMT_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(ONMT_E_UNSUPPORTED, "requires an sm_100 (B200) device");
+  std::unique_ptr<onmt_model> m(new onmt_model());
+  m->device = device;
+  m->prec = prec;
+  m->use_tc = prec == ONMT_PREC_BF16;
+  m->num_sms = prop.multiProcessorCount;
+  ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
+  m->stream = m->own_stream;
+  load_model(m.get(), path);
+  *out = m.release();
+  return ONMT_OK;
+  ONMT_API_END
+}
+
+onmt_status onmt_model_get_info(const onmt_model* m, onmt_model_info* o) {
+  if (!m || !o) return fail(ONMT_E_INVALID_ARG, "null argument");
+  o->layers = m->L; o->emb = m->E; o->hidden = m->H; o->v_src = m->Vs; o->v_tgt = m->Vt;
+  o->bidir = m->bidir; o->attn_general = m->general; o->precision = m->prec;
+  return ONMT_OK;
+}
+
+onmt_status onmt_set_stream(onmt_model* m, void* s) {
+  if (!m) return fail(ONMT_E_INVALID_ARG, "null model");
+  m->stream = s ? (cudaStream_t)s : m->own_stream;
+  return ONMT_OK;
+}
+
+onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
+  if (!m || !name) return fail(ONMT_E_INVALID_ARG, "null argument");
+  std::string n(name);
+  if (n == "gemm_backend") {
+    if (v != 0 && v != 1) return fail(ONMT_E_INVALID_ARG, "gemm_backend must be 0 or 1");
+    m->use_tc = (v == 0) && m->prec == ONMT_PREC_BF16;
+  } else if (n == "profile") {
+    m->profile = v != 0;
+  } else if (n == "use_graph") {
+    m->use_graph = v != 0;
+  } else {
+    return fail(ONMT_E_INVALID_ARG, "unknown option " + n);
+  }
+  return ONMT_OK;
+}
+
+static onmt_status validate(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
+                            bool check_ids) {
+  if (!m) return fail(ONMT_E_INVALID_ARG, "null model");
+  if (B < 0) return fail(ONMT_E_INVALID_ARG, "B < 0");
+  if (B == 0) return ONMT_OK;
+  if (S_max < 1) return fail(ONMT_E_INVALID_ARG, "S_max < 1");
+  if (!lens || (check_ids && !ids)) return fail(ONMT_E_INVALID_ARG, "null source pointer");
+  for (int b = 0; b < B; ++b) {
+    if (lens[b] < 1) return fail(ONMT_E_EMPTY_SOURCE, "empty source sentence " + std::to_string(b));
+    if (lens[b] > S_max) return fail(ONMT_E_INVALID_ARG, "src_len > S_max");
+  }
+  if (check_ids)
+    for (int b = 0; b < B; ++b)
+      for (int s = 0; s < lens[b]; ++s) {
+        int v = ids[(size_t)b * S_max + s];
+        if (v < 0 || v >= m->Vs) return fail(ONMT_E_ID_RANGE, "source id out of range");
+      }
+  return ONMT_OK;
+}
+
+static void upload_src(onmt_model* m, const int32_t* ids, const int32_t* lens, int B, int S_max) {
+  m->d_ids.ensure((size_t)B * S_max * 4);
+  m->d_lens.ensure((size_t)B * 4);
+  // ids at padded positions are ignored by contract; sanitize them so gathers stay in range
+  std::vector<int32_t> clean((size_t)B * S_max, 0);
+  for (int b = 0; b < B; ++b)
+    for (int s = 0; s < lens[b]; ++s) clean[(size_t)b * S_max + s] = ids[(size_t)b * S_max + s];
+  ONMT_CUDA(cudaMemcpyAsync(m->d_ids.p, clean.data(), clean.size() * 4, cudaMemcpyHostToDevice, m->stream));
+  ONMT_CUDA(cudaMemcpyAsync(m->d_lens.p, lens, (size_t)B * 4, cudaMemcpyHostToDevice, m->stream));
+}
+
+onmt_status onmt_encode(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
+                        float* out_memory, float* out_h, float* out_c) {
+  onmt_status s = validate(m, ids, lens, B, S_max, true);
+  if (s != ONMT_OK || B == 0) return s;
+  ONMT_API_BEGIN
+  ONMT_CUDA(cudaSetDevice(m->device));
+  upload_src(m, ids, lens, B, S_max);
+  run_encoder(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max);
+  if (out_memory)
+    ONMT_CUDA(cudaMemcpyAsync(out_memory, m->mem.p, (size_t)B * S_max * m->H * 4, cudaMemcpyDeviceToHost, m->stream));
+  if (out_h) ONMT_CUDA(cudaMemcpyAsync(out_h, m->enc_h.p, (size_t)m->L * B * m->H * 4, cudaMemcpyDeviceToHost, m->stream));
+  if (out_c) ONMT_CUDA(cudaMemcpyAsync(out_c, m->enc_c.p, (size_t)m->L * B * m->H * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaStreamSynchronize(m->stream));
+  return ONMT_OK;
+  ONMT_API_END
+}
+
+static onmt_status check_decode_args(int32_t beam, int32_t max_len, float alpha) {
+  if (beam < 1) return fail(ONMT_E_INVALID_ARG, "beam < 1");
+  if (beam > ONMT_K_MAX) return fail(ONMT_E_UNSUPPORTED, "beam > ONMT_K_MAX");
+  if (max_len < 1) return fail(ONMT_E_INVALID_ARG, "max_len < 1");
+  if (!(alpha >= 0.f)) return fail(ONMT_E_INVALID_ARG, "length_penalty must be >= 0");
+  return ONMT_OK;
+}
+
+static onmt_status translate_impl(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
+                                  int32_t beam, int32_t max_len, float alpha, int32_t* hyps, int32_t* olens,
+                                  float* scores, float* raw, float* tlogp, int32_t* sel_parent, int32_t* sel_token,
+                                  double* sel_score) {
+  onmt_status s = validate(m, ids, lens, B, S_max, true);
+  if (s != ONMT_OK) return s;
+  s = check_decode_args(beam, max_len, alpha);
+  if (s != ONMT_OK) return s;
+  if (B == 0) return ONMT_OK;
+  if (!hyps || !olens || !scores) return fail(ONMT_E_INVALID_ARG, "null output pointer");
+  const bool trace = sel_parent || sel_token || sel_score;
+  ONMT_API_BEGIN
+  ONMT_CUDA(cudaSetDevice(m->device));
+  upload_src(m, ids, lens, B, S_max);
+  m->o_hyps.ensure((size_t)B * max_len * 4);
+  m->o_lens.ensure((size_t)B * 4);
+  m->o_scores.ensure((size_t)B * 4);
+  m->o_raw.ensure((size_t)B * 4);
+  m->o_tlogp.ensure((size_t)B * max_len * 4);
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (m->profile) { ev = m->ev_enc.next(); ONMT_CUDA(cudaEventRecord(ev.first, m->stream)); }
+  run_encoder(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max);
+  if (m->profile) ONMT_CUDA(cudaEventRecord(ev.second, m->stream));
+  DecodeOut o{m->o_hyps.as<int>(), m->o_lens.as<int>(), m->o_scores.as<float>(), m->o_raw.as<float>(),
+              m->o_tlogp.as<float>()};
+  run_decoder(m, m->d_lens.as<int>(), B, S_max, beam, max_len, alpha, trace, o);
+  ONMT_CUDA(cudaMemcpyAsync(hyps, o.hyps, (size_t)B * max_len * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaMemcpyAsync(olens, o.lens, (size_t)B * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaMemcpyAsync(scores, o.scores, (size_t)B * 4, cudaMemcpyDeviceToHost, m->stream));
+  if (raw) ONMT_CUDA(cudaMemcpyAsync(raw, o.raw, (size_t)B * 4, cudaMemcpyDeviceToHost, m->stream));
+  if (tlogp) ONMT_CUDA(cudaMemcpyAsync(tlogp, o.tlogp, (size_t)B * max_len * 4, cudaMemcpyDeviceToHost, m->stream));
+  const size_t n = (size_t)max_len * B * beam;
+  if (sel_parent) ONMT_CUDA(cudaMemcpyAsync(sel_parent, m->s_par.p, n * 4, cudaMemcpyDeviceToHost, m->stream));
+  if (sel_token) ONMT_CUDA(cudaMemcpyAsync(sel_token, m->h_tok.p, n * 4, cudaMemcpyDeviceToHost, m->stream));
+  if (sel_score) ONMT_CUDA(cudaMemcpyAsync(sel_score, m->s_score.p, n * 8, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaStreamSynchronize(m->stream));
+  return ONMT_OK;
+  ONMT_API_END
+}
+
+onmt_status onmt_translate(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
+                           int32_t beam, int32_t max_len, float alpha, int32_t* hyps, int32_t* olens, float* scores,
+                           float* raw, float* tlogp) {
+  return translate_impl(m, ids, lens, B, S_max, beam, max_len, alpha, hyps, olens, scores, raw, tlogp, nullptr,
+                        nullptr, nullptr);
+}
+
+onmt_status onmt_translate_trace(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
+                                 int32_t beam, int32_t max_len, float alpha, int32_t* hyps, int32_t* olens,
+                                 float* scores, float* raw, float* tlogp, int32_t* sel_parent, int32_t* sel_token,
+                                 double* sel_score) {
+  if (!sel_parent || !sel_token || !sel_score) return fail(ONMT_E_INVALID_ARG, "null trace pointer");
+  return translate_impl(m, ids, lens, B, S_max, beam, max_len, alpha, hyps, olens, scores, raw, tlogp, sel_parent,
+                        sel_token, sel_score);
+}
+
+onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_ids, const int32_t* d_lens, const int32_t* lens_host,
+                               int32_t B, int32_t S_max, int32_t beam, int32_t max_len, float alpha, int32_t* d_hyps,
+                               int32_t* d_olens, float* d_scores, float* d_raw, float* d_tlogp) {
+  if (!m) return fail(ONMT_E_INVALID_ARG, "null model");
+  if (B < 0) return fail(ONMT_E_INVALID_ARG, "B < 0");
+  onmt_status s = check_decode_args(beam, max_len, alpha);
+  if (s != ONMT_OK) return s;
+  if (B == 0) return ONMT_OK;
+  if (S_max < 1) return fail(ONMT_E_INVALID_ARG, "S_max < 1");
+  if (lens_host) {
+    s = validate(m, nullptr, lens_host, B, S_max, false);
+    if (s != ONMT_OK) return s;
+  }
+  if (!d_ids || !d_lens || !d_hyps || !d_olens || !d_scores) return fail(ONMT_E_INVALID_ARG, "null device pointer");
+  ONMT_API_BEGIN
+  ONMT_CUDA(cudaSetDevice(m->device));
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (m->profile) { ev = m->ev_enc.next(); ONMT_CUDA(cudaEventRecord(ev.first, m->stream)); }
+  run_encoder(m, d_ids, d_lens, B, S_max);
+  if (m->profile) ONMT_CUDA(cudaEventRecord(ev.second, m->stream));
+  m->o_raw.ensure((size_t)B * 4);
+  m->o_tlogp.ensure((size_t)B * max_len * 4);
+  DecodeOut o{d_hyps, d_olens, d_scores, d_raw ? d_raw : m->o_raw.as<float>(),
+              d_tlogp ? d_tlogp : m->o_tlogp.as<float>()};
+  run_decoder(m, d_lens, B, S_max, beam, max_len, alpha, false, o);
+  return ONMT_OK;
+  ONMT_API_END
+}
+
+onmt_status onmt_get_kernel_time(onmt_model* m, const char* name, int32_t reset, double* total_ms, int64_t* launches) {
+  if (!m || !name || !total_ms || !launches) return fail(ONMT_E_INVALID_ARG, "null argument");
+  ONMT_API_BEGIN
+  EventPairs* e = nullptr;
+  std::string n(name);
+  if (n == "gen") e = &m->ev_gen;
+  else if (n == "step") e = &m->ev_step;
+  else if (n == "encode") e = &m->ev_enc;
+  else return fail(ONMT_E_INVALID_ARG, "unknown kernel family " + n);
+  ONMT_CUDA(cudaStreamSynchronize(m->stream));
+  e->drain();
+  *total_ms = e->acc_ms;
+  *launches = e->count;
+  if (reset) { e->acc_ms = 0; e->count = 0; }
+  return ONMT_OK;
+  ONMT_API_END
+}
+
+onmt_status onmt_kernel_launches(onmt_model* m, int32_t reset, int64_t* launches) {
+  if (!m || !launches) return fail(ONMT_E_INVALID_ARG, "null argument");
+  *launches = m->launches;
+  if (reset) m->launches = 0;
+  return ONMT_OK;
+}
+
+void onmt_free(onmt_model* m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  cudaStreamSynchronize(m->stream);
+  delete m;
+}
+
+onmt_status onmt_test_gemm(onmt_model* m, const float* W, const float* X, int32_t M, int32_t N, int32_t K,
+                           int32_t splits, float* out) {
+  if (!m || !W || !X || !out || M < 1 || N < 1 || K < 1 || splits < 0) return fail(ONMT_E_INVALID_ARG, "bad args");
+  ONMT_API_BEGIN
+  ONMT_CUDA(cudaSetDevice(m->device));
+  const bool bfm = m->prec == ONMT_PREC_BF16;
+  Mat w;
+  int mp = round_up(M, kTileM), kp = round_up(K, kBK);
+  std::vector<float> hw((size_t)mp * kp, 0.f);
+  for (int i = 0; i < M; ++i)
+    for (int k = 0; k < K; ++k) hw[(size_t)i * kp + k] = bfm ? bf16_round_host(W[(size_t)i * K + k]) : W[(size_t)i * K + k];
+  w.upload(hw, M, K, bfm);
+  Act x;
+  x.ensure(N, K, bfm);
+  std::vector<float> hx((size_t)x.rows_pad * kp, 0.f);
+  for (int n = 0; n < N; ++n)
+    for (int k = 0; k < K; ++k) hx[(size_t)n * kp + k] = X[(size_t)n * K + k];
+  ONMT_CUDA(cudaMemcpy(x.f32.p, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice));
+  if (bfm) {
+    std::vector<__nv_bfloat16> hl(2 * hx.size());
+    for (size_t i = 0; i < hx.size(); ++i) {
+      __nv_bfloat16 hi = __float2bfloat16_rn(hx[i]);
+      hl[i] = hi;
+      hl[hx.size() + i] = __float2bfloat16_rn(hx[i] - __bfloat162float(hi));
+    }
+    ONMT_CUDA(cudaMemcpy(x.hl.p, hl.data(), hl.size() * 2, cudaMemcpyHostToDevice));
+  }
+  DevBuf P;
+  P.ensure((size_t)16 * x.rows_pad * w.m_pad * 4);
+  int eff = gemm(m, w, x, N, splits == 0 ? 0 : std::min(splits, 16), P.as<float>(), StepCtl{nullptr, 0});
+  std::vector<float> hp((size_t)eff * x.rows_pad * w.m_pad);
+  ONMT_CUDA(cudaMemcpyAsync(hp.data(), P.p, hp.size() * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaStreamSynchronize(m->stream));
+  for (int n = 0; n < N; ++n)
+    for (int i = 0; i < M; ++i) {
+      float s = 0.f;
+      for (int z = 0; z < eff; ++z) s += hp[((size_t)z * x.rows_pad + n) * w.m_pad + i];
+      out[(size_t)n * M + i] = s;
+    }
+  return ONMT_OK;
+  ONMT_API_END
+}
+
+onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t k, float* lse, float* top_z,
+                          int32_t* top_id) {
+  if (!m || !htilde || !lse || !top_z || !top_id || R < 1 || k < 1 || k > ONMT_K_MAX)
+    return fail(ONMT_E_INVALID_ARG, "bad args");
+  ONMT_API_BEGIN
+  ONMT_CUDA(cudaSetDevice(m->device));
+  const bool bfm = m->prec == ONMT_PREC_BF16;
+  Act x;
+  x.ensure(R, m->H, bfm);
+  std::vector<float> hx((size_t)x.rows_pad * x.k_pad, 0.f);
+  for (int r = 0; r < R; ++r)
+    for (int j = 0; j < m->H; ++j) hx[(size_t)r * x.k_pad + j] = htilde[(size_t)r * m->H + j];
+  ONMT_CUDA(cudaMemcpy(x.f32.p, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice));
+  if (bfm) {
+    std::vector<__nv_bfloat16> hl(2 * hx.size());
+    for (size_t i = 0; i < hx.size(); ++i) {
+      __nv_bfloat16 hi = __float2bfloat16_rn(hx[i]);
+      hl[i] = hi;
+      hl[hx.size() + i] = __float2bfloat16_rn(hx[i] - __bfloat162float(hi));
+    }
+    ONMT_CUDA(cudaMemcpy(x.hl.p, hl.data(), hl.size() * 2, cudaMemcpyHostToDevice));
+  }
+  const int n_vt = (m->Vt + kVTile - 1) / kVTile;
+  DevBuf ms, tz, ti, dl, dz, di;
+  ms.ensure((size_t)n_vt * x.rows_pad * 8);
+  tz.ensure((size_t)n_vt * x.rows_pad * k * 4);
+  ti.ensure((size_t)n_vt * x.rows_pad * k * 4);
+  dl.ensure((size_t)R * 4);
+  dz.ensure((size_t)R * k * 4);
+  di.ensure((size_t)R * k * 4);
+  GenOut g{ms.as<float2>(), tz.as<float>(), ti.as<int>(), m->gen_b.as<float>(), m->Vt, k, R, x.rows_pad};
+  gen(m, x, g, StepCtl{nullptr, 0});
+  launch_row_reduce(g.ms, g.tz, g.ti, n_vt, x.rows_pad, R, k, dl.as<float>(), dz.as<float>(), di.as<int>(), m->stream);
+  ONMT_CUDA(cudaGetLastError());
+  ONMT_CUDA(cudaMemcpyAsync(lse, dl.p, (size_t)R * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaMemcpyAsync(top_z, dz.p, (size_t)R * k * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaMemcpyAsync(top_id, di.p, (size_t)R * k * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaStreamSynchronize(m->stream));
+  return ONMT_OK;
+  ONMT_API_END
+}
+
+}  // extern "C"

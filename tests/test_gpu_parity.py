@@ -1,0 +1,228 @@
+"""End-to-end GPU parity through the C-ABI (onmt_encode / onmt_translate_trace) against the
+fp64 oracle, with the DESIGN.md §4 protocol (tests/parity.py)."""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import OracleModel, beam_search, greedy, load_model_tensors
+from parity import compare_batch
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    import paper_1805_11462_b200 as ob
+    return ob
+
+
+_cache = {}
+
+
+def model_pair(workload, weight_cache, precision=None, overrides=None, tag=""):
+    key = (workload, precision, tag)
+    if key not in _cache:
+        w = synth.WORKLOADS[workload]
+        prec = precision or w.decode.precision
+        path = synth.weights_file(workload, weight_cache, overrides=overrides, tag=tag)
+        _cache[key] = (_lib().Model(path, 0, prec), OracleModel(load_model_tensors(path, prec)), prec)
+    return _cache[key]
+
+
+def toy_pair(cfg, seed, scale, weight_cache, precision, overrides=None, name="toy"):
+    key = (name, seed, scale, precision, str(cfg))
+    if key not in _cache:
+        t = synth.random_model_tensors(cfg, seed, scale)
+        if overrides:
+            t.update(overrides)
+        path = os.path.join(weight_cache, f"{name}_{seed}_{abs(hash(str(cfg))) % 10**8}.mnmt")
+        synth.write_mnmt(path, t)
+        _cache[key] = (_lib().Model(path, 0, precision), OracleModel(load_model_tensors(path, precision)), precision)
+    return _cache[key]
+
+
+def run_parity(gm, om, prec, ids, lens, K, max_len, alpha):
+    gpu = gm.translate(ids, lens, K, max_len, alpha, trace=True)
+    res = compare_batch(om, ids, lens, gpu, K, max_len, alpha, prec)
+    fails = [d for s, d in res["details"] if s == "fail"]
+    assert res["fail"] == 0, fails
+    return res, gpu
+
+
+# ------------------------------------------------------------------ encoder
+@pytest.mark.parametrize("workload", ["c1", "c3"])
+def test_encoder_parity(workload, weight_cache):
+    gm, om, prec = model_pair(workload, weight_cache)
+    ids, lens = synth.make_corpus(workload, 4 if workload != "c1" else None)
+    mem, h, c = gm.encode(ids, lens)
+    tol = 1e-5 if prec == "fp32" else 2e-4
+    for b in range(len(lens)):
+        ref_mem, finals = om.encode([int(v) for v in ids[b, :lens[b]]])
+        np.testing.assert_allclose(mem[b, :lens[b]], ref_mem, atol=tol)
+        assert (mem[b, lens[b]:] == 0).all()
+        for l in range(om.L):
+            np.testing.assert_allclose(h[l, b], finals[l][0], atol=tol)
+            np.testing.assert_allclose(c[l, b], finals[l][1], atol=tol)
+
+
+# ------------------------------------------------------------------ end to end
+def test_c1_fp32_parity(weight_cache):
+    """BASELINE configs[0] exactly: fp32 mode, exact sequences, token log p within 1e-5."""
+    gm, om, prec = model_pair("c1", weight_cache)
+    ids, lens = synth.make_corpus("c1")
+    res, gpu = run_parity(gm, om, prec, ids, lens, 3, 10, 0.0)
+    assert res["match"] == 2
+
+
+@pytest.mark.parametrize("workload,n,max_len", [("c2", 4, 24), ("c3", 3, 16), ("c5", 2, 12), ("c4", 2, 8)])
+def test_bf16_parity_subset(workload, n, max_len, weight_cache):
+    gm, om, prec = model_pair(workload, weight_cache)
+    w = synth.WORKLOADS[workload]
+    ids, lens = synth.make_corpus(workload, n)
+    res, _ = run_parity(gm, om, prec, ids, lens, w.decode.beam, max_len, w.decode.alpha)
+    assert res["match"] + res["excused"] == n
+
+
+def test_c2_full_length_sentence(weight_cache):
+    """One c2 sentence decoded to BASELINE's max_len = 100 (full-size launch config)."""
+    gm, om, prec = model_pair("c2", weight_cache)
+    ids, lens = synth.make_corpus("c2", 30)
+    gpu = gm.translate(ids, lens, 5, 100, 0.0, trace=True)
+    assert (gpu["lens"] == 100).all()          # random weights: every sentence runs to max_len
+    sub = [0]
+    res = compare_batch(om, ids[sub], lens[sub], {k: (v[:, sub] if k.startswith("sel_") else v[sub])
+                                                  for k, v in gpu.items()}, 5, 100, 0.0, prec)
+    assert res["fail"] == 0, res["details"]
+
+
+def test_fp32_mode_c2_model_subset(weight_cache):
+    """fp32 mode on the c2 model (SIMT path): token log p within 1e-5."""
+    gm, om, prec = model_pair("c2", weight_cache, precision="fp32")
+    ids, lens = synth.make_corpus("c2", 2)
+    run_parity(gm, om, prec, ids, lens, 5, 8, 0.0)
+
+
+# ------------------------------------------------------------------ decode rules on toy models
+TOY = synth.ModelConfig(2, 16, 32, 60, 40, False, True)
+TOY_BI = synth.ModelConfig(2, 16, 32, 60, 40, True, False)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("cfg", [TOY, TOY_BI])
+@pytest.mark.parametrize("K,alpha", [(1, 0.0), (3, 0.6), (5, 0.0), (16, 1.0)])
+def test_toy_models_peaky(prec, cfg, K, alpha, weight_cache):
+    """Peaky toy models (U(-1.5, 1.5)) finish early on EOS: exercises banking, stop
+    rules, dead slots and the final choice against the oracle."""
+    gm, om, p = toy_pair(cfg, 11, 1.5, weight_cache, prec)
+    rng = np.random.default_rng(K)
+    lens = rng.integers(1, 12, 6).astype(np.int32)
+    ids = np.zeros((6, 12), np.int32)
+    for b in range(6):
+        ids[b, :lens[b]] = rng.integers(4, 60, lens[b])
+    res, gpu = run_parity(gm, om, p, ids, lens, K, 15, alpha)
+    assert res["match"] + res["excused"] == 6
+
+
+def test_beam1_equals_oracle_greedy(weight_cache):
+    gm, om, p = toy_pair(TOY, 5, 1.2, weight_cache, "fp32")
+    rng = np.random.default_rng(0)
+    lens = np.array([7, 3, 1], np.int32)
+    ids = np.zeros((3, 7), np.int32)
+    for b in range(3):
+        ids[b, :lens[b]] = rng.integers(4, 60, lens[b])
+    gpu = gm.translate(ids, lens, 1, 12, 0.0)
+    for b in range(3):
+        g = greedy(om, [int(v) for v in ids[b, :lens[b]]], 12)
+        assert list(gpu["hyps"][b, :gpu["lens"][b]]) == g["tokens"]
+
+
+def test_forced_eos_model(weight_cache):
+    b = np.zeros(40, np.float32); b[3] = 50.0
+    gm, om, p = toy_pair(TOY, 2, 0.3, weight_cache, "fp32",
+                         overrides={"gen.w": np.zeros((40, 32), np.float32), "gen.b": b}, name="forced")
+    ids = np.array([[5, 6, 7]], np.int32)
+    out = gm.translate(ids, np.array([3], np.int32), 4, 10, 0.0)
+    assert out["lens"][0] == 1 and out["hyps"][0, 0] == 3
+    assert abs(out["raw"][0]) < 1e-6
+
+
+# ------------------------------------------------------------------ invariants
+def test_batch_equivalence_permutation_and_padding(weight_cache):
+    gm, om, p = model_pair("c2", weight_cache)
+    ids, lens = synth.make_corpus("c2", 6)
+    full = gm.translate(ids, lens, 5, 12, 0.0)
+    again = gm.translate(ids, lens, 5, 12, 0.0)
+    for k in full:
+        np.testing.assert_array_equal(full[k], again[k])        # bitwise determinism
+    perm = np.array([3, 0, 5, 1, 4, 2])
+    pm = gm.translate(ids[perm], lens[perm], 5, 12, 0.0)
+    np.testing.assert_array_equal(pm["hyps"], full["hyps"][perm])
+    np.testing.assert_allclose(pm["token_logp"], full["token_logp"][perm], atol=2e-5)
+    # garbage at padded positions and a wider S_max change nothing
+    ids2 = np.concatenate([ids, np.full((6, 7), 17, np.int32)], axis=1)
+    for b in range(6):
+        ids2[b, lens[b]:] = 999
+    pd = gm.translate(ids2, lens, 5, 12, 0.0)
+    np.testing.assert_array_equal(pd["hyps"], full["hyps"])
+    np.testing.assert_allclose(pd["token_logp"], full["token_logp"], atol=2e-5)
+    # singles
+    for b in (0, 4):
+        one = gm.translate(ids[b:b + 1, :lens[b]], lens[b:b + 1], 5, 12, 0.0)
+        np.testing.assert_array_equal(one["hyps"][0], full["hyps"][b])
+        np.testing.assert_allclose(one["token_logp"][0], full["token_logp"][b], atol=2e-5)
+
+
+def test_translate_dev_matches_host(weight_cache):
+    import torch
+    gm, om, p = model_pair("c2", weight_cache)
+    ids, lens = synth.make_corpus("c2", 5)
+    host = gm.translate(ids, lens, 5, 10, 0.0)
+    dev = torch.device("cuda:0")
+    out = {"hyps": torch.zeros((5, 10), dtype=torch.int32, device=dev),
+           "lens": torch.zeros(5, dtype=torch.int32, device=dev),
+           "scores": torch.zeros(5, dtype=torch.float32, device=dev),
+           "raw": torch.zeros(5, dtype=torch.float32, device=dev),
+           "token_logp": torch.zeros((5, 10), dtype=torch.float32, device=dev)}
+    s = torch.cuda.current_stream()
+    gm.set_stream(s.cuda_stream)
+    gm.translate_dev(torch.from_numpy(ids).to(dev), torch.from_numpy(lens).to(dev), 5, 10, 0.0, out, lens)
+    torch.cuda.synchronize()
+    gm.set_stream(None)
+    for k in host:
+        np.testing.assert_array_equal(out[k].cpu().numpy(), host[k])
+
+
+def test_errors_and_edge_cases(weight_cache):
+    ob = _lib()
+    gm, om, p = model_pair("c1", weight_cache)
+    ids, lens = synth.make_corpus("c1")
+    empty = gm.translate(np.zeros((0, 1), np.int32), np.zeros(0, np.int32), 3, 10)
+    assert empty["hyps"].shape == (0, 10)
+    with pytest.raises(ob.OnmtError) as e:
+        gm.translate(ids, np.array([8, 0], np.int32), 3, 10)
+    assert e.value.name == "EMPTY_SOURCE"
+    bad = ids.copy(); bad[0, 0] = 100
+    with pytest.raises(ob.OnmtError) as e:
+        gm.translate(bad, lens, 3, 10)
+    assert e.value.name == "ID_RANGE"
+    bad[0, 0] = 5; bad[1, 6] = 100000          # padded position: ignored
+    gm.translate(bad, lens, 3, 10)
+    for kw, name in [(dict(beam=17), "UNSUPPORTED"), (dict(beam=0), "INVALID_ARG"),
+                     (dict(max_len=0), "INVALID_ARG"), (dict(length_penalty=-1.0), "INVALID_ARG")]:
+        args = dict(beam=3, max_len=10, length_penalty=0.0)
+        args.update(kw)
+        with pytest.raises(ob.OnmtError) as e:
+            gm.translate(ids, lens, **args)
+        assert e.value.name == name
+    with pytest.raises(ob.OnmtError) as e:
+        gm.translate(ids, np.array([9, 5], np.int32), 3, 10)   # len > S_max
+    assert e.value.name == "INVALID_ARG"
+    with pytest.raises(ob.OnmtError) as e:
+        ob.Model("/nonexistent.mnmt", 0, "fp32")
+    assert e.value.name == "IO"
+    # S_b = 1 and max_len = 1
+    one = gm.translate(np.array([[7]], np.int32), np.array([1], np.int32), 3, 1)
+    assert one["lens"][0] == 1
+    ref = beam_search(om, [7], 3, 1)
+    assert one["hyps"][0, 0] == ref["tokens"][0]
