@@ -1,0 +1,328 @@
+"""Benchmark: batched beam-5 translation (BASELINE.json metric) on synthetic c2 inputs.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path (encoder + every decode step + beam
+bookkeeping + finalize, DESIGN.md §2 A1-A11) over one batch of synthetic input, through
+the C-ABI (onmt_translate_dev: inputs already resident in HBM).  `e2e` re-measures the
+same metric through the host-buffer C-ABI call (onmt_translate), H2D/D2H copies inside
+the timed region.  Multi-GPU (torchrun, one process per GPU): every rank translates its
+own fixed-size batch from one seeded corpus (weak scaling), then hypotheses are
+all-gathered over NCCL (the only collective of the path); time is the max
+over ranks of the device-timed steps.  L2 is flushed (a 512 MB write) between timed
+steps.  `--impl reference` times the fp64 CPU oracle on a bounded sample instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASELINE["metric"]
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def peaks():
+    if os.path.exists(PEAKS_PATH):
+        p = json.load(open(PEAKS_PATH))
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"],
+                "bf16_tflops_sustained": p.get("bf16_tflops_sustained", p["bf16_tflops"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def gen_roofline_terms(w: synth.Workload, R: int):
+    """Algorithmic bytes / flops of ONE generator launch:
+    bytes = 2*H*V (bf16 W_gen) + 4*V (fp32 bias); flops = 2*R*H*V."""
+    H, V = w.model.hidden, w.model.v_tgt
+    return 2.0 * H * V + 4.0 * V, 2.0 * R * H * V
+
+
+# ---------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1805_11462_b200 as ob
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = synth.WORKLOADS[args.workload]
+    B, K, ML, alpha = w.data.batch, w.decode.beam, w.decode.max_len, w.decode.alpha
+    cache = os.environ.get("ONMT_WEIGHT_CACHE", os.path.join(tempfile.gettempdir(), "onmt_weights"))
+    if rank == 0 or ws == 1:
+        path = synth.weights_file(args.workload, cache)
+    if ws > 1:
+        dist.barrier()
+        path = synth.weights_file(args.workload, cache)
+    model = ob.Model(path, local, w.decode.precision)
+    # weak scaling: rank r translates sentences [r*B, (r+1)*B) of one seeded corpus
+    ids_all, lens_all = synth.make_corpus(args.workload, B * ws)
+    ids = np.ascontiguousarray(ids_all[rank * B:(rank + 1) * B])
+    lens = np.ascontiguousarray(lens_all[rank * B:(rank + 1) * B])
+    S = int(lens.max())
+    ids = np.ascontiguousarray(ids[:, :S])
+    stream = torch.cuda.Stream(device=dev)
+    model.set_stream(stream.cuda_stream)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    with torch.cuda.stream(stream):
+        ids_d = torch.from_numpy(ids).to(dev)
+        lens_d = torch.from_numpy(lens).to(dev)
+        out = {"hyps": torch.zeros((B, ML), dtype=torch.int32, device=dev),
+               "lens": torch.zeros(B, dtype=torch.int32, device=dev),
+               "scores": torch.zeros(B, dtype=torch.float32, device=dev),
+               "raw": torch.zeros(B, dtype=torch.float32, device=dev),
+               "token_logp": torch.zeros((B, ML), dtype=torch.float32, device=dev)}
+        gathered = torch.zeros((ws, B, ML), dtype=torch.int32, device=dev)
+        gathered_lens = torch.zeros((ws, B), dtype=torch.int32, device=dev)
+
+    def step():
+        model.translate_dev(ids_d, lens_d, K, ML, alpha, out, lens)
+        if ws > 1:
+            dist.all_gather_into_tensor(gathered, out["hyps"])
+            dist.all_gather_into_tensor(gathered_lens, out["lens"])
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        stream.synchronize()
+        model.launches(reset=True)
+        model.set_option("profile", 1)
+        model.kernel_time("gen", reset=True)
+        model.kernel_time("step", reset=True)
+        model.kernel_time("encode", reset=True)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        clk = ClockSampler(local)
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk.start()
+        tokens = 0
+        for i in range(args.steps):
+            flush.zero_()                                   # L2 flush between timed steps
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        clocks = clk.stop()
+        launches = model.launches(reset=True)
+        gen_ms, gen_n = model.kernel_time("gen", reset=True)
+        step_ms, step_n = model.kernel_time("step", reset=True)
+        enc_ms, enc_n = model.kernel_time("encode", reset=True)
+        model.set_option("profile", 0)
+    tokens = int(out["lens"].sum().item()) * args.steps
+    t_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if ws > 1:
+        tt = torch.tensor([t_ms, float(tokens)], dtype=torch.float64, device=dev)
+        tmax = tt.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+        t_ms, tokens = float(tmax[0].item()), int(tt[1].item())
+    value = tokens / (t_ms / 1e3)
+
+    # ---- e2e: host buffers through onmt_translate, H2D / D2H inside the timed region
+    model.set_stream(None)
+    e2e_ms = []
+    for i in range(max(1, args.steps)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = model.translate(ids, lens, K, ML, alpha)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_tokens = int(r["lens"].sum()) * len(e2e_ms)
+    e2e_t = sum(e2e_ms)
+    if ws > 1:
+        tt = torch.tensor([e2e_t, float(e2e_tokens)], dtype=torch.float64, device=dev)
+        tm = tt.clone()
+        dist.all_reduce(tm[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+        e2e_t, e2e_tokens = float(tm[0].item()), int(tt[1].item())
+    h2d = ids.nbytes + lens.nbytes
+    d2h = B * ML * 4 * 2 + B * 4 * 3
+
+    if rank == 0:
+        pk = peaks()
+        R = B * K
+        gbytes, gflops = gen_roofline_terms(w, R)
+        gen_avg_s = (gen_ms / gen_n) / 1e3 if gen_n else float("nan")
+        achieved = gbytes / gen_avg_s / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"gen_traffic_{args.workload}.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "target tok/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded U(-0.1,0.1) weights, Zipf(1.1) ids; DESIGN.md §3)",
+            "config": {"workload": args.workload, "model": "2x500 LSTM enc-dec, general attn, input feed, V=50k"
+                       if args.workload == "c2" else args.workload,
+                       "global_batch": B * ws, "batch_per_gpu": B, "beam": K, "max_len": ML,
+                       "length_penalty": alpha, "src_len": [w.data.len_lo, w.data.len_hi],
+                       "parallelism": f"dp{ws} (sentence-sharded, NCCL all-gather of hypotheses)",
+                       "l2": "flushed (512 MB write) between timed steps; weights stay L2-resident "
+                             "across the decode steps of one step"},
+            "e2e": {"value": round(e2e_tokens / (e2e_t / 1e3), 1), "unit": "target tok/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "roofline": {"kernel": "tc_gemm_kernel<MODE_GEN> (fused generator + log-softmax + top-k)",
+                         "bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
+                         "peak_src": pk["src"],
+                         "algorithmic_bytes_per_launch": gbytes, "flops_per_launch": gflops,
+                         "avg_launch_us": round(gen_avg_s * 1e6, 3), "launches": gen_n,
+                         "tensor_tflops_algorithmic": round(gflops / gen_avg_s / 1e12, 1),
+                         "gen_share_of_step": round(gen_ms / step_ms, 4) if step_ms else None},
+            "phases_ms_per_step": {"encode": round(enc_ms / max(enc_n, 1), 4),
+                                   "decode_step_avg_us": round(1e3 * step_ms / max(step_n, 1), 3)},
+            "clocks": clocks,
+            "tokens_per_step": tokens // args.steps,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.workload, path, args.cpu_sample_steps)
+        print(json.dumps(line), flush=True)
+    model.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------- oracle
+def oracle_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        th = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(max(th)) if th else 1
+    except Exception:
+        return 1
+
+
+def cpu_baseline(workload: str, path: str, sample_steps: int):
+    """The fp64 oracle (as it stands) on a bounded sample: the first sentence of the batch,
+    decoded for `sample_steps` steps (target tokens/s = steps / seconds)."""
+    from oracle import OracleModel, beam_search, load_model_tensors
+    w = synth.WORKLOADS[workload]
+    om = OracleModel(load_model_tensors(path, w.decode.precision))
+    ids, lens = synth.make_corpus(workload)
+    src = [int(v) for v in ids[0, :lens[0]]]
+    t0 = time.perf_counter()
+    r = beam_search(om, src, w.decode.beam, sample_steps, w.decode.alpha)
+    dt = time.perf_counter() - t0
+    n = len(r["tokens"])
+    return {"value": round(n / dt, 3), "unit": "target tok/s", "cores": oracle_cores(), "kind": "oracle",
+            "sample": f"1 sentence (len {lens[0]}) of the {workload} batch, beam {w.decode.beam}, "
+                      f"max_len {sample_steps} (encoder + {n} decode steps), fp64 numpy, {dt:.1f} s",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    w = synth.WORKLOADS[args.workload]
+    cache = os.environ.get("ONMT_WEIGHT_CACHE", os.path.join(tempfile.gettempdir(), "onmt_weights"))
+    path = synth.weights_file(args.workload, cache)
+    from oracle import OracleModel, beam_search, load_model_tensors
+    om = OracleModel(load_model_tensors(path, w.decode.precision))
+    ids, lens = synth.make_corpus(args.workload)
+    src = [int(v) for v in ids[0, :lens[0]]]
+    per = max(2, args.cpu_sample_steps // 4)
+    for _ in range(args.warmup):
+        beam_search(om, src, w.decode.beam, 2, w.decode.alpha)
+    t0 = time.perf_counter()
+    toks = 0
+    for i in range(args.steps):
+        r = beam_search(om, [int(v) for v in ids[i % len(lens), :lens[i % len(lens)]]], w.decode.beam, per,
+                        w.decode.alpha)
+        toks += len(r["tokens"])
+    dt = time.perf_counter() - t0
+    v = toks / dt
+    cores = oracle_cores()
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "target tok/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "beam": w.decode.beam, "max_len_sample": per},
+            "cpu_baseline": {"value": round(v, 3), "unit": "target tok/s", "cores": cores, "kind": "oracle",
+                             "sample": f"per step: 1 sentence of the {args.workload} batch, max_len {per}"},
+            "e2e": {"value": round(v, 3), "unit": "target tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=list(synth.WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -436,11 +436,13 @@ static void load_model(onmt_model* m, const char* path) {
       const auto& whh = get(t, p + "w_hh", {4 * Hd, Hd}, seen);
       const auto& bih = get(t, p + "b_ih", {4 * Hd}, seen);
       const auto& bhh = get(t, p + "b_hh", {4 * Hd}, seen);
-      int K;
+      int Ka, Kb;
+      auto ha = gate_interleave(wih, nullptr, (int)Hd, Ka);
+      auto hb = gate_interleave(whh, nullptr, (int)Hd, Kb);
       auto a = std::make_unique<Mat>();
-      a->upload(gate_interleave(wih, nullptr, (int)Hd, K), 4 * (int)Hd, K, bf);
+      a->upload(ha, 4 * (int)Hd, Ka, bf);
       auto b = std::make_unique<Mat>();
-      b->upload(gate_interleave(whh, nullptr, (int)Hd, K), 4 * (int)Hd, K, bf);
+      b->upload(hb, 4 * (int)Hd, Kb, bf);
       auto bb = std::make_unique<DevBuf>();
       upload_f32(*bb, gate_bias(bih, bhh, (int)Hd));
       m->enc_wih.push_back(std::move(a));
@@ -457,8 +459,9 @@ static void load_model(onmt_model* m, const char* path) {
     const auto& bih = get(t, p + "b_ih", {4 * H}, seen);
     const auto& bhh = get(t, p + "b_hh", {4 * H}, seen);
     int K;
+    auto hw = gate_interleave(wih, &whh, (int)H, K);
     auto w = std::make_unique<Mat>();
-    w->upload(gate_interleave(wih, &whh, (int)H, K), 4 * (int)H, K, bf);
+    w->upload(hw, 4 * (int)H, K, bf);
     auto bb = std::make_unique<DevBuf>();
     upload_f32(*bb, gate_bias(bih, bhh, (int)H));
     m->dec_w.push_back(std::move(w));

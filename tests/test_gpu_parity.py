@@ -30,10 +30,20 @@ def model_pair(workload, weight_cache, precision=None, overrides=None, tag=""):
     return _cache[key]
 
 
-def toy_pair(cfg, seed, scale, weight_cache, precision, overrides=None, name="toy"):
-    key = (name, seed, scale, precision, str(cfg))
+def toy_pair(cfg, seed, scale, weight_cache, precision, overrides=None, name="toy", peaky=False):
+    key = (name, seed, scale, precision, str(cfg), peaky)
     if key not in _cache:
         t = synth.random_model_tensors(cfg, seed, scale)
+        if peaky:
+            # near-unigram output layer with a strong token 7 and EOS just below it: EOS is
+            # selected (and banked) at ranks > 0 at every step, slots die, the final choice
+            # runs over many bank entries; the recurrence stays non-chaotic (scale 0.3)
+            b = np.random.default_rng(0).uniform(0, 2, cfg.v_tgt).astype(np.float32)
+            b[7] = 3.0
+            b[synth.EOS] = peaky
+            t["gen.b"] = b
+            t["attn.w_out"] = t["attn.w_out"] * 0.5
+            t["gen.w"] = t["gen.w"] * 3.0
         if overrides:
             t.update(overrides)
         path = os.path.join(weight_cache, f"{name}_{seed}_{abs(hash(str(cfg))) % 10**8}.mnmt")
@@ -111,10 +121,11 @@ TOY_BI = synth.ModelConfig(2, 16, 32, 60, 40, True, False)
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
 @pytest.mark.parametrize("cfg", [TOY, TOY_BI])
 @pytest.mark.parametrize("K,alpha", [(1, 0.0), (3, 0.6), (5, 0.0), (16, 1.0)])
-def test_toy_models_peaky(prec, cfg, K, alpha, weight_cache):
-    """Peaky toy models (U(-1.5, 1.5)) finish early on EOS: exercises banking, stop
-    rules, dead slots and the final choice against the oracle."""
-    gm, om, p = toy_pair(cfg, 11, 1.5, weight_cache, prec)
+@pytest.mark.parametrize("eos_bias", [2.4, 2.8])
+def test_toy_models_peaky(prec, cfg, K, alpha, eos_bias, weight_cache):
+    """Toy models whose EOS is nearly the best token: exercises EOS banking at every
+    rank, dead slots, the rank-0 EOS stop and the final choice against the oracle."""
+    gm, om, p = toy_pair(cfg, 11, 0.3, weight_cache, prec, peaky=eos_bias)
     rng = np.random.default_rng(K)
     lens = rng.integers(1, 12, 6).astype(np.int32)
     ids = np.zeros((6, 12), np.int32)
@@ -122,10 +133,12 @@ def test_toy_models_peaky(prec, cfg, K, alpha, weight_cache):
         ids[b, :lens[b]] = rng.integers(4, 60, lens[b])
     res, gpu = run_parity(gm, om, p, ids, lens, K, 15, alpha)
     assert res["match"] + res["excused"] == 6
+    if K > 1:
+        assert (gpu["sel_token"] == synth.EOS).any()     # the EOS banking path really ran
 
 
 def test_beam1_equals_oracle_greedy(weight_cache):
-    gm, om, p = toy_pair(TOY, 5, 1.2, weight_cache, "fp32")
+    gm, om, p = toy_pair(TOY, 5, 0.3, weight_cache, "fp32", peaky=2.8)
     rng = np.random.default_rng(0)
     lens = np.array([7, 3, 1], np.int32)
     ids = np.zeros((3, 7), np.int32)
@@ -179,15 +192,17 @@ def test_translate_dev_matches_host(weight_cache):
     ids, lens = synth.make_corpus("c2", 5)
     host = gm.translate(ids, lens, 5, 10, 0.0)
     dev = torch.device("cuda:0")
-    out = {"hyps": torch.zeros((5, 10), dtype=torch.int32, device=dev),
-           "lens": torch.zeros(5, dtype=torch.int32, device=dev),
-           "scores": torch.zeros(5, dtype=torch.float32, device=dev),
-           "raw": torch.zeros(5, dtype=torch.float32, device=dev),
-           "token_logp": torch.zeros((5, 10), dtype=torch.float32, device=dev)}
-    s = torch.cuda.current_stream()
-    gm.set_stream(s.cuda_stream)
-    gm.translate_dev(torch.from_numpy(ids).to(dev), torch.from_numpy(lens).to(dev), 5, 10, 0.0, out, lens)
-    torch.cuda.synchronize()
+    s = torch.cuda.Stream()            # a real stream: NULL means "the handle's own stream"
+    with torch.cuda.stream(s):
+        out = {"hyps": torch.zeros((5, 10), dtype=torch.int32, device=dev),
+               "lens": torch.zeros(5, dtype=torch.int32, device=dev),
+               "scores": torch.zeros(5, dtype=torch.float32, device=dev),
+               "raw": torch.zeros(5, dtype=torch.float32, device=dev),
+               "token_logp": torch.zeros((5, 10), dtype=torch.float32, device=dev)}
+        ids_d, lens_d = torch.from_numpy(ids).to(dev), torch.from_numpy(lens).to(dev)
+        gm.set_stream(s.cuda_stream)
+        gm.translate_dev(ids_d, lens_d, 5, 10, 0.0, out, lens)
+    s.synchronize()
     gm.set_stream(None)
     for k in host:
         np.testing.assert_array_equal(out[k].cpu().numpy(), host[k])
