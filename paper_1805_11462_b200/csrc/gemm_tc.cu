@@ -148,6 +148,377 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
 }
 
+// ------------------------------------------------------------------ persistent generator
+// One CTA per SM (grid = groups x C).  CTA (g, i) owns the hypothesis rows of N-group g
+// and the contiguous vocabulary tiles [i*n_vt/C, (i+1)*n_vt/C).  Warp roles:
+//   warp 0      TMA producer (A = 128 W_gen rows x 64 K, B = hi/lo activation planes)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; accumulators are
+//               double-buffered in TMEM (2 x 256 columns) so the epilogue of tile j
+//               overlaps the MMAs of tile j+1
+//   warps 2-9   epilogue: TMEM -> registers (+bias) -> transposed smem staging (two warps
+//               per TMEM lane quarter split the column chunks), then one thread per
+//               hypothesis row keeps a running (max, sum exp, top-k) over all of the
+//               CTA's vocabulary tiles; logits never reach HBM.
+// Output: one partial per (CTA, row) - C partials per row instead of V/128.
+struct GenPArgs {
+  int n_rows_pad, n_group, k_blocks, stages, n_vt, C;
+  int sc;         // staged columns per pass (n_group or half of it)
+  StepCtl ctl;
+  unsigned long long* dbg;   // optional timeline (%globaltimer) of CTA 0, debug builds only
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ---- epilogue building blocks (4 lanes per hypothesis row, 32 logits each per tile)
+constexpr int kColsPerPass = 64;   // 8 epilogue warps x 8 rows
+constexpr int kSLD = 132;          // staging row stride: (row*132 + lane part) hits distinct banks
+
+// branch-free sorted insertion of (x, xi) into a (z desc, id asc) list
+template <int KMAX>
+__device__ __forceinline__ void list_insert(float (&tz)[KMAX], int (&ti)[KMAX], float x, int xi) {
+  bool gt[KMAX];
+#pragma unroll
+  for (int q = 0; q < KMAX; ++q) gt[q] = better(x, xi, tz[q], ti[q]);
+#pragma unroll
+  for (int q = KMAX - 1; q >= 1; --q) {
+    const float nz = gt[q - 1] ? tz[q - 1] : x;
+    const int ni = gt[q - 1] ? ti[q - 1] : xi;
+    tz[q] = gt[q] ? nz : tz[q];
+    ti[q] = gt[q] ? ni : ti[q];
+  }
+  tz[0] = gt[0] ? x : tz[0];
+  ti[0] = gt[0] ? xi : ti[0];
+}
+
+template <int KMAX>
+__device__ __forceinline__ int list_count(const float (&tz)[KMAX]) {
+  int n = 0;
+#pragma unroll
+  for (int q = 0; q < KMAX; ++q) n += tz[q] != -INFINITY;
+  return n;
+}
+
+// One row's update with one tile: the 4 lanes of a group each scan 32 logits
+// (v = part + 4i, increasing ids), then combine (max, sum exp) and top-k by butterfly
+// shuffles.  The row's running state lives in shared memory (st: [m, s, z[KMAX], id[KMAX]])
+// so the pass loop stays rolled (instruction-cache footprint).  All shuffles are executed
+// by the whole warp (rows without work feed neutral values).
+template <int KMAX>
+__device__ __forceinline__ void list_shift_pop(float (&z)[KMAX], int (&id)[KMAX]) {
+#pragma unroll
+  for (int q = 0; q < KMAX - 1; ++q) { z[q] = z[q + 1]; id[q] = id[q + 1]; }
+  z[KMAX - 1] = -INFINITY;
+  id[KMAX - 1] = 0x7fffffff;
+}
+
+template <int KMAX>
+__device__ __noinline__ void group_update(const float* __restrict__ col, bool valid, int part, int vbase,
+                                          float* __restrict__ st, int kk, unsigned long long* dbg) {
+  constexpr float L2E = 1.4426950408889634f;
+  if (dbg) dbg[0] = gtimer();
+  float m = valid ? st[0] : -INFINITY;
+  float s = valid ? st[1] : 0.f;
+  float z[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) z[i] = valid ? col[part + 4 * i] : -INFINITY;
+  float own = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) own = fmaxf(own, z[i]);
+  float lm = fmaxf(own, __shfl_xor_sync(0xffffffffu, own, 1));
+  lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, 2));
+  const float mn = fmaxf(m, lm);
+  float ls = 0.f;
+  if (mn != -INFINITY) {
+    const float mo = mn * L2E;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      a0 += ex2(fmaf(z[i], L2E, -mo)); a1 += ex2(fmaf(z[i + 1], L2E, -mo));
+      a2 += ex2(fmaf(z[i + 2], L2E, -mo)); a3 += ex2(fmaf(z[i + 3], L2E, -mo));
+    }
+    ls = (a0 + a1) + (a2 + a3);
+  }
+  ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+  ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+  if (valid && part == 0 && mn != -INFINITY) {
+    st[0] = mn;
+    st[1] = (m == -INFINITY ? 0.f : s * ex2((m - mn) * L2E)) + ls;
+  }
+  if (dbg) dbg[1] = gtimer();
+  // top-k: rounds of group-wide argmax over the 4 x 32 register-resident logits; a
+  // round's winner enters the running list; stop when no group's winner can beat its
+  // running k-th best (warm lists usually stop after one round)
+  float rz[KMAX];
+  int ri[KMAX];
+#pragma unroll
+  for (int q = 0; q < KMAX; ++q) { rz[q] = valid ? st[2 + q] : INFINITY; ri[q] = valid ? __float_as_int(st[2 + KMAX + q]) : 0; }
+  bool dirty = false;
+  const int K = kk;
+#pragma unroll 1
+  for (int round = 0; round < K; ++round) {
+    // the K-th running entry (static-index select keeps the list in registers)
+    float tk = rz[0];
+    int tki = ri[0];
+#pragma unroll
+    for (int q = 1; q < KMAX; ++q) if (q == K - 1) { tk = rz[q]; tki = ri[q]; }
+    // lane argmax by a depth-5 tree over (value, index); left subtrees hold lower indices
+    float tv[16];
+    int tx[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const bool l = z[2 * i] >= z[2 * i + 1];
+      tv[i] = l ? z[2 * i] : z[2 * i + 1];
+      tx[i] = l ? 2 * i : 2 * i + 1;
+    }
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1) {
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const bool l = tv[2 * i] >= tv[2 * i + 1];
+        tv[i] = l ? tv[2 * i] : tv[2 * i + 1];
+        tx[i] = l ? tx[2 * i] : tx[2 * i + 1];
+      }
+    }
+    float bm = tv[0];
+    int bid = bm == -INFINITY ? 0x7fffffff : vbase + part + 4 * tx[0];
+    // group argmax (z desc, id asc) over the 4 lanes
+#pragma unroll
+    for (int lvl = 1; lvl <= 2; lvl <<= 1) {
+      const float oz = __shfl_xor_sync(0xffffffffu, bm, lvl);
+      const int oi = __shfl_xor_sync(0xffffffffu, bid, lvl);
+      if (better(oz, oi, bm, bid)) { bm = oz; bid = oi; }
+    }
+    const bool take = better(bm, bid, tk, tki);
+    if (!__any_sync(0xffffffffu, take)) break;
+    if (take) { list_insert<KMAX>(rz, ri, bm, bid); dirty = true; }
+    // the owner lane removes the winner from its registers
+    const bool own_it = bid != 0x7fffffff && ((bid - vbase) & 3) == part;
+    const int mine = own_it ? (bid - vbase - part) >> 2 : -1;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) z[i] = i == mine ? -INFINITY : z[i];
+  }
+  if (dbg) dbg[2] = gtimer();
+  if (dbg) dbg[3] = gtimer();
+  if (!valid || part != 0 || !dirty) { if (dbg) dbg[4] = gtimer(); return; }
+#pragma unroll
+  for (int q = 0; q < KMAX; ++q) { st[2 + q] = rz[q]; st[2 + KMAX + q] = __int_as_float(ri[q]); }
+  if (dbg) dbg[4] = gtimer();
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(320, 1)
+gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GenPArgs a,
+                      GenOut g) {
+  if (all_done(a.ctl)) return;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t a_bytes = kTileM * 128, b_bytes = a.n_group * 128;
+  const uint32_t stage_bytes = a_bytes + 2 * b_bytes;
+  float* stg = reinterpret_cast<float*>(smem + a.stages * stage_bytes);
+  float* rstate = stg + (size_t)kColsPerPass * kSLD;            // [n_group][2 + 2*KMAX]
+  constexpr int SW = 2 + 2 * KMAX;
+  uint64_t* full = reinterpret_cast<uint64_t*>(rstate + (size_t)a.n_group * SW);
+  uint64_t* empty = full + a.stages;
+  uint64_t* tfull = empty + a.stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = blockIdx.x / a.C, ci = blockIdx.x % a.C;
+  const int t0 = (int)((long long)ci * a.n_vt / a.C), t1 = (int)((long long)(ci + 1) * a.n_vt / a.C);
+  const int ntiles = t1 - t0;
+  const int n0 = grp * a.n_group;
+
+  if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) a.dbg[200] = gtimer();
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+    for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int j = 0; j < ntiles; ++j) {
+        const int m0 = (t0 + j) * kTileM;
+        for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
+          const int s = it % a.stages;
+          if (it >= a.stages) mbar_wait(&empty[s], ((it / a.stages) & 1) ^ 1);
+          if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it] = gtimer();
+          uint8_t* st = smem + s * stage_bytes;
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          tma_load_2d(st, &tmW, kb * kBK, m0, &full[s]);
+          tma_load_2d(st + a_bytes, &tmX, kb * kBK, n0, &full[s]);
+          tma_load_2d(st + a_bytes + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_group);
+      int it = 0;
+      for (int j = 0; j < ntiles; ++j) {
+        const int acc = j & 1;
+        if (j >= 2) mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * 256;
+        for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
+          const int s = it % a.stages;
+          mbar_wait(&full[s], (it / a.stages) & 1);
+          if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[64 + it] = gtimer();
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * stage_bytes);
+          const uint32_t sbh = sa + a_bytes, sbl = sa + a_bytes + b_bytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t da = umma_desc_sw128(sa + kk * 32);
+            tc_mma_bf16(d, da, umma_desc_sw128(sbh + kk * 32), idesc, (kb | kk) != 0);
+            tc_mma_bf16(d, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
+          }
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[acc]);
+        if (a.dbg && blockIdx.x == 0 && j < 8) a.dbg[128 + j] = gtimer();
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue warps 2..9
+    const int et = threadIdx.x - 64;                     // 0..255
+    const int q = warp & 3, par = (warp - 2) >> 2;       // TMEM quarter, column-chunk parity
+    const int vr = q * 32 + lane;                        // vocabulary row (TMEM lane) this thread drains
+    const int gcol = (et >> 5) * 8 + (lane >> 2);        // row (column) within a pass, 0..63
+    const int part = lane & 3;
+    const int npass = (a.n_group + kColsPerPass - 1) / kColsPerPass;
+    for (int i = et; i < a.n_group; i += 256) {
+      float* st = rstate + (size_t)i * SW;
+      st[0] = -INFINITY; st[1] = 0.f;
+      for (int qq = 0; qq < KMAX; ++qq) { st[2 + qq] = -INFINITY; st[2 + KMAX + qq] = __int_as_float(0x7fffffff); }
+    }
+    named_bar(1, 256);
+    for (int j = 0; j < ntiles; ++j) {
+      const int acc = j & 1;
+      const int vt = t0 + j;
+      mbar_wait(&tfull[acc], (j >> 1) & 1);
+      if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8) a.dbg[144 + j] = gtimer();
+      tc_fence_after();
+      const int vid = vt * kTileM + vr;
+      const float bias = vid < g.V ? g.bias[vid] : -INFINITY;
+      const uint32_t trow = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int h = 0; h < npass; ++h) {
+        const int cbeg = h * kColsPerPass;
+        const int cend = min(a.n_group, cbeg + kColsPerPass);
+        for (int c0 = cbeg + par * 16; c0 < cend; c0 += 32) {
+          float v[16];
+          tmem_ld16(trow + c0, v);
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) stg[(c0 - cbeg + jj) * kSLD + vr] = v[jj] + bias;
+        }
+        if (h == npass - 1) {                          // accumulator drained: hand it back
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        named_bar(1, 256);
+        if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[160 + 2 * j + h] = gtimer();
+        const int c = cbeg + gcol;
+        const bool valid = c < cend && n0 + c < g.rows_valid;
+        unsigned long long* gd = (a.dbg && blockIdx.x == 0 && et == 0 && j < 2 && h < 2) ? a.dbg + 210 + 8 * (2 * j + h) : nullptr;
+        group_update<KMAX>(stg + gcol * kSLD, valid, part, vt * kTileM, rstate + (size_t)min(c, a.n_group - 1) * SW, g.K, gd);
+        named_bar(1, 256);
+        if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[176 + 2 * j + h] = gtimer();
+      }
+    }
+    for (int c = et; c < a.n_group; c += 256) {
+      const int r = n0 + c;
+      if (r >= g.rows_valid) continue;
+      const float* st = rstate + (size_t)c * SW;
+      g.ms[(size_t)ci * g.rows_pad + r] = make_float2(st[0], st[1]);
+      const size_t base = ((size_t)ci * g.rows_pad + r) * g.K;
+      for (int qq = 0; qq < g.K; ++qq) { g.tz[base + qq] = st[2 + qq]; g.ti[base + qq] = __float_as_int(st[2 + KMAX + qq]); }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) { a.dbg[201] = gtimer(); a.dbg[202] = ntiles; a.dbg[203] = a.stages; }
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+static size_t genp_smem_bytes(int n_group, int stages, int kmax) {
+  return 1024 + (size_t)stages * (kTileM * 128 + 2 * (size_t)n_group * 128) + (size_t)kColsPerPass * kSLD * 4 +
+         (size_t)n_group * (2 + 2 * kmax) * 4 + (2 * stages + 4) * 8 + 16;
+}
+
+// number of partials per row the persistent generator writes (C)
+int gen_persistent_parts(int n_vt, int n_groups, int num_sms) {
+  int C = num_sms / n_groups;
+  if (C < 1) C = 1;
+  if (C > n_vt) C = n_vt;
+  return C;
+}
+
+template <int KMAX>
+static cudaError_t launch_genp(const CUtensorMap& tmW, const CUtensorMap& tmX, const GenPArgs& a, const GenOut& g,
+                               int grid, cudaStream_t st) {
+  size_t smem = genp_smem_bytes(a.n_group, a.stages, KMAX);
+  auto fn = gen_persistent_kernel<KMAX>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fn<<<grid, 320, smem, st>>>(tmW, tmX, a, g);
+  return cudaGetLastError();
+}
+
+unsigned long long* g_gen_dbg = nullptr;   // set by the runtime when ONMT_GEN_TRACE is on
+
+cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
+                              int k_blocks, int num_sms, const GenOut& g, StepCtl ctl, cudaStream_t st) {
+  GenPArgs a{};
+  a.dbg = g_gen_dbg;
+  a.n_rows_pad = n_rows_pad;
+  a.n_group = n_group;
+  a.k_blocks = k_blocks;
+  a.n_vt = n_vt;
+  const int groups = n_rows_pad / n_group;
+  a.C = gen_persistent_parts(n_vt, groups, num_sms);
+  a.ctl = ctl;
+  const size_t limit = 227 * 1024;
+  const int kmax = g.K <= 1 ? 1 : g.K <= 2 ? 2 : g.K <= 4 ? 4 : g.K <= 8 ? 8 : 16;
+  a.sc = n_group;
+  int stages = 8;
+  while (stages > 2 && genp_smem_bytes(n_group, stages, kmax) > limit) --stages;
+  if (stages > k_blocks * 2) stages = k_blocks * 2;
+  a.stages = stages;
+  if (genp_smem_bytes(n_group, stages, kmax) > limit) return cudaErrorInvalidConfiguration;
+  const int grid = a.C * groups;
+  if (g.K <= 1) return launch_genp<1>(tmW, tmX, a, g, grid, st);
+  if (g.K <= 2) return launch_genp<2>(tmW, tmX, a, g, grid, st);
+  if (g.K <= 4) return launch_genp<4>(tmW, tmX, a, g, grid, st);
+  if (g.K <= 8) return launch_genp<8>(tmW, tmX, a, g, grid, st);
+  return launch_genp<16>(tmW, tmX, a, g, grid, st);
+}
+
 // ------------------------------------------------------------------ host launchers
 static size_t tc_smem_bytes(int n_group, int stages, int mode) {
   size_t stage = kTileM * 128 + 2 * (size_t)n_group * 128;

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -32,6 +33,10 @@ cudaError_t tc_gemm_partial(const CUtensorMap& tmW, const CUtensorMap& tmX, int 
                             int n_valid, int k_blocks, int splits, float* out, StepCtl ctl, cudaStream_t st);
 cudaError_t tc_gemm_gen(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                         int k_blocks, const GenOut& g, StepCtl ctl, cudaStream_t st);
+cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
+                              int k_blocks, int num_sms, const GenOut& g, StepCtl ctl, cudaStream_t st);
+int gen_persistent_parts(int n_vt, int n_groups, int num_sms);
+extern unsigned long long* g_gen_dbg;
 cudaError_t simt_gemm_partial(const void* W, bool w_bf16, int m_pad, int k_pad, const float* X, int n_rows_pad,
                               int n_valid, int splits, float* out, StepCtl ctl, cudaStream_t st);
 int simt_effective_splits(int k_pad, int splits);
@@ -47,14 +52,17 @@ void launch_dec_cell(const float* P, int splits, int p_rows_pad, int p_ld, const
                      float* c_out, float* h_out, int H, int R, CellDst dst, StepCtl ctl, cudaStream_t st);
 cudaError_t launch_attention(const float* Pq, int splits, int p_rows_pad, int p_ld, const float* htop,
                              const float* mem, const int* lens, int B, int S_max, int H, int K, XOut xo,
-                             const int* done, StepCtl ctl, cudaStream_t st);
+                             const int* done, float* part_m, float* part_s, float* part_c, int* tickets, StepCtl ctl,
+                             cudaStream_t st);
+int attention_chunks(int S_max);
 void launch_attn_out(const float* P, int splits, int p_rows_pad, int p_ld, float* htilde, int H, int R, XOut xg,
                      StepCtl ctl, cudaStream_t st);
 void launch_init_decode(const BeamState& bs, int B, int K, const float* enc_h, const float* enc_c, int L, int H,
                         float* dec_h, float* dec_c, int dec_rows_pad, float* htilde, cudaStream_t st);
 void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepCtl ctl, cudaStream_t st);
 void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int B, int K, int t,
-                       int max_len, float alpha, const BeamState& bs, StepCtl ctl, cudaStream_t st);
+                       int max_len, float alpha, const BeamState& bs, const GatherArgs& ga, StepCtl ctl,
+                       cudaStream_t st);
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
                      float* tlogp, cudaStream_t st);
 void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int R, int K,
@@ -106,6 +114,8 @@ static CUtensorMap make_tmap(const void* base, int k_pad, int rows, int box_rows
 }
 
 // ------------------------------------------------------------------ device buffers
+static uint64_t g_alloc_gen = 0;   // bumped on every device (re)allocation: invalidates cached graphs
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -117,6 +127,7 @@ struct DevBuf {
     bytes = 0;
     ONMT_CUDA(cudaMalloc(&p, n));
     bytes = n;
+    ++g_alloc_gen;
   }
   template <typename T> T* as() const { return static_cast<T*>(p); }
 };
@@ -191,32 +202,56 @@ struct Act {
   }
 };
 
+struct EvPair {
+  cudaEvent_t a, b;
+};
+// CUDA-event pairs around a kernel family.  Pairs recorded by direct launches return to the
+// free list after drain(); pairs baked into a cached graph stay owned by the graph and are
+// re-queued after every replay.
 struct EventPairs {
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
-  size_t used = 0;
+  std::vector<EvPair> all, free_;
+  std::vector<std::pair<EvPair, bool>> pending;
   double acc_ms = 0;
   int64_t count = 0;
   ~EventPairs() {
-    for (auto& p : pool) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    for (auto& p : all) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   }
-  std::pair<cudaEvent_t, cudaEvent_t> next() {
-    if (used == pool.size()) {
-      cudaEvent_t a, b;
-      ONMT_CUDA(cudaEventCreate(&a));
-      ONMT_CUDA(cudaEventCreate(&b));
-      pool.push_back({a, b});
+  EvPair acquire() {
+    if (free_.empty()) {
+      EvPair p;
+      ONMT_CUDA(cudaEventCreate(&p.a));
+      ONMT_CUDA(cudaEventCreate(&p.b));
+      all.push_back(p);
+      free_.push_back(p);
     }
-    return pool[used++];
+    EvPair p = free_.back();
+    free_.pop_back();
+    return p;
   }
+  void release(const std::vector<EvPair>& v) { free_.insert(free_.end(), v.begin(), v.end()); }
   void drain() {
-    for (size_t i = 0; i < used; ++i) {
+    for (auto& pp : pending) {
       float ms = 0;
-      ONMT_CUDA(cudaEventElapsedTime(&ms, pool[i].first, pool[i].second));
+      ONMT_CUDA(cudaEventElapsedTime(&ms, pp.first.a, pp.first.b));
       acc_ms += ms;
       ++count;
+      if (pp.second) free_.push_back(pp.first);
     }
-    used = 0;
+    pending.clear();
   }
+};
+
+// Event record usable both on a plain stream and inside stream capture (external node).
+static void ev_record(cudaEvent_t e, cudaStream_t s, bool capturing) {
+  if (capturing) ONMT_CUDA(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+  else ONMT_CUDA(cudaEventRecord(e, s));
+}
+
+struct GraphCache {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<int64_t> key;
+  int64_t kernels = 0;
+  std::vector<EvPair> gen_ev, step_ev;
 };
 
 }  // namespace onmt
@@ -230,7 +265,7 @@ struct onmt_model {
   bool bidir = false, general = false;
   bool use_tc = false;       // tcgen05 GEMM backend (bf16 models)
   bool profile = false;
-  bool use_graph = false;
+  bool use_graph = true;
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
   int64_t launches = 0;
@@ -253,13 +288,17 @@ struct onmt_model {
   Act xq, xo, xg;
   DevBuf dec_p, st_h, st_c, st_cg, htilde, logits;
   DevBuf g_ms, g_tz, g_ti;
+  DevBuf a_pm, a_ps, a_pc, a_tick;
   DevBuf b_cum, b_live, b_y, b_prow, b_done, b_ndone, b_bt, b_br, b_braw, b_bnorm;
   DevBuf h_par, h_tok, h_lp, s_score, s_par;
   DevBuf o_hyps, o_lens, o_scores, o_raw, o_tlogp;
 
   EventPairs ev_gen, ev_step, ev_enc;
+  bool capturing = false;
+  GraphCache graph;
 
   ~onmt_model() {
+    if (graph.exec) cudaGraphExecDestroy(graph.exec);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
@@ -294,12 +333,18 @@ static int gemm(onmt_model* m, const Mat& W, const Act& X, int n_valid, int spli
   return eff;
 }
 
+// partials per row written by the generator for operand X
+static int gen_parts(onmt_model* m, const Act& X) {
+  const int n_vt = (m->Vt + kVTile - 1) / kVTile;
+  return m->use_tc ? gen_persistent_parts(n_vt, X.rows_pad / X.n_group, m->num_sms) : n_vt;
+}
+
 static void gen(onmt_model* m, const Act& X, const GenOut& g, StepCtl ctl) {
-  std::pair<cudaEvent_t, cudaEvent_t> ev{};
-  if (m->profile) { ev = m->ev_gen.next(); ONMT_CUDA(cudaEventRecord(ev.first, m->stream)); }
+  EvPair ev{};
+  if (m->profile) { ev = m->ev_gen.acquire(); ev_record(ev.a, m->stream, m->capturing); }
   if (m->use_tc) {
-    ONMT_CUDA(tc_gemm_gen(m->gen_w.tmap, X.tmap, m->gen_w.m_pad, X.rows_pad, X.n_group, m->gen_w.k_pad / kBK, g, ctl,
-                          m->stream));
+    ONMT_CUDA(tc_gen_persistent(m->gen_w.tmap, X.tmap, m->gen_w.m_pad / kTileM, X.rows_pad, X.n_group,
+                                m->gen_w.k_pad / kBK, m->num_sms, g, ctl, m->stream));
     count(m);
   } else {
     m->logits.ensure((size_t)X.rows_pad * m->gen_w.m_pad * 4);
@@ -308,7 +353,11 @@ static void gen(onmt_model* m, const Act& X, const GenOut& g, StepCtl ctl) {
     ONMT_CUDA(simt_gen_partials(m->logits.as<float>(), m->gen_w.m_pad, g, ctl, m->stream));
     count(m, 2);
   }
-  if (m->profile) ONMT_CUDA(cudaEventRecord(ev.second, m->stream));
+  if (m->profile) {
+    ev_record(ev.b, m->stream, m->capturing);
+    if (m->capturing) m->graph.gen_ev.push_back(ev);
+    else m->ev_gen.pending.push_back({ev, true});
+  }
 }
 
 // ------------------------------------------------------------------ loader
@@ -574,10 +623,20 @@ static void run_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int 
   m->st_c.ensure((size_t)L * rp * H * 4);
   m->st_cg.ensure((size_t)L * rp * H * 4);
   m->htilde.ensure((size_t)rp * H * 4);
-  const int n_vt = (m->Vt + kVTile - 1) / kVTile;
+  const int n_vt = gen_parts(m, m->xg);
   m->g_ms.ensure((size_t)n_vt * rp * 8);
   m->g_tz.ensure((size_t)n_vt * rp * K * 4);
   m->g_ti.ensure((size_t)n_vt * rp * K * 4);
+  {
+    const size_t nch = attention_chunks(S_max);
+    m->a_pm.ensure(B * nch * K * 4);
+    m->a_ps.ensure(B * nch * K * 4);
+    m->a_pc.ensure(B * nch * K * (size_t)H * 4);
+    if (m->a_tick.bytes < (size_t)B * 4) {
+      m->a_tick.ensure((size_t)B * 4);
+      ONMT_CUDA(cudaMemset(m->a_tick.p, 0, m->a_tick.bytes));
+    }
+  }
   m->b_cum.ensure((size_t)R * 8);
   m->b_live.ensure((size_t)R * 4);
   m->b_y.ensure((size_t)R * 4);
@@ -626,9 +685,11 @@ static void run_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int 
   g.rows_valid = R;
   g.rows_pad = rp;
   float* P = m->dec_p.as<float>();
+  if (!m->use_tc) m->logits.ensure((size_t)m->xg.rows_pad * m->gen_w.m_pad * 4);   // before any capture
+  auto enqueue_steps = [&]() {
   for (int t = 1; t <= max_len; ++t) {
-    std::pair<cudaEvent_t, cudaEvent_t> ev{};
-    if (m->profile) { ev = m->ev_step.next(); ONMT_CUDA(cudaEventRecord(ev.first, m->stream)); }
+    EvPair ev{};
+    if (m->profile) { ev = m->ev_step.acquire(); ev_record(ev.a, m->stream, m->capturing); }
     for (int l = 0; l < L; ++l) {
       const Mat& W = *m->dec_w[l];
       int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
@@ -647,10 +708,12 @@ static void run_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int 
     if (m->general) {
       int s = gemm(m, m->attn_win, m->xq, R, 0, P, ctl);
       ONMT_CUDA(launch_attention(P, s, m->xq.rows_pad, m->attn_win.m_pad, nullptr, m->mem.as<float>(), d_lens, B,
-                                 S_max, H, K, m->xo.xo(bf), bs.done, ctl, m->stream));
+                                 S_max, H, K, m->xo.xo(bf), bs.done, m->a_pm.as<float>(), m->a_ps.as<float>(),
+                                 m->a_pc.as<float>(), m->a_tick.as<int>(), ctl, m->stream));
     } else {
       ONMT_CUDA(launch_attention(nullptr, 0, 0, 0, htop, m->mem.as<float>(), d_lens, B, S_max, H, K, m->xo.xo(bf),
-                                 bs.done, ctl, m->stream));
+                                 bs.done, m->a_pm.as<float>(), m->a_ps.as<float>(), m->a_pc.as<float>(),
+                                 m->a_tick.as<int>(), ctl, m->stream));
     }
     count(m);
     {
@@ -660,10 +723,57 @@ static void run_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int 
       count(m);
     }
     gen(m, m->xg, g, ctl);
-    launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, B, K, t, max_len, alpha, bs, ctl, m->stream);
+    launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, B, K, t, max_len, alpha, bs, ga, ctl, m->stream);
     count(m);
-    if (t < max_len) { launch_gather(bs, ga, R, K, ctl, m->stream); count(m); }
-    if (m->profile) ONMT_CUDA(cudaEventRecord(ev.second, m->stream));
+    if (m->profile) {
+      ev_record(ev.b, m->stream, m->capturing);
+      if (m->capturing) m->graph.step_ev.push_back(ev);
+      else m->ev_step.pending.push_back({ev, true});
+    }
+  }
+  };
+  if (!m->use_graph) {
+    enqueue_steps();
+  } else {
+    // the whole max_len-step loop as one CUDA graph, cached per shape / buffer set
+    std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc,
+                                (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
+    GraphCache& gc = m->graph;
+    if (!gc.exec || gc.key != key) {
+      if (gc.exec) {
+        ONMT_CUDA(cudaStreamSynchronize(m->stream));
+        ONMT_CUDA(cudaGraphExecDestroy(gc.exec));
+        gc.exec = nullptr;
+        m->ev_gen.release(gc.gen_ev);
+        m->ev_step.release(gc.step_ev);
+        gc.gen_ev.clear();
+        gc.step_ev.clear();
+      }
+      cudaGraph_t graph;
+      const int64_t before = m->launches;
+      ONMT_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+      m->capturing = true;
+      try {
+        enqueue_steps();
+      } catch (...) {
+        m->capturing = false;
+        cudaGraph_t junk;
+        cudaStreamEndCapture(m->stream, &junk);
+        if (junk) cudaGraphDestroy(junk);
+        throw;
+      }
+      m->capturing = false;
+      ONMT_CUDA(cudaStreamEndCapture(m->stream, &graph));
+      ONMT_CUDA(cudaGraphInstantiate(&gc.exec, graph, 0));
+      ONMT_CUDA(cudaGraphDestroy(graph));
+      gc.kernels = m->launches - before;
+      m->launches = before;
+      gc.key = key;
+    }
+    ONMT_CUDA(cudaGraphLaunch(gc.exec, m->stream));
+    m->launches += gc.kernels;
+    for (auto& p : gc.gen_ev) m->ev_gen.pending.push_back({p, false});
+    for (auto& p : gc.step_ev) m->ev_step.pending.push_back({p, false});
   }
   launch_finalize(bs, B, K, max_len, out.hyps, out.lens, out.scores, out.raw, out.tlogp, m->stream);
   count(m);
@@ -716,6 +826,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   m->prec = prec;
   m->use_tc = prec == ONMT_PREC_BF16;
   m->num_sms = prop.multiProcessorCount;
+  if (const char* ev = std::getenv("ONMT_USE_GRAPH")) m->use_graph = std::atoi(ev) != 0;   // ncu runs use 0
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
   load_model(m.get(), path);
@@ -759,6 +870,7 @@ static onmt_status validate(onmt_model* m, const int32_t* ids, const int32_t* le
   if (B < 0) return fail(ONMT_E_INVALID_ARG, "B < 0");
   if (B == 0) return ONMT_OK;
   if (S_max < 1) return fail(ONMT_E_INVALID_ARG, "S_max < 1");
+  if (S_max > 2048) return fail(ONMT_E_UNSUPPORTED, "S_max > 2048");
   if (!lens || (check_ids && !ids)) return fail(ONMT_E_INVALID_ARG, "null source pointer");
   for (int b = 0; b < B; ++b) {
     if (lens[b] < 1) return fail(ONMT_E_EMPTY_SOURCE, "empty source sentence " + std::to_string(b));
@@ -828,10 +940,10 @@ static onmt_status translate_impl(onmt_model* m, const int32_t* ids, const int32
   m->o_scores.ensure((size_t)B * 4);
   m->o_raw.ensure((size_t)B * 4);
   m->o_tlogp.ensure((size_t)B * max_len * 4);
-  std::pair<cudaEvent_t, cudaEvent_t> ev{};
-  if (m->profile) { ev = m->ev_enc.next(); ONMT_CUDA(cudaEventRecord(ev.first, m->stream)); }
+  EvPair ev{};
+  if (m->profile) { ev = m->ev_enc.acquire(); ONMT_CUDA(cudaEventRecord(ev.a, m->stream)); }
   run_encoder(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max);
-  if (m->profile) ONMT_CUDA(cudaEventRecord(ev.second, m->stream));
+  if (m->profile) { ONMT_CUDA(cudaEventRecord(ev.b, m->stream)); m->ev_enc.pending.push_back({ev, true}); }
   DecodeOut o{m->o_hyps.as<int>(), m->o_lens.as<int>(), m->o_scores.as<float>(), m->o_raw.as<float>(),
               m->o_tlogp.as<float>()};
   run_decoder(m, m->d_lens.as<int>(), B, S_max, beam, max_len, alpha, trace, o);
@@ -874,6 +986,7 @@ onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_ids, const int32_
   if (s != ONMT_OK) return s;
   if (B == 0) return ONMT_OK;
   if (S_max < 1) return fail(ONMT_E_INVALID_ARG, "S_max < 1");
+  if (S_max > 2048) return fail(ONMT_E_UNSUPPORTED, "S_max > 2048");
   if (lens_host) {
     s = validate(m, nullptr, lens_host, B, S_max, false);
     if (s != ONMT_OK) return s;
@@ -881,10 +994,10 @@ onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_ids, const int32_
   if (!d_ids || !d_lens || !d_hyps || !d_olens || !d_scores) return fail(ONMT_E_INVALID_ARG, "null device pointer");
   ONMT_API_BEGIN
   ONMT_CUDA(cudaSetDevice(m->device));
-  std::pair<cudaEvent_t, cudaEvent_t> ev{};
-  if (m->profile) { ev = m->ev_enc.next(); ONMT_CUDA(cudaEventRecord(ev.first, m->stream)); }
+  EvPair ev{};
+  if (m->profile) { ev = m->ev_enc.acquire(); ONMT_CUDA(cudaEventRecord(ev.a, m->stream)); }
   run_encoder(m, d_ids, d_lens, B, S_max);
-  if (m->profile) ONMT_CUDA(cudaEventRecord(ev.second, m->stream));
+  if (m->profile) { ONMT_CUDA(cudaEventRecord(ev.b, m->stream)); m->ev_enc.pending.push_back({ev, true}); }
   m->o_raw.ensure((size_t)B * 4);
   m->o_tlogp.ensure((size_t)B * max_len * 4);
   DecodeOut o{d_hyps, d_olens, d_scores, d_raw ? d_raw : m->o_raw.as<float>(),
@@ -991,7 +1104,8 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
     }
     ONMT_CUDA(cudaMemcpy(x.hl.p, hl.data(), hl.size() * 2, cudaMemcpyHostToDevice));
   }
-  const int n_vt = (m->Vt + kVTile - 1) / kVTile;
+  const int n_vt = std::max(gen_parts(m, x), (m->Vt + kVTile - 1) / kVTile);
+  const int n_parts = gen_parts(m, x);
   DevBuf ms, tz, ti, dl, dz, di;
   ms.ensure((size_t)n_vt * x.rows_pad * 8);
   tz.ensure((size_t)n_vt * x.rows_pad * k * 4);
@@ -1000,8 +1114,32 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
   dz.ensure((size_t)R * k * 4);
   di.ensure((size_t)R * k * 4);
   GenOut g{ms.as<float2>(), tz.as<float>(), ti.as<int>(), m->gen_b.as<float>(), m->Vt, k, R, x.rows_pad};
+  DevBuf dbg;
+  const bool trace_gen = std::getenv("ONMT_GEN_TRACE") != nullptr;
+  if (trace_gen) {
+    dbg.ensure(256 * 8);
+    ONMT_CUDA(cudaMemset(dbg.p, 0, 256 * 8));
+    g_gen_dbg = dbg.as<unsigned long long>();
+  }
   gen(m, x, g, StepCtl{nullptr, 0});
-  launch_row_reduce(g.ms, g.tz, g.ti, n_vt, x.rows_pad, R, k, dl.as<float>(), dz.as<float>(), di.as<int>(), m->stream);
+  g_gen_dbg = nullptr;
+  if (trace_gen) {
+    std::vector<unsigned long long> h(256);
+    ONMT_CUDA(cudaStreamSynchronize(m->stream));
+    ONMT_CUDA(cudaMemcpy(h.data(), dbg.p, 256 * 8, cudaMemcpyDeviceToHost));
+    const unsigned long long t0 = h[200];
+    auto rel = [&](unsigned long long v) { return v ? (long long)(v - t0) : -1LL; };
+    std::fprintf(stderr, "gen trace CTA0: tiles=%llu stages=%llu total=%lld ns\n", h[202], h[203], rel(h[201]));
+    for (int i = 0; i < 32; ++i) std::fprintf(stderr, "  kb%02d tma_issue=%lld mma_start=%lld\n", i, rel(h[i]), rel(h[64 + i]));
+    for (int p = 0; p < 4; ++p)
+      std::fprintf(stderr, "  gu%d: start=%lld sum=%lld cand=%lld merge=%lld end=%lld\n", p, rel(h[210 + 8 * p]),
+                   rel(h[211 + 8 * p]), rel(h[212 + 8 * p]), rel(h[213 + 8 * p]), rel(h[214 + 8 * p]));
+    for (int j = 0; j < 4; ++j)
+      std::fprintf(stderr, "  tile%d mma_done=%lld epi_start=%lld scan0=%lld end0=%lld scan1=%lld end1=%lld\n", j,
+                   rel(h[128 + j]), rel(h[144 + j]), rel(h[160 + 2 * j]), rel(h[176 + 2 * j]), rel(h[161 + 2 * j]),
+                   rel(h[177 + 2 * j]));
+  }
+  launch_row_reduce(g.ms, g.tz, g.ti, n_parts, x.rows_pad, R, k, dl.as<float>(), dz.as<float>(), di.as<int>(), m->stream);
   ONMT_CUDA(cudaGetLastError());
   ONMT_CUDA(cudaMemcpyAsync(lse, dl.p, (size_t)R * 4, cudaMemcpyDeviceToHost, m->stream));
   ONMT_CUDA(cudaMemcpyAsync(top_z, dz.p, (size_t)R * k * 4, cudaMemcpyDeviceToHost, m->stream));
