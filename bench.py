@@ -79,6 +79,9 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+FAMILIES = ["gen", "step", "encode", "gemm", "cell", "attention", "attn_out", "merge"]
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -148,9 +151,8 @@ def run_ours(args):
         step()                                  # (re)capture the profiled decode graph outside timing
         stream.synchronize()
         model.launches(reset=True)
-        model.kernel_time("gen", reset=True)
-        model.kernel_time("step", reset=True)
-        model.kernel_time("encode", reset=True)
+        for fam in FAMILIES:
+            model.kernel_time(fam, reset=True)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         clk = ClockSampler(local)
         if ws > 1:
@@ -168,9 +170,10 @@ def run_ours(args):
             dist.barrier()
         clocks = clk.stop()
         launches = model.launches(reset=True)
-        gen_ms, gen_n = model.kernel_time("gen", reset=True)
-        step_ms, step_n = model.kernel_time("step", reset=True)
-        enc_ms, enc_n = model.kernel_time("encode", reset=True)
+        fam_t = {fam: model.kernel_time(fam, reset=True) for fam in FAMILIES}
+        gen_ms, gen_n = fam_t["gen"]
+        step_ms, step_n = fam_t["step"]
+        enc_ms, enc_n = fam_t["encode"]
         model.set_option("profile", 0)
     tokens = int(out["lens"].sum().item()) * args.steps
     t_ms = sum(a.elapsed_time(b) for a, b in evs)
@@ -237,6 +240,8 @@ def run_ours(args):
                          "gen_share_of_step": round(gen_ms / step_ms, 4) if step_ms else None},
             "phases_ms_per_step": {"encode": round(enc_ms / max(enc_n, 1), 4),
                                    "decode_step_avg_us": round(1e3 * step_ms / max(step_n, 1), 3)},
+            "decode_step_breakdown_us": {fam: round(1e3 * fam_t[fam][0] / max(step_n, 1), 3)
+                                         for fam in FAMILIES if fam not in ("step", "encode")},
             "clocks": clocks,
             "tokens_per_step": tokens // args.steps,
         }

@@ -5,7 +5,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace onmt {
+
+// Programmatic dependent launch (PDL): every decode-step kernel lets its successor launch
+// early and waits for its predecessor's memory before touching any input.  Every CTA calls
+// pdl_wait() before exiting (even on early-exit paths) so completion stays transitive.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 constexpr int kKMax = 16;     // ONMT_K_MAX
 constexpr int kBK = 64;       // K block (64 bf16 = 128 B = one swizzle row)
@@ -118,11 +126,11 @@ struct CellDst {
 
 // Device beam state (DESIGN.md §5 layout); histories are [max_len][B*K].
 struct BeamState {
-  double* cum;        // [B*K] cumulative raw log-prob of live slots
-  int* live;          // [B*K]
+  double* cum;        // [2][B*K] cumulative raw log-prob of live slots (step t uses buffer t & 1)
+  int* live;          // [2][B*K]
   int* y;             // [B*K] token fed at the next step
   int* prow;          // [B*K] row (b*K + parent slot) whose state slot r continues
-  int* done;          // [B]
+  int* done;          // [B] 0 = running, else the step after which the sentence stopped
   int* n_done;        // [1]
   int* best_t;        // [B] banked best entry: step (1-based), 0 = none
   int* best_r;        // [B]
@@ -146,5 +154,24 @@ struct GatherArgs {
   int rows_pad;
   XOut x[8];           // x[0] = layer-0 operand; x[l] = layer-l operand
 };
+
+
+// launch with the programmatic-stream-serialization attribute (captured as a programmatic
+// edge inside CUDA graphs)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 }  // namespace onmt

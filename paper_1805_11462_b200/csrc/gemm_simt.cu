@@ -17,6 +17,8 @@ template <typename TW>
 __global__ void __launch_bounds__(256) simt_gemm_kernel(const TW* __restrict__ W, int m_pad, int k_pad,
                                                         const float* __restrict__ X, int n_rows_pad, int n_valid,
                                                         int k_per_split, float* __restrict__ out, StepCtl ctl) {
+  pdl_trigger();
+  pdl_wait();
   if (all_done(ctl)) return;
   __shared__ float Ws[16][64 + 4];
   __shared__ float Xs[16][64 + 4];
@@ -62,6 +64,8 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const TW* __restrict__ W
 
 template <int KMAX>
 __global__ void gen_from_logits_kernel(const float* __restrict__ logits, int v_pad, GenOut g, StepCtl ctl) {
+  pdl_trigger();
+  pdl_wait();
   if (all_done(ctl)) return;
   const int vt = blockIdx.x;
   for (int r = threadIdx.x; r < g.rows_valid; r += blockDim.x) {

@@ -40,7 +40,7 @@ template <int MODE, int KMAX>
 __global__ void __launch_bounds__(128, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, TcGemmArgs a,
                GenOut g) {
-  if (all_done(a.ctl)) return;
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_bytes = kTileM * 128;
@@ -67,9 +67,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
   }
   if (warp == 0) tmem_alloc_dyn(tslot, a.tmem_cols);
   tc_fence_before();
+  pdl_wait();                                   // predecessor's outputs (X, flags) now visible
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (all_done(a.ctl)) {                        // uniform: every thread read the same flag
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
+    return;
+  }
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
@@ -322,7 +328,7 @@ template <int KMAX>
 __global__ void __launch_bounds__(320, 1)
 gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GenPArgs a,
                       GenOut g) {
-  if (all_done(a.ctl)) return;
+  pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t a_bytes = kTileM * 128, b_bytes = a.n_group * 128;
@@ -352,9 +358,15 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
   }
   if (warp == 1) tmem_alloc<512>(tslot);
   tc_fence_before();
+  pdl_wait();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (all_done(a.ctl)) {
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+    return;
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -486,7 +498,7 @@ static cudaError_t launch_genp(const CUtensorMap& tmW, const CUtensorMap& tmX, c
   auto fn = gen_persistent_kernel<KMAX>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, 320, smem, st>>>(tmW, tmX, a, g);
+  return launch_pdl(fn, dim3(grid), dim3(320), smem, st, tmW, tmX, a, g);
   return cudaGetLastError();
 }
 
@@ -543,7 +555,7 @@ static cudaError_t launch_tc(const CUtensorMap& tmW, const CUtensorMap& tmX, con
   auto fn = tc_gemm_kernel<MODE, KMAX>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, 128, smem, st>>>(tmW, tmX, a, g);
+  return launch_pdl(fn, grid, dim3(128), smem, st, tmW, tmX, a, g);
   return cudaGetLastError();
 }
 

@@ -37,6 +37,7 @@ cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, in
                               int k_blocks, int num_sms, const GenOut& g, StepCtl ctl, cudaStream_t st);
 int gen_persistent_parts(int n_vt, int n_groups, int num_sms);
 extern unsigned long long* g_gen_dbg;
+
 cudaError_t simt_gemm_partial(const void* W, bool w_bf16, int m_pad, int k_pad, const float* X, int n_rows_pad,
                               int n_valid, int splits, float* out, StepCtl ctl, cudaStream_t st);
 int simt_effective_splits(int k_pad, int splits);
@@ -50,19 +51,18 @@ void launch_enc_cell(const float* Z, int z_ld, const float* P, int splits, int p
                      int mem_col, cudaStream_t st);
 void launch_dec_cell(const float* P, int splits, int p_rows_pad, int p_ld, const float* bias, const float* cg,
                      float* c_out, float* h_out, int H, int R, CellDst dst, StepCtl ctl, cudaStream_t st);
-cudaError_t launch_attention(const float* Pq, int splits, int p_rows_pad, int p_ld, const float* htop,
-                             const float* mem, const int* lens, int B, int S_max, int H, int K, XOut xo,
-                             const int* done, float* part_m, float* part_s, float* part_c, int* tickets, StepCtl ctl,
-                             cudaStream_t st);
+cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, const float* mem, const int* lens,
+                             int B, int S_max, int H, int K, XOut xo, const int* done, float* part_m, float* part_s,
+                             float* part_c, int* tickets, StepCtl ctl, cudaStream_t st);
 int attention_chunks(int S_max);
 void launch_attn_out(const float* P, int splits, int p_rows_pad, int p_ld, float* htilde, int H, int R, XOut xg,
                      StepCtl ctl, cudaStream_t st);
 void launch_init_decode(const BeamState& bs, int B, int K, const float* enc_h, const float* enc_c, int L, int H,
                         float* dec_h, float* dec_c, int dec_rows_pad, float* htilde, cudaStream_t st);
 void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepCtl ctl, cudaStream_t st);
-void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int B, int K, int t,
-                       int max_len, float alpha, const BeamState& bs, const GatherArgs& ga, StepCtl ctl,
-                       cudaStream_t st);
+void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_parts, int rows_pad, int B, int K,
+                       int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga, float* row_lse,
+                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st);
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
                      float* tlogp, cudaStream_t st);
 void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int R, int K,
@@ -251,7 +251,7 @@ struct GraphCache {
   cudaGraphExec_t exec = nullptr;
   std::vector<int64_t> key;
   int64_t kernels = 0;
-  std::vector<EvPair> gen_ev, step_ev;
+  std::vector<std::pair<std::string, EvPair>> ev_nodes;   // profiling events baked into the graph
 };
 
 }  // namespace onmt
@@ -276,24 +276,26 @@ struct onmt_model {
   std::vector<std::unique_ptr<DevBuf>> enc_bias;
   std::vector<std::unique_ptr<Mat>> dec_w;
   std::vector<std::unique_ptr<DevBuf>> dec_bias;
-  Mat attn_win, attn_wout, gen_w;
+  Mat attn_win, attn_win_t, attn_wout, gen_w;
   DevBuf gen_b;
 
   // encoder workspace
   DevBuf d_ids, d_lens;
   Act enc_in0, enc_mid[2], enc_rec[2];
-  DevBuf enc_z[2], enc_p, mem, enc_h, enc_c;
+  DevBuf enc_z[2], enc_p, mem, enc_h, enc_c, keys;
+  Act mem_x;                                 // memory bank as a GEMM operand ('general' keys)
   // decoder workspace
   std::vector<std::unique_ptr<Act>> xdec;    // [L]
-  Act xq, xo, xg;
+  Act xo, xg;
   DevBuf dec_p, st_h, st_c, st_cg, htilde, logits;
   DevBuf g_ms, g_tz, g_ti;
   DevBuf a_pm, a_ps, a_pc, a_tick;
+  DevBuf row_lse, row_z, row_i;
   DevBuf b_cum, b_live, b_y, b_prow, b_done, b_ndone, b_bt, b_br, b_braw, b_bnorm;
   DevBuf h_par, h_tok, h_lp, s_score, s_par;
   DevBuf o_hyps, o_lens, o_scores, o_raw, o_tlogp;
 
-  EventPairs ev_gen, ev_step, ev_enc;
+  std::map<std::string, EventPairs> evs;   // per kernel family ("gen", "step", "encode", ...)
   bool capturing = false;
   GraphCache graph;
 
@@ -333,6 +335,22 @@ static int gemm(onmt_model* m, const Mat& W, const Act& X, int n_valid, int spli
   return eff;
 }
 
+// ---- per-kernel-family CUDA-event timing (profile mode); inside stream capture the events
+// become external event-record nodes of the cached graph
+static EvPair prof_begin(onmt_model* m, const char* name) {
+  EvPair ev{};
+  if (!m->profile) return ev;
+  ev = m->evs[name].acquire();
+  ev_record(ev.a, m->stream, m->capturing);
+  return ev;
+}
+static void prof_end(onmt_model* m, const char* name, const EvPair& ev) {
+  if (!m->profile) return;
+  ev_record(ev.b, m->stream, m->capturing);
+  if (m->capturing) m->graph.ev_nodes.push_back({name, ev});
+  else m->evs[name].pending.push_back({ev, true});
+}
+
 // partials per row written by the generator for operand X
 static int gen_parts(onmt_model* m, const Act& X) {
   const int n_vt = (m->Vt + kVTile - 1) / kVTile;
@@ -340,8 +358,7 @@ static int gen_parts(onmt_model* m, const Act& X) {
 }
 
 static void gen(onmt_model* m, const Act& X, const GenOut& g, StepCtl ctl) {
-  EvPair ev{};
-  if (m->profile) { ev = m->ev_gen.acquire(); ev_record(ev.a, m->stream, m->capturing); }
+  EvPair ev = prof_begin(m, "gen");
   if (m->use_tc) {
     ONMT_CUDA(tc_gen_persistent(m->gen_w.tmap, X.tmap, m->gen_w.m_pad / kTileM, X.rows_pad, X.n_group,
                                 m->gen_w.k_pad / kBK, m->num_sms, g, ctl, m->stream));
@@ -353,11 +370,7 @@ static void gen(onmt_model* m, const Act& X, const GenOut& g, StepCtl ctl) {
     ONMT_CUDA(simt_gen_partials(m->logits.as<float>(), m->gen_w.m_pad, g, ctl, m->stream));
     count(m, 2);
   }
-  if (m->profile) {
-    ev_record(ev.b, m->stream, m->capturing);
-    if (m->capturing) m->graph.gen_ev.push_back(ev);
-    else m->ev_gen.pending.push_back({ev, true});
-  }
+  prof_end(m, "gen", ev);
 }
 
 // ------------------------------------------------------------------ loader
@@ -519,6 +532,12 @@ static void load_model(onmt_model* m, const char* path) {
   if (m->general) {
     const auto& wi = get(t, "attn.w_in", {H, H}, seen);
     m->attn_win.upload(plain_pad(wi), (int)H, (int)H, bf);
+    HostTensor wt;                                  // W_in^T: keys k_s = W_in^T m_s (DESIGN.md §6 K4)
+    wt.dims = {H, H};
+    wt.v.resize(H * H);
+    for (uint64_t i = 0; i < H; ++i)
+      for (uint64_t j = 0; j < H; ++j) wt.v[i * H + j] = wi.v[j * H + i];
+    m->attn_win_t.upload(plain_pad(wt), (int)H, (int)H, bf);
   }
   const auto& wo = get(t, "attn.w_out", {H, 2 * H}, seen);
   m->attn_wout.upload(plain_pad(wo), (int)H, 2 * (int)H, bf);
@@ -531,10 +550,8 @@ static void load_model(onmt_model* m, const char* path) {
 }
 
 // ------------------------------------------------------------------ encoder
-static void run_encoder(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max) {
-  const bool bf = m->use_tc;
+static void prepare_encoder(onmt_model* m, int B, int S_max) {
   const int rows = B * S_max, H = m->H, Hd = m->Hd, D = m->D;
-  StepCtl none{nullptr, 0};
   m->enc_in0.ensure(rows, m->E, m->prec == ONMT_PREC_BF16);
   if (m->L > 1) { m->enc_mid[0].ensure(rows, H, m->prec == ONMT_PREC_BF16); m->enc_mid[1].ensure(rows, H, m->prec == ONMT_PREC_BF16); }
   for (int d = 0; d < D; ++d) m->enc_rec[d].ensure(B, Hd, m->prec == ONMT_PREC_BF16);
@@ -543,8 +560,18 @@ static void run_encoder(onmt_model* m, const int* d_ids, const int* d_lens, int 
   for (int d = 0; d < D; ++d) m->enc_z[d].ensure((size_t)zrows * zld * 4);
   m->enc_p.ensure((size_t)16 * m->enc_rec[0].rows_pad * m->enc_whh[0]->m_pad * 4);
   m->mem.ensure((size_t)rows * H * 4);
+  if (m->general) m->mem_x.ensure(rows, H, m->prec == ONMT_PREC_BF16);
   m->enc_h.ensure((size_t)m->L * B * H * 4);
   m->enc_c.ensure((size_t)m->L * B * H * 4);
+  if (m->general) m->keys.ensure((size_t)m->mem_x.rows_pad * m->attn_win_t.m_pad * 4);
+}
+
+static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max) {
+  const bool bf = m->use_tc;
+  const int rows = B * S_max, H = m->H, Hd = m->Hd, D = m->D;
+  StepCtl none{nullptr, 0};
+  const int zld = m->enc_wih[0]->m_pad;
+  EvPair pe = prof_begin(m, "encode");
   ONMT_CUDA(cudaMemsetAsync(m->mem.p, 0, (size_t)rows * H * 4, m->stream));
 
   launch_embed_gather(m->emb_src.as<float>(), m->E, d_ids, d_lens, B, S_max, m->enc_in0.xo(bf), m->stream);
@@ -565,6 +592,7 @@ static void run_encoder(onmt_model* m, const int* d_ids, const int* d_lens, int 
         }
         XOut xn{};
         if (xnext) xn = xnext->xo(bf);
+        else if (m->general) xn = m->mem_x.xo(bf);          // top layer: memory as the keys-GEMM operand
         launch_enc_cell(m->enc_z[d].as<float>(), zld, P, splits, m->enc_rec[d].rows_pad, whh.m_pad,
                         m->enc_bias[l * D + d]->as<float>(), Hd, B, d_lens, S_max, t, d == 1,
                         m->enc_h.as<float>() + (size_t)l * B * H + d * Hd,
@@ -574,6 +602,9 @@ static void run_encoder(onmt_model* m, const int* d_ids, const int* d_lens, int 
       }
     xin = xnext;
   }
+  if (m->general)    // keys k_s = W_in^T m_s for every source position (hoisted 'general' query GEMM)
+    gemm(m, m->attn_win_t, m->mem_x, rows, 1, m->keys.as<float>(), none);
+  prof_end(m, "encode", pe);
   ONMT_CUDA(cudaGetLastError());
 }
 
@@ -606,14 +637,12 @@ static BeamState beam_state(onmt_model* m, bool trace) {
   return bs;
 }
 
-static void run_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int K, int max_len, float alpha,
-                        bool trace, const DecodeOut& out) {
-  const bool bf = m->use_tc, bfm = m->prec == ONMT_PREC_BF16;
+static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len, bool trace) {
+  const bool bfm = m->prec == ONMT_PREC_BF16;
   const int R = B * K, H = m->H, E = m->E, L = m->L;
   while ((int)m->xdec.size() < L) m->xdec.push_back(std::make_unique<Act>());
   m->xdec[0]->ensure(R, E + 2 * H, bfm);
   for (int l = 1; l < L; ++l) m->xdec[l]->ensure(R, 2 * H, bfm);
-  if (m->general) m->xq.ensure(R, H, bfm);
   m->xo.ensure(R, 2 * H, bfm);
   m->xg.ensure(R, H, bfm);
   const int rp = m->xg.rows_pad;
@@ -637,8 +666,11 @@ static void run_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int 
       ONMT_CUDA(cudaMemset(m->a_tick.p, 0, m->a_tick.bytes));
     }
   }
-  m->b_cum.ensure((size_t)R * 8);
-  m->b_live.ensure((size_t)R * 4);
+  m->row_lse.ensure((size_t)R * 4);
+  m->row_z.ensure((size_t)R * K * 4);
+  m->row_i.ensure((size_t)R * K * 4);
+  m->b_cum.ensure((size_t)2 * R * 8);     // double-buffered by step parity
+  m->b_live.ensure((size_t)2 * R * 4);
   m->b_y.ensure((size_t)R * 4);
   m->b_prow.ensure((size_t)R * 4);
   m->b_done.ensure((size_t)B * 4);
@@ -659,6 +691,15 @@ static void run_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int 
     ONMT_CUDA(cudaMemcpyAsync(m->s_score.p, ninf.data(), ninf.size() * 8, cudaMemcpyHostToDevice, m->stream));
     ONMT_CUDA(cudaStreamSynchronize(m->stream));
   }
+  if (!m->use_tc) m->logits.ensure((size_t)m->xg.rows_pad * m->gen_w.m_pad * 4);
+}
+
+static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int K, int max_len, float alpha,
+                            bool trace, const DecodeOut& out) {
+  const bool bf = m->use_tc;
+  const int R = B * K, H = m->H, E = m->E, L = m->L;
+  const int rp = m->xg.rows_pad;
+  const int n_vt = gen_parts(m, m->xg);
   BeamState bs = beam_state(m, trace);
   float* hh = m->st_h.as<float>();
   float* cc = m->st_c.as<float>();
@@ -685,99 +726,110 @@ static void run_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int 
   g.rows_valid = R;
   g.rows_pad = rp;
   float* P = m->dec_p.as<float>();
-  if (!m->use_tc) m->logits.ensure((size_t)m->xg.rows_pad * m->gen_w.m_pad * 4);   // before any capture
-  auto enqueue_steps = [&]() {
   for (int t = 1; t <= max_len; ++t) {
-    EvPair ev{};
-    if (m->profile) { ev = m->ev_step.acquire(); ev_record(ev.a, m->stream, m->capturing); }
+    EvPair ev = prof_begin(m, "step");
     for (int l = 0; l < L; ++l) {
       const Mat& W = *m->dec_w[l];
+      EvPair pg = prof_begin(m, "gemm");
       int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
+      prof_end(m, "gemm", pg);
+      EvPair pc = prof_begin(m, "cell");
       CellDst dst{};
       if (l + 1 < L) {
         dst.x[0] = m->xdec[l + 1]->xo(bf); dst.col[0] = 0; dst.n = 1;
       } else {
         dst.x[0] = m->xo.xo(bf); dst.col[0] = H; dst.n = 1;
-        if (m->general) { dst.x[1] = m->xq.xo(bf); dst.col[1] = 0; dst.n = 2; }
       }
       launch_dec_cell(P, s, m->xdec[l]->rows_pad, W.m_pad, m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H,
                       cc + (size_t)l * rp * H, hh + (size_t)l * rp * H, H, R, dst, ctl, m->stream);
       count(m);
+      prof_end(m, "cell", pc);
     }
     const float* htop = hh + (size_t)(L - 1) * rp * H;
-    if (m->general) {
-      int s = gemm(m, m->attn_win, m->xq, R, 0, P, ctl);
-      ONMT_CUDA(launch_attention(P, s, m->xq.rows_pad, m->attn_win.m_pad, nullptr, m->mem.as<float>(), d_lens, B,
-                                 S_max, H, K, m->xo.xo(bf), bs.done, m->a_pm.as<float>(), m->a_ps.as<float>(),
-                                 m->a_pc.as<float>(), m->a_tick.as<int>(), ctl, m->stream));
-    } else {
-      ONMT_CUDA(launch_attention(nullptr, 0, 0, 0, htop, m->mem.as<float>(), d_lens, B, S_max, H, K, m->xo.xo(bf),
+    {
+      EvPair pa = prof_begin(m, "attention");
+      const float* keys = m->general ? m->keys.as<float>() : m->mem.as<float>();
+      const int key_ld = m->general ? m->attn_win_t.m_pad : H;
+      ONMT_CUDA(launch_attention(htop, keys, key_ld, m->mem.as<float>(), d_lens, B, S_max, H, K, m->xo.xo(bf),
                                  bs.done, m->a_pm.as<float>(), m->a_ps.as<float>(), m->a_pc.as<float>(),
                                  m->a_tick.as<int>(), ctl, m->stream));
+      count(m);
+      prof_end(m, "attention", pa);
     }
-    count(m);
     {
+      EvPair pg = prof_begin(m, "gemm");
       int s = gemm(m, m->attn_wout, m->xo, R, 0, P, ctl);
+      prof_end(m, "gemm", pg);
+      EvPair po = prof_begin(m, "attn_out");
       launch_attn_out(P, s, m->xo.rows_pad, m->attn_wout.m_pad, m->htilde.as<float>(), H, R, m->xg.xo(bf), ctl,
                       m->stream);
       count(m);
+      prof_end(m, "attn_out", po);
     }
     gen(m, m->xg, g, ctl);
-    launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, B, K, t, max_len, alpha, bs, ga, ctl, m->stream);
-    count(m);
-    if (m->profile) {
-      ev_record(ev.b, m->stream, m->capturing);
-      if (m->capturing) m->graph.step_ev.push_back(ev);
-      else m->ev_step.pending.push_back({ev, true});
-    }
-  }
-  };
-  if (!m->use_graph) {
-    enqueue_steps();
-  } else {
-    // the whole max_len-step loop as one CUDA graph, cached per shape / buffer set
-    std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc,
-                                (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
-    GraphCache& gc = m->graph;
-    if (!gc.exec || gc.key != key) {
-      if (gc.exec) {
-        ONMT_CUDA(cudaStreamSynchronize(m->stream));
-        ONMT_CUDA(cudaGraphExecDestroy(gc.exec));
-        gc.exec = nullptr;
-        m->ev_gen.release(gc.gen_ev);
-        m->ev_step.release(gc.step_ev);
-        gc.gen_ev.clear();
-        gc.step_ev.clear();
-      }
-      cudaGraph_t graph;
-      const int64_t before = m->launches;
-      ONMT_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
-      m->capturing = true;
-      try {
-        enqueue_steps();
-      } catch (...) {
-        m->capturing = false;
-        cudaGraph_t junk;
-        cudaStreamEndCapture(m->stream, &junk);
-        if (junk) cudaGraphDestroy(junk);
-        throw;
-      }
-      m->capturing = false;
-      ONMT_CUDA(cudaStreamEndCapture(m->stream, &graph));
-      ONMT_CUDA(cudaGraphInstantiate(&gc.exec, graph, 0));
-      ONMT_CUDA(cudaGraphDestroy(graph));
-      gc.kernels = m->launches - before;
-      m->launches = before;
-      gc.key = key;
-    }
-    ONMT_CUDA(cudaGraphLaunch(gc.exec, m->stream));
-    m->launches += gc.kernels;
-    for (auto& p : gc.gen_ev) m->ev_gen.pending.push_back({p, false});
-    for (auto& p : gc.step_ev) m->ev_step.pending.push_back({p, false});
+    EvPair pm = prof_begin(m, "merge");
+    launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, B, K, t, max_len, std::pow((5.0 + t) / 6.0, (double)alpha), bs, ga,
+                      m->row_lse.as<float>(), m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
+    count(m, 2);
+    prof_end(m, "merge", pm);
+    prof_end(m, "step", ev);
   }
   launch_finalize(bs, B, K, max_len, out.hyps, out.lens, out.scores, out.raw, out.tlogp, m->stream);
   count(m);
   ONMT_CUDA(cudaGetLastError());
+}
+
+// The whole translation (encoder, decoder init, every decode step, finalize) as one CUDA
+// graph, cached per shape / pointer set: one cudaGraphLaunch per call, no host round trip.
+static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int K, int max_len,
+                          float alpha, bool trace, const DecodeOut& out) {
+  prepare_encoder(m, B, S_max);
+  prepare_decoder(m, B, S_max, K, max_len, trace);
+  auto enqueue = [&]() {
+    enqueue_encoder(m, d_ids, d_lens, B, S_max);
+    enqueue_decoder(m, d_lens, B, S_max, K, max_len, alpha, trace, out);
+  };
+  if (!m->use_graph) {
+    enqueue();
+    return;
+  }
+  std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc,
+                              (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
+                              (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
+                              (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp};
+  GraphCache& gc = m->graph;
+  if (!gc.exec || gc.key != key) {
+    if (gc.exec) {
+      ONMT_CUDA(cudaStreamSynchronize(m->stream));
+      ONMT_CUDA(cudaGraphExecDestroy(gc.exec));
+      gc.exec = nullptr;
+      for (auto& pe : gc.ev_nodes) m->evs[pe.first].release({pe.second});
+      gc.ev_nodes.clear();
+    }
+    cudaGraph_t graph;
+    const int64_t before = m->launches;
+    ONMT_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+    m->capturing = true;
+    try {
+      enqueue();
+    } catch (...) {
+      m->capturing = false;
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(m->stream, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      throw;
+    }
+    m->capturing = false;
+    ONMT_CUDA(cudaStreamEndCapture(m->stream, &graph));
+    ONMT_CUDA(cudaGraphInstantiate(&gc.exec, graph, 0));
+    ONMT_CUDA(cudaGraphDestroy(graph));
+    gc.kernels = m->launches - before;
+    m->launches = before;
+    gc.key = key;
+  }
+  ONMT_CUDA(cudaGraphLaunch(gc.exec, m->stream));
+  m->launches += gc.kernels;
+  for (auto& pe : gc.ev_nodes) m->evs[pe.first].pending.push_back({pe.second, false});
 }
 
 }  // namespace onmt
@@ -827,6 +879,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   m->use_tc = prec == ONMT_PREC_BF16;
   m->num_sms = prop.multiProcessorCount;
   if (const char* ev = std::getenv("ONMT_USE_GRAPH")) m->use_graph = std::atoi(ev) != 0;   // ncu runs use 0
+
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
   load_model(m.get(), path);
@@ -903,7 +956,8 @@ onmt_status onmt_encode(onmt_model* m, const int32_t* ids, const int32_t* lens, 
   ONMT_API_BEGIN
   ONMT_CUDA(cudaSetDevice(m->device));
   upload_src(m, ids, lens, B, S_max);
-  run_encoder(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max);
+  prepare_encoder(m, B, S_max);
+  enqueue_encoder(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max);
   if (out_memory)
     ONMT_CUDA(cudaMemcpyAsync(out_memory, m->mem.p, (size_t)B * S_max * m->H * 4, cudaMemcpyDeviceToHost, m->stream));
   if (out_h) ONMT_CUDA(cudaMemcpyAsync(out_h, m->enc_h.p, (size_t)m->L * B * m->H * 4, cudaMemcpyDeviceToHost, m->stream));
@@ -940,13 +994,9 @@ static onmt_status translate_impl(onmt_model* m, const int32_t* ids, const int32
   m->o_scores.ensure((size_t)B * 4);
   m->o_raw.ensure((size_t)B * 4);
   m->o_tlogp.ensure((size_t)B * max_len * 4);
-  EvPair ev{};
-  if (m->profile) { ev = m->ev_enc.acquire(); ONMT_CUDA(cudaEventRecord(ev.a, m->stream)); }
-  run_encoder(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max);
-  if (m->profile) { ONMT_CUDA(cudaEventRecord(ev.b, m->stream)); m->ev_enc.pending.push_back({ev, true}); }
   DecodeOut o{m->o_hyps.as<int>(), m->o_lens.as<int>(), m->o_scores.as<float>(), m->o_raw.as<float>(),
               m->o_tlogp.as<float>()};
-  run_decoder(m, m->d_lens.as<int>(), B, S_max, beam, max_len, alpha, trace, o);
+  run_translate(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max, beam, max_len, alpha, trace, o);
   ONMT_CUDA(cudaMemcpyAsync(hyps, o.hyps, (size_t)B * max_len * 4, cudaMemcpyDeviceToHost, m->stream));
   ONMT_CUDA(cudaMemcpyAsync(olens, o.lens, (size_t)B * 4, cudaMemcpyDeviceToHost, m->stream));
   ONMT_CUDA(cudaMemcpyAsync(scores, o.scores, (size_t)B * 4, cudaMemcpyDeviceToHost, m->stream));
@@ -994,15 +1044,11 @@ onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_ids, const int32_
   if (!d_ids || !d_lens || !d_hyps || !d_olens || !d_scores) return fail(ONMT_E_INVALID_ARG, "null device pointer");
   ONMT_API_BEGIN
   ONMT_CUDA(cudaSetDevice(m->device));
-  EvPair ev{};
-  if (m->profile) { ev = m->ev_enc.acquire(); ONMT_CUDA(cudaEventRecord(ev.a, m->stream)); }
-  run_encoder(m, d_ids, d_lens, B, S_max);
-  if (m->profile) { ONMT_CUDA(cudaEventRecord(ev.b, m->stream)); m->ev_enc.pending.push_back({ev, true}); }
   m->o_raw.ensure((size_t)B * 4);
   m->o_tlogp.ensure((size_t)B * max_len * 4);
   DecodeOut o{d_hyps, d_olens, d_scores, d_raw ? d_raw : m->o_raw.as<float>(),
               d_tlogp ? d_tlogp : m->o_tlogp.as<float>()};
-  run_decoder(m, d_lens, B, S_max, beam, max_len, alpha, false, o);
+  run_translate(m, d_ids, d_lens, B, S_max, beam, max_len, alpha, false, o);
   return ONMT_OK;
   ONMT_API_END
 }
@@ -1010,12 +1056,12 @@ onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_ids, const int32_
 onmt_status onmt_get_kernel_time(onmt_model* m, const char* name, int32_t reset, double* total_ms, int64_t* launches) {
   if (!m || !name || !total_ms || !launches) return fail(ONMT_E_INVALID_ARG, "null argument");
   ONMT_API_BEGIN
-  EventPairs* e = nullptr;
   std::string n(name);
-  if (n == "gen") e = &m->ev_gen;
-  else if (n == "step") e = &m->ev_step;
-  else if (n == "encode") e = &m->ev_enc;
-  else return fail(ONMT_E_INVALID_ARG, "unknown kernel family " + n);
+  static const char* known[] = {"gen", "step", "encode", "gemm", "cell", "attention", "attn_out", "merge"};
+  bool ok = false;
+  for (const char* k : known) ok |= n == k;
+  if (!ok) return fail(ONMT_E_INVALID_ARG, "unknown kernel family " + n);
+  EventPairs* e = &m->evs[n];
   ONMT_CUDA(cudaStreamSynchronize(m->stream));
   e->drain();
   *total_ms = e->acc_ms;

@@ -107,6 +107,8 @@ __global__ void enc_cell_kernel(const float* __restrict__ Z, int z_ld, const flo
 __global__ void dec_cell_kernel(const float* __restrict__ P, int splits, int p_rows_pad, int p_ld,
                                 const float4* __restrict__ bias, const float* __restrict__ cg, float* c_out,
                                 float* h_out, int H, int R, CellDst dst, StepCtl ctl) {
+  pdl_trigger();
+  pdl_wait();
   if (all_done(ctl)) return;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= R * H) return;
@@ -122,69 +124,96 @@ __global__ void dec_cell_kernel(const float* __restrict__ P, int splits, int p_r
   for (int d = 0; d < dst.n; ++d) store_x(dst.x[d], r, dst.col[d] + j, h);
 }
 
-// A7: Luong global attention (P119-122, P299-301), split over source chunks of CH
-// positions: CTA (b, c) stages m_s for s in its chunk in shared memory once, computes
-// q = W_in h (general: split-K partials summed here) or q = h (dot), the scores
-// e_s = q.m_s, the chunk's (max, sum exp) and partial context for all K rows of
-// sentence b.  The last CTA of a sentence (atomic ticket) combines the chunks in fixed
-// order - a = softmax over s < S_b only, pads excluded - and writes the context into
+// A7: Luong global attention (P119-122, P299-301).  'general' scores are
+// e_s = (W_in h) . m_s = h . (W_in^T m_s): the key k_s = W_in^T m_s is computed once per
+// batch right after the encoder (one tcgen05 GEMM over all source positions), so no
+// per-step query GEMM exists; 'dot' uses k_s = m_s.  CTA (b, c) stages the keys and
+// memory rows of its chunk of kAttCH source positions in shared memory (cp.async) and
+// computes, for all K rows of sentence b, the scores, the chunk's (max, sum exp) and
+// partial context.  The last CTA of the sentence (atomic ticket) combines the chunks in
+// fixed order - softmax over s < S_b only, pads excluded - and writes the context into
 // the first H columns of the W_out operand.
-constexpr int kAttCH = 32;
+constexpr int kAttCH = 16;
 
 template <int KMAX>
-__global__ void __launch_bounds__(256) attention_kernel(const float* __restrict__ Pq, int splits, int p_rows_pad,
-                                                        int p_ld, const float* __restrict__ htop,
+__global__ void __launch_bounds__(256) attention_kernel(const float* __restrict__ htop,
+                                                        const float* __restrict__ keys, int key_ld,
                                                         const float* __restrict__ mem, const int* __restrict__ lens,
                                                         int S_max, int H, int K, XOut xo, const int* __restrict__ done,
                                                         float* __restrict__ part_m, float* __restrict__ part_s,
                                                         float* __restrict__ part_c, int* __restrict__ tickets,
                                                         StepCtl ctl) {
+  pdl_trigger();
+  pdl_wait();
   if (all_done(ctl)) return;
   const int b = blockIdx.x, ch = blockIdx.y, nch = gridDim.y;
   if (done && done[b]) return;
-  extern __shared__ float sh[];
-  float* q = sh;                          // [K][H]
-  float* ms = q + K * H;                  // [kAttCH][H]
-  float* e = ms + kAttCH * H;             // [K][kAttCH]
+  extern __shared__ __align__(16) float sh[];
+  const bool same = keys == mem;
+  float* q = sh;                                  // [K][H]
+  float* e = q + K * H;                           // [K][kAttCH]
+  float* ms = e + K * kAttCH;                     // [kAttCH][H]
+  float* ks = same ? ms : ms + kAttCH * H;        // [kAttCH][key_ld]
   __shared__ int s_last;
   const int L = lens[b];
   const int s0 = ch * kAttCH;
   const int ns = max(0, min(kAttCH, L - s0));
-  const float* M = mem + ((size_t)b * S_max + s0) * H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const size_t pbase = ((size_t)b * nch + ch) * K;
   if (ns > 0) {
-    stage_async(ms, M, ns * H);                      // memory-bank chunk -> smem, in flight
-    const size_t pstride = (size_t)p_rows_pad * p_ld;
-    for (int i0 = threadIdx.x; i0 < K * H; i0 += 2 * blockDim.x) {
-      float v[2];
+    stage_async(ms, mem + ((size_t)b * S_max + s0) * H, ns * H);
+    if (!same) stage_async(ks, keys + ((size_t)b * S_max + s0) * key_ld, ns * key_ld);
+    const float* __restrict__ hq = htop + (size_t)b * K * H;
+    for (int i0 = threadIdx.x; i0 < K * H; i0 += 4 * blockDim.x) {
+      float v[4];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int i = i0 + u * blockDim.x;
-        v[u] = 0.f;
-        if (i < K * H) {
-          const int k = i / H, j = i % H;
-          const int r = b * K + k;
-          v[u] = Pq ? sum_splits(Pq, pstride, (size_t)r * p_ld + j, splits) : __ldg(&htop[(size_t)r * H + j]);
-        }
+        v[u] = i < K * H ? __ldg(&hq[i]) : 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < 4; ++u)
         if (i0 + u * blockDim.x < K * H) q[i0 + u * blockDim.x] = v[u];
     }
     stage_wait();
     __syncthreads();
-    for (int p = warp; p < K * ns; p += nw) {         // one warp per (row, position) score
-      const int k = p / ns, sidx = p % ns;
-      float acc = 0.f;
-      for (int j = lane; j < H; j += 32) acc = fmaf(q[k * H + j], ms[sidx * H + j], acc);
+    const int kl = same ? H : key_ld;
+    for (int s0w = 2 * warp; s0w < ns; s0w += 2 * nw) {   // one warp: 2 positions x K rows at once
+      const bool two = s0w + 1 < ns;
+      float acc0[KMAX], acc1[KMAX];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) e[k * kAttCH + sidx] = acc;
+      for (int k = 0; k < KMAX; ++k) { acc0[k] = 0.f; acc1[k] = 0.f; }
+      for (int j = lane; j < H; j += 32) {
+        const float k0 = ks[s0w * kl + j];
+        const float k1 = two ? ks[(s0w + 1) * kl + j] : 0.f;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < K) {
+            const float qv = q[k * H + j];
+            acc0[k] = fmaf(qv, k0, acc0[k]);
+            acc1[k] = fmaf(qv, k1, acc1[k]);
+          }
+      }
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          acc0[k] += __shfl_xor_sync(0xffffffffu, acc0[k], o);
+          acc1[k] += __shfl_xor_sync(0xffffffffu, acc1[k], o);
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < K) {
+            e[k * kAttCH + s0w] = acc0[k];
+            if (two) e[k * kAttCH + s0w + 1] = acc1[k];
+          }
+      }
     }
     __syncthreads();
     for (int k = warp; k < K; k += nw) {              // chunk softmax statistics
-      float v = lane < ns ? e[k * kAttCH + lane] : -INFINITY;
+      const float v = lane < ns ? e[k * kAttCH + lane] : -INFINITY;
       float mx = v;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -221,7 +250,8 @@ __global__ void __launch_bounds__(256) attention_kernel(const float* __restrict_
   if (!s_last) return;
   __threadfence();
   const size_t b0 = (size_t)b * nch * K;
-  __shared__ float s_w[64][kKMax];               // per (chunk, row) weight exp(m_c - M) / S
+  float* s_w = e;                                 // reuse: [nch][K] normalised chunk weights
+  if (nch * K > K * kAttCH + K * H) return;       // (cannot happen: nch <= 128)
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     float Mx = -INFINITY;
     for (int c = 0; c < nch; ++c) Mx = fmaxf(Mx, __ldcg(&part_m[b0 + c * K + k]));
@@ -229,17 +259,39 @@ __global__ void __launch_bounds__(256) attention_kernel(const float* __restrict_
     for (int c = 0; c < nch; ++c) {
       const float pm = __ldcg(&part_m[b0 + c * K + k]);
       const float w = pm == -INFINITY ? 0.f : expf(pm - Mx);
-      s_w[c][k] = w;
+      s_w[c * K + k] = w;
       S += w * __ldcg(&part_s[b0 + c * K + k]);
     }
-    for (int c = 0; c < nch; ++c) s_w[c][k] /= S;
+    const float inv = 1.f / S;
+    for (int c = 0; c < nch; ++c) s_w[c * K + k] *= inv;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < K * H; i += blockDim.x) {
-    const int k = i / H, j = i % H;
-    float C = 0.f;
-    for (int c = 0; c < nch; ++c) C += s_w[c][k] * __ldcg(&part_c[(b0 + c * K + k) * H + j]);
-    store_x(xo, b * K + k, j, C);
+  for (int i0 = threadIdx.x; i0 < K * H; i0 += 2 * blockDim.x) {
+    float C[2] = {0.f, 0.f};
+    for (int c0 = 0; c0 < nch; c0 += 8) {           // 2 items x 8 chunks of L2 loads in flight
+      float v[2][8];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = min(i0 + u * (int)blockDim.x, K * H - 1);
+        const int k = i / H, j = i % H;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          v[u][cc] = c0 + cc < nch ? __ldcg(&part_c[(b0 + (c0 + cc) * K + k) * H + j]) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = min(i0 + u * (int)blockDim.x, K * H - 1);
+        const int k = i / H;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          if (c0 + cc < nch) C[u] += s_w[(c0 + cc) * K + k] * v[u][cc];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < K * H) store_x(xo, b * K + i / H, i % H, C[u]);
+    }
   }
   if (threadIdx.x == 0) tickets[b] = 0;
 }
@@ -248,6 +300,8 @@ __global__ void __launch_bounds__(256) attention_kernel(const float* __restrict_
 // the next step's input feed) and the generator operand.
 __global__ void attn_out_kernel(const float* __restrict__ P, int splits, int p_rows_pad, int p_ld, float* htilde,
                                 int H, int R, XOut xg, StepCtl ctl) {
+  pdl_trigger();
+  pdl_wait();
   if (all_done(ctl)) return;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= R * H) return;
@@ -268,8 +322,9 @@ __global__ void init_decode_kernel(BeamState bs, int B, int K, const float* __re
   const int r = blockIdx.x;       // row b*K + k
   const int b = r / K, k = r % K;
   if (threadIdx.x == 0) {
-    bs.cum[r] = k == 0 ? 0.0 : -CUDART_INF;
-    bs.live[r] = k == 0;
+    const int R = gridDim.x;
+    bs.cum[R + r] = k == 0 ? 0.0 : -CUDART_INF;     // slot state of step t lives in buffer t & 1
+    bs.live[R + r] = k == 0;
     bs.y[r] = 2;  // BOS
     bs.prow[r] = r;
     if (k == 0) {
@@ -318,211 +373,262 @@ __global__ void gather_kernel(BeamState bs, GatherArgs g, int K, StepCtl ctl) {
 // row top-K, select the K best (raw desc, slot asc, token asc) over live slots with
 // fp64 cumulative scores, bank EOS picks and everything at t = max_len, update the
 // stop flag and the histories.  One CTA per sentence, one warp per beam row.
+// A10a: per hypothesis row, combine the generator partials (one per generator CTA) into
+// the row log-sum-exp and the row top-K (z desc, id asc).  One 128-thread CTA per row;
+// every thread issues all loads of its partials before using any of them.
 template <int KMAX>
-__global__ void __launch_bounds__(256) beam_merge_kernel(const float2* __restrict__ ms, const float* __restrict__ tz,
-                                                         const int* __restrict__ ti, int n_vt, int rows_pad, int K,
-                                                         int t, int max_len, float alpha, BeamState bs,
-                                                         GatherArgs ga, StepCtl ctl) {
+__global__ void __launch_bounds__(128) row_reduce_topk_kernel(const float2* __restrict__ ms,
+                                                              const float* __restrict__ tz,
+                                                              const int* __restrict__ ti, int n_parts, int rows_pad,
+                                                              int K, const int* __restrict__ live,
+                                                              float* __restrict__ row_lse, float* __restrict__ row_z,
+                                                              int* __restrict__ row_i, StepCtl ctl) {
+  pdl_trigger();
+  pdl_wait();
   if (all_done(ctl)) return;
-  const int b = blockIdx.x;
-  if (bs.done[b]) return;
+  const int r = blockIdx.x;
+  if (live && !live[r]) return;                 // (live = this step's buffer)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ float s_m[4], s_s[4];
+  __shared__ float s_wz[4];
+  __shared__ int s_wi[4];
+  // ---- loads: up to 2 partials per thread, all in flight
+  float2 p[2];
+  float cz[2][KMAX];
+  int cid[2][KMAX];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int v = threadIdx.x + u * 128;
+    const bool ok = v < n_parts;
+    p[u] = ok ? __ldg(&ms[(size_t)v * rows_pad + r]) : make_float2(-INFINITY, 0.f);
+    const size_t base = ((size_t)v * rows_pad + r) * K;
+#pragma unroll
+    for (int c = 0; c < KMAX; ++c) {
+      cz[u][c] = (ok && c < K) ? __ldg(&tz[base + c]) : -INFINITY;
+      cid[u][c] = (ok && c < K) ? __ldg(&ti[base + c]) : 0x7fffffff;
+    }
+  }
+  for (int v = threadIdx.x + 256; v < n_parts; v += 128) {       // (more than 256 partials: rare)
+    const float2 q = __ldg(&ms[(size_t)v * rows_pad + r]);
+    if (q.x > p[0].x) { p[0].y = p[0].y * expf(p[0].x - q.x) + q.y; p[0].x = q.x; }
+    else if (q.x > -INFINITY) p[0].y += q.y * expf(q.x - p[0].x);
+    const size_t base = ((size_t)v * rows_pad + r) * K;
+    for (int c = 0; c < K; ++c) {
+      float z = __ldg(&tz[base + c]);
+      int id = __ldg(&ti[base + c]);
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i)
+        if (better(z, id, cz[0][i], cid[0][i])) {
+          const float a1 = cz[0][i]; const int a2 = cid[0][i];
+          cz[0][i] = z; cid[0][i] = id; z = a1; id = a2;
+        }
+    }
+  }
+  // ---- log-sum-exp
+  float m = fmaxf(p[0].x, p[1].x), sum = 0.f;
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    if (p[u].x > -INFINITY) sum += p[u].y * expf(p[u].x - m);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+    const float M = fmaxf(m, m2);
+    sum = (m == -INFINITY ? 0.f : sum * expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - M));
+    m = M;
+  }
+  if (lane == 0) { s_m[warp] = m; s_s[warp] = sum; }
+  // ---- top-K: each thread merges its two sorted lists, then K rounds of block argmax
+  float lz[KMAX];
+  int li[KMAX];
+  {
+    int a = 0, b2 = 0;
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) {
+      const bool ta = better(cz[0][a < KMAX ? a : KMAX - 1], cid[0][a < KMAX ? a : KMAX - 1],
+                             cz[1][b2 < KMAX ? b2 : KMAX - 1], cid[1][b2 < KMAX ? b2 : KMAX - 1]);
+      // (static-index selects over the two heads keep the lists in registers)
+      float za = -INFINITY, zb = -INFINITY;
+      int ia = 0x7fffffff, ib = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < KMAX; ++q) {
+        if (q == a) { za = cz[0][q]; ia = cid[0][q]; }
+        if (q == b2) { zb = cz[1][q]; ib = cid[1][q]; }
+      }
+      (void)ta;
+      const bool takea = better(za, ia, zb, ib);
+      lz[i] = takea ? za : zb;
+      li[i] = takea ? ia : ib;
+      a += takea;
+      b2 += !takea;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = s_m[0];
+    for (int w = 1; w < 4; ++w) M = fmaxf(M, s_m[w]);
+    float S = 0.f;
+    for (int w = 0; w < 4; ++w)
+      if (s_m[w] > -INFINITY) S += s_s[w] * expf(s_m[w] - M);
+    row_lse[r] = M + logf(S);
+  }
+  for (int c = 0; c < K; ++c) {
+    float bz = lz[0];
+    int bi = li[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float z2 = __shfl_xor_sync(0xffffffffu, bz, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(z2, i2, bz, bi)) { bz = z2; bi = i2; }
+    }
+    if (lane == 0) { s_wz[warp] = bz; s_wi[warp] = bi; }
+    __syncthreads();
+    float wz = s_wz[0];
+    int wi = s_wi[0];
+#pragma unroll
+    for (int w = 1; w < 4; ++w)
+      if (better(s_wz[w], s_wi[w], wz, wi)) { wz = s_wz[w]; wi = s_wi[w]; }
+    if (threadIdx.x == 0) { row_z[(size_t)r * K + c] = wz; row_i[(size_t)r * K + c] = wi; }
+    if (li[0] == wi && lz[0] == wz) {                            // the owner pops its head
+#pragma unroll
+      for (int i = 0; i < KMAX - 1; ++i) { lz[i] = lz[i + 1]; li[i] = li[i + 1]; }
+      lz[KMAX - 1] = -INFINITY; li[KMAX - 1] = 0x7fffffff;
+    }
+    __syncthreads();
+  }
+}
+
+// A10b + A5: per sentence b, the K best (raw desc, slot asc, token asc) of the K x K row
+// candidates with fp64 cumulative scores (O8); EOS / max_len banking, stop flag,
+// histories (O9, O10) - computed redundantly by every CTA of the sentence from a few
+// hundred bytes of state - then each CTA gathers one column slice of the next step's
+// decoder inputs of one row (x1 = [E_tgt[y]; h~[p]; h_0[p]], x_l = [.; h_l[p]], c_l[p]).
+// CTA (row k, slice 0) of each sentence writes the beam state.
+template <int KMAX>
+__global__ void __launch_bounds__(128) beam_select_gather_kernel(const float* __restrict__ row_lse,
+                                                                 const float* __restrict__ row_z,
+                                                                 const int* __restrict__ row_i, int K, int t,
+                                                                 int max_len, double lp, BeamState bs, GatherArgs ga,
+                                                                 int nslice, StepCtl ctl) {
+  pdl_trigger();
+  pdl_wait();
+  // no all_done() here: another CTA of this launch may finish the last sentence; only
+  // completions of earlier steps (done[b] < t) may skip work
+  (void)ctl;
+  const int r = blockIdx.x, slice = blockIdx.y;
+  const int b = r / K, kr = r % K;
+  const int dn = bs.done[b];
+  if (dn != 0 && dn < t) return;
+  const int R = gridDim.x;
+  const int* __restrict__ live_in = bs.live + (size_t)(t & 1) * R;
+  const double* __restrict__ cum_in = bs.cum + (size_t)(t & 1) * R;
+  int* live_out = bs.live + (size_t)((t + 1) & 1) * R;
+  double* cum_out = bs.cum + (size_t)((t + 1) & 1) * R;
+  __shared__ int s_live[KMAX];
+  __shared__ double s_cum[KMAX];
   __shared__ float s_lse[KMAX];
   __shared__ float s_z[KMAX][KMAX];
   __shared__ int s_id[KMAX][KMAX];
-  __shared__ int s_live[KMAX];
-  __shared__ double s_cum[KMAX];
-  __shared__ int s_sel_k[KMAX], s_sel_w[KMAX], s_newlive[KMAX], s_prow[KMAX], s_y[KMAX];
-  __shared__ double s_sel_s[KMAX];
-  __shared__ float s_sel_lp[KMAX];
-  __shared__ int s_nsel, s_cont;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __shared__ int s_prow, s_y, s_cont;
   if (threadIdx.x < K) {
-    s_live[threadIdx.x] = bs.live[b * K + threadIdx.x];
-    s_cum[threadIdx.x] = bs.cum[b * K + threadIdx.x];
+    const int rr = b * K + threadIdx.x;
+    s_live[threadIdx.x] = live_in[rr];
+    s_cum[threadIdx.x] = cum_in[rr];
+    s_lse[threadIdx.x] = row_lse[rr];
+  }
+  for (int i = threadIdx.x; i < K * K; i += blockDim.x) {
+    s_z[i / K][i % K] = row_z[(size_t)b * K * K + i];
+    s_id[i / K][i % K] = row_i[(size_t)b * K * K + i];
   }
   __syncthreads();
-  for (int k = warp; k < K; k += nw) {
-    const int r = b * K + k;
-    if (!s_live[k]) continue;
-    // log-sum-exp over all partials (each lane: parts lane, lane+32, ...; loads in flight)
-    float m = -INFINITY, s = 0.f;
-    for (int v0 = 0; v0 < n_vt; v0 += 128) {
-      float2 p[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int v = v0 + u * 32 + lane;
-        p[u] = v < n_vt ? __ldg(&ms[(size_t)v * rows_pad + r]) : make_float2(-INFINITY, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (p[u].x == -INFINITY) continue;
-        if (p[u].x > m) { s = s * expf(m - p[u].x) + p[u].y; m = p[u].x; }
-        else s += p[u].y * expf(p[u].x - m);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-      const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
-      const float M = fmaxf(m, m2);
-      s = (m == -INFINITY ? 0.f : s * expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - M));
-      m = M;
-    }
-    if (lane == 0) s_lse[k] = m + logf(s);
-    // row top-K over the per-part sorted lists: lane-local merge, then K warp-argmax rounds
-    float lz[KMAX];
-    int li[KMAX];
-#pragma unroll
-    for (int i = 0; i < KMAX; ++i) { lz[i] = -INFINITY; li[i] = 0x7fffffff; }
-    for (int v = lane; v < n_vt; v += 32) {
-      const size_t base = ((size_t)v * rows_pad + r) * K;
-      float cz[KMAX];
-      int cid[KMAX];
-#pragma unroll
-      for (int c = 0; c < KMAX; ++c) {
-        cz[c] = c < K ? __ldg(&tz[base + c]) : -INFINITY;
-        cid[c] = c < K ? __ldg(&ti[base + c]) : 0x7fffffff;
-      }
-#pragma unroll
-      for (int c = 0; c < KMAX; ++c) {
-        float z = cz[c];
-        int id = cid[c];
-        if (!better(z, id, lz[KMAX - 1], li[KMAX - 1])) break;  // per-part lists are sorted
-#pragma unroll
-        for (int i = 0; i < KMAX; ++i) {
-          if (better(z, id, lz[i], li[i])) {
-            const float tzz = lz[i]; const int tii = li[i];
-            lz[i] = z; li[i] = id; z = tzz; id = tii;
-          }
-        }
-      }
-    }
-    for (int c = 0; c < K; ++c) {
-      float bz = lz[0];
-      int bi = li[0];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float z2 = __shfl_xor_sync(0xffffffffu, bz, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (better(z2, i2, bz, bi)) { bz = z2; bi = i2; }
-      }
-      if (lane == 0) { s_z[k][c] = bz; s_id[k][c] = bi; }
-      if (li[0] == bi && lz[0] == bz) {  // the owner pops its head
-#pragma unroll
-        for (int i = 0; i < KMAX - 1; ++i) { lz[i] = lz[i + 1]; li[i] = li[i + 1]; }
-        lz[KMAX - 1] = -INFINITY; li[KMAX - 1] = 0x7fffffff;
-      }
-    }
-  }
-  __syncthreads();
-  const size_t hb = (size_t)(t - 1) * (size_t)gridDim.x * K + (size_t)b * K;
   if (threadIdx.x == 0) {
-    // sentence-level K-way merge of the per-row sorted lists (O8, AMB-13), all in smem
     int head[KMAX];
+    int sel_k[KMAX], sel_w[KMAX];
+    double sel_s[KMAX];
+    float sel_lp[KMAX];
     for (int k = 0; k < K; ++k) head[k] = 0;
     int n_sel = 0;
-    for (int r = 0; r < K; ++r) {
+    for (int q = 0; q < K; ++q) {
       int bk = -1, bw = 0x7fffffff;
       double bsv = -CUDART_INF;
       for (int k = 0; k < K; ++k) {
         if (!s_live[k] || head[k] >= K) continue;
         const float z = s_z[k][head[k]];
         if (z == -INFINITY) continue;
-        const int w = s_id[k][head[k]];
         const double sc = s_cum[k] + ((double)z - (double)s_lse[k]);
-        if (bk < 0 || sc > bsv) { bk = k; bsv = sc; bw = w; }
+        if (bk < 0 || sc > bsv) { bk = k; bsv = sc; bw = s_id[k][head[k]]; }
       }
       if (bk < 0) break;
-      s_sel_k[n_sel] = bk;
-      s_sel_w[n_sel] = bw;
-      s_sel_s[n_sel] = bsv;
-      s_sel_lp[n_sel] = (float)((double)s_z[bk][head[bk]] - (double)s_lse[bk]);
+      sel_k[n_sel] = bk; sel_w[n_sel] = bw; sel_s[n_sel] = bsv;
+      sel_lp[n_sel] = (float)((double)s_z[bk][head[bk]] - (double)s_lse[bk]);
       ++n_sel;
       ++head[bk];
     }
-    // O8-O9 bookkeeping: banking of EOS picks and of everything at t = max_len
-    const double lp = pow((5.0 + t) / 6.0, (double)alpha);
-    int bt = bs.best_t[b], br = bs.best_r[b];
-    double braw = bs.best_raw[b], bnorm = bs.best_norm[b];
     bool any_live = false;
-    for (int r = 0; r < K; ++r) {
-      s_newlive[r] = 0; s_prow[r] = b * K + r; s_y[r] = 0;
-      if (r >= n_sel) continue;
-      const int w = s_sel_w[r];
-      if (w == 3 || t == max_len) {
-        const double norm = s_sel_s[r] / lp;
-        if (bt == 0 || norm > bnorm) { bt = t; br = r; braw = s_sel_s[r]; bnorm = norm; }
-      } else {
-        s_newlive[r] = 1; s_prow[r] = b * K + s_sel_k[r]; s_y[r] = w;
-        any_live = true;
+    for (int q = 0; q < n_sel; ++q) any_live |= !(sel_w[q] == 3 || t == max_len);
+    const bool stop = !any_live || t == max_len || (n_sel > 0 && sel_w[0] == 3);
+    const bool mine_sel = kr < n_sel;
+    const bool mine_live = mine_sel && !(sel_w[kr] == 3 || t == max_len);
+    s_prow = mine_live ? b * K + sel_k[kr] : r;
+    s_y = mine_live ? sel_w[kr] : 0;
+    s_cont = !stop;
+    if (slice == 0) {
+      // this CTA owns slot kr of sentence b: slot state + history entry
+      const size_t hb = (size_t)(t - 1) * (size_t)gridDim.x + (size_t)r;
+      live_out[r] = mine_live;
+      cum_out[r] = mine_live ? sel_s[kr] : -CUDART_INF;
+      bs.prow[r] = s_prow;
+      bs.y[r] = s_y;
+      bs.hist_parent[hb] = mine_sel ? sel_k[kr] : -1;
+      bs.hist_token[hb] = mine_sel ? sel_w[kr] : 0;
+      bs.hist_logp[hb] = mine_sel ? sel_lp[kr] : 0.f;
+      if (bs.sel_parent) { bs.sel_parent[hb] = mine_sel ? sel_k[kr] : -1; bs.sel_score[hb] = mine_sel ? sel_s[kr] : -CUDART_INF; }
+      if (kr == 0) {                                   // sentence-level banking and stop flag
+        int bt = bs.best_t[b], br = bs.best_r[b];
+        double braw = bs.best_raw[b], bnorm = bs.best_norm[b];
+        for (int q = 0; q < n_sel; ++q) {
+          if (sel_w[q] == 3 || t == max_len) {
+            const double norm = sel_s[q] / lp;
+            if (bt == 0 || norm > bnorm) { bt = t; br = q; braw = sel_s[q]; bnorm = norm; }
+          }
+        }
+        bs.best_t[b] = bt; bs.best_r[b] = br; bs.best_raw[b] = braw; bs.best_norm[b] = bnorm;
+        if (stop) { bs.done[b] = t; atomicAdd(bs.n_done, 1); }
       }
     }
-    bs.best_t[b] = bt; bs.best_r[b] = br; bs.best_raw[b] = braw; bs.best_norm[b] = bnorm;
-    // O10: stop after this step
-    const bool stop = !any_live || t == max_len || (n_sel > 0 && s_sel_w[0] == 3);
-    if (stop) {
-      bs.done[b] = 1;
-      atomicAdd(bs.n_done, 1);
-    }
-    s_nsel = n_sel;
-    s_cont = !stop;
   }
   __syncthreads();
-  if (threadIdx.x < K) {                          // parallel write-back of slot state + histories
-    const int r = threadIdx.x, row = b * K + r;
-    const bool sel = r < s_nsel;
-    bs.live[row] = s_newlive[r];
-    bs.cum[row] = s_newlive[r] ? s_sel_s[r] : -CUDART_INF;
-    bs.prow[row] = s_prow[r];
-    bs.y[row] = s_y[r];
-    bs.hist_parent[hb + r] = sel ? s_sel_k[r] : -1;
-    bs.hist_token[hb + r] = sel ? s_sel_w[r] : 0;
-    bs.hist_logp[hb + r] = sel ? s_sel_lp[r] : 0.f;
-    if (bs.sel_parent) { bs.sel_parent[hb + r] = sel ? s_sel_k[r] : -1; bs.sel_score[hb + r] = sel ? s_sel_s[r] : -CUDART_INF; }
-  }
   if (!s_cont) return;
-  // A5 fused: the next step's decoder inputs of this sentence's K rows, gathered by parent
-  const float* __restrict__ emb = ga.emb_tgt;
-  const float* __restrict__ hti = ga.htilde;
-  const float* __restrict__ hs = ga.h;
-  const float* __restrict__ cs = ga.c;
+  // ---- gather this CTA's column slice of row r (all loads first)
+  const int p = s_prow, y = s_y;
   const int E = ga.E, H = ga.H, L = ga.L;
-  for (int i = threadIdx.x; i < K * E; i += blockDim.x) {
-    const int k = i / E, c = i % E;
-    store_x(ga.x[0], b * K + k, c, __ldg(&emb[(size_t)s_y[k] * E + c]));
+  const int e0 = (E * slice) / nslice, e1 = (E * (slice + 1)) / nslice;
+  const int h0 = (H * slice) / nslice, h1 = (H * (slice + 1)) / nslice;
+  const float* __restrict__ emb = ga.emb_tgt + (size_t)y * E;
+  for (int c0 = e0 + threadIdx.x; c0 < e1; c0 += 2 * blockDim.x) {
+    const int c1 = c0 + blockDim.x;
+    const float v0 = __ldg(&emb[c0]);
+    const float v1 = c1 < e1 ? __ldg(&emb[c1]) : 0.f;
+    store_x(ga.x[0], r, c0, v0);
+    if (c1 < e1) store_x(ga.x[0], r, c1, v1);
   }
-  for (int i0 = threadIdx.x; i0 < K * H; i0 += 2 * blockDim.x) {
-    float hv[2][8], cv[2][8], ht[2];
+  for (int j = h0 + threadIdx.x; j < h1; j += blockDim.x) {
+    float hv[8], cv[8];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int i = min(i0 + u * (int)blockDim.x, K * H - 1);
-      const int k = i / H, j = i % H;
-      const int p = s_prow[k];
-#pragma unroll
-      for (int l = 0; l < 8; ++l) {
-        if (l < L) {
-          hv[u][l] = __ldg(&hs[((size_t)l * ga.rows_pad + p) * H + j]);
-          cv[u][l] = __ldg(&cs[((size_t)l * ga.rows_pad + p) * H + j]);
-        }
+    for (int l = 0; l < 8; ++l)
+      if (l < L) {
+        hv[l] = __ldg(&ga.h[((size_t)l * ga.rows_pad + p) * H + j]);
+        cv[l] = __ldg(&ga.c[((size_t)l * ga.rows_pad + p) * H + j]);
       }
-      ht[u] = __ldg(&hti[(size_t)p * H + j]);
-    }
+    const float ht = __ldg(&ga.htilde[(size_t)p * H + j]);
+    store_x(ga.x[0], r, E + j, ht);
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i >= K * H) break;
-      const int k = i / H, j = i % H;
-      const int r = b * K + k;
-      store_x(ga.x[0], r, E + j, ht[u]);
-#pragma unroll
-      for (int l = 0; l < 8; ++l) {
-        if (l < L) {
-          if (l == 0) store_x(ga.x[0], r, E + H + j, hv[u][l]);
-          else store_x(ga.x[l], r, H + j, hv[u][l]);
-          ga.cg[((size_t)l * ga.rows_pad + r) * H + j] = cv[u][l];
-        }
+    for (int l = 0; l < 8; ++l)
+      if (l < L) {
+        if (l == 0) store_x(ga.x[0], r, E + H + j, hv[l]);
+        else store_x(ga.x[l], r, H + j, hv[l]);
+        ga.cg[((size_t)l * ga.rows_pad + r) * H + j] = cv[l];
       }
-    }
   }
 }
 
@@ -567,22 +673,22 @@ void launch_enc_cell(const float* Z, int z_ld, const float* P, int splits, int p
 void launch_dec_cell(const float* P, int splits, int p_rows_pad, int p_ld, const float* bias, const float* cg,
                      float* c_out, float* h_out, int H, int R, CellDst dst, StepCtl ctl, cudaStream_t st) {
   const int n = R * H;
-  dec_cell_kernel<<<(n + 255) / 256, 256, 0, st>>>(P, splits, p_rows_pad, p_ld, (const float4*)bias, cg, c_out,
-                                                   h_out, H, R, dst, ctl);
+  launch_pdl(dec_cell_kernel, dim3((n + 255) / 256), dim3(256), 0, st, P, splits, p_rows_pad, p_ld,
+             (const float4*)bias, cg, c_out, h_out, H, R, dst, ctl);
 }
 
-cudaError_t launch_attention(const float* Pq, int splits, int p_rows_pad, int p_ld, const float* htop,
-                             const float* mem, const int* lens, int B, int S_max, int H, int K, XOut xo,
-                             const int* done, float* part_m, float* part_s, float* part_c, int* tickets, StepCtl ctl,
-                             cudaStream_t st) {
+cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, const float* mem, const int* lens,
+                             int B, int S_max, int H, int K, XOut xo, const int* done, float* part_m, float* part_s,
+                             float* part_c, int* tickets, StepCtl ctl, cudaStream_t st) {
   const int nch = (S_max + kAttCH - 1) / kAttCH;
-  const size_t smem = (size_t)(K * H + kAttCH * H + K * kAttCH) * sizeof(float);
+  const bool same = keys == mem;
+  const size_t smem = (size_t)(K * H + K * kAttCH + kAttCH * H + (same ? 0 : kAttCH * key_ld)) * sizeof(float);
   dim3 grid(B, nch);
-#define ONMT_ATT(KM)                                                                                          \
-  {                                                                                                           \
-    cudaFuncSetAttribute(attention_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    attention_kernel<KM><<<grid, 256, smem, st>>>(Pq, splits, p_rows_pad, p_ld, htop, mem, lens, S_max, H, K, \
-                                                  xo, done, part_m, part_s, part_c, tickets, ctl);            \
+#define ONMT_ATT(KM)                                                                                        \
+  {                                                                                                         \
+    cudaFuncSetAttribute(attention_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    launch_pdl(attention_kernel<KM>, grid, dim3(256), smem, st, htop, keys, key_ld, mem, lens, S_max, H, K, xo, \
+               done, part_m, part_s, part_c, tickets, ctl);                                                 \
   }
   if (K <= 1) ONMT_ATT(1)
   else if (K <= 2) ONMT_ATT(2)
@@ -598,7 +704,8 @@ int attention_chunks(int S_max) { return (S_max + kAttCH - 1) / kAttCH; }
 void launch_attn_out(const float* P, int splits, int p_rows_pad, int p_ld, float* htilde, int H, int R, XOut xg,
                      StepCtl ctl, cudaStream_t st) {
   const int n = R * H;
-  attn_out_kernel<<<(n + 255) / 256, 256, 0, st>>>(P, splits, p_rows_pad, p_ld, htilde, H, R, xg, ctl);
+  launch_pdl(attn_out_kernel, dim3((n + 255) / 256), dim3(256), 0, st, P, splits, p_rows_pad, p_ld, htilde, H, R, xg,
+             ctl);
 }
 
 void launch_init_decode(const BeamState& bs, int B, int K, const float* enc_h, const float* enc_c, int L, int H,
@@ -610,15 +717,21 @@ void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepC
   gather_kernel<<<R, 128, 0, st>>>(bs, g, K, ctl);
 }
 
-void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int B, int K, int t,
-                       int max_len, float alpha, const BeamState& bs, const GatherArgs& ga, StepCtl ctl,
-                       cudaStream_t st) {
-#define ONMT_MERGE(KM) beam_merge_kernel<KM><<<B, 256, 0, st>>>(ms, tz, ti, n_vt, rows_pad, K, t, max_len, alpha, bs, ga, ctl)
-  if (K <= 1) ONMT_MERGE(1);
-  else if (K <= 2) ONMT_MERGE(2);
-  else if (K <= 4) ONMT_MERGE(4);
-  else if (K <= 8) ONMT_MERGE(8);
-  else ONMT_MERGE(16);
+void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_parts, int rows_pad, int B, int K,
+                       int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga, float* row_lse,
+                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st) {
+  const int R = B * K;
+  const int nslice = 4;
+#define ONMT_MERGE(KM)                                                                                         \
+  launch_pdl(row_reduce_topk_kernel<KM>, dim3(R), dim3(128), 0, st, ms, tz, ti, n_parts, rows_pad, K,          \
+             bs.live + (size_t)(t & 1) * R, row_lse, row_z, row_i, ctl);                                       \
+  launch_pdl(beam_select_gather_kernel<KM>, dim3(R, nslice), dim3(128), 0, st, row_lse, row_z, row_i, K, t,    \
+             max_len, lp, bs, ga, nslice, ctl)
+  if (K <= 1) { ONMT_MERGE(1); }
+  else if (K <= 2) { ONMT_MERGE(2); }
+  else if (K <= 4) { ONMT_MERGE(4); }
+  else if (K <= 8) { ONMT_MERGE(8); }
+  else { ONMT_MERGE(16); }
 #undef ONMT_MERGE
 }
 
