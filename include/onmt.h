@@ -151,8 +151,8 @@ ONMT_API onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_src_ids,
  * onmt_set_option - tuning / measurement switches (name, integer value):
  *   "gemm_backend"  0 = tcgen05 tensor cores (bf16 models; default), 1 = SIMT FFMA
  *                   (always used for fp32 models).  Both compute the same sums.
- *   "profile"       1 = record CUDA events around every generator launch (see
- *                   onmt_get_kernel_time); 0 = off (default).
+ *   "profile"       1 = record CUDA events around every generator launch, 2 = around
+ *                   every kernel family (see onmt_get_kernel_time); 0 = off (default).
  *   "use_graph"     1 = replay the decode step as a CUDA graph (default), 0 = launch.
  * INVALID_ARG on an unknown name or value.
  */

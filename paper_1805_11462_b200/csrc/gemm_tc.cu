@@ -172,6 +172,11 @@ struct GenPArgs {
   StepCtl ctl;
   unsigned long long* dbg;   // optional timeline (%globaltimer) of CTA 0, debug builds only
 };
+#ifdef ONMT_GEN_TRACE
+#define GEN_DBG(stmt) stmt
+#else
+#define GEN_DBG(stmt)
+#endif
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -234,7 +239,7 @@ template <int KMAX>
 __device__ __noinline__ void group_update(const float* __restrict__ col, bool valid, int part, int vbase,
                                           float* __restrict__ st, int kk, unsigned long long* dbg) {
   constexpr float L2E = 1.4426950408889634f;
-  if (dbg) dbg[0] = gtimer();
+  GEN_DBG(if (dbg) dbg[0] = gtimer();)
   float m = valid ? st[0] : -INFINITY;
   float s = valid ? st[1] : 0.f;
   float z[32];
@@ -263,7 +268,7 @@ __device__ __noinline__ void group_update(const float* __restrict__ col, bool va
     st[0] = mn;
     st[1] = (m == -INFINITY ? 0.f : s * ex2((m - mn) * L2E)) + ls;
   }
-  if (dbg) dbg[1] = gtimer();
+  GEN_DBG(if (dbg) dbg[1] = gtimer();)
   // top-k: rounds of group-wide argmax over the 4 x 32 register-resident logits; a
   // round's winner enters the running list; stop when no group's winner can beat its
   // running k-th best (warm lists usually stop after one round)
@@ -316,12 +321,12 @@ __device__ __noinline__ void group_update(const float* __restrict__ col, bool va
 #pragma unroll
     for (int i = 0; i < 32; ++i) z[i] = i == mine ? -INFINITY : z[i];
   }
-  if (dbg) dbg[2] = gtimer();
-  if (dbg) dbg[3] = gtimer();
-  if (!valid || part != 0 || !dirty) { if (dbg) dbg[4] = gtimer(); return; }
+  GEN_DBG(if (dbg) dbg[2] = gtimer();)
+  GEN_DBG(if (dbg) dbg[3] = gtimer();)
+  if (!valid || part != 0 || !dirty) { GEN_DBG(if (dbg) dbg[4] = gtimer();) return; }
 #pragma unroll
   for (int q = 0; q < KMAX; ++q) { st[2 + q] = rz[q]; st[2 + KMAX + q] = __int_as_float(ri[q]); }
-  if (dbg) dbg[4] = gtimer();
+  GEN_DBG(if (dbg) dbg[4] = gtimer();)
 }
 
 template <int KMAX>
@@ -348,7 +353,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
   const int ntiles = t1 - t0;
   const int n0 = grp * a.n_group;
 
-  if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) a.dbg[200] = gtimer();
+  GEN_DBG(if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) a.dbg[200] = gtimer();)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
@@ -376,7 +381,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
         for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
           const int s = it % a.stages;
           if (it >= a.stages) mbar_wait(&empty[s], ((it / a.stages) & 1) ^ 1);
-          if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it] = gtimer();
+          GEN_DBG(if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it] = gtimer();)
           uint8_t* st = smem + s * stage_bytes;
           mbar_arrive_expect_tx(&full[s], stage_bytes);
           tma_load_2d(st, &tmW, kb * kBK, m0, &full[s]);
@@ -398,7 +403,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
         for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
           const int s = it % a.stages;
           mbar_wait(&full[s], (it / a.stages) & 1);
-          if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[64 + it] = gtimer();
+          GEN_DBG(if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[64 + it] = gtimer();)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
           const uint32_t sbh = sa + a_bytes, sbl = sa + a_bytes + b_bytes;
@@ -411,7 +416,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
           tc_commit(&empty[s]);
         }
         tc_commit(&tfull[acc]);
-        if (a.dbg && blockIdx.x == 0 && j < 8) a.dbg[128 + j] = gtimer();
+        GEN_DBG(if (a.dbg && blockIdx.x == 0 && j < 8) a.dbg[128 + j] = gtimer();)
       }
     }
     __syncwarp();
@@ -433,7 +438,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
       const int acc = j & 1;
       const int vt = t0 + j;
       mbar_wait(&tfull[acc], (j >> 1) & 1);
-      if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8) a.dbg[144 + j] = gtimer();
+      GEN_DBG(if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8) a.dbg[144 + j] = gtimer();)
       tc_fence_after();
       const int vid = vt * kTileM + vr;
       const float bias = vid < g.V ? g.bias[vid] : -INFINITY;
@@ -454,13 +459,17 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
         named_bar(1, 256);
-        if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[160 + 2 * j + h] = gtimer();
+        GEN_DBG(if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[160 + 2 * j + h] = gtimer();)
         const int c = cbeg + gcol;
         const bool valid = c < cend && n0 + c < g.rows_valid;
+#ifdef ONMT_GEN_TRACE
         unsigned long long* gd = (a.dbg && blockIdx.x == 0 && et == 0 && j < 2 && h < 2) ? a.dbg + 210 + 8 * (2 * j + h) : nullptr;
+#else
+        unsigned long long* gd = nullptr;
+#endif
         group_update<KMAX>(stg + gcol * kSLD, valid, part, vt * kTileM, rstate + (size_t)min(c, a.n_group - 1) * SW, g.K, gd);
         named_bar(1, 256);
-        if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[176 + 2 * j + h] = gtimer();
+        GEN_DBG(if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[176 + 2 * j + h] = gtimer();)
       }
     }
     for (int c = et; c < a.n_group; c += 256) {
@@ -474,7 +483,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
   }
   tc_fence_before();
   __syncthreads();
-  if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) { a.dbg[201] = gtimer(); a.dbg[202] = ntiles; a.dbg[203] = a.stages; }
+  GEN_DBG(if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) { a.dbg[201] = gtimer(); a.dbg[202] = ntiles; a.dbg[203] = a.stages; })
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 

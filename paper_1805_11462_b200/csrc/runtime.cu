@@ -264,7 +264,7 @@ struct onmt_model {
   int L = 0, E = 0, H = 0, Hd = 0, Vs = 0, Vt = 0, D = 1;
   bool bidir = false, general = false;
   bool use_tc = false;       // tcgen05 GEMM backend (bf16 models)
-  bool profile = false;
+  int profile = 0;             // 0 off, 1 generator launches only, 2 every kernel family
   bool use_graph = true;
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -337,15 +337,18 @@ static int gemm(onmt_model* m, const Mat& W, const Act& X, int n_valid, int spli
 
 // ---- per-kernel-family CUDA-event timing (profile mode); inside stream capture the events
 // become external event-record nodes of the cached graph
+static bool prof_on(onmt_model* m, const char* name) {
+  return m->profile >= 2 || (m->profile == 1 && std::strcmp(name, "gen") == 0);
+}
 static EvPair prof_begin(onmt_model* m, const char* name) {
   EvPair ev{};
-  if (!m->profile) return ev;
+  if (!prof_on(m, name)) return ev;
   ev = m->evs[name].acquire();
   ev_record(ev.a, m->stream, m->capturing);
   return ev;
 }
 static void prof_end(onmt_model* m, const char* name, const EvPair& ev) {
-  if (!m->profile) return;
+  if (!prof_on(m, name)) return;
   ev_record(ev.b, m->stream, m->capturing);
   if (m->capturing) m->graph.ev_nodes.push_back({name, ev});
   else m->evs[name].pending.push_back({ev, true});
@@ -908,7 +911,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     if (v != 0 && v != 1) return fail(ONMT_E_INVALID_ARG, "gemm_backend must be 0 or 1");
     m->use_tc = (v == 0) && m->prec == ONMT_PREC_BF16;
   } else if (n == "profile") {
-    m->profile = v != 0;
+    if (v < 0 || v > 2) return fail(ONMT_E_INVALID_ARG, "profile must be 0, 1 or 2");
+    m->profile = (int)v;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
   } else {
