@@ -153,7 +153,10 @@ ONMT_API onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_src_ids,
  *                   (always used for fp32 models).  Both compute the same sums.
  *   "profile"       1 = record CUDA events around every generator launch, 2 = around
  *                   every kernel family (see onmt_get_kernel_time); 0 = off (default).
- *   "use_graph"     1 = replay the decode step as a CUDA graph (default), 0 = launch.
+ *   "use_graph"     1 = replay the whole translation as one cached CUDA graph (default),
+ *                   0 = launch every kernel directly (profilers that cannot replay graph nodes).
+ *   "gen_multicast" 1 = share the generator's activation tiles across 4-CTA clusters by
+ *                   TMA multicast; 0 = off (default; measured slower at c2).
  * INVALID_ARG on an unknown name or value.
  */
 ONMT_API onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t value);

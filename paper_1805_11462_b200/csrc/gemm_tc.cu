@@ -16,6 +16,8 @@
 //   MODE_GEN:     generator (PAPER.md P118-119 softmax layer): logits z = D + b for 128
 //                 vocabulary rows never leave the SM; per (tile, row) the kernel emits
 //                 the online (max, sum exp) and the tile top-k by logit (DESIGN.md §6 K6).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -171,6 +173,7 @@ struct GenPArgs {
   int sc;         // staged columns per pass (n_group or half of it)
   StepCtl ctl;
   unsigned long long* dbg;   // optional timeline (%globaltimer) of CTA 0, debug builds only
+  int epi_mode;              // ablation (ONMT_GEN_EPI_MODE): 0 full, 1 stage only, 2 drain only
 };
 #ifdef ONMT_GEN_TRACE
 #define GEN_DBG(stmt) stmt
@@ -194,8 +197,11 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 // ---- epilogue building blocks (4 lanes per hypothesis row, 32 logits each per tile)
-constexpr int kColsPerPass = 64;   // 8 epilogue warps x 8 rows
-constexpr int kSLD = 132;          // staging row stride: (row*132 + lane part) hits distinct banks
+constexpr int kEpiWarps = 16;      // epilogue warps (4 per SMSP)
+constexpr int kLPR = 8;            // lanes per hypothesis row
+constexpr int kVPL = kTileM / kLPR;  // logits per lane per tile (16)
+constexpr int kColsPerPass = kEpiWarps * 32 / kLPR;   // 64 rows per pass
+constexpr int kSLD = 136;          // staging row stride: (row*136 + part) % 32 distinct across a warp
 
 // branch-free sorted insertion of (x, xi) into a (z desc, id asc) list
 template <int KMAX>
@@ -236,103 +242,132 @@ __device__ __forceinline__ void list_shift_pop(float (&z)[KMAX], int (&id)[KMAX]
 }
 
 template <int KMAX>
-__device__ __noinline__ void group_update(const float* __restrict__ col, bool valid, int part, int vbase,
-                                          float* __restrict__ st, int kk, unsigned long long* dbg) {
+__device__ __forceinline__ void group_update(const float* __restrict__ col, bool valid, int part, int vbase,
+                                             float* __restrict__ st, int kk, unsigned char* __restrict__ cbuf,
+                                             unsigned long long* dbg) {
   constexpr float L2E = 1.4426950408889634f;
   GEN_DBG(if (dbg) dbg[0] = gtimer();)
+  const unsigned FULL = 0xffffffffu;
+  const int gbase = (threadIdx.x & 31) & ~(kLPR - 1);     // first lane of this row's group
   float m = valid ? st[0] : -INFINITY;
   float s = valid ? st[1] : 0.f;
-  float z[32];
+  float z[kVPL];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) z[i] = valid ? col[part + 4 * i] : -INFINITY;
+  for (int i = 0; i < kVPL; ++i) z[i] = valid ? col[part + kLPR * i] : -INFINITY;
   float own = -INFINITY;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) own = fmaxf(own, z[i]);
-  float lm = fmaxf(own, __shfl_xor_sync(0xffffffffu, own, 1));
-  lm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, 2));
+  for (int i = 0; i < kVPL; ++i) own = fmaxf(own, z[i]);
+  float lm = own;
+#pragma unroll
+  for (int lvl = 1; lvl < kLPR; lvl <<= 1) lm = fmaxf(lm, __shfl_xor_sync(FULL, lm, lvl));
   const float mn = fmaxf(m, lm);
   float ls = 0.f;
   if (mn != -INFINITY) {
     const float mo = mn * L2E;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; i += 4) {
+    for (int i = 0; i < kVPL; i += 4) {
       a0 += ex2(fmaf(z[i], L2E, -mo)); a1 += ex2(fmaf(z[i + 1], L2E, -mo));
       a2 += ex2(fmaf(z[i + 2], L2E, -mo)); a3 += ex2(fmaf(z[i + 3], L2E, -mo));
     }
     ls = (a0 + a1) + (a2 + a3);
   }
-  ls += __shfl_xor_sync(0xffffffffu, ls, 1);
-  ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+#pragma unroll
+  for (int lvl = 1; lvl < kLPR; lvl <<= 1) ls += __shfl_xor_sync(FULL, ls, lvl);
   if (valid && part == 0 && mn != -INFINITY) {
     st[0] = mn;
     st[1] = (m == -INFINITY ? 0.f : s * ex2((m - mn) * L2E)) + ls;
   }
   GEN_DBG(if (dbg) dbg[1] = gtimer();)
-  // top-k: rounds of group-wide argmax over the 4 x 32 register-resident logits; a
-  // round's winner enters the running list; stop when no group's winner can beat its
-  // running k-th best (warm lists usually stop after one round)
+  // ---- top-k by threshold filtering.  The running list (right-aligned, +inf sentinels in
+  // the first KMAX-K slots) is owned by the row leader (part 0).  theta = max(running K-th
+  // best, K-th largest of the kLPR lane maxima) is a lower bound of the K-th best of
+  // (running list U tile): both are K-th bests of subsets of that union.  Only logits
+  // >= theta can enter; they are shuffled to the leader and inserted.
+  const int K = kk;
   float rz[KMAX];
   int ri[KMAX];
+  if (part == 0) {
 #pragma unroll
-  for (int q = 0; q < KMAX; ++q) { rz[q] = valid ? st[2 + q] : INFINITY; ri[q] = valid ? __float_as_int(st[2 + KMAX + q]) : 0; }
-  bool dirty = false;
-  const int K = kk;
-#pragma unroll 1
-  for (int round = 0; round < K; ++round) {
-    // the K-th running entry (static-index select keeps the list in registers)
-    float tk = rz[0];
-    int tki = ri[0];
+    for (int q = 0; q < KMAX; ++q) { rz[q] = valid ? st[2 + q] : INFINITY; ri[q] = valid ? __float_as_int(st[2 + KMAX + q]) : 0; }
+  }
+  const float tk = __shfl_sync(FULL, part == 0 ? rz[KMAX - 1] : 0.f, gbase);
+  float theta = tk;
+  if (K <= 2 * kLPR) {
+    // K-th largest of the 2*kLPR lane top-2 values (elements of the tile, so a lower bound
+    // of the tile's K-th best): count, for each of my two values, how many of the group's
+    // 16 values beat it ((value, lane, slot) order breaks ties)
+    float m1 = -INFINITY, m2 = -INFINITY;
 #pragma unroll
-    for (int q = 1; q < KMAX; ++q) if (q == K - 1) { tk = rz[q]; tki = ri[q]; }
-    // lane argmax by a depth-5 tree over (value, index); left subtrees hold lower indices
-    float tv[16];
-    int tx[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const bool l = z[2 * i] >= z[2 * i + 1];
-      tv[i] = l ? z[2 * i] : z[2 * i + 1];
-      tx[i] = l ? 2 * i : 2 * i + 1;
+    for (int i = 0; i < kVPL; ++i) {
+      const float v = z[i];
+      m2 = fmaxf(m2, fminf(m1, v));
+      m1 = fmaxf(m1, v);
     }
+    int r1 = 1, r2 = 0;                          // m1 beats m2 of the same lane (slot order)
 #pragma unroll
-    for (int w = 8; w >= 1; w >>= 1) {
+    for (int o = 1; o < kLPR; ++o) {
+      const int src = gbase + ((part + o) & (kLPR - 1));
+      const int op = (part + o) & (kLPR - 1);
+      const float o1 = __shfl_sync(FULL, m1, src), o2 = __shfl_sync(FULL, m2, src);
+      r1 += (o1 > m1 || (o1 == m1 && op < part)) + (o2 > m1 || (o2 == m1 && op < part));
+      r2 += (o1 > m2 || (o1 == m2 && op < part)) + (o2 > m2 || (o2 == m2 && op < part));
+    }
+    r1 -= 1;                                     // (m1 itself was pre-counted above; keep rank = #greater)
+    r2 += (m1 > m2 || m1 == m2);                 // own m1 ranks ahead of own m2
+    const unsigned h1 = __ballot_sync(FULL, r1 == K - 1), h2 = __ballot_sync(FULL, r2 == K - 1);
+    const unsigned g1 = (h1 >> gbase) & ((1u << kLPR) - 1), g2 = (h2 >> gbase) & ((1u << kLPR) - 1);
+    const float k1 = __shfl_sync(FULL, m1, g1 ? gbase + __ffs(g1) - 1 : gbase);
+    const float k2 = __shfl_sync(FULL, m2, g2 ? gbase + __ffs(g2) - 1 : gbase);
+    const float kth = g1 ? k1 : (g2 ? k2 : -INFINITY);
+    theta = fmaxf(theta, kth);
+  }
+  unsigned cm = 0;
 #pragma unroll
-      for (int i = 0; i < w; ++i) {
-        const bool l = tv[2 * i] >= tv[2 * i + 1];
-        tv[i] = l ? tv[2 * i] : tv[2 * i + 1];
-        tx[i] = l ? tx[2 * i] : tx[2 * i + 1];
+  for (int i = 0; i < kVPL; ++i) cm |= (valid && z[i] >= theta && z[i] >= tk) ? (1u << i) : 0u;
+  // compact the group's candidate offsets (0..127 within the tile row) into cbuf, then
+  // the leader inserts only real candidates
+  const int cnt = __popc(cm);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < kLPR; o <<= 1) {
+    const int v = __shfl_up_sync(FULL, incl, o);
+    if (part >= o) incl += v;
+  }
+  const int total = __shfl_sync(FULL, incl, gbase + kLPR - 1);
+  int pos = incl - cnt;
+  while (cm) {
+    const int i = __ffs(cm) - 1;
+    cm &= cm - 1;
+    cbuf[pos++] = (unsigned char)(part + kLPR * i);
+  }
+  __syncwarp();
+  bool dirty = false;
+  if (part == 0) {
+    for (int c = 0; c < total; ++c) {
+      const int off = cbuf[c];
+      const float zc = col[off];
+      const int idc = vbase + off;
+      if (better(zc, idc, rz[KMAX - 1], ri[KMAX - 1])) {
+        list_insert<KMAX>(rz, ri, zc, idc);
+        dirty = true;
       }
     }
-    float bm = tv[0];
-    int bid = bm == -INFINITY ? 0x7fffffff : vbase + part + 4 * tx[0];
-    // group argmax (z desc, id asc) over the 4 lanes
-#pragma unroll
-    for (int lvl = 1; lvl <= 2; lvl <<= 1) {
-      const float oz = __shfl_xor_sync(0xffffffffu, bm, lvl);
-      const int oi = __shfl_xor_sync(0xffffffffu, bid, lvl);
-      if (better(oz, oi, bm, bid)) { bm = oz; bid = oi; }
-    }
-    const bool take = better(bm, bid, tk, tki);
-    if (!__any_sync(0xffffffffu, take)) break;
-    if (take) { list_insert<KMAX>(rz, ri, bm, bid); dirty = true; }
-    // the owner lane removes the winner from its registers
-    const bool own_it = bid != 0x7fffffff && ((bid - vbase) & 3) == part;
-    const int mine = own_it ? (bid - vbase - part) >> 2 : -1;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) z[i] = i == mine ? -INFINITY : z[i];
   }
+  __syncwarp();
   GEN_DBG(if (dbg) dbg[2] = gtimer();)
-  GEN_DBG(if (dbg) dbg[3] = gtimer();)
-  if (!valid || part != 0 || !dirty) { GEN_DBG(if (dbg) dbg[4] = gtimer();) return; }
+  if (!valid || part != 0 || !dirty) return;
 #pragma unroll
   for (int q = 0; q < KMAX; ++q) { st[2 + q] = rz[q]; st[2 + KMAX + q] = __int_as_float(ri[q]); }
-  GEN_DBG(if (dbg) dbg[4] = gtimer();)
 }
 
-template <int KMAX>
-__global__ void __launch_bounds__(320, 1)
+template <int KMAX, int CS>
+__global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
 gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GenPArgs a,
                       GenOut g) {
+  // CS > 1: thread-block cluster of CS CTAs sharing the activation (B) tiles by TMA
+  // multicast - CTA rank r loads rows [r*n_group/CS, (r+1)*n_group/CS) of each B tile for
+  // all CS CTAs - so the B operand crosses L2 -> SM once per cluster instead of once per CTA.
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -341,7 +376,8 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
   float* stg = reinterpret_cast<float*>(smem + a.stages * stage_bytes);
   float* rstate = stg + (size_t)kColsPerPass * kSLD;            // [n_group][2 + 2*KMAX]
   constexpr int SW = 2 + 2 * KMAX;
-  uint64_t* full = reinterpret_cast<uint64_t*>(rstate + (size_t)a.n_group * SW);
+  unsigned char* cbufs = reinterpret_cast<unsigned char*>(rstate + (size_t)a.n_group * SW);   // [64][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(cbufs + kColsPerPass * kTileM);
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
   uint64_t* tempty = tfull + 2;
@@ -349,16 +385,22 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = blockIdx.x / a.C, ci = blockIdx.x % a.C;
-  const int t0 = (int)((long long)ci * a.n_vt / a.C), t1 = (int)((long long)(ci + 1) * a.n_vt / a.C);
-  const int ntiles = t1 - t0;
+  const int rank = CS > 1 ? (int)cluster_ctarank() : 0;
+  const int Q = a.C / CS, qi = ci / CS;                       // cluster index within the group
+  const int tb = (int)((long long)qi * a.n_vt / Q), te = (int)((long long)(qi + 1) * a.n_vt / Q);
+  const int rounds = (te - tb + CS - 1) / CS;                 // lock-step rounds of the cluster
+  const int ntiles = max(0, (te - tb - rank + CS - 1) / CS);  // this CTA's real tiles: tb + rank + CS*j
   const int n0 = grp * a.n_group;
+  const uint16_t cmask = (uint16_t)((1u << CS) - 1);
+  const int slice_rows = a.n_group / CS;
+  const uint32_t slice_bytes = slice_rows * 128;
 
   GEN_DBG(if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) a.dbg[200] = gtimer();)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
-    for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+    for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CS); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kEpiWarps); }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -367,26 +409,36 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  if (all_done(a.ctl)) {
+  if (all_done(a.ctl)) {                     // uniform over the grid: no cluster traffic happened yet
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
     return;
   }
+  if (CS > 1) cluster_sync_all();            // peers' barriers initialised before any multicast
 
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
-      for (int j = 0; j < ntiles; ++j) {
-        const int m0 = (t0 + j) * kTileM;
+      for (int j = 0; j < rounds; ++j) {
+        const bool has = tb + rank + CS * j < te;
+        const int m0 = (tb + rank + CS * j) * kTileM;
         for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
           const int s = it % a.stages;
           if (it >= a.stages) mbar_wait(&empty[s], ((it / a.stages) & 1) ^ 1);
           GEN_DBG(if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it] = gtimer();)
           uint8_t* st = smem + s * stage_bytes;
-          mbar_arrive_expect_tx(&full[s], stage_bytes);
-          tma_load_2d(st, &tmW, kb * kBK, m0, &full[s]);
-          tma_load_2d(st + a_bytes, &tmX, kb * kBK, n0, &full[s]);
-          tma_load_2d(st + a_bytes + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[s]);
+          const bool ldA = has && a.epi_mode != 4, ldB = a.epi_mode != 3;   // (ablation modes 3/4)
+          mbar_arrive_expect_tx(&full[s], (ldA ? a_bytes : 0u) + (ldB ? 2 * b_bytes : 0u));
+          if (ldA) tma_load_2d(st, &tmW, kb * kBK, m0, &full[s]);
+          if (!ldB) {
+          } else if (CS > 1) {
+            tma_load_2d_mc(st + a_bytes + rank * slice_bytes, &tmX, kb * kBK, n0 + rank * slice_rows, &full[s], cmask);
+            tma_load_2d_mc(st + a_bytes + b_bytes + rank * slice_bytes, &tmX, kb * kBK,
+                           a.n_rows_pad + n0 + rank * slice_rows, &full[s], cmask);
+          } else {
+            tma_load_2d(st + a_bytes, &tmX, kb * kBK, n0, &full[s]);
+            tma_load_2d(st + a_bytes + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[s]);
+          }
         }
       }
     }
@@ -394,10 +446,11 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_group);
-      int it = 0;
-      for (int j = 0; j < ntiles; ++j) {
-        const int acc = j & 1;
-        if (j >= 2) mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+      int it = 0, jj = 0;
+      for (int j = 0; j < rounds; ++j) {
+        const bool has = tb + rank + CS * j < te;
+        const int acc = jj & 1;
+        if (has && jj >= 2) mbar_wait(&tempty[acc], ((jj >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * 256;
         for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
@@ -405,38 +458,49 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
           mbar_wait(&full[s], (it / a.stages) & 1);
           GEN_DBG(if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[64 + it] = gtimer();)
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * stage_bytes);
-          const uint32_t sbh = sa + a_bytes, sbl = sa + a_bytes + b_bytes;
+          if (has && a.epi_mode != 5) {
+            const uint32_t sa = smem_u32(smem + s * stage_bytes);
+            const uint32_t sbh = sa + a_bytes, sbl = sa + a_bytes + b_bytes;
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint64_t da = umma_desc_sw128(sa + kk * 32);
-            tc_mma_bf16(d, da, umma_desc_sw128(sbh + kk * 32), idesc, (kb | kk) != 0);
-            tc_mma_bf16(d, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              const uint64_t da = umma_desc_sw128(sa + kk * 32);
+              tc_mma_bf16(d, da, umma_desc_sw128(sbh + kk * 32), idesc, (kb | kk) != 0);
+              tc_mma_bf16(d, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
+            }
           }
-          tc_commit(&empty[s]);
+          if (CS > 1) tc_commit_mc(&empty[s], cmask);      // stage s free in every peer's view
+          else tc_commit(&empty[s]);
         }
-        tc_commit(&tfull[acc]);
-        GEN_DBG(if (a.dbg && blockIdx.x == 0 && j < 8) a.dbg[128 + j] = gtimer();)
+        if (has) {
+          tc_commit(&tfull[acc]);
+          GEN_DBG(if (a.dbg && blockIdx.x == 0 && jj < 8) a.dbg[128 + jj] = gtimer();)
+          ++jj;
+        }
       }
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue warps 2..9
-    const int et = threadIdx.x - 64;                     // 0..255
-    const int q = warp & 3, par = (warp - 2) >> 2;       // TMEM quarter, column-chunk parity
+    // ---------------- epilogue warps 2..(2+kEpiWarps)
+    const int et = threadIdx.x - 64;                     // 0..32*kEpiWarps-1
+    const int q = warp & 3, par = (warp - 2) >> 2;       // TMEM quarter, column-chunk index (0..3)
     const int vr = q * 32 + lane;                        // vocabulary row (TMEM lane) this thread drains
-    const int gcol = (et >> 5) * 8 + (lane >> 2);        // row (column) within a pass, 0..63
-    const int part = lane & 3;
+    const int gcol = (et >> 5) * (32 / kLPR) + lane / kLPR;   // row (column) within a pass
+    const int part = lane % kLPR;
+    constexpr int kNPar = kEpiWarps / 4;                 // warps sharing one TMEM lane quarter
     const int npass = (a.n_group + kColsPerPass - 1) / kColsPerPass;
-    for (int i = et; i < a.n_group; i += 256) {
+    for (int i = et; i < a.n_group; i += 32 * kEpiWarps) {
       float* st = rstate + (size_t)i * SW;
       st[0] = -INFINITY; st[1] = 0.f;
-      for (int qq = 0; qq < KMAX; ++qq) { st[2 + qq] = -INFINITY; st[2 + KMAX + qq] = __int_as_float(0x7fffffff); }
+      for (int qq = 0; qq < KMAX; ++qq) {
+        const bool sentinel = qq < KMAX - g.K;
+        st[2 + qq] = sentinel ? INFINITY : -INFINITY;
+        st[2 + KMAX + qq] = __int_as_float(sentinel ? -1 : 0x7fffffff);
+      }
     }
-    named_bar(1, 256);
+    named_bar(1, 32 * kEpiWarps);
     for (int j = 0; j < ntiles; ++j) {
       const int acc = j & 1;
-      const int vt = t0 + j;
+      const int vt = tb + rank + CS * j;
       mbar_wait(&tfull[acc], (j >> 1) & 1);
       GEN_DBG(if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8) a.dbg[144 + j] = gtimer();)
       tc_fence_after();
@@ -447,7 +511,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
       for (int h = 0; h < npass; ++h) {
         const int cbeg = h * kColsPerPass;
         const int cend = min(a.n_group, cbeg + kColsPerPass);
-        for (int c0 = cbeg + par * 16; c0 < cend; c0 += 32) {
+        for (int c0 = cbeg + par * 16; c0 < cend && a.epi_mode != 2 && a.epi_mode < 3 && a.epi_mode != 5; c0 += 16 * kNPar) {
           float v[16];
           tmem_ld16(trow + c0, v);
 #pragma unroll
@@ -458,7 +522,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        named_bar(1, 256);
+        named_bar(1, 32 * kEpiWarps);
         GEN_DBG(if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[160 + 2 * j + h] = gtimer();)
         const int c = cbeg + gcol;
         const bool valid = c < cend && n0 + c < g.rows_valid;
@@ -467,62 +531,91 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
 #else
         unsigned long long* gd = nullptr;
 #endif
-        group_update<KMAX>(stg + gcol * kSLD, valid, part, vt * kTileM, rstate + (size_t)min(c, a.n_group - 1) * SW, g.K, gd);
-        named_bar(1, 256);
+        if (a.epi_mode == 0)
+          group_update<KMAX>(stg + gcol * kSLD, valid, part, vt * kTileM, rstate + (size_t)min(c, a.n_group - 1) * SW, g.K, cbufs + gcol * kTileM, gd);
+        named_bar(1, 32 * kEpiWarps);
         GEN_DBG(if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[176 + 2 * j + h] = gtimer();)
       }
     }
-    for (int c = et; c < a.n_group; c += 256) {
+    for (int c = et; c < a.n_group; c += 32 * kEpiWarps) {
       const int r = n0 + c;
       if (r >= g.rows_valid) continue;
       const float* st = rstate + (size_t)c * SW;
       g.ms[(size_t)ci * g.rows_pad + r] = make_float2(st[0], st[1]);
       const size_t base = ((size_t)ci * g.rows_pad + r) * g.K;
-      for (int qq = 0; qq < g.K; ++qq) { g.tz[base + qq] = st[2 + qq]; g.ti[base + qq] = __float_as_int(st[2 + KMAX + qq]); }
+      for (int qq = 0; qq < g.K; ++qq) {
+        g.tz[base + qq] = st[2 + KMAX - g.K + qq];
+        g.ti[base + qq] = __float_as_int(st[2 + 2 * KMAX - g.K + qq]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (CS > 1) cluster_sync_all();            // no peer may still multicast into / arrive on us
   GEN_DBG(if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) { a.dbg[201] = gtimer(); a.dbg[202] = ntiles; a.dbg[203] = a.stages; })
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 static size_t genp_smem_bytes(int n_group, int stages, int kmax) {
   return 1024 + (size_t)stages * (kTileM * 128 + 2 * (size_t)n_group * 128) + (size_t)kColsPerPass * kSLD * 4 +
-         (size_t)n_group * (2 + 2 * kmax) * 4 + (2 * stages + 4) * 8 + 16;
+         (size_t)n_group * (2 + 2 * kmax) * 4 + kColsPerPass * kTileM + (2 * stages + 4) * 8 + 16;
 }
 
-// number of partials per row the persistent generator writes (C)
-int gen_persistent_parts(int n_vt, int n_groups, int num_sms) {
+// cluster size for the activation multicast (1 = off): needs n_group % (8*CS) == 0
+int gen_cluster_size(int n_group, int n_vt, int n_groups, int num_sms) {
+  const int cs = 4;
+  if (n_group % (8 * cs) != 0) return 1;
+  if (num_sms / n_groups < cs || n_vt < cs) return 1;
+  return cs;
+}
+
+// number of partials per row the persistent generator writes (C = CTAs per N-group)
+int gen_persistent_parts(int n_vt, int n_groups, int num_sms, int cs) {
   int C = num_sms / n_groups;
-  if (C < 1) C = 1;
   if (C > n_vt) C = n_vt;
+  C = C / cs * cs;
+  if (C < cs) C = cs;
   return C;
 }
 
-template <int KMAX>
+template <int KMAX, int CS>
 static cudaError_t launch_genp(const CUtensorMap& tmW, const CUtensorMap& tmX, const GenPArgs& a, const GenOut& g,
                                int grid, cudaStream_t st) {
   size_t smem = genp_smem_bytes(a.n_group, a.stages, KMAX);
-  auto fn = gen_persistent_kernel<KMAX>;
+  auto fn = gen_persistent_kernel<KMAX, CS>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(fn, dim3(grid), dim3(320), smem, st, tmW, tmX, a, g);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(64 + 32 * kEpiWarps);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CS;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, fn, tmW, tmX, a, g);
 }
 
 unsigned long long* g_gen_dbg = nullptr;   // set by the runtime when ONMT_GEN_TRACE is on
 
+// tmX: activation planes with box rows n_group (CS = 1) or n_group / CS (multicast slices)
 cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
-                              int k_blocks, int num_sms, const GenOut& g, StepCtl ctl, cudaStream_t st) {
+                              int k_blocks, int num_sms, int cs, const GenOut& g, StepCtl ctl, cudaStream_t st) {
   GenPArgs a{};
   a.dbg = g_gen_dbg;
+  if (const char* em = std::getenv("ONMT_GEN_EPI_MODE")) a.epi_mode = std::atoi(em);
   a.n_rows_pad = n_rows_pad;
   a.n_group = n_group;
   a.k_blocks = k_blocks;
   a.n_vt = n_vt;
   const int groups = n_rows_pad / n_group;
-  a.C = gen_persistent_parts(n_vt, groups, num_sms);
+  a.C = gen_persistent_parts(n_vt, groups, num_sms, cs);
   a.ctl = ctl;
   const size_t limit = 227 * 1024;
   const int kmax = g.K <= 1 ? 1 : g.K <= 2 ? 2 : g.K <= 4 ? 4 : g.K <= 8 ? 8 : 16;
@@ -533,11 +626,14 @@ cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, in
   a.stages = stages;
   if (genp_smem_bytes(n_group, stages, kmax) > limit) return cudaErrorInvalidConfiguration;
   const int grid = a.C * groups;
-  if (g.K <= 1) return launch_genp<1>(tmW, tmX, a, g, grid, st);
-  if (g.K <= 2) return launch_genp<2>(tmW, tmX, a, g, grid, st);
-  if (g.K <= 4) return launch_genp<4>(tmW, tmX, a, g, grid, st);
-  if (g.K <= 8) return launch_genp<8>(tmW, tmX, a, g, grid, st);
-  return launch_genp<16>(tmW, tmX, a, g, grid, st);
+#define ONMT_GENP(KM)                                                     \
+  return cs == 4 ? launch_genp<KM, 4>(tmW, tmX, a, g, grid, st) : launch_genp<KM, 1>(tmW, tmX, a, g, grid, st)
+  if (g.K <= 1) ONMT_GENP(1);
+  if (g.K <= 2) ONMT_GENP(2);
+  if (g.K <= 4) ONMT_GENP(4);
+  if (g.K <= 8) ONMT_GENP(8);
+  ONMT_GENP(16);
+#undef ONMT_GENP
 }
 
 // ------------------------------------------------------------------ host launchers

@@ -34,8 +34,9 @@ cudaError_t tc_gemm_partial(const CUtensorMap& tmW, const CUtensorMap& tmX, int 
 cudaError_t tc_gemm_gen(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                         int k_blocks, const GenOut& g, StepCtl ctl, cudaStream_t st);
 cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
-                              int k_blocks, int num_sms, const GenOut& g, StepCtl ctl, cudaStream_t st);
-int gen_persistent_parts(int n_vt, int n_groups, int num_sms);
+                              int k_blocks, int num_sms, int cs, const GenOut& g, StepCtl ctl, cudaStream_t st);
+int gen_persistent_parts(int n_vt, int n_groups, int num_sms, int cs);
+int gen_cluster_size(int n_group, int n_vt, int n_groups, int num_sms);
 extern unsigned long long* g_gen_dbg;
 
 cudaError_t simt_gemm_partial(const void* W, bool w_bf16, int m_pad, int k_pad, const float* X, int n_rows_pad,
@@ -178,7 +179,7 @@ struct Act {
   int rows = 0, rows_pad = 0, n_group = 0, k = 0, k_pad = 0;
   bool bf16 = false;
   DevBuf f32, hl;
-  CUtensorMap tmap;
+  CUtensorMap tmap, tmap_q;   // box rows n_group / box rows n_group/4 (generator multicast slices)
   void ensure(int rows_, int k_, bool bf) {
     RowPlan rp = plan_rows(rows_);
     int kp = round_up(k_, kBK);
@@ -190,6 +191,7 @@ struct Act {
       hl.ensure((size_t)2 * rows_pad * k_pad * 2);
       ONMT_CUDA(cudaMemset(hl.p, 0, (size_t)2 * rows_pad * k_pad * 2));
       tmap = make_tmap(hl.p, k_pad, 2 * rows_pad, n_group);
+      if (n_group % 32 == 0) tmap_q = make_tmap(hl.p, k_pad, 2 * rows_pad, n_group / 4);
     }
   }
   XOut xo(bool use_tc) const {
@@ -265,6 +267,7 @@ struct onmt_model {
   bool bidir = false, general = false;
   bool use_tc = false;       // tcgen05 GEMM backend (bf16 models)
   int profile = 0;             // 0 off, 1 generator launches only, 2 every kernel family
+  bool gen_mc = false;         // generator activation multicast across 4-CTA clusters (measured slower on c2)
   bool use_graph = true;
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -355,16 +358,21 @@ static void prof_end(onmt_model* m, const char* name, const EvPair& ev) {
 }
 
 // partials per row written by the generator for operand X
+static int gen_cs(onmt_model* m, const Act& X) {
+  const int n_vt = (m->Vt + kVTile - 1) / kVTile;
+  return m->gen_mc ? gen_cluster_size(X.n_group, n_vt, X.rows_pad / X.n_group, m->num_sms) : 1;
+}
 static int gen_parts(onmt_model* m, const Act& X) {
   const int n_vt = (m->Vt + kVTile - 1) / kVTile;
-  return m->use_tc ? gen_persistent_parts(n_vt, X.rows_pad / X.n_group, m->num_sms) : n_vt;
+  return m->use_tc ? gen_persistent_parts(n_vt, X.rows_pad / X.n_group, m->num_sms, gen_cs(m, X)) : n_vt;
 }
 
 static void gen(onmt_model* m, const Act& X, const GenOut& g, StepCtl ctl) {
   EvPair ev = prof_begin(m, "gen");
   if (m->use_tc) {
-    ONMT_CUDA(tc_gen_persistent(m->gen_w.tmap, X.tmap, m->gen_w.m_pad / kTileM, X.rows_pad, X.n_group,
-                                m->gen_w.k_pad / kBK, m->num_sms, g, ctl, m->stream));
+    const int cs = gen_cs(m, X);
+    ONMT_CUDA(tc_gen_persistent(m->gen_w.tmap, cs > 1 ? X.tmap_q : X.tmap, m->gen_w.m_pad / kTileM, X.rows_pad,
+                                X.n_group, m->gen_w.k_pad / kBK, m->num_sms, cs, g, ctl, m->stream));
     count(m);
   } else {
     m->logits.ensure((size_t)X.rows_pad * m->gen_w.m_pad * 4);
@@ -882,6 +890,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   m->use_tc = prec == ONMT_PREC_BF16;
   m->num_sms = prop.multiProcessorCount;
   if (const char* ev = std::getenv("ONMT_USE_GRAPH")) m->use_graph = std::atoi(ev) != 0;   // ncu runs use 0
+  if (const char* ev = std::getenv("ONMT_GEN_MULTICAST")) m->gen_mc = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
@@ -913,6 +922,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
   } else if (n == "profile") {
     if (v < 0 || v > 2) return fail(ONMT_E_INVALID_ARG, "profile must be 0, 1 or 2");
     m->profile = (int)v;
+  } else if (n == "gen_multicast") {
+    m->gen_mc = v != 0;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
   } else {
