@@ -197,11 +197,11 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 // ---- epilogue building blocks (4 lanes per hypothesis row, 32 logits each per tile)
-constexpr int kEpiWarps = 16;      // epilogue warps (4 per SMSP)
-constexpr int kLPR = 8;            // lanes per hypothesis row
-constexpr int kVPL = kTileM / kLPR;  // logits per lane per tile (16)
-constexpr int kColsPerPass = kEpiWarps * 32 / kLPR;   // 64 rows per pass
-constexpr int kSLD = 136;          // staging row stride: (row*136 + part) % 32 distinct across a warp
+constexpr int kEpiWarps = 10;      // epilogue warps
+constexpr int kLPR = 4;            // lanes per hypothesis row
+constexpr int kVPL = kTileM / kLPR;  // logits per lane per tile (32)
+constexpr int kColsPerPass = kEpiWarps * 32 / kLPR;   // 80 rows staged per pass
+constexpr int kSLD = 132;          // staging row stride: (row*132 + part) % 32 distinct across a warp
 
 // branch-free sorted insertion of (x, xi) into a (z desc, id asc) list
 template <int KMAX>
@@ -241,25 +241,43 @@ __device__ __forceinline__ void list_shift_pop(float (&z)[KMAX], int (&id)[KMAX]
   id[KMAX - 1] = 0x7fffffff;
 }
 
+// One row's update with one tile: the kLPR lanes of a row each hold kVPL logits in
+// registers (v = part + kLPR*i, increasing ids).  (max, sum exp) are combined by
+// shuffles; top-k by threshold filtering: theta = max(running K-th best, K-th largest of
+// the lanes' top-3 - computed on cold tiles only) is a lower bound of the K-th best of
+// (running list U tile) - both are K-th bests of subsets - so only logits >= theta can
+// enter; the leader (part 0) inserts the row's candidates (partner masks via shuffles,
+// values re-read from staging).  Scans use independent sub-chains for ILP.
+template <int KMAX>
+__device__ __forceinline__ void top3_merge(float& a1, float& a2, float& a3, float b1, float b2, float b3) {
+  // top-3 of two sorted triples
+  const float x1 = fmaxf(a1, b1);
+  const float y1 = fminf(a1, b1);                      // the other head
+  const float x2 = fmaxf(y1, fmaxf(a2, b2));
+  const float x3 = fmaxf(fminf(y1, fmaxf(a2, b2)), fmaxf(fminf(a2, b2), fmaxf(a3, b3)));
+  a1 = x1; a2 = x2; a3 = x3;
+}
+
 template <int KMAX>
 __device__ __forceinline__ void group_update(const float* __restrict__ col, bool valid, int part, int vbase,
-                                             float* __restrict__ st, int kk, unsigned char* __restrict__ cbuf,
-                                             unsigned long long* dbg) {
+                                             float* __restrict__ st, int K, unsigned long long* dbg) {
   constexpr float L2E = 1.4426950408889634f;
-  GEN_DBG(if (dbg) dbg[0] = gtimer();)
   const unsigned FULL = 0xffffffffu;
-  const int gbase = (threadIdx.x & 31) & ~(kLPR - 1);     // first lane of this row's group
-  float m = valid ? st[0] : -INFINITY;
-  float s = valid ? st[1] : 0.f;
+  const int gbase = (threadIdx.x & 31) & ~(kLPR - 1);
+  GEN_DBG(if (dbg) dbg[0] = gtimer();)
   float z[kVPL];
 #pragma unroll
   for (int i = 0; i < kVPL; ++i) z[i] = valid ? col[part + kLPR * i] : -INFINITY;
-  float own = -INFINITY;
+  // row max (4 independent chains)
+  float x0 = -INFINITY, x1 = -INFINITY, x2 = -INFINITY, x3 = -INFINITY;
 #pragma unroll
-  for (int i = 0; i < kVPL; ++i) own = fmaxf(own, z[i]);
-  float lm = own;
+  for (int i = 0; i < kVPL; i += 4) {
+    x0 = fmaxf(x0, z[i]); x1 = fmaxf(x1, z[i + 1]); x2 = fmaxf(x2, z[i + 2]); x3 = fmaxf(x3, z[i + 3]);
+  }
+  float lm = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
 #pragma unroll
   for (int lvl = 1; lvl < kLPR; lvl <<= 1) lm = fmaxf(lm, __shfl_xor_sync(FULL, lm, lvl));
+  const float m = valid ? st[0] : -INFINITY;
   const float mn = fmaxf(m, lm);
   float ls = 0.f;
   if (mn != -INFINITY) {
@@ -274,78 +292,70 @@ __device__ __forceinline__ void group_update(const float* __restrict__ col, bool
   }
 #pragma unroll
   for (int lvl = 1; lvl < kLPR; lvl <<= 1) ls += __shfl_xor_sync(FULL, ls, lvl);
-  if (valid && part == 0 && mn != -INFINITY) {
-    st[0] = mn;
-    st[1] = (m == -INFINITY ? 0.f : s * ex2((m - mn) * L2E)) + ls;
-  }
-  GEN_DBG(if (dbg) dbg[1] = gtimer();)
-  // ---- top-k by threshold filtering.  The running list (right-aligned, +inf sentinels in
-  // the first KMAX-K slots) is owned by the row leader (part 0).  theta = max(running K-th
-  // best, K-th largest of the kLPR lane maxima) is a lower bound of the K-th best of
-  // (running list U tile): both are K-th bests of subsets of that union.  Only logits
-  // >= theta can enter; they are shuffled to the leader and inserted.
-  const int K = kk;
   float rz[KMAX];
   int ri[KMAX];
-  if (part == 0) {
+  float tk = INFINITY;
+  if (valid && part == 0) {
+    const float s0 = st[1];
+    st[0] = mn;
+    st[1] = (m == -INFINITY ? 0.f : s0 * ex2((m - mn) * L2E)) + ls;
 #pragma unroll
-    for (int q = 0; q < KMAX; ++q) { rz[q] = valid ? st[2 + q] : INFINITY; ri[q] = valid ? __float_as_int(st[2 + KMAX + q]) : 0; }
+    for (int q = 0; q < KMAX; ++q) { rz[q] = st[2 + q]; ri[q] = __float_as_int(st[2 + KMAX + q]); }
+    tk = rz[KMAX - 1];
   }
-  const float tk = __shfl_sync(FULL, part == 0 ? rz[KMAX - 1] : 0.f, gbase);
+  tk = __shfl_sync(FULL, tk, gbase);
   float theta = tk;
-  if (K <= 2 * kLPR) {
-    // K-th largest of the 2*kLPR lane top-2 values (elements of the tile, so a lower bound
-    // of the tile's K-th best): count, for each of my two values, how many of the group's
-    // 16 values beat it ((value, lane, slot) order breaks ties)
-    float m1 = -INFINITY, m2 = -INFINITY;
+  GEN_DBG(if (dbg) dbg[1] = gtimer();)
+  if (__any_sync(FULL, tk == -INFINITY) && K <= 3 * kLPR) {
+    // cold row(s): K-th largest of the lanes' top-3 (two independent sub-chains)
+    float p1 = -INFINITY, p2 = -INFINITY, p3 = -INFINITY, q1 = -INFINITY, q2 = -INFINITY, q3 = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < kVPL; ++i) {
-      const float v = z[i];
-      m2 = fmaxf(m2, fminf(m1, v));
-      m1 = fmaxf(m1, v);
+    for (int i = 0; i < kVPL; i += 2) {
+      const float u = z[i], w = z[i + 1];
+      p3 = fmaxf(p3, fminf(p2, u)); p2 = fmaxf(p2, fminf(p1, u)); p1 = fmaxf(p1, u);
+      q3 = fmaxf(q3, fminf(q2, w)); q2 = fmaxf(q2, fminf(q1, w)); q1 = fmaxf(q1, w);
     }
-    int r1 = 1, r2 = 0;                          // m1 beats m2 of the same lane (slot order)
+    top3_merge<KMAX>(p1, p2, p3, q1, q2, q3);
+    // rank each of my three values among the row's 3*kLPR values ((value, lane, slot) order)
+    int r[3] = {0, 1, 2};
+    const float mine[3] = {p1, p2, p3};
 #pragma unroll
     for (int o = 1; o < kLPR; ++o) {
-      const int src = gbase + ((part + o) & (kLPR - 1));
+      const int srcl = gbase + ((part + o) & (kLPR - 1));
       const int op = (part + o) & (kLPR - 1);
-      const float o1 = __shfl_sync(FULL, m1, src), o2 = __shfl_sync(FULL, m2, src);
-      r1 += (o1 > m1 || (o1 == m1 && op < part)) + (o2 > m1 || (o2 == m1 && op < part));
-      r2 += (o1 > m2 || (o1 == m2 && op < part)) + (o2 > m2 || (o2 == m2 && op < part));
+      const float o1 = __shfl_sync(FULL, p1, srcl), o2 = __shfl_sync(FULL, p2, srcl), o3 = __shfl_sync(FULL, p3, srcl);
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const float v = mine[u];
+        r[u] += (o1 > v || (o1 == v && op < part)) + (o2 > v || (o2 == v && op < part)) +
+                (o3 > v || (o3 == v && op < part));
+      }
     }
-    r1 -= 1;                                     // (m1 itself was pre-counted above; keep rank = #greater)
-    r2 += (m1 > m2 || m1 == m2);                 // own m1 ranks ahead of own m2
-    const unsigned h1 = __ballot_sync(FULL, r1 == K - 1), h2 = __ballot_sync(FULL, r2 == K - 1);
-    const unsigned g1 = (h1 >> gbase) & ((1u << kLPR) - 1), g2 = (h2 >> gbase) & ((1u << kLPR) - 1);
-    const float k1 = __shfl_sync(FULL, m1, g1 ? gbase + __ffs(g1) - 1 : gbase);
-    const float k2 = __shfl_sync(FULL, m2, g2 ? gbase + __ffs(g2) - 1 : gbase);
-    const float kth = g1 ? k1 : (g2 ? k2 : -INFINITY);
-    theta = fmaxf(theta, kth);
+    float kth = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const unsigned h = __ballot_sync(FULL, r[u] == K - 1);
+      const unsigned gm = (h >> gbase) & ((1u << kLPR) - 1);
+      const float v = __shfl_sync(FULL, mine[u], gm ? gbase + __ffs(gm) - 1 : gbase);
+      if (gm) kth = v;
+    }
+    if (tk == -INFINITY) theta = kth;
   }
   unsigned cm = 0;
 #pragma unroll
-  for (int i = 0; i < kVPL; ++i) cm |= (valid && z[i] >= theta && z[i] >= tk) ? (1u << i) : 0u;
-  // compact the group's candidate offsets (0..127 within the tile row) into cbuf, then
-  // the leader inserts only real candidates
-  const int cnt = __popc(cm);
-  int incl = cnt;
+  for (int i = 0; i < kVPL; ++i) cm |= (valid && z[i] >= theta) ? (1u << i) : 0u;
+  unsigned pm[kLPR];
 #pragma unroll
-  for (int o = 1; o < kLPR; o <<= 1) {
-    const int v = __shfl_up_sync(FULL, incl, o);
-    if (part >= o) incl += v;
-  }
-  const int total = __shfl_sync(FULL, incl, gbase + kLPR - 1);
-  int pos = incl - cnt;
-  while (cm) {
-    const int i = __ffs(cm) - 1;
-    cm &= cm - 1;
-    cbuf[pos++] = (unsigned char)(part + kLPR * i);
-  }
-  __syncwarp();
+  for (int o = 0; o < kLPR; ++o) pm[o] = __shfl_sync(FULL, cm, gbase + o);
+  if (!valid || part != 0) return;
   bool dirty = false;
-  if (part == 0) {
-    for (int c = 0; c < total; ++c) {
-      const int off = cbuf[c];
+#pragma unroll
+  for (int src = 0; src < kLPR; ++src) {
+    unsigned w = pm[src];
+    while (w) {
+      const int i = __ffs(w) - 1;
+      w &= w - 1;
+      const int off = src + kLPR * i;
       const float zc = col[off];
       const int idc = vbase + off;
       if (better(zc, idc, rz[KMAX - 1], ri[KMAX - 1])) {
@@ -354,9 +364,8 @@ __device__ __forceinline__ void group_update(const float* __restrict__ col, bool
       }
     }
   }
-  __syncwarp();
   GEN_DBG(if (dbg) dbg[2] = gtimer();)
-  if (!valid || part != 0 || !dirty) return;
+  if (!dirty) return;
 #pragma unroll
   for (int q = 0; q < KMAX; ++q) { st[2 + q] = rz[q]; st[2 + KMAX + q] = __int_as_float(ri[q]); }
 }
@@ -376,8 +385,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
   float* stg = reinterpret_cast<float*>(smem + a.stages * stage_bytes);
   float* rstate = stg + (size_t)kColsPerPass * kSLD;            // [n_group][2 + 2*KMAX]
   constexpr int SW = 2 + 2 * KMAX;
-  unsigned char* cbufs = reinterpret_cast<unsigned char*>(rstate + (size_t)a.n_group * SW);   // [64][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(cbufs + kColsPerPass * kTileM);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rstate + (size_t)a.n_group * SW);
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
   uint64_t* tempty = tfull + 2;
@@ -482,11 +490,12 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
   } else {
     // ---------------- epilogue warps 2..(2+kEpiWarps)
     const int et = threadIdx.x - 64;                     // 0..32*kEpiWarps-1
-    const int q = warp & 3, par = (warp - 2) >> 2;       // TMEM quarter, column-chunk index (0..3)
+    const int q = warp & 3;                              // TMEM lane quarter of this warp
+    const int par = (warp - 2 - ((q - 2) & 3)) >> 2;     // index among the warps sharing quarter q
+    const int nwq = (kEpiWarps - ((q - 2) & 3) + 3) >> 2; // warps sharing quarter q
     const int vr = q * 32 + lane;                        // vocabulary row (TMEM lane) this thread drains
-    const int gcol = (et >> 5) * (32 / kLPR) + lane / kLPR;   // row (column) within a pass
+    const int gcol = et / kLPR;                          // row (column) within a pass (et < 160 scan)
     const int part = lane % kLPR;
-    constexpr int kNPar = kEpiWarps / 4;                 // warps sharing one TMEM lane quarter
     const int npass = (a.n_group + kColsPerPass - 1) / kColsPerPass;
     for (int i = et; i < a.n_group; i += 32 * kEpiWarps) {
       float* st = rstate + (size_t)i * SW;
@@ -511,7 +520,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
       for (int h = 0; h < npass; ++h) {
         const int cbeg = h * kColsPerPass;
         const int cend = min(a.n_group, cbeg + kColsPerPass);
-        for (int c0 = cbeg + par * 16; c0 < cend && a.epi_mode != 2 && a.epi_mode < 3 && a.epi_mode != 5; c0 += 16 * kNPar) {
+        for (int c0 = cbeg + par * 16; c0 < cend && a.epi_mode != 2 && a.epi_mode < 3 && a.epi_mode != 5; c0 += 16 * nwq) {
           float v[16];
           tmem_ld16(trow + c0, v);
 #pragma unroll
@@ -525,14 +534,15 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
         named_bar(1, 32 * kEpiWarps);
         GEN_DBG(if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[160 + 2 * j + h] = gtimer();)
         const int c = cbeg + gcol;
-        const bool valid = c < cend && n0 + c < g.rows_valid;
+        const bool valid = gcol < kColsPerPass && c < cend && n0 + c < g.rows_valid;
 #ifdef ONMT_GEN_TRACE
         unsigned long long* gd = (a.dbg && blockIdx.x == 0 && et == 0 && j < 2 && h < 2) ? a.dbg + 210 + 8 * (2 * j + h) : nullptr;
 #else
         unsigned long long* gd = nullptr;
 #endif
         if (a.epi_mode == 0)
-          group_update<KMAX>(stg + gcol * kSLD, valid, part, vt * kTileM, rstate + (size_t)min(c, a.n_group - 1) * SW, g.K, cbufs + gcol * kTileM, gd);
+          group_update<KMAX>(stg + min(gcol, kColsPerPass - 1) * kSLD, valid, part, vt * kTileM,
+                             rstate + (size_t)min(c, a.n_group - 1) * SW, g.K, gd);
         named_bar(1, 32 * kEpiWarps);
         GEN_DBG(if (a.dbg && blockIdx.x == 0 && et == 0 && j < 8 && h < 2) a.dbg[176 + 2 * j + h] = gtimer();)
       }
@@ -558,7 +568,7 @@ gen_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_cons
 
 static size_t genp_smem_bytes(int n_group, int stages, int kmax) {
   return 1024 + (size_t)stages * (kTileM * 128 + 2 * (size_t)n_group * 128) + (size_t)kColsPerPass * kSLD * 4 +
-         (size_t)n_group * (2 + 2 * kmax) * 4 + kColsPerPass * kTileM + (2 * stages + 4) * 8 + 16;
+         (size_t)n_group * (2 + 2 * kmax) * 4 + (2 * stages + 4) * 8 + 16;
 }
 
 // cluster size for the activation multicast (1 = off): needs n_group % (8*CS) == 0
