@@ -42,6 +42,11 @@ extern unsigned long long* g_gen_dbg;
 cudaError_t simt_gemm_partial(const void* W, bool w_bf16, int m_pad, int k_pad, const float* X, int n_rows_pad,
                               int n_valid, int splits, float* out, StepCtl ctl, cudaStream_t st);
 int simt_effective_splits(int k_pad, int splits);
+cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
+                         int n_valid, int k_blocks, const float* bias, const float* cg, float* c_out, float* h_out,
+                         int H, CellDst dst, StepCtl ctl, cudaStream_t st);
+cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
+                         int n_valid, int k_blocks, int H, float* htilde, XOut xg, StepCtl ctl, cudaStream_t st);
 cudaError_t simt_gen_partials(const float* logits, int v_pad, const GenOut& g, StepCtl ctl, cudaStream_t st);
 
 void launch_embed_gather(const float* emb, int E, const int* ids, const int* lens, int B, int S_max, XOut x,
@@ -268,6 +273,8 @@ struct onmt_model {
   bool use_tc = false;       // tcgen05 GEMM backend (bf16 models)
   int profile = 0;             // 0 off, 1 generator launches only, 2 every kernel family
   bool gen_mc = false;         // generator activation multicast across 4-CTA clusters (measured slower on c2)
+  bool fused = false;          // cluster split-K reduction fused with the cell / tanh epilogues (opt-in:
+                               // measured slower than GEMM + separate epilogue kernel)
   bool use_graph = true;
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -741,16 +748,27 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
     EvPair ev = prof_begin(m, "step");
     for (int l = 0; l < L; ++l) {
       const Mat& W = *m->dec_w[l];
-      EvPair pg = prof_begin(m, "gemm");
-      int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
-      prof_end(m, "gemm", pg);
-      EvPair pc = prof_begin(m, "cell");
       CellDst dst{};
       if (l + 1 < L) {
         dst.x[0] = m->xdec[l + 1]->xo(bf); dst.col[0] = 0; dst.n = 1;
       } else {
         dst.x[0] = m->xo.xo(bf); dst.col[0] = H; dst.n = 1;
       }
+      if (m->use_tc && m->fused) {
+        // gates GEMM + split-K cluster reduction + LSTM cell in one kernel
+        EvPair pg = prof_begin(m, "gemm");
+        const Act& X = *m->xdec[l];
+        ONMT_CUDA(tc_gemm_cell(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, R, W.k_pad / kBK,
+                               m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H, cc + (size_t)l * rp * H,
+                               hh + (size_t)l * rp * H, H, dst, ctl, m->stream));
+        count(m);
+        prof_end(m, "gemm", pg);
+        continue;
+      }
+      EvPair pg = prof_begin(m, "gemm");
+      int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
+      prof_end(m, "gemm", pg);
+      EvPair pc = prof_begin(m, "cell");
       launch_dec_cell(P, s, m->xdec[l]->rows_pad, W.m_pad, m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H,
                       cc + (size_t)l * rp * H, hh + (size_t)l * rp * H, H, R, dst, ctl, m->stream);
       count(m);
@@ -767,7 +785,13 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       count(m);
       prof_end(m, "attention", pa);
     }
-    {
+    if (m->use_tc && m->fused) {
+      EvPair pg = prof_begin(m, "gemm");
+      ONMT_CUDA(tc_gemm_tanh(m->attn_wout.tmap, m->xo.tmap, m->attn_wout.m_pad, m->xo.rows_pad, m->xo.n_group, R,
+                             m->attn_wout.k_pad / kBK, H, m->htilde.as<float>(), m->xg.xo(bf), ctl, m->stream));
+      count(m);
+      prof_end(m, "gemm", pg);
+    } else {
       EvPair pg = prof_begin(m, "gemm");
       int s = gemm(m, m->attn_wout, m->xo, R, 0, P, ctl);
       prof_end(m, "gemm", pg);
@@ -891,6 +915,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   m->num_sms = prop.multiProcessorCount;
   if (const char* ev = std::getenv("ONMT_USE_GRAPH")) m->use_graph = std::atoi(ev) != 0;   // ncu runs use 0
   if (const char* ev = std::getenv("ONMT_GEN_MULTICAST")) m->gen_mc = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_FUSED_GEMM")) m->fused = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
@@ -922,6 +947,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
   } else if (n == "profile") {
     if (v < 0 || v > 2) return fail(ONMT_E_INVALID_ARG, "profile must be 0, 1 or 2");
     m->profile = (int)v;
+  } else if (n == "fused_gemm") {
+    m->fused = v != 0;
   } else if (n == "gen_multicast") {
     m->gen_mc = v != 0;
   } else if (n == "use_graph") {

@@ -241,3 +241,17 @@ def test_errors_and_edge_cases(weight_cache):
     assert one["lens"][0] == 1
     ref = beam_search(om, [7], 3, 1)
     assert one["hyps"][0, 0] == ref["tokens"][0]
+
+
+def test_fused_cluster_gemm_matches_unfused(weight_cache):
+    """The cluster split-K reduction + fused cell/tanh path equals the partial-GEMM +
+    consumer-kernel path up to fp32 summation order."""
+    gm, om, p = model_pair("c2", weight_cache)
+    ids, lens = synth.make_corpus("c2", 6)
+    gm.set_option("fused_gemm", 1)
+    a = gm.translate(ids, lens, 5, 12, 0.0)
+    gm.set_option("fused_gemm", 0)
+    b = gm.translate(ids, lens, 5, 12, 0.0)
+    gm.set_option("fused_gemm", 1)
+    np.testing.assert_array_equal(a["hyps"], b["hyps"])
+    np.testing.assert_allclose(a["token_logp"], b["token_logp"], atol=2e-5)
