@@ -155,10 +155,10 @@ ONMT_API onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_src_ids,
  *                   every kernel family (see onmt_get_kernel_time); 0 = off (default).
  *   "use_graph"     1 = replay the whole translation as one cached CUDA graph (default),
  *                   0 = launch every kernel directly (profilers that cannot replay graph nodes).
- *   "fused_gemm"    1 = decoder gate and W_out GEMMs reduce their split-K partials inside
- *                   a thread-block cluster and apply the LSTM cell / tanh in the same
- *                   kernel; 0 = separate partial GEMM + consumer kernels (default; the
- *                   fused form measured slower at c2).
+ *   "fused_gemm"    1 = decoder gate and W_out GEMMs reduce their split-K partials in the
+ *                   same kernel (L2 round trip + per-tile arrival counter) and apply the
+ *                   LSTM cell / tanh there (default); 0 = separate partial GEMM + consumer
+ *                   kernels.  Both give the same result up to fp32 summation order.
  *   "gen_multicast" 1 = share the generator's activation tiles across 4-CTA clusters by
  *                   TMA multicast; 0 = off (default; measured slower at c2).
  * INVALID_ARG on an unknown name or value.

@@ -1,11 +1,24 @@
-// Split-K tcgen05 GEMM with the split reduction done inside a thread-block cluster and the
-// consumer fused in (decoder LSTM cell, PAPER.md P129-136; or h~ = tanh(W_out [c; h]),
-// P69).  Cluster = the S split-K CTAs of one 128-row weight tile: each CTA streams its
-// K-slice (TMA -> smem -> tcgen05.mma, hi/lo activation planes into one fp32 TMEM
-// accumulator), parks its partial tile in its own shared memory, and after a cluster
-// barrier CTA s reduces rows [s*128/S, (s+1)*128/S) over all S partials through
-// distributed shared memory in fixed order (deterministic), then applies the epilogue.
-// Removes the separate cell / tanh launches and the partial round trip through L2.
+// Split-K tcgen05 GEMM with the split reduction and the consumer fused into the same
+// kernel: the decoder LSTM cell (PAPER.md P129-136, gates = W [x; h] + b) or the
+// attentional vector h~ = tanh(W_out [c; h]) (P69) - SURVEY §8(a) rows A6 / A8.
+//
+// Grid = tiles x S (tile = 128 weight rows x one N-group of hypothesis rows, S = split-K
+// ways), one CTA per SM and grid <= #SMs, so every CTA is co-resident.
+//   1. The producer thread TMA-loads the CTA's whole weight K-slice BEFORE
+//      griddepcontrol.wait (weights are constants: the loads overlap the previous kernel),
+//      then the hi/lo activation planes after it.  The slice stays resident (one smem
+//      slot per K block).
+//   2. One thread issues tcgen05.mma (M = 128 weight rows, N = n_group, hi and lo planes
+//      accumulate into one fp32 TMEM accumulator).  Meanwhile warps 2-3 prefetch the
+//      epilogue's side inputs (bias, gathered c_prev) into shared memory.
+//   3. The partial tile goes TMEM -> registers -> global scratch [tile][S][n][128]
+//      (coalesced, L2-resident), then a per-tile arrival counter (release / acquire,
+//      generation-counted so it never needs a reset) waits for the tile's S splits.
+//   4. CTA s owns hypothesis columns [s*NC, (s+1)*NC): one bulk copy per split pulls
+//      those columns of every partial into shared memory, they are summed in fixed split
+//      order (deterministic) and the epilogue runs on them.
+// A DSMEM exchange inside a cluster was measured slower (~20 B/clk per SM) than this L2
+// round trip for 80 KB partial tiles.
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -15,7 +28,10 @@ enum { EPI_CELL = 0, EPI_TANH = 1 };
 
 struct FusedArgs {
   int n_rows_pad, n_group, n_valid, k_blocks, kb_per_split, stages, tmem_cols, S;
+  int NC;                  // hypothesis columns owned per split (multiple of 4)
   int M;                   // valid weight rows (4H for the cell, H for tanh)
+  float* scratch;          // [tiles][S][n_group][128] fp32 partial tiles
+  unsigned int* counters;  // [tiles] generation-counted arrivals
   // EPI_CELL
   const float4* bias;      // [H] interleaved (i,f,g,o) pre-summed biases
   const float* cg;         // [rows_pad][H] c_prev gathered by parent
@@ -27,93 +43,114 @@ struct FusedArgs {
   float* htilde;
   XOut xg;
   StepCtl ctl;
+  int dbg;                 // microbenchmark ablations (ONMT_KTRACE builds only)
 };
-
-__device__ __forceinline__ float4 ld_peer_f4(const float* local, uint32_t peer) {
-  uint32_t ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(peer));
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"   // ordered after the cluster barrier
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)                // (volatile), independent otherwise
-               : "r"(ra));
-  return v;
-}
 
 // sigmoid / tanh via the fast exponential (ex2.approx, rel. error ~2^-21): well inside the
 // fp32 (1e-5) and bf16 (2e-3) log-prob bars; avoids the IEEE-division / tanhf slow paths
-__device__ __forceinline__ float sigmf(float x) { return __frcp_rn(1.f + __expf(-x)); }
+__device__ __forceinline__ float sigmf(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
 __device__ __forceinline__ float tanhfast(float x) {
   const float e = __expf(-2.f * fabsf(x));
-  const float t = (1.f - e) * __frcp_rn(1.f + e);
+  const float t = __fdividef(1.f - e, 1.f + e);
   return copysignf(t, x);
 }
 
+#ifdef ONMT_KTRACE            // phase timestamps (microbenchmarks only): [cta][12]
+__device__ unsigned long long* g_ktrace;
+#define KT(i)                                                                                   \
+  do {                                                                                          \
+    if (threadIdx.x == 0 && g_ktrace) {                                                         \
+      unsigned long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                     \
+      g_ktrace[blockIdx.x * 12 + (i)] = t_;                                                      \
+    }                                                                                           \
+  } while (0)
+#else
+#define KT(i) do {} while (0)
+#endif
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 template <int EPI>
-__global__ void __launch_bounds__(128, 1)
-tc_gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                       FusedArgs a) {
+__global__ void __launch_bounds__(256, 1)
+tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                     FusedArgs a) {
+  KT(0);
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t a_bytes = kTileM * 128, b_bytes = a.n_group * 128;
   const uint32_t stage_bytes = a_bytes + 2 * b_bytes;
   const size_t ring = (size_t)a.stages * stage_bytes;
-  const size_t part_bytes = (size_t)a.n_group * kTileM * 4;
-  float* part = reinterpret_cast<float*>(smem);                         // [n_group][128] (reuses the ring)
-  const int RM = kTileM / a.S;                                          // rows this CTA reduces
-  float* red = reinterpret_cast<float*>(smem + (ring > part_bytes ? ring : part_bytes));   // [n_group][RM]
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + (size_t)a.n_group * RM);
-  uint64_t* empty = full + a.stages;
-  uint64_t* done = empty + a.stages;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const size_t recv_bytes = (size_t)(a.S + 1) * a.NC * kTileM * 4;   // recv [S][NC][128] + red [NC][128]
+  float* recv = reinterpret_cast<float*>(smem);                  // [S][NC][128], overlays the ring
+  uint8_t* tail = smem + (ring > recv_bytes ? ring : recv_bytes);
+  float4* s_bias = reinterpret_cast<float4*>(tail);               // [32] (cell)
+  float* s_cg = reinterpret_cast<float*>(tail + 32 * 16);         // [NC][32] (cell)
+  uint64_t* full = reinterpret_cast<uint64_t*>(tail + 32 * 16 + (size_t)a.NC * 32 * 4);
+  uint64_t* done = full + a.stages;
+  uint64_t* rbar = done + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t split = cluster_ctarank();
-  const int mt = blockIdx.x / a.S;
+  const int tile = blockIdx.x / a.S;
+  const int split = blockIdx.x % a.S;
+  const int n_groups = a.n_rows_pad / a.n_group;
+  const int mt = tile / n_groups, grp = tile % n_groups;
   const int m0 = mt * kTileM;
-  const int n0 = blockIdx.y * a.n_group;
+  const int n0 = grp * a.n_group;
   const int kb0 = split * a.kb_per_split;
   int nkb = a.k_blocks - kb0;
   if (nkb > a.kb_per_split) nkb = a.kb_per_split;
   if (nkb < 0) nkb = 0;
+  const int c_own = split * a.NC;                                 // first hypothesis column I own
+  const int ncols = max(0, min(a.NC, a.n_group - c_own));
 
+  // ---- prologue (overlaps the predecessor under PDL): barriers, TMEM, weight prefetch
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
-    for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < a.stages; ++s) mbar_init(&full[s], 1);
     mbar_init(done, 1);
+    mbar_init(rbar, 1);
     fence_mbar_init();
+    for (int i = 0; i < nkb; ++i) {
+      mbar_expect_tx(&full[i], a_bytes);
+      tma_load_2d(smem + i * stage_bytes, &tmW, (kb0 + i) * kBK, m0, &full[i]);
+    }
   }
   if (warp == 0) tmem_alloc_dyn(tslot, a.tmem_cols);
   tc_fence_before();
-  pdl_wait();
+  pdl_wait();                                    // activations / c_prev / n_done now visible
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  if (all_done(a.ctl)) {
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
-    return;
-  }
+  const bool quit = all_done(a.ctl);             // uniform over the grid
+  KT(1);
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < nkb; ++i) {
-      const int s = i % a.stages;
-      if (i >= a.stages) mbar_wait(&empty[s], ((i / a.stages) & 1) ^ 1);
-      uint8_t* st = smem + s * stage_bytes;
-      mbar_arrive_expect_tx(&full[s], stage_bytes);
-      const int kx = (kb0 + i) * kBK;
-      tma_load_2d(st, &tmW, kx, m0, &full[s]);
-      tma_load_2d(st + a_bytes, &tmX, kx, n0, &full[s]);
-      tma_load_2d(st + a_bytes + b_bytes, &tmX, kx, a.n_rows_pad + n0, &full[s]);
+      uint8_t* st = smem + i * stage_bytes;
+      if (quit) {
+        mbar_arrive_local(&full[i]);
+      } else {
+        mbar_arrive_expect_tx(&full[i], 2 * b_bytes);
+        tma_load_2d(st + a_bytes, &tmX, (kb0 + i) * kBK, n0, &full[i]);
+        tma_load_2d(st + a_bytes + b_bytes, &tmX, (kb0 + i) * kBK, a.n_rows_pad + n0, &full[i]);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_group);
     for (int i = 0; i < nkb; ++i) {
-      const int s = i % a.stages;
-      mbar_wait(&full[s], (i / a.stages) & 1);
+      mbar_wait(&full[i], 0);
       tc_fence_after();
-      const uint32_t sa = smem_u32(smem + s * stage_bytes);
+      if (quit) continue;
+      const uint32_t sa = smem_u32(smem + i * stage_bytes);
       const uint32_t sbh = sa + a_bytes, sbl = sa + a_bytes + b_bytes;
 #pragma unroll
       for (int kk = 0; kk < kBK / 16; ++kk) {
@@ -121,195 +158,253 @@ tc_gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_con
         tc_mma_bf16(tmem, da, umma_desc_sw128(sbh + kk * 32), idesc, (i | kk) != 0);
         tc_mma_bf16(tmem, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
       }
-      tc_commit(&empty[s]);
     }
-    tc_commit(done);
-  }
-  __syncwarp();
-  if (nkb > 0) {
-    mbar_wait(done, 0);
-    tc_fence_after();
-  }
-  __syncthreads();                               // ring no longer read by the tensor core
-  // ---- park the partial tile: part[n][m] (column-major over TMEM lanes: conflict-free)
-  {
-    const int q = warp & 3;
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    const int m = q * 32 + lane;
-    for (int c0 = 0; c0 < a.n_group; c0 += 16) {
-      float v[16];
-      if (nkb > 0) {
-        tmem_ld16(trow + c0, v);
-      } else {
+    tc_commit(done);                             // also fires with no MMA issued
+  } else if (warp >= 2 && EPI == EPI_CELL && !quit) {
+    // side inputs of my columns: bias of the tile's 32 units, c_prev[r][j]
+    const int t = threadIdx.x - 64;               // 192 threads
+    if (t < 32) {
+      const int j = m0 / 4 + t;
+      s_bias[t] = j < a.H ? __ldg(&a.bias[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int i0 = t; i0 < ncols * 32; i0 += 192 * 8) {   // 8 loads in flight per thread
+      float v[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + 192 * u;
+        const int c = i / 32, ul = i % 32;
+        const int r = n0 + c_own + c, j = m0 / 4 + ul;
+        v[u] = (i < ncols * 32 && r < a.n_valid && j < a.H) ? __ldg(&a.cg[(size_t)r * a.H + j]) : 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 16; ++j) part[(c0 + j) * kTileM + m] = v[j];
+      for (int u = 0; u < 8; ++u)
+        if (i0 + 192 * u < ncols * 32) s_cg[i0 + 192 * u] = v[u];
+    }
+  }
+  __syncwarp();
+  mbar_wait(done, 0);
+  tc_fence_after();
+  KT(2);
+  if (quit) {                                    // every TMA landed (waited above); nothing else in flight
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
+    return;
+  }
+  // ---- (3) partial tile: TMEM -> registers -> global scratch [tile][split][n/4][128][4]
+  //      (each thread stores float4 = 4 consecutive columns of its row: a warp writes 512
+  //      contiguous bytes), then release the tile counter
+  {
+    const int q = warp & 3, half = warp >> 2;                    // warps q and q+4 share a lane quarter
+    const int m = q * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const int hcols = (a.n_group / 2 + 3) & ~3;
+    const int cb = half * hcols, ce = half ? a.n_group : hcols;
+    float4* out = reinterpret_cast<float4*>(a.scratch + ((size_t)(tile * a.S + split) * a.n_group) * kTileM) + m;
+    for (int c0 = cb; c0 < ce; c0 += 32) {
+      uint32_t r[32];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (c0 + 4 * k < ce && nkb > 0)
+          tmem_ld4_nw(trow + c0 + 4 * k, r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+        else
+          r[4 * k] = r[4 * k + 1] = r[4 * k + 2] = r[4 * k + 3] = 0u;
+      }
+      tmem_wait_ld();
+      tmem_fence_regs(r);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (c0 + 4 * k < ce)
+          __stcg(out + (size_t)((c0 >> 2) + k) * kTileM,
+                 make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]), __uint_as_float(r[4 * k + 2]),
+                             __uint_as_float(r[4 * k + 3])));
     }
   }
   tc_fence_before();
-  cluster_sync_all();
-  // ---- reduce my RM rows over the S partials (fixed peer order) into red[n][RM]
-  const int mr0 = split * RM;
-  const int RM4 = RM / 4;
-  for (int it0 = threadIdx.x; it0 < a.n_group * RM4; it0 += 2 * blockDim.x) {
-    float4 v[2][8];                               // 2 items x 8 peers of remote loads in flight
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int it = min(it0 + u * (int)blockDim.x, a.n_group * RM4 - 1);
-      const int n = it / RM4, m4 = (it % RM4) * 4;
-      const float* loc = part + n * kTileM + mr0 + m4;
-#pragma unroll
-      for (int p = 0; p < 8; ++p) v[u][p] = p < a.S ? ld_peer_f4(loc, p) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int it = it0 + u * blockDim.x;
-      if (it >= a.n_group * RM4) break;
-      const int n = it / RM4, m4 = (it % RM4) * 4;
-      float4 acc = v[u][0];                       // fixed peer order: deterministic
-#pragma unroll
-      for (int p = 1; p < 8; ++p) { acc.x += v[u][p].x; acc.y += v[u][p].y; acc.z += v[u][p].z; acc.w += v[u][p].w; }
-      *reinterpret_cast<float4*>(red + n * RM + m4) = acc;
-    }
-  }
+  __threadfence();
   __syncthreads();
-  // ---- fused epilogue on rows [m0 + mr0, m0 + mr0 + RM)
-  if (EPI == EPI_CELL) {
-    const int U = RM / 4;                        // LSTM units in my rows (rows 4u+g interleaved)
-    const int u0 = (m0 + mr0) / 4;
-    const int nit = U * a.n_group;
-    for (int b0 = threadIdx.x; b0 < nit; b0 += 4 * blockDim.x) {
-      float4 bb[4];
-      float cp[4];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {               // all global loads of 4 items first
-        const int it = b0 + v * blockDim.x;
-        const int ul = it % U, n = it / U;
-        const int r = n0 + n, j = u0 + ul;
-        const bool ok = it < nit && r < a.n_valid && j < a.H;
-        bb[v] = ok ? __ldg(&a.bias[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
-        cp[v] = ok ? __ldg(&a.cg[(size_t)r * a.H + j]) : 0.f;
-      }
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int it = b0 + v * blockDim.x;
-        const int ul = it % U, n = it / U;
-        const int r = n0 + n, j = u0 + ul;
-        if (!(it < nit && r < a.n_valid && j < a.H)) continue;
-        const float* gz = red + n * RM + 4 * ul;
-        const float i_ = sigmf(gz[0] + bb[v].x), f_ = sigmf(gz[1] + bb[v].y), g_ = tanhfast(gz[2] + bb[v].z),
-                    o_ = sigmf(gz[3] + bb[v].w);
-        const float c = f_ * cp[v] + i_ * g_;
-        const float h = o_ * tanhfast(c);
-        a.c_out[(size_t)r * a.H + j] = c;
-        a.h_out[(size_t)r * a.H + j] = h;
-        for (int d = 0; d < a.dst.n; ++d) store_x(a.dst.x[d], r, a.dst.col[d] + j, h);
-      }
+  KT(3);
+  if (threadIdx.x == 0) {
+    // arrive; wait for the S splits of this tile (generation count: no reset needed)
+    const unsigned int old = atomicAdd(&a.counters[tile], 1u);
+    const unsigned int target = (old / (unsigned)a.S + 1u) * (unsigned)a.S;
+    while (true) {
+      unsigned int v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.counters + tile) : "memory");
+      if ((int)(v - target) >= 0) break;
     }
-  } else {
-    for (int it = threadIdx.x; it < RM * a.n_group; it += blockDim.x) {
-      const int ml = it % RM, n = it / RM;
-      const int r = n0 + n, j = m0 + mr0 + ml;
-      if (r >= a.n_valid || j >= a.M) continue;
-      const float h = tanhfast(red[n * RM + ml]);
-      a.htilde[(size_t)r * a.M + j] = h;
-      store_x(a.xg, r, j, h);
+    asm volatile("fence.proxy.async;" ::: "memory");
+    KT(4);
+    // (4) my columns of every split's partial: S contiguous blocks of NC/4 x 128 x 4 floats
+    if (ncols > 0) {
+      const uint32_t bytes = (uint32_t)ncols * kTileM * 4;
+      mbar_arrive_expect_tx(rbar, bytes * a.S);
+      for (int p = 0; p < a.S; ++p)
+        bulk_g2s(recv + (size_t)p * a.NC * kTileM,
+                 a.scratch + ((size_t)(tile * a.S + p) * a.n_group + c_own) * kTileM, bytes, rbar);
+    } else {
+      mbar_arrive_local(rbar);
     }
   }
-  cluster_sync_all();                            // peers finished reading my partial
+  mbar_wait(rbar, 0);
+  KT(5);
+  // fixed-order split sum, written transposed into red[c][128] (conflict-free epilogue reads)
+  float* red = recv + (size_t)a.S * a.NC * kTileM;
+  if (ncols > 0) {
+    const size_t slot = (size_t)a.NC * kTileM;
+    const int nit = (ncols / 4) * kTileM;       // (c4 block, m) items, float4 each
+    for (int it0 = threadIdx.x; it0 < nit; it0 += 2 * blockDim.x) {
+      float4 v[2][16];                           // 2 items x up to 16 splits in flight
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const size_t off = (size_t)min(it0 + u * (int)blockDim.x, nit - 1) * 4;
+#pragma unroll
+        for (int p = 0; p < 16; ++p)
+          v[u][p] = p < a.S ? *reinterpret_cast<const float4*>(recv + p * slot + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int it = it0 + u * blockDim.x;
+        float4 acc = v[u][0];                    // fixed split order: deterministic
+#pragma unroll
+        for (int p = 1; p < 16; ++p) { acc.x += v[u][p].x; acc.y += v[u][p].y; acc.z += v[u][p].z; acc.w += v[u][p].w; }
+        if (it < nit) {
+          const int c4 = it / kTileM, m = it % kTileM;
+          float* o = red + (size_t)(4 * c4) * kTileM + m;
+          o[0] = acc.x; o[kTileM] = acc.y; o[2 * kTileM] = acc.z; o[3 * kTileM] = acc.w;
+        }
+      }
+    }
+  }
+  KT(8);
+  __syncthreads();
+  KT(9);
+  if (ncols > 0) {
+    if (EPI == EPI_CELL) {
+      // rows m = 4u + g (gate-interleaved): unit j = m0/4 + ul, 32 units per tile
+      const int nit = 32 * ncols;
+      for (int it0 = threadIdx.x; it0 < nit; it0 += 2 * blockDim.x) {
+        float4 gz[2], bb[2];
+        float cp[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int it = min(it0 + u * (int)blockDim.x, nit - 1);
+          const int ul = it % 32, c = it / 32;
+          gz[u] = *reinterpret_cast<const float4*>(red + (size_t)c * kTileM + 4 * ul);
+          bb[u] = s_bias[ul];
+          cp[u] = s_cg[it];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int it = it0 + u * blockDim.x;
+          const int ul = it % 32, c = it / 32;
+          const int r = n0 + c_own + c, j = m0 / 4 + ul;
+          const float i_ = sigmf(gz[u].x + bb[u].x), f_ = sigmf(gz[u].y + bb[u].y),
+                      g_ = tanhfast(gz[u].z + bb[u].z), o_ = sigmf(gz[u].w + bb[u].w);
+          const float cn = f_ * cp[u] + i_ * g_;
+          const float h = o_ * tanhfast(cn);
+          if (it >= nit || r >= a.n_valid || j >= a.H) continue;
+#ifdef ONMT_KTRACE
+          if (a.dbg == 2) { if (h == 12345.f) a.c_out[0] = cn; continue; }
+          if (a.dbg == 3) { a.c_out[(size_t)r * a.H + j] = cn; continue; }
+#endif
+          a.c_out[(size_t)r * a.H + j] = cn;
+          a.h_out[(size_t)r * a.H + j] = h;
+#ifdef ONMT_KTRACE
+          if (a.dbg == 1) continue;
+#endif
+          for (int d = 0; d < a.dst.n; ++d) store_x(a.dst.x[d], r, a.dst.col[d] + j, h);
+        }
+      }
+    } else {
+      for (int it = threadIdx.x; it < kTileM * ncols; it += blockDim.x) {
+        const int m = it % kTileM, c = it / kTileM;
+        const int r = n0 + c_own + c, j = m0 + m;
+        if (r >= a.n_valid || j >= a.M) continue;
+        const float h = tanhfast(red[(size_t)c * kTileM + m]);
+        a.htilde[(size_t)r * a.M + j] = h;
+        store_x(a.xg, r, j, h);
+      }
+    }
+  }
+  KT(6);
+  tc_fence_before();
+  __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
+  KT(7);
 }
 
-static size_t fused_smem_bytes(int n_group, int stages, int S) {
+static size_t fused_smem_bytes(int n_group, int stages, int S, int NC) {
   const size_t ring = (size_t)stages * (kTileM * 128 + 2 * (size_t)n_group * 128);
-  const size_t part = (size_t)n_group * kTileM * 4;
-  return 1024 + (ring > part ? ring : part) + (size_t)n_group * (kTileM / S) * 4 + (2 * stages + 1) * 8 + 16;
+  const size_t recv = (size_t)(S + 1) * kTileM * NC * 4;
+  return 1024 + (ring > recv ? ring : recv) + 32 * 16 + (size_t)NC * 32 * 4 + (stages + 2) * 8 + 16;
 }
 
-template <int EPI>
-static cudaError_t launch_fused(const CUtensorMap& tmW, const CUtensorMap& tmX, const FusedArgs& a, int m_tiles,
-                                int n_groups, cudaStream_t st) {
-  const size_t smem = fused_smem_bytes(a.n_group, a.stages, a.S);
-  auto fn = tc_gemm_cluster_kernel<EPI>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(m_tiles * a.S, n_groups);
-  cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = a.S;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, fn, tmW, tmX, a);
-}
-
-template <int EPI>
-static int max_active_clusters(int n_group, int stages, int S) {
-  static int cache[2][9][512 / 16 + 1][5] = {};
-  int& c = cache[EPI][S][n_group / 16][stages];
-  if (c) return c;
-  const size_t smem = fused_smem_bytes(n_group, stages, S);
-  auto fn = tc_gemm_cluster_kernel<EPI>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(S * 64);
-  cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = S;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n < 1) n = 1;
-  c = n;
-  return n;
-}
-
-template <int EPI>
-static void fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, int k_blocks, int M, int m_tiles) {
+// Split S: the largest S <= 16 such that every split has >= 1 K block, the split's whole
+// K-slice fits the shared-memory ring, and tiles * S <= #SMs (one co-resident wave: the
+// tile counter wait needs every split resident).  1 CTA per SM (smem > half an SM).
+static bool fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, int k_blocks, int M, int m_tiles,
+                        int num_sms) {
   a.n_rows_pad = n_rows_pad;
   a.n_group = n_group;
   a.n_valid = n_valid;
   a.k_blocks = k_blocks;
-  const int groups = n_rows_pad / n_group;
-  int S = 8;
-  for (;; S >>= 1) {
-    if (S == 1) break;
-    if ((k_blocks + S - 1) / S * (S - 1) >= k_blocks) continue;            // every split gets >= 1 block
+  const int tiles = m_tiles * (n_rows_pad / n_group);
+  const size_t limit = 227 * 1024;
+  for (int S = 16; S >= 1; --S) {
     const int kbps = (k_blocks + S - 1) / S;
-    int st = kbps < 4 ? kbps : 4;
-    while (st > 1 && fused_smem_bytes(n_group, st, S) > 227 * 1024) --st;
-    if (m_tiles * groups <= max_active_clusters<EPI>(n_group, st, S)) break;   // one wave of clusters
+    if ((k_blocks + kbps - 1) / kbps != S) continue;     // no empty split
+    if (tiles * S > num_sms) continue;
+    int NC = (n_group + S - 1) / S;
+    NC = (NC + 3) / 4 * 4;
+    const size_t sm = fused_smem_bytes(n_group, kbps, S, NC);
+    if (sm > limit) continue;
+    a.S = S;
+    a.NC = NC;
+    a.kb_per_split = kbps;
+    a.stages = kbps;
+    int tc = 32;
+    while (tc < n_group) tc <<= 1;
+    a.tmem_cols = tc;
+    a.M = M;
+    return true;
   }
-  a.S = S;
-  a.kb_per_split = (k_blocks + S - 1) / S;
-  int stages = a.kb_per_split < 4 ? a.kb_per_split : 4;
-  while (stages > 1 && fused_smem_bytes(n_group, stages, S) > 227 * 1024) --stages;
-  a.stages = stages < 1 ? 1 : stages;
-  int tc = 32;
-  while (tc < n_group) tc <<= 1;
-  a.tmem_cols = tc;
-  a.M = M;
+  return false;
+}
+
+template <int EPI>
+static cudaError_t launch_fused(const CUtensorMap& tmW, const CUtensorMap& tmX, const FusedArgs& a, int tiles,
+                                cudaStream_t st) {
+  // at least 116 KB of shared memory: never two CTAs of this kernel on one SM (the tile wait
+  // relies on one CTA per SM with grid <= #SMs)
+  size_t smem = fused_smem_bytes(a.n_group, a.stages, a.S, a.NC);
+  if (smem < 116 * 1024) smem = 116 * 1024;
+  auto fn = tc_gemm_fused_kernel<EPI>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(fn, dim3(tiles * a.S), dim3(256), smem, st, tmW, tmX, a);
+}
+
+// scratch floats a fused call needs (0 = no fused configuration fits)
+size_t fused_scratch_floats(int m_pad, int n_rows_pad, int n_group, int k_blocks, int num_sms) {
+  FusedArgs a{};
+  const int m_tiles = m_pad / kTileM;
+  if (!fill_common(a, n_rows_pad, n_group, n_group, k_blocks, 1, m_tiles, num_sms)) return 0;
+  return (size_t)m_tiles * (n_rows_pad / n_group) * a.S * n_group * kTileM;
 }
 
 // decoder LSTM layer: gates = W [x; h] (+ bias), cell update, h written to dst operands
+int g_fused_dbg = 0;
 cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                          int n_valid, int k_blocks, const float* bias, const float* cg, float* c_out, float* h_out,
-                         int H, CellDst dst, StepCtl ctl, cudaStream_t st) {
+                         int H, CellDst dst, float* scratch, unsigned int* counters, int num_sms, StepCtl ctl,
+                         cudaStream_t st) {
   FusedArgs a{};
-  fill_common<EPI_CELL>(a, n_rows_pad, n_group, n_valid, k_blocks, 4 * H, m_pad / kTileM);
+  a.dbg = g_fused_dbg;
+  if (!fill_common(a, n_rows_pad, n_group, n_valid, k_blocks, 4 * H, m_pad / kTileM, num_sms))
+    return cudaErrorInvalidConfiguration;
+  a.scratch = scratch;
+  a.counters = counters;
   a.bias = reinterpret_cast<const float4*>(bias);
   a.cg = cg;
   a.c_out = c_out;
@@ -317,18 +412,28 @@ cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_p
   a.H = H;
   a.dst = dst;
   a.ctl = ctl;
-  return launch_fused<EPI_CELL>(tmW, tmX, a, m_pad / kTileM, n_rows_pad / n_group, st);
+  return launch_fused<EPI_CELL>(tmW, tmX, a, m_pad / kTileM * (n_rows_pad / n_group), st);
 }
 
 // attentional vector: h~ = tanh(W_out [c; h])
 cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
-                         int n_valid, int k_blocks, int H, float* htilde, XOut xg, StepCtl ctl, cudaStream_t st) {
+                         int n_valid, int k_blocks, int H, float* htilde, XOut xg, float* scratch,
+                         unsigned int* counters, int num_sms, StepCtl ctl, cudaStream_t st) {
   FusedArgs a{};
-  fill_common<EPI_TANH>(a, n_rows_pad, n_group, n_valid, k_blocks, H, m_pad / kTileM);
+  if (!fill_common(a, n_rows_pad, n_group, n_valid, k_blocks, H, m_pad / kTileM, num_sms))
+    return cudaErrorInvalidConfiguration;
+  a.scratch = scratch;
+  a.counters = counters;
   a.htilde = htilde;
   a.xg = xg;
   a.ctl = ctl;
-  return launch_fused<EPI_TANH>(tmW, tmX, a, m_pad / kTileM, n_rows_pad / n_group, st);
+  return launch_fused<EPI_TANH>(tmW, tmX, a, m_pad / kTileM * (n_rows_pad / n_group), st);
+}
+
+// split the fused kernels use for a shape (tests / DESIGN numbers; 0 = unfused)
+int fused_split(int n_group, int n_rows_pad, int k_blocks, int m_tiles, int num_sms) {
+  FusedArgs a{};
+  return fill_common(a, n_rows_pad, n_group, n_group, k_blocks, 1, m_tiles, num_sms) ? a.S : 0;
 }
 
 }  // namespace onmt

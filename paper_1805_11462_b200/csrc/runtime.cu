@@ -44,9 +44,12 @@ cudaError_t simt_gemm_partial(const void* W, bool w_bf16, int m_pad, int k_pad, 
 int simt_effective_splits(int k_pad, int splits);
 cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                          int n_valid, int k_blocks, const float* bias, const float* cg, float* c_out, float* h_out,
-                         int H, CellDst dst, StepCtl ctl, cudaStream_t st);
+                         int H, CellDst dst, float* scratch, unsigned int* counters, int num_sms, StepCtl ctl,
+                         cudaStream_t st);
 cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
-                         int n_valid, int k_blocks, int H, float* htilde, XOut xg, StepCtl ctl, cudaStream_t st);
+                         int n_valid, int k_blocks, int H, float* htilde, XOut xg, float* scratch,
+                         unsigned int* counters, int num_sms, StepCtl ctl, cudaStream_t st);
+size_t fused_scratch_floats(int m_pad, int n_rows_pad, int n_group, int k_blocks, int num_sms);
 cudaError_t simt_gen_partials(const float* logits, int v_pad, const GenOut& g, StepCtl ctl, cudaStream_t st);
 
 void launch_embed_gather(const float* emb, int E, const int* ids, const int* lens, int B, int S_max, XOut x,
@@ -273,8 +276,8 @@ struct onmt_model {
   bool use_tc = false;       // tcgen05 GEMM backend (bf16 models)
   int profile = 0;             // 0 off, 1 generator launches only, 2 every kernel family
   bool gen_mc = false;         // generator activation multicast across 4-CTA clusters (measured slower on c2)
-  bool fused = false;          // cluster split-K reduction fused with the cell / tanh epilogues (opt-in:
-                               // measured slower than GEMM + separate epilogue kernel)
+  bool fused = true;           // split-K GEMM with the reduction and the cell / tanh epilogue fused in
+                               // (one launch per layer instead of GEMM + consumer kernel)
   bool use_graph = true;
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -298,6 +301,7 @@ struct onmt_model {
   std::vector<std::unique_ptr<Act>> xdec;    // [L]
   Act xo, xg;
   DevBuf dec_p, st_h, st_c, st_cg, htilde, logits;
+  DevBuf f_scratch, f_count;                 // fused GEMM partial tiles + per-tile arrival counters
   DevBuf g_ms, g_tz, g_ti;
   DevBuf a_pm, a_ps, a_pc, a_tick;
   DevBuf row_lse, row_z, row_i;
@@ -710,6 +714,19 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
     ONMT_CUDA(cudaStreamSynchronize(m->stream));
   }
   if (!m->use_tc) m->logits.ensure((size_t)m->xg.rows_pad * m->gen_w.m_pad * 4);
+  if (m->use_tc) {
+    size_t fs = fused_scratch_floats(m->attn_wout.m_pad, m->xo.rows_pad, m->xo.n_group, m->attn_wout.k_pad / kBK,
+                                     m->num_sms);
+    for (int l = 0; l < L; ++l)
+      fs = std::max(fs, fused_scratch_floats(m->dec_w[l]->m_pad, m->xdec[l]->rows_pad, m->xdec[l]->n_group,
+                                             m->dec_w[l]->k_pad / kBK, m->num_sms));
+    m->f_scratch.ensure(std::max<size_t>(fs, 1) * 4);
+    const size_t nc = (size_t)(L + 1) * 1024 * 4;
+    if (m->f_count.bytes < nc) {
+      m->f_count.ensure(nc);
+      ONMT_CUDA(cudaMemset(m->f_count.p, 0, nc));
+    }
+  }
 }
 
 static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int K, int max_len, float alpha,
@@ -758,12 +775,16 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
         // gates GEMM + split-K cluster reduction + LSTM cell in one kernel
         EvPair pg = prof_begin(m, "gemm");
         const Act& X = *m->xdec[l];
-        ONMT_CUDA(tc_gemm_cell(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, R, W.k_pad / kBK,
-                               m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H, cc + (size_t)l * rp * H,
-                               hh + (size_t)l * rp * H, H, dst, ctl, m->stream));
-        count(m);
+        cudaError_t e = tc_gemm_cell(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, R, W.k_pad / kBK,
+                                     m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H, cc + (size_t)l * rp * H,
+                                     hh + (size_t)l * rp * H, H, dst, m->f_scratch.as<float>(),
+                                     m->f_count.as<unsigned int>() + (size_t)l * 1024, m->num_sms, ctl, m->stream);
         prof_end(m, "gemm", pg);
-        continue;
+        if (e != cudaErrorInvalidConfiguration) {   // (no cluster shape fits: unfused path below)
+          ONMT_CUDA(e);
+          count(m);
+          continue;
+        }
       }
       EvPair pg = prof_begin(m, "gemm");
       int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
@@ -785,13 +806,19 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       count(m);
       prof_end(m, "attention", pa);
     }
+    cudaError_t fe = cudaErrorInvalidConfiguration;
     if (m->use_tc && m->fused) {
       EvPair pg = prof_begin(m, "gemm");
-      ONMT_CUDA(tc_gemm_tanh(m->attn_wout.tmap, m->xo.tmap, m->attn_wout.m_pad, m->xo.rows_pad, m->xo.n_group, R,
-                             m->attn_wout.k_pad / kBK, H, m->htilde.as<float>(), m->xg.xo(bf), ctl, m->stream));
-      count(m);
+      fe = tc_gemm_tanh(m->attn_wout.tmap, m->xo.tmap, m->attn_wout.m_pad, m->xo.rows_pad, m->xo.n_group, R,
+                        m->attn_wout.k_pad / kBK, H, m->htilde.as<float>(), m->xg.xo(bf), m->f_scratch.as<float>(),
+                        m->f_count.as<unsigned int>() + (size_t)L * 1024, m->num_sms, ctl, m->stream);
       prof_end(m, "gemm", pg);
-    } else {
+      if (fe != cudaErrorInvalidConfiguration) {
+        ONMT_CUDA(fe);
+        count(m);
+      }
+    }
+    if (fe == cudaErrorInvalidConfiguration) {
       EvPair pg = prof_begin(m, "gemm");
       int s = gemm(m, m->attn_wout, m->xo, R, 0, P, ctl);
       prof_end(m, "gemm", pg);

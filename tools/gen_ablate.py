@@ -11,7 +11,7 @@ h = np.tanh(np.random.default_rng(0).normal(size=(150, 500))).astype(np.float32)
 ref = None
 for mc in (0,):
     m.set_option("gen_multicast", mc)
-    for mode in ["0", "1", "2", "3", "4"]:
+    for mode in ["0", "1", "2", "3", "4", "5"]:
         os.environ["ONMT_GEN_EPI_MODE"] = mode
         m.set_option("profile", 1)
         for i in range(3):
