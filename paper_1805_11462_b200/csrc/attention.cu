@@ -1,0 +1,359 @@
+// A7: Luong global attention for one decoder step (PAPER.md P119-122, P299-301; SURVEY
+// §8(a) A7).  'general' scores are e_s = (W_in h) . m_s = h . (W_in^T m_s): the keys
+// k_s = W_in^T m_s are computed once per batch after the encoder (one tcgen05 GEMM over
+// every source position), so no per-step query GEMM exists; 'dot' uses k_s = m_s.
+// a = softmax over s < S_b only (pads excluded), c_t = sum_s a_s m_s.
+//
+// One thread-block cluster per sentence b; cluster rank r owns source positions
+// [r*CH, (r+1)*CH) (CH = ceil(S_max / nch), nch <= 8).  Each CTA
+//   * prefetches its keys / memory rows with cp.async before griddepcontrol.wait (they are
+//     constants of the translation), in sub-chunks of kSC positions, double-buffered;
+//   * computes the K x kSC scores (one warp per position, lanes over H), and keeps an
+//     online softmax per beam row (running max m_k, sum l_k) plus the unnormalised
+//     context in registers (thread = columns j, all K rows);
+//   * parks (m_k, l_k, ctx_k) in its shared memory; after a cluster barrier CTA r combines
+//     column slice r over all nch chunks through distributed shared memory, in fixed chunk
+//     order (deterministic), and writes the context into the W_out operand (columns [0, H)).
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace onmt {
+
+constexpr int kSCMax = 16;       // positions per staged sub-chunk (16, or 8 for wide H)
+constexpr int kAttThreads = 256;
+
+__device__ __forceinline__ void cp_async_rows(float* dst, const float* src, int n) {
+  const bool al = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 && (n & 3) == 0;
+  if (al) {
+    for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 4 * i)), "l"(src + 4 * i)
+                   : "memory");
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst + i)), "l"(src + i) : "memory");
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ float ld_peer(const float* local, uint32_t peer) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(mapa_peer(smem_u32(local), peer)) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 ld_peer4(const float* local, uint32_t peer) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(mapa_peer(smem_u32(local), peer))
+               : "memory");
+  return v;
+}
+
+template <int KMAX, int JPT>
+__global__ void __launch_bounds__(kAttThreads)
+attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict__ keys, int key_ld,
+                         const float* __restrict__ mem, const int* __restrict__ lens, int S_max, int H, int K, int CH,
+                         int SC, XOut xo, const int* __restrict__ done, StepCtl ctl) {
+  KT(0);
+  pdl_trigger();
+  extern __shared__ __align__(16) float sh[];
+  const int nch = gridDim.x;                      // cluster = the chunks of one sentence
+  const uint32_t r = cluster_ctarank();
+  const int b = blockIdx.y;
+  const bool same = keys == mem;
+  const int kl = same ? H : key_ld;
+  const bool vec = (H & 3) == 0 && (kl & 3) == 0;
+  auto r4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
+  // layout: q [K][H] (later: partial context) | m, l, scale [KMAX] | e [KMAX][16] |
+  //         2 x (mem [SC][H], keys [SC][kl])
+  float* q = sh;
+  float* s_m = q + r4((size_t)K * H);              // (every region 16-byte aligned)
+  float* s_l = s_m + kKMax;
+  float* s_scale = s_l + kKMax;
+  float* e = s_scale + kKMax;
+  float* buf = e + kKMax * kSCMax;
+  const size_t mb = r4((size_t)SC * H), kb = same ? 0 : r4((size_t)SC * kl);
+  auto mbuf = [&](int i) { return buf + (size_t)(i & 1) * (mb + kb); };
+  auto kbuf = [&](int i) { return same ? mbuf(i) : mbuf(i) + mb; };
+
+  // source rows [s_beg, s_lim) of this chunk, prefetched before griddepcontrol.wait without
+  // waiting for the length (rows past S_b are loaded but masked)
+  const int s_beg = (int)r * CH;
+  const int s_lim = min(S_max, s_beg + CH);
+  const int nsub_max = s_lim > s_beg ? (s_lim - s_beg + SC - 1) / SC : 0;
+  auto stage = [&](int i) {
+    const int s0 = s_beg + i * SC;
+    const int ns = min(SC, s_lim - s0);
+    cp_async_rows(mbuf(i), mem + ((size_t)b * S_max + s0) * H, ns * H);
+    if (!same) cp_async_rows(kbuf(i), keys + ((size_t)b * S_max + s0) * key_ld, ns * key_ld);
+    cp_async_commit();
+  };
+  if (nsub_max > 0) stage(0);
+  if (nsub_max > 1) stage(1);
+  KT(1);
+  pdl_wait();                                      // h_top, done flags of this step now visible
+  const bool quit = all_done(ctl) || (done && done[b]);   // uniform over the cluster
+  if (quit) {
+    cp_async_wait<0>();
+    return;
+  }
+  cp_async_rows(q, htop + (size_t)b * K * H, K * H);   // queries: the K beam rows of sentence b
+  cp_async_commit();
+  const int L = lens[b];
+  const int s_end = min(L, s_lim);
+  const int nsub = s_end > s_beg ? (s_end - s_beg + SC - 1) / SC : 0;
+  if (threadIdx.x < KMAX) { s_m[threadIdx.x] = -INFINITY; s_l[threadIdx.x] = 0.f; }
+  KT(2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float acc[KMAX][JPT];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) acc[k][u] = 0.f;
+
+  for (int i = 0; i < nsub; ++i) {
+    if (i == 0 || i + 1 >= nsub_max) cp_async_wait<0>();   // (iteration 0 also needs q)
+    else cp_async_wait<1>();
+    __syncthreads();
+    if (i == 0) KT(3);
+    const int s0 = s_beg + i * SC;
+    const int ns = min(SC, s_end - s0);
+    const float* ms = mbuf(i);
+    const float* ks = kbuf(i);
+    // ---- scores: warp w -> positions w and w + 8 (they share the q loads)
+    {
+      const int pa = warp, pb = warp + 8;
+      const bool ha = pa < ns, hb = pb < ns;
+      if (ha) {
+        float da[KMAX], db[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) { da[k] = 0.f; db[k] = 0.f; }
+        const float* kra = ks + (size_t)pa * kl;
+        const float* krb = ks + (size_t)(hb ? pb : pa) * kl;
+        if (vec) {
+          for (int j = 4 * lane; j < H; j += 128) {
+            const float4 ka = *reinterpret_cast<const float4*>(kra + j);
+            const float4 kbv = *reinterpret_cast<const float4*>(krb + j);
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k)
+              if (k < K) {
+                const float4 qv = *reinterpret_cast<const float4*>(q + (size_t)k * H + j);
+                da[k] = fmaf(qv.x, ka.x, fmaf(qv.y, ka.y, fmaf(qv.z, ka.z, fmaf(qv.w, ka.w, da[k]))));
+                db[k] = fmaf(qv.x, kbv.x, fmaf(qv.y, kbv.y, fmaf(qv.z, kbv.z, fmaf(qv.w, kbv.w, db[k]))));
+              }
+          }
+        } else {
+          for (int j = lane; j < H; j += 32) {
+            const float ka = kra[j], kbv = krb[j];
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k)
+              if (k < K) {
+                const float qv = q[(size_t)k * H + j];
+                da[k] = fmaf(qv, ka, da[k]);
+                db[k] = fmaf(qv, kbv, db[k]);
+              }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            da[k] += __shfl_xor_sync(0xffffffffu, da[k], o);
+            db[k] += __shfl_xor_sync(0xffffffffu, db[k], o);
+          }
+        if (lane == 0) {
+#pragma unroll
+          for (int k = 0; k < KMAX; ++k)
+            if (k < K) {
+              e[k * kSCMax + pa] = da[k];
+              if (hb) e[k * kSCMax + pb] = db[k];
+            }
+        }
+      }
+    }
+    __syncthreads();
+    if (i == 0) KT(4);
+    // ---- online softmax per beam row (warp k, lanes = positions)
+    for (int k = warp; k < K; k += kAttThreads / 32) {
+      const float v = lane < ns ? e[k * kSCMax + lane] : -INFINITY;
+      float mx = v;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float mo = s_m[k];
+      const float mn = fmaxf(mo, mx);
+      const float w = lane < ns ? expf(v - mn) : 0.f;
+      float sum = w;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane < kSCMax) e[k * kSCMax + lane] = w;
+      if (lane == 0) {
+        const float sc = mo == -INFINITY ? 0.f : expf(mo - mn);
+        s_scale[k] = sc;
+        s_l[k] = s_l[k] * sc + sum;
+        s_m[k] = mn;
+      }
+    }
+    __syncthreads();
+    // ---- context: thread owns columns j = tid + u*256
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) {
+      const int j = threadIdx.x + u * kAttThreads;
+      if (j >= H) continue;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) acc[k][u] *= s_scale[k];
+      for (int s = 0; s < ns; ++s) {
+        const float mv = ms[(size_t)s * H + j];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+          if (k < K) acc[k][u] = fmaf(e[k * kSCMax + s], mv, acc[k][u]);
+      }
+    }
+    __syncthreads();                               // buffer (i & 1) free for sub-chunk i + 2
+    if (i + 2 < nsub_max) stage(i + 2);
+  }
+  cp_async_wait<0>();                              // (q, and prefetches past S_b)
+  __syncthreads();
+  // ---- park the unnormalised partial context in q's place (q is no longer read)
+#pragma unroll
+  for (int u = 0; u < JPT; ++u) {
+    const int j = threadIdx.x + u * kAttThreads;
+    if (j >= H) continue;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (k < K) q[(size_t)k * H + j] = acc[k][u];
+  }
+  KT(5);
+  cluster_arrive();
+  cluster_wait();
+  KT(6);
+  // ---- combine: CTA r finalises columns [j0, j1) of every beam row over all chunks
+  float* coef = e;                                 // [8][KMAX] (e is free now)
+  if (threadIdx.x < K) {
+    const int k = threadIdx.x;
+    float mp[8], lp[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      mp[p] = p < nch ? ld_peer(s_m + k, p) : -INFINITY;
+      lp[p] = p < nch ? ld_peer(s_l + k, p) : 0.f;
+    }
+    float M = -INFINITY;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) M = fmaxf(M, mp[p]);
+    float Ls = 0.f;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const float w = mp[p] == -INFINITY ? 0.f : expf(mp[p] - M);
+      mp[p] = w;
+      Ls += lp[p] * w;
+    }
+    const float inv = 1.f / Ls;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) coef[p * KMAX + k] = mp[p] * inv;
+  }
+  __syncthreads();
+  if (vec) {
+    const int H4 = H >> 2;
+    const int j0 = (int)((long long)H4 * r / nch), j1 = (int)((long long)H4 * (r + 1) / nch);
+    const int wj = j1 - j0;
+    for (int it = threadIdx.x; it < K * wj; it += blockDim.x) {
+      const int k = it / wj, j = 4 * (j0 + it % wj);
+      float4 v[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) v[p] = p < nch ? ld_peer4(q + (size_t)k * H + j, p) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const float w = coef[p * KMAX + k];
+        c.x = fmaf(w, v[p].x, c.x); c.y = fmaf(w, v[p].y, c.y); c.z = fmaf(w, v[p].z, c.z); c.w = fmaf(w, v[p].w, c.w);
+      }
+      store_x(xo, b * K + k, j, c.x);
+      store_x(xo, b * K + k, j + 1, c.y);
+      store_x(xo, b * K + k, j + 2, c.z);
+      store_x(xo, b * K + k, j + 3, c.w);
+    }
+  } else {
+    const int j0 = (int)((long long)H * r / nch), j1 = (int)((long long)H * (r + 1) / nch);
+    const int wj = j1 - j0;
+    for (int it = threadIdx.x; it < K * wj; it += blockDim.x) {
+      const int k = it / wj, j = j0 + it % wj;
+      float v[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) v[p] = p < nch ? ld_peer(q + (size_t)k * H + j, p) : 0.f;
+      float c = 0.f;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) c = fmaf(coef[p * KMAX + k], v[p], c);
+      store_x(xo, b * K + k, j, c);
+    }
+  }
+  KT(7);
+  cluster_arrive();                                // peers may still be reading my partial
+  cluster_wait();
+  KT(8);
+}
+
+// chunks per sentence: fill the SMs with one wave of clusters (<= 8 CTAs, >= 4 positions each)
+static int att_nch(int B, int S_max, int num_sms) {
+  int nch = num_sms / (B > 0 ? B : 1);
+  nch = nch > 8 ? 8 : nch < 1 ? 1 : nch;
+  const int pos_cap = (S_max + 3) / 4;
+  return nch > pos_cap ? (pos_cap < 1 ? 1 : pos_cap) : nch;
+}
+
+template <int KMAX, int JPT>
+static cudaError_t launch_att(dim3 grid, int nch, size_t smem, cudaStream_t st, const float* htop, const float* keys,
+                              int key_ld, const float* mem, const int* lens, int S_max, int H, int K, int CH, int SC,
+                              XOut xo, const int* done, StepCtl ctl) {
+  auto fn = attention_cluster_kernel<KMAX, JPT>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kAttThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = nch;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, fn, htop, keys, key_ld, mem, lens, S_max, H, K, CH, SC, xo, done, ctl);
+}
+
+cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, const float* mem, const int* lens,
+                             int B, int S_max, int H, int K, XOut xo, const int* done, int num_sms, StepCtl ctl,
+                             cudaStream_t st) {
+  if (H > 4 * kAttThreads || K > kKMax) return cudaErrorInvalidValue;
+  const int nch = att_nch(B, S_max, num_sms);
+  const int CH = (S_max + nch - 1) / nch;
+  const bool same = keys == mem;
+  const int kl = same ? H : key_ld;
+  auto r4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
+  auto bytes = [&](int SC) {
+    return (r4((size_t)K * H) + 3 * 16 + 16 * kSCMax + 2 * (r4((size_t)SC * H) + (same ? 0 : r4((size_t)SC * kl)))) * 4;
+  };
+  const int SC = bytes(16) <= 200 * 1024 ? 16 : 8;
+  const size_t smem = bytes(SC);
+  const dim3 grid(nch, B);
+#define ONMT_ATT(KM)                                                                                              \
+  return H <= 2 * kAttThreads                                                                                     \
+             ? launch_att<KM, 2>(grid, nch, smem, st, htop, keys, key_ld, mem, lens, S_max, H, K, CH, SC, xo, done, \
+                                 ctl)                                                                             \
+             : launch_att<KM, 4>(grid, nch, smem, st, htop, keys, key_ld, mem, lens, S_max, H, K, CH, SC, xo, done, \
+                                 ctl)
+  if (K <= 1) ONMT_ATT(1);
+  if (K <= 2) ONMT_ATT(2);
+  if (K <= 4) ONMT_ATT(4);
+  if (K <= 8) ONMT_ATT(8);
+  ONMT_ATT(16);
+#undef ONMT_ATT
+}
+
+}  // namespace onmt

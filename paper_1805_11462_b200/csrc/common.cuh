@@ -15,6 +15,31 @@ namespace onmt {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Optional per-CTA phase timestamps for microbenchmarks (tools/ubench, -DONMT_KTRACE):
+// thread 0 of CTA (x, y) writes %globaltimer into g_ktrace[(y * gridDim.x + x) * 12 + i].
+#ifdef ONMT_KTRACE
+__device__ unsigned long long* g_ktrace;
+#define KT(i)                                                                                   \
+  do {                                                                                          \
+    if (threadIdx.x == 0 && g_ktrace) {                                                         \
+      unsigned long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                     \
+      g_ktrace[(blockIdx.y * gridDim.x + blockIdx.x) * 12 + (i)] = t_;                          \
+    }                                                                                           \
+  } while (0)
+#define KTX(i, cond)                                                                            \
+  do {                                                                                          \
+    if ((cond) && g_ktrace) {                                                                   \
+      unsigned long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                     \
+      g_ktrace[(blockIdx.y * gridDim.x + blockIdx.x) * 12 + (i)] = t_;                          \
+    }                                                                                           \
+  } while (0)
+#else
+#define KT(i) do {} while (0)
+#define KTX(i, cond) do {} while (0)
+#endif
+
 constexpr int kKMax = 16;     // ONMT_K_MAX
 constexpr int kBK = 64;       // K block (64 bf16 = 128 B = one swizzle row)
 constexpr int kTileM = 128;   // weight rows per tcgen05 tile (TMEM lanes)
@@ -155,6 +180,27 @@ struct GatherArgs {
   XOut x[8];           // x[0] = layer-0 operand; x[l] = layer-l operand
 };
 
+
+// Software barrier among n co-resident CTAs (thread 0 of each calls it).  One 32-bit word:
+// bits 0-15 count arrivals, bits 16-31 the generation.  The last arriver resets the count
+// and bumps the generation with a single atomic, so consecutive episodes may use a
+// different n (grids of different shapes sharing a counter).  Every participant must be
+// resident (callers guarantee grid <= #SMs at one CTA per SM, or a cluster).
+__device__ __forceinline__ void cta_group_barrier(unsigned int* b, unsigned int n) {
+  __threadfence();
+  const unsigned int old = atomicAdd(b, 1u);
+  if ((old & 0xffffu) == n - 1u) {
+    atomicAdd(b, 0x10000u - n);
+  } else {
+    const unsigned int gen = old >> 16;
+    while (true) {
+      unsigned int v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(b) : "memory");
+      if ((v >> 16) != gen) break;
+    }
+  }
+  __threadfence();
+}
 
 // launch with the programmatic-stream-serialization attribute (captured as a programmatic
 // edge inside CUDA graphs)

@@ -12,8 +12,8 @@
 //      accumulate into one fp32 TMEM accumulator).  Meanwhile warps 2-3 prefetch the
 //      epilogue's side inputs (bias, gathered c_prev) into shared memory.
 //   3. The partial tile goes TMEM -> registers -> global scratch [tile][S][n][128]
-//      (coalesced, L2-resident), then a per-tile arrival counter (release / acquire,
-//      generation-counted so it never needs a reset) waits for the tile's S splits.
+//      (coalesced, L2-resident), then a per-tile arrival barrier (release / acquire)
+//      waits for the tile's S splits.
 //   4. CTA s owns hypothesis columns [s*NC, (s+1)*NC): one bulk copy per split pulls
 //      those columns of every partial into shared memory, they are summed in fixed split
 //      order (deterministic) and the epilogue runs on them.
@@ -31,7 +31,7 @@ struct FusedArgs {
   int NC;                  // hypothesis columns owned per split (multiple of 4)
   int M;                   // valid weight rows (4H for the cell, H for tanh)
   float* scratch;          // [tiles][S][n_group][128] fp32 partial tiles
-  unsigned int* counters;  // [tiles] generation-counted arrivals
+  unsigned int* counters;  // [tiles][2] arrival barrier {count, generation}
   // EPI_CELL
   const float4* bias;      // [H] interleaved (i,f,g,o) pre-summed biases
   const float* cg;         // [rows_pad][H] c_prev gathered by parent
@@ -55,19 +55,7 @@ __device__ __forceinline__ float tanhfast(float x) {
   return copysignf(t, x);
 }
 
-#ifdef ONMT_KTRACE            // phase timestamps (microbenchmarks only): [cta][12]
-__device__ unsigned long long* g_ktrace;
-#define KT(i)                                                                                   \
-  do {                                                                                          \
-    if (threadIdx.x == 0 && g_ktrace) {                                                         \
-      unsigned long long t_;                                                                    \
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                     \
-      g_ktrace[blockIdx.x * 12 + (i)] = t_;                                                      \
-    }                                                                                           \
-  } while (0)
-#else
-#define KT(i) do {} while (0)
-#endif
+
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -225,14 +213,7 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   __syncthreads();
   KT(3);
   if (threadIdx.x == 0) {
-    // arrive; wait for the S splits of this tile (generation count: no reset needed)
-    const unsigned int old = atomicAdd(&a.counters[tile], 1u);
-    const unsigned int target = (old / (unsigned)a.S + 1u) * (unsigned)a.S;
-    while (true) {
-      unsigned int v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.counters + tile) : "memory");
-      if ((int)(v - target) >= 0) break;
-    }
+    cta_group_barrier(a.counters + 2 * tile, (unsigned)a.S);   // the tile's S splits are stored
     asm volatile("fence.proxy.async;" ::: "memory");
     KT(4);
     // (4) my columns of every split's partial: S contiguous blocks of NC/4 x 128 x 4 floats

@@ -1,0 +1,591 @@
+// One persistent kernel for the tail of a decoder step (SURVEY §8(a) A9 + A10 + A5):
+//
+//   phase A  generator + log-softmax statistics + per-CTA top-K (PAPER.md P118-119):
+//            z = W_gen h~ + b for every vocabulary id, logits never written to HBM.
+//   phase B  per hypothesis row: combine the CTA partials into log-sum-exp and row top-K.
+//   phase C  per sentence: beam selection / EOS banking / histories and the gather of the
+//            next step's decoder inputs (P136-139; beam_device.cuh).
+//
+// Grid = groups x C CTAs, one per SM (grid <= #SMs), so software grid barriers between
+// the phases are safe.  Phase A is "K-outer": CTA (g, i) owns a contiguous run of nt
+// vocabulary tiles (128 rows each) of N-group g and keeps all nt accumulators in TMEM
+// (nt * n_group <= 512 columns), so every activation K-block (hi/lo planes, the MMA B
+// operand) crosses L2 -> SM once per CTA instead of once per tile.
+//   warp 0   TMA producer: per K-block the hi/lo activation tiles + nt weight tiles
+//   warp 1   TMEM allocator + single-thread tcgen05.mma issuer (hi and lo into one fp32
+//            accumulator per tile)
+//   warps 2+ epilogue: TMEM -> registers (+bias) -> transposed shared staging (double
+//            buffered across tiles) -> two threads per hypothesis row keep a running
+//            (max, sum exp, top-K) over the CTA's vocabulary; one partial per (CTA, row).
+#include <math_constants.h>
+
+#include "beam_device.cuh"
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace onmt {
+
+constexpr int kGsStageWarps = 4;               // TMEM -> smem stagers (one per TMEM lane quarter)
+constexpr int kGsScanWarps = 10;                // scanners (2 threads x 160 hypothesis rows)
+constexpr int kGsThreads = 32 * (2 + kGsStageWarps + kGsScanWarps);
+constexpr int kGsSLD = 132;                     // staging row stride (floats)
+
+struct GenStepArgs {
+  int n_rows_pad, n_group, groups, k_blocks, n_vt, C, nt_max, stages;
+  int P;                                        // threads per hypothesis row in the scan (1 or 2)
+  const float* bias;
+  int V, K, R, rows_pad;
+  float2* ms;                                   // partials [rows_pad][C]
+  float* tz;                                    // [rows_pad][C][K]
+  int* ti;
+  float* row_lse;                               // [R]
+  float* row_z;                                 // [R][K]
+  int* row_i;
+  int phases;                                   // 1 = A, 2 = A + B, 3 = A + B + C
+  int t, max_len;
+  double lp;
+  BeamState bs;
+  GatherArgs ga;
+  unsigned int* gbar;                           // grid barrier {count, generation}
+  StepCtl ctl;
+  int dbg;                                      // microbenchmark ablations (ONMT_KTRACE builds)
+};
+
+__device__ __forceinline__ float gs_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void gs_named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// all CTAs of the grid (co-resident by construction) meet
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) cta_group_barrier(bar, gridDim.x);
+  __syncthreads();
+}
+
+// sorted (z desc, id asc) insertion into a register list (branch-free network)
+template <int KMAX>
+__device__ __forceinline__ void gs_insert(float (&tz)[KMAX], int (&ti)[KMAX], float x, int xi) {
+  bool gt[KMAX];
+#pragma unroll
+  for (int q = 0; q < KMAX; ++q) gt[q] = better(x, xi, tz[q], ti[q]);
+#pragma unroll
+  for (int q = KMAX - 1; q >= 1; --q) {
+    const float nz = gt[q - 1] ? tz[q - 1] : x;
+    const int ni = gt[q - 1] ? ti[q - 1] : xi;
+    tz[q] = gt[q] ? nz : tz[q];
+    ti[q] = gt[q] ? ni : ti[q];
+  }
+  tz[0] = gt[0] ? x : tz[0];
+  ti[0] = gt[0] ? xi : ti[0];
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kGsThreads, 1)
+gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GenStepArgs a) {
+  KT(0);
+  pdl_trigger();
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t a_bytes = kTileM * 128, b_bytes = a.n_group * 128;
+  const uint32_t stage_bytes = 2 * b_bytes + a.nt_max * a_bytes;
+  const size_t ring = (size_t)a.stages * stage_bytes;
+  const size_t stg_bytes = (size_t)a.n_group * kGsSLD * 4;
+  const size_t body = ring > 2 * stg_bytes ? ring : 2 * stg_bytes;
+  float* stg = reinterpret_cast<float*>(smem);                     // 2 x [n_group][132], overlays the ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + body);
+  uint64_t* empty = full + a.stages;
+  uint64_t* tfull = empty + a.stages;
+  uint64_t* tempty = tfull + 1;
+  uint64_t* sfull = tempty + 1;                                    // [2] staging buffer filled (stagers)
+  uint64_t* sempty = sfull + 2;                                    // [2] staging buffer scanned (scanners)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = blockIdx.x / a.C, ci = blockIdx.x % a.C;
+  const int tb = (int)((long long)ci * a.n_vt / a.C), te = (int)((long long)(ci + 1) * a.n_vt / a.C);
+  const int n0 = grp * a.n_group;
+  const int nbatch = (te - tb + a.nt_max - 1) / a.nt_max;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+    for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, kGsStageWarps);
+    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], kGsStageWarps); mbar_init(&sempty[b], kGsScanWarps); }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tslot);
+  tc_fence_before();
+  pdl_wait();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (all_done(a.ctl)) {                                           // uniform over the grid
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+    return;
+  }
+  KT(1);
+
+  // ================================================================ phase A
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int bt = 0; bt < nbatch; ++bt) {
+        const int t0 = tb + bt * a.nt_max;
+        const int nt = min(a.nt_max, te - t0);
+        if (bt > 0) mbar_wait(tempty, (bt - 1) & 1);              // staging (ring overlay) finished
+        for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
+          const int s = it % a.stages;
+          if (it >= a.stages) mbar_wait(&empty[s], ((it / a.stages) & 1) ^ 1);
+          uint8_t* st = smem + (size_t)s * stage_bytes;
+          mbar_arrive_expect_tx(&full[s], 2 * b_bytes + nt * a_bytes);
+          tma_load_2d(st, &tmX, kb * kBK, n0, &full[s]);
+          tma_load_2d(st + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[s]);
+          for (int j = 0; j < nt; ++j) tma_load_2d(st + 2 * b_bytes + j * a_bytes, &tmW, kb * kBK, (t0 + j) * kTileM, &full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_group);
+      int it = 0;
+      for (int bt = 0; bt < nbatch; ++bt) {
+        const int nt = min(a.nt_max, te - (tb + bt * a.nt_max));
+        for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
+          const int s = it % a.stages;
+          mbar_wait(&full[s], (it / a.stages) & 1);
+          tc_fence_after();
+          KTX(7, it == 0);
+          const uint32_t sb = smem_u32(smem + (size_t)s * stage_bytes);
+          for (int j = 0; j < nt; ++j) {
+            const uint32_t sa = sb + 2 * b_bytes + j * a_bytes;
+            const uint32_t d = tmem + j * a.n_group;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              const uint64_t da = umma_desc_sw128(sa + kk * 32);
+              tc_mma_bf16(d, da, umma_desc_sw128(sb + kk * 32), idesc, (kb | kk) != 0);
+              tc_mma_bf16(d, da, umma_desc_sw128(sb + b_bytes + kk * 32), idesc, 1u);
+            }
+          }
+          tc_commit(&empty[s]);
+        }
+        tc_commit(tfull);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 2 + kGsStageWarps) {
+    // ---------------- stagers: accumulator j -> (+bias) -> smem buf[j & 1][c][v] (transposed)
+    const int q = warp & 3;                                        // TMEM lane quarter of this warp
+    const int vr = q * 32 + lane;                                  // vocabulary row this thread stages
+    for (int bt = 0; bt < nbatch; ++bt) {
+      const int t0 = tb + bt * a.nt_max;
+      const int nt = min(a.nt_max, te - t0);
+      float bias_r[4];                                             // bias of my vocabulary row, loaded
+#pragma unroll                                                     // while the MMAs run
+      for (int j = 0; j < 4; ++j) {
+        const int vid = (t0 + j) * kTileM + vr;
+        bias_r[j] = (j < nt && vid < a.V) ? __ldg(&a.bias[vid]) : -INFINITY;
+      }
+      mbar_wait(tfull, bt & 1);
+      tc_fence_after();
+      KTX(2, threadIdx.x == 64 && bt == 0);
+      for (int j = 0; j < nt; ++j) {
+        const int jj = bt * a.nt_max + j;                          // staging sequence number
+        const int buf = jj & 1;
+        if (jj >= 2) mbar_wait(&sempty[buf], ((jj >> 1) - 1) & 1);
+        KTX(6, threadIdx.x == 64 && jj == 2);
+#ifdef ONMT_KTRACE
+        if (a.dbg != 1)
+#endif
+        {
+          const float bias = j == 0 ? bias_r[0] : j == 1 ? bias_r[1] : j == 2 ? bias_r[2] : bias_r[3];
+          const uint32_t trow = tmem + j * a.n_group + ((uint32_t)(q * 32) << 16);
+          float* dst = stg + (size_t)buf * a.n_group * kGsSLD + vr;
+          // 32-column chunks, software-pipelined: the load of chunk i+1 is in flight while
+          // chunk i is stored (n_group is a multiple of 16: a last half chunk uses x16)
+          auto issue = [&](int c0, uint32_t* r) {
+            if (c0 + 32 <= a.n_group) tmem_ld32_nw(trow + c0, r);
+            else tmem_ld16_nw(trow + c0, r);
+          };
+          auto put = [&](int c0, uint32_t* r) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              if (c0 + k < a.n_group) dst[(size_t)(c0 + k) * kGsSLD] = __uint_as_float(r[k]) + bias;
+          };
+          uint32_t ra[32], rb[32];
+          issue(0, ra);
+          tmem_wait_ld();
+          tmem_fence_regs(ra);
+          for (int c0 = 0; c0 < a.n_group; c0 += 64) {
+            if (c0 + 32 < a.n_group) issue(c0 + 32, rb);
+            put(c0, ra);
+            tmem_wait_ld();
+            tmem_fence_regs(rb);
+            if (c0 + 32 >= a.n_group) break;
+            if (c0 + 64 < a.n_group) issue(c0 + 64, ra);
+            put(c0 + 32, rb);
+            tmem_wait_ld();
+            tmem_fence_regs(ra);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(&sfull[buf]);
+        KTX(10, threadIdx.x == 64 && bt == 0 && j == 0);
+      }
+      tc_fence_before();                                           // batch's accumulators drained
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(tempty);
+    }
+  } else {
+    // ---------------- scanners: P threads per hypothesis row keep (max, sum exp, top-K)
+    const int et = threadIdx.x - 32 * (2 + kGsStageWarps);         // 0 .. 32*kGsScanWarps-1
+    const int P = a.P;
+    const int c = et / P, part = et % P;                           // hypothesis row (column) and part
+    const int nv = kTileM / P;                                     // vocabulary rows scanned per tile
+    const bool row_ok = c < a.n_group && n0 + c < a.R;
+    constexpr float L2E = 1.4426950408889634f;
+    float run_m = -INFINITY, run_s = 0.f;
+    float tz[KMAX];
+    int ti[KMAX];
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) {                               // sentinels: effective length K
+      const bool sent = i < KMAX - a.K;
+      tz[i] = sent ? INFINITY : -INFINITY;
+      ti[i] = sent ? -1 : 0x7fffffff;
+    }
+    int jj = 0;
+    for (int bt = 0; bt < nbatch; ++bt) {
+      const int t0 = tb + bt * a.nt_max;
+      const int nt = min(a.nt_max, te - t0);
+      for (int j = 0; j < nt; ++j, ++jj) {
+        const int buf = jj & 1;
+        mbar_wait(&sfull[buf], (jj >> 1) & 1);
+#ifdef ONMT_KTRACE
+        if (a.dbg == 2) { __syncwarp(); if (lane == 0) mbar_arrive_local(&sempty[buf]); continue; }
+#endif
+        if (row_ok) {
+          const float* col = stg + (size_t)buf * a.n_group * kGsSLD + (size_t)c * kGsSLD + part * nv;
+          const int vbase = (t0 + j) * kTileM + part * nv;
+          for (int u0 = 0; u0 < nv; u0 += 64) {                    // 64 logits per chunk, in registers
+            float z[64];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const float4 w = *reinterpret_cast<const float4*>(col + u0 + 4 * k);
+              z[4 * k] = w.x; z[4 * k + 1] = w.y; z[4 * k + 2] = w.z; z[4 * k + 3] = w.w;
+            }
+            float g[16];                                           // group maxima (groups of 4)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) g[k] = fmaxf(fmaxf(z[4 * k], z[4 * k + 1]), fmaxf(z[4 * k + 2], z[4 * k + 3]));
+            float cmax = g[0];
+#pragma unroll
+            for (int k = 1; k < 16; ++k) cmax = fmaxf(cmax, g[k]);
+            const float mn = fmaxf(run_m, cmax);
+#ifdef ONMT_KTRACE
+            if (a.dbg == 4) { run_m = mn; } else
+#endif
+            if (mn != -INFINITY) {
+              const float mo = mn * L2E;
+              float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+              for (int k = 0; k < 64; k += 4) {
+                s0 += gs_ex2(fmaf(z[k], L2E, -mo)); s1 += gs_ex2(fmaf(z[k + 1], L2E, -mo));
+                s2 += gs_ex2(fmaf(z[k + 2], L2E, -mo)); s3 += gs_ex2(fmaf(z[k + 3], L2E, -mo));
+              }
+              run_s = (run_m == -INFINITY ? 0.f : run_s * gs_ex2((run_m - mn) * L2E)) + ((s0 + s1) + (s2 + s3));
+              run_m = mn;
+            }
+#ifdef ONMT_KTRACE
+            if (a.dbg == 3) continue;
+#endif
+            // top-K.  Candidates: z > list tail, and z >= the K-th largest group maximum of
+            // this chunk (a lower bound of the chunk's K-th value - it is the K-th largest of
+            // a subset - so nothing below it can enter).  The bound matters on the first
+            // chunks, when the list is still cold.  Ids increase along the scan, so a value
+            // compare decides every insertion (a tie never displaces an earlier id).
+            float th = tz[KMAX - 1];
+            if (cmax > th) {
+              if (th == -INFINITY || u0 == 0) {
+                float gk = -INFINITY;                              // K-th largest of g (K <= 16)
+#pragma unroll
+                for (int rnd = 0; rnd < KMAX; ++rnd) {
+                  if (rnd < a.K) {
+                    float mx = g[0];
+#pragma unroll
+                    for (int k = 1; k < 16; ++k) mx = fmaxf(mx, g[k]);
+                    gk = mx;
+                    bool hit = false;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                      const bool h = !hit && g[k] == mx;
+                      g[k] = h ? -INFINITY : g[k];
+                      hit |= h;
+                    }
+                  }
+                }
+                th = fmaxf(th, gk);
+              }
+              unsigned m0 = 0, m1 = 0;
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                m0 |= (z[k] >= th) ? (1u << k) : 0u;
+                m1 |= (z[k + 32] >= th) ? (1u << k) : 0u;
+              }
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                unsigned msk = h ? m1 : m0;
+                while (msk) {                                      // candidates in id order
+                  const int k = __ffs(msk) - 1 + 32 * h;
+                  msk &= msk - 1;
+                  const float zk = col[u0 + k];
+                  if (zk > tz[KMAX - 1]) gs_insert<KMAX>(tz, ti, zk, vbase + u0 + k);
+#ifdef ONMT_GS_DEBUG
+                  if (c == 0 && blockIdx.x == 0)
+                    printf("part %d cand id %d z %f -> [%f %f %f %f] [%d %d %d %d] th %f\n", part, vbase + u0 + k, zk,
+                           tz[0], tz[1 % KMAX], tz[2 % KMAX], tz[3 % KMAX], ti[0], ti[1 % KMAX], ti[2 % KMAX], ti[3 % KMAX], th);
+#endif
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(&sempty[buf]);
+      }
+    }
+    KTX(8, et == 0);
+    // ---- combine the P parts of a row (adjacent lanes, butterfly) and write the CTA's partial
+    for (int o = 1; o < P; o <<= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, run_m, o), os = __shfl_xor_sync(0xffffffffu, run_s, o);
+      const float M = fmaxf(run_m, om);
+      float S = 0.f;
+      if (run_m != -INFINITY) S += run_s * gs_ex2((run_m - M) * L2E);
+      if (om != -INFINITY) S += os * gs_ex2((om - M) * L2E);
+      run_m = M;
+      run_s = S;
+      float oz[KMAX];
+      int oi[KMAX];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) {
+        oz[i] = __shfl_xor_sync(0xffffffffu, tz[i], o);
+        oi[i] = __shfl_xor_sync(0xffffffffu, ti[i], o);
+      }
+#pragma unroll
+      for (int i = KMAX - 1; i >= 0; --i)                         // both lists hold K real entries at the tail
+        if (i >= KMAX - a.K && better(oz[i], oi[i], tz[KMAX - 1], ti[KMAX - 1])) gs_insert<KMAX>(tz, ti, oz[i], oi[i]);
+    }
+    KTX(9, et == 0);
+#ifdef ONMT_GS_DEBUG
+    if (c == 0 && blockIdx.x == 0)
+      printf("final part %d [%f %f %f %f] [%d %d %d %d]\n", part, tz[0], tz[1 % KMAX], tz[2 % KMAX], tz[3 % KMAX], ti[0],
+             ti[1 % KMAX], ti[2 % KMAX], ti[3 % KMAX]);
+#endif
+    if (row_ok && part == 0) {
+      const int r = n0 + c;
+      a.ms[(size_t)r * a.C + ci] = make_float2(run_m, run_s);
+      const size_t base = ((size_t)r * a.C + ci) * a.K;
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i)
+        if (i >= KMAX - a.K) {
+          a.tz[base + i - (KMAX - a.K)] = tz[i];
+          a.ti[base + i - (KMAX - a.K)] = ti[i];
+        }
+    }
+  }
+  KT(3);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (a.phases < 2) return;
+
+  // ================================================================ phase B
+  // CTA i reduces rows i, i + G, ...: its warps split the C partials of the row (one
+  // partial per lane, all loads in flight), then warp and CTA merges in fixed order.
+  grid_barrier(a.gbar);
+  KT(4);
+  {
+    __shared__ float sb_m[16], sb_s[16];
+    __shared__ float sb_z[16][kKMax];
+    __shared__ int sb_i[16][kKMax];
+    const int nw = blockDim.x >> 5;
+    const int per_w = (a.C + nw - 1) / nw;                          // partials per warp (<= 32)
+    for (int r = blockIdx.x; r < a.R; r += gridDim.x) {
+      const int p = warp * per_w + lane;
+      const bool ok = lane < per_w && p < a.C;
+      float2 v = ok ? __ldcg(&a.ms[(size_t)r * a.C + p]) : make_float2(-INFINITY, 0.f);
+      float lz[KMAX];
+      int li[KMAX];
+      const size_t base = ((size_t)r * a.C + p) * a.K;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        const bool ck = ok && k < a.K;
+        lz[k] = ck ? __ldcg(&a.tz[base + k]) : -INFINITY;
+        li[k] = ck ? __ldcg(&a.ti[base + k]) : 0x7fffffff;
+      }
+      float m = v.x, sm = v.x == -INFINITY ? 0.f : v.y;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sm, o);
+        const float M = fmaxf(m, m2);
+        sm = (m == -INFINITY ? 0.f : sm * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
+        m = M;
+      }
+      // warp top-K: K rounds of arg-max over the lanes' sorted lists (heads at index 0)
+      for (int k = 0; k < a.K; ++k) {
+        float bz = lz[0];
+        int bi = li[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float z2 = __shfl_xor_sync(0xffffffffu, bz, o);
+          const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (better(z2, i2, bz, bi)) { bz = z2; bi = i2; }
+        }
+        if (lane == 0) { sb_z[warp][k] = bz; sb_i[warp][k] = bi; }
+        if (li[0] == bi && lz[0] == bz) {
+#pragma unroll
+          for (int i = 0; i < KMAX - 1; ++i) { lz[i] = lz[i + 1]; li[i] = li[i + 1]; }
+          lz[KMAX - 1] = -INFINITY;
+          li[KMAX - 1] = 0x7fffffff;
+        }
+      }
+      if (lane == 0) { sb_m[warp] = m; sb_s[warp] = sm; }
+      __syncthreads();
+      if (warp == 0) {                                              // CTA merge of the nw warp results
+        float M = lane < nw ? sb_m[lane] : -INFINITY;
+        float S = lane < nw ? sb_s[lane] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float m2 = __shfl_xor_sync(0xffffffffu, M, o), s2 = __shfl_xor_sync(0xffffffffu, S, o);
+          const float Mx = fmaxf(M, m2);
+          S = (M == -INFINITY ? 0.f : S * __expf(M - Mx)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - Mx));
+          M = Mx;
+        }
+        if (lane == 0) a.row_lse[r] = M + logf(S);
+        int h = 0;                                                  // lane w walks warp w's sorted list
+        for (int k = 0; k < a.K; ++k) {
+          float bz = (lane < nw && h < a.K) ? sb_z[lane][h] : -INFINITY;
+          int bi = (lane < nw && h < a.K) ? sb_i[lane][h] : 0x7fffffff;
+          const float mz = bz;
+          const int mi = bi;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const float z2 = __shfl_xor_sync(0xffffffffu, bz, o);
+            const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (better(z2, i2, bz, bi)) { bz = z2; bi = i2; }
+          }
+          if (lane == 0) { a.row_z[(size_t)r * a.K + k] = bz; a.row_i[(size_t)r * a.K + k] = bi; }
+          if (mz == bz && mi == bi && lane < nw) ++h;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (a.phases < 3) return;
+
+  // ================================================================ phase C
+  grid_barrier(a.gbar);
+  KT(5);
+  for (int r = blockIdx.x; r < a.R; r += gridDim.x) {
+    select_gather_row<KMAX>(r, 0, 1, a.R, a.row_lse, a.row_z, a.row_i, a.K, a.t, a.max_len, a.lp, a.bs, a.ga);
+    __syncthreads();
+  }
+  KTX(11, threadIdx.x == 0);
+}
+
+static size_t gs_smem_bytes(int n_group, int nt_max, int stages) {
+  const size_t ring = (size_t)stages * (2 * (size_t)n_group * 128 + (size_t)nt_max * kTileM * 128);
+  const size_t stg = 2 * (size_t)n_group * kGsSLD * 4;
+  return 1024 + (ring > stg ? ring : stg) + (2 * stages + 6) * 8 + 16;
+}
+
+struct GsPlan {
+  int C, nt_max, stages, P;
+};
+static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, GsPlan& p) {
+  p.C = num_sms / groups;
+  if (p.C > n_vt) p.C = n_vt;
+  if (p.C < 1) return false;
+  p.nt_max = 512 / ((n_group + 31) / 32 * 32);                      // accumulators in TMEM
+  if (p.nt_max > 4) p.nt_max = 4;                                    // (bias registers of the stagers)
+  const int need = (n_vt + p.C - 1) / p.C;
+  if (p.nt_max > need) p.nt_max = need;
+  if (p.nt_max < 1) return false;
+  p.P = 2 * n_group <= 32 * kGsScanWarps ? 2 : 1;
+  if (n_group > 32 * kGsScanWarps) return false;
+  const size_t limit = 227 * 1024 - 6144;         // (static shared memory of phases B / C: <= 4.5 KB)
+  p.stages = 4;
+  while (p.stages > 2 && gs_smem_bytes(n_group, p.nt_max, p.stages) > limit) --p.stages;
+  while (p.nt_max > 1 && gs_smem_bytes(n_group, p.nt_max, p.stages) > limit) --p.nt_max;
+  return gs_smem_bytes(n_group, p.nt_max, p.stages) <= limit;
+}
+
+// parts per row written by the step kernel's phase A (0 = not applicable)
+int g_gs_dbg = 0;
+int gen_step_parts(int n_vt, int n_group, int groups, int num_sms) {
+  GsPlan p;
+  return gs_plan(n_vt, n_group, groups, num_sms, p) ? p.C : 0;
+}
+
+template <int KMAX>
+static cudaError_t launch_gs(const CUtensorMap& tmW, const CUtensorMap& tmX, const GenStepArgs& a, int grid,
+                             size_t smem, cudaStream_t st) {
+  auto fn = gen_step_kernel<KMAX>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(fn, dim3(grid), dim3(kGsThreads), smem, st, tmW, tmX, a);
+}
+
+// phases: 1 = generator partials, 2 = + row LSE / top-K, 3 = + beam step and gather
+cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
+                     int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i,
+                     int phases, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
+                     unsigned int* gbar, StepCtl ctl, cudaStream_t st) {
+  const int groups = n_rows_pad / n_group;
+  GsPlan p;
+  if (!gs_plan(n_vt, n_group, groups, num_sms, p)) return cudaErrorInvalidConfiguration;
+  GenStepArgs a{};
+  a.n_rows_pad = n_rows_pad;
+  a.n_group = n_group;
+  a.groups = groups;
+  a.k_blocks = k_blocks;
+  a.n_vt = n_vt;
+  a.C = p.C;
+  a.nt_max = p.nt_max;
+  a.stages = p.stages;
+  a.P = p.P;
+  a.bias = g.bias;
+  a.V = g.V;
+  a.K = g.K;
+  a.R = g.rows_valid;
+  a.rows_pad = g.rows_pad;
+  a.ms = g.ms;
+  a.tz = g.tz;
+  a.ti = g.ti;
+  a.row_lse = row_lse;
+  a.row_z = row_z;
+  a.row_i = row_i;
+  a.phases = phases;
+  a.t = t;
+  a.max_len = max_len;
+  a.lp = lp;
+  a.bs = bs;
+  a.ga = ga;
+  a.gbar = gbar;
+  a.ctl = ctl;
+  a.dbg = g_gs_dbg;
+  const int grid = p.C * groups;
+  const size_t smem = gs_smem_bytes(n_group, p.nt_max, p.stages);
+  if (g.K <= 1) return launch_gs<1>(tmW, tmX, a, grid, smem, st);
+  if (g.K <= 2) return launch_gs<2>(tmW, tmX, a, grid, smem, st);
+  if (g.K <= 4) return launch_gs<4>(tmW, tmX, a, grid, smem, st);
+  if (g.K == 5) return launch_gs<5>(tmW, tmX, a, grid, smem, st);     // (the paper's beam size)
+  if (g.K <= 8) return launch_gs<8>(tmW, tmX, a, grid, smem, st);
+  return launch_gs<16>(tmW, tmX, a, grid, smem, st);
+}
+
+}  // namespace onmt

@@ -36,6 +36,11 @@ cudaError_t tc_gemm_gen(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pa
 cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                               int k_blocks, int num_sms, int cs, const GenOut& g, StepCtl ctl, cudaStream_t st);
 int gen_persistent_parts(int n_vt, int n_groups, int num_sms, int cs);
+int gen_step_parts(int n_vt, int n_group, int groups, int num_sms);
+cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
+                     int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i,
+                     int phases, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
+                     unsigned int* gbar, StepCtl ctl, cudaStream_t st);
 int gen_cluster_size(int n_group, int n_vt, int n_groups, int num_sms);
 extern unsigned long long* g_gen_dbg;
 
@@ -61,15 +66,14 @@ void launch_enc_cell(const float* Z, int z_ld, const float* P, int splits, int p
 void launch_dec_cell(const float* P, int splits, int p_rows_pad, int p_ld, const float* bias, const float* cg,
                      float* c_out, float* h_out, int H, int R, CellDst dst, StepCtl ctl, cudaStream_t st);
 cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, const float* mem, const int* lens,
-                             int B, int S_max, int H, int K, XOut xo, const int* done, float* part_m, float* part_s,
-                             float* part_c, int* tickets, StepCtl ctl, cudaStream_t st);
-int attention_chunks(int S_max);
+                             int B, int S_max, int H, int K, XOut xo, const int* done, int num_sms, StepCtl ctl,
+                             cudaStream_t st);
 void launch_attn_out(const float* P, int splits, int p_rows_pad, int p_ld, float* htilde, int H, int R, XOut xg,
                      StepCtl ctl, cudaStream_t st);
 void launch_init_decode(const BeamState& bs, int B, int K, const float* enc_h, const float* enc_c, int L, int H,
                         float* dec_h, float* dec_c, int dec_rows_pad, float* htilde, cudaStream_t st);
 void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepCtl ctl, cudaStream_t st);
-void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_parts, int rows_pad, int B, int K,
+void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_parts, int ps, int rs, int B, int K,
                        int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga, float* row_lse,
                        float* row_z, int* row_i, StepCtl ctl, cudaStream_t st);
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
@@ -278,6 +282,7 @@ struct onmt_model {
   bool gen_mc = false;         // generator activation multicast across 4-CTA clusters (measured slower on c2)
   bool fused = true;           // split-K GEMM with the reduction and the cell / tanh epilogue fused in
                                // (one launch per layer instead of GEMM + consumer kernel)
+  bool gen_step = true;        // generator + row reduce + beam step as one persistent kernel (gen_step.cu)
   bool use_graph = true;
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -302,8 +307,8 @@ struct onmt_model {
   Act xo, xg;
   DevBuf dec_p, st_h, st_c, st_cg, htilde, logits;
   DevBuf f_scratch, f_count;                 // fused GEMM partial tiles + per-tile arrival counters
+  DevBuf g_bar;                              // grid barrier counter of the generator step kernel
   DevBuf g_ms, g_tz, g_ti;
-  DevBuf a_pm, a_ps, a_pc, a_tick;
   DevBuf row_lse, row_z, row_i;
   DevBuf b_cum, b_live, b_y, b_prow, b_done, b_ndone, b_bt, b_br, b_braw, b_bnorm;
   DevBuf h_par, h_tok, h_lp, s_score, s_par;
@@ -373,8 +378,13 @@ static int gen_cs(onmt_model* m, const Act& X) {
   const int n_vt = (m->Vt + kVTile - 1) / kVTile;
   return m->gen_mc ? gen_cluster_size(X.n_group, n_vt, X.rows_pad / X.n_group, m->num_sms) : 1;
 }
+static bool use_gen_step(onmt_model* m, const Act& X) {
+  const int n_vt = (m->Vt + kVTile - 1) / kVTile;
+  return m->use_tc && m->gen_step && gen_step_parts(n_vt, X.n_group, X.rows_pad / X.n_group, m->num_sms) > 0;
+}
 static int gen_parts(onmt_model* m, const Act& X) {
   const int n_vt = (m->Vt + kVTile - 1) / kVTile;
+  if (use_gen_step(m, X)) return gen_step_parts(n_vt, X.n_group, X.rows_pad / X.n_group, m->num_sms);
   return m->use_tc ? gen_persistent_parts(n_vt, X.rows_pad / X.n_group, m->num_sms, gen_cs(m, X)) : n_vt;
 }
 
@@ -678,16 +688,6 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
   m->g_ms.ensure((size_t)n_vt * rp * 8);
   m->g_tz.ensure((size_t)n_vt * rp * K * 4);
   m->g_ti.ensure((size_t)n_vt * rp * K * 4);
-  {
-    const size_t nch = attention_chunks(S_max);
-    m->a_pm.ensure(B * nch * K * 4);
-    m->a_ps.ensure(B * nch * K * 4);
-    m->a_pc.ensure(B * nch * K * (size_t)H * 4);
-    if (m->a_tick.bytes < (size_t)B * 4) {
-      m->a_tick.ensure((size_t)B * 4);
-      ONMT_CUDA(cudaMemset(m->a_tick.p, 0, m->a_tick.bytes));
-    }
-  }
   m->row_lse.ensure((size_t)R * 4);
   m->row_z.ensure((size_t)R * K * 4);
   m->row_i.ensure((size_t)R * K * 4);
@@ -721,7 +721,11 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
       fs = std::max(fs, fused_scratch_floats(m->dec_w[l]->m_pad, m->xdec[l]->rows_pad, m->xdec[l]->n_group,
                                              m->dec_w[l]->k_pad / kBK, m->num_sms));
     m->f_scratch.ensure(std::max<size_t>(fs, 1) * 4);
-    const size_t nc = (size_t)(L + 1) * 1024 * 4;
+    if (!m->g_bar.p) {
+      m->g_bar.ensure(256);
+      ONMT_CUDA(cudaMemset(m->g_bar.p, 0, 256));
+    }
+    const size_t nc = (size_t)(L + 1) * 2048 * 4;
     if (m->f_count.bytes < nc) {
       m->f_count.ensure(nc);
       ONMT_CUDA(cudaMemset(m->f_count.p, 0, nc));
@@ -778,7 +782,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
         cudaError_t e = tc_gemm_cell(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, R, W.k_pad / kBK,
                                      m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H, cc + (size_t)l * rp * H,
                                      hh + (size_t)l * rp * H, H, dst, m->f_scratch.as<float>(),
-                                     m->f_count.as<unsigned int>() + (size_t)l * 1024, m->num_sms, ctl, m->stream);
+                                     m->f_count.as<unsigned int>() + (size_t)l * 2048, m->num_sms, ctl, m->stream);
         prof_end(m, "gemm", pg);
         if (e != cudaErrorInvalidConfiguration) {   // (no cluster shape fits: unfused path below)
           ONMT_CUDA(e);
@@ -801,8 +805,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       const float* keys = m->general ? m->keys.as<float>() : m->mem.as<float>();
       const int key_ld = m->general ? m->attn_win_t.m_pad : H;
       ONMT_CUDA(launch_attention(htop, keys, key_ld, m->mem.as<float>(), d_lens, B, S_max, H, K, m->xo.xo(bf),
-                                 bs.done, m->a_pm.as<float>(), m->a_ps.as<float>(), m->a_pc.as<float>(),
-                                 m->a_tick.as<int>(), ctl, m->stream));
+                                 bs.done, m->num_sms, ctl, m->stream));
       count(m);
       prof_end(m, "attention", pa);
     }
@@ -811,7 +814,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       EvPair pg = prof_begin(m, "gemm");
       fe = tc_gemm_tanh(m->attn_wout.tmap, m->xo.tmap, m->attn_wout.m_pad, m->xo.rows_pad, m->xo.n_group, R,
                         m->attn_wout.k_pad / kBK, H, m->htilde.as<float>(), m->xg.xo(bf), m->f_scratch.as<float>(),
-                        m->f_count.as<unsigned int>() + (size_t)L * 1024, m->num_sms, ctl, m->stream);
+                        m->f_count.as<unsigned int>() + (size_t)L * 2048, m->num_sms, ctl, m->stream);
       prof_end(m, "gemm", pg);
       if (fe != cudaErrorInvalidConfiguration) {
         ONMT_CUDA(fe);
@@ -828,12 +831,28 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       count(m);
       prof_end(m, "attn_out", po);
     }
-    gen(m, m->xg, g, ctl);
-    EvPair pm = prof_begin(m, "merge");
-    launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, B, K, t, max_len, std::pow((5.0 + t) / 6.0, (double)alpha), bs, ga,
-                      m->row_lse.as<float>(), m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
-    count(m, 2);
-    prof_end(m, "merge", pm);
+    const double lp = std::pow((5.0 + t) / 6.0, (double)alpha);
+    if (use_gen_step(m, m->xg)) {
+      // K-outer generator (phase A of gen_step.cu), partials [row][C]; then row reduce + beam step
+      EvPair pgs = prof_begin(m, "gen");
+      ONMT_CUDA(gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
+                         m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
+                         m->row_i.as<int>(), 1, t, max_len, lp, bs, ga, m->g_bar.as<unsigned int>(), ctl, m->stream));
+      count(m);
+      prof_end(m, "gen", pgs);
+      EvPair pm = prof_begin(m, "merge");
+      launch_beam_merge(g.ms, g.tz, g.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
+                        m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
+      count(m, 2);
+      prof_end(m, "merge", pm);
+    } else {
+      gen(m, m->xg, g, ctl);
+      EvPair pm = prof_begin(m, "merge");
+      launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, 1, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
+                        m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
+      count(m, 2);
+      prof_end(m, "merge", pm);
+    }
     prof_end(m, "step", ev);
   }
   launch_finalize(bs, B, K, max_len, out.hyps, out.lens, out.scores, out.raw, out.tlogp, m->stream);
@@ -943,6 +962,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   if (const char* ev = std::getenv("ONMT_USE_GRAPH")) m->use_graph = std::atoi(ev) != 0;   // ncu runs use 0
   if (const char* ev = std::getenv("ONMT_GEN_MULTICAST")) m->gen_mc = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_FUSED_GEMM")) m->fused = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_GEN_STEP")) m->gen_step = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
@@ -978,6 +998,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->fused = v != 0;
   } else if (n == "gen_multicast") {
     m->gen_mc = v != 0;
+  } else if (n == "gen_step") {
+    m->gen_step = v != 0;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
   } else {
@@ -1236,7 +1258,18 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
     ONMT_CUDA(cudaMemset(dbg.p, 0, 256 * 8));
     g_gen_dbg = dbg.as<unsigned long long>();
   }
-  gen(m, x, g, StepCtl{nullptr, 0});
+  const bool gs = use_gen_step(m, x);
+  if (gs) {
+    if (!m->g_bar.p) {
+      m->g_bar.ensure(256);
+      ONMT_CUDA(cudaMemset(m->g_bar.p, 0, 256));
+    }
+    ONMT_CUDA(gen_step(m->gen_w.tmap, x.tmap, (m->Vt + kVTile - 1) / kVTile, x.rows_pad, x.n_group,
+                       m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 2, 0, 0, 1.0,
+                       BeamState{}, GatherArgs{}, m->g_bar.as<unsigned int>(), StepCtl{nullptr, 0}, m->stream));
+  } else {
+    gen(m, x, g, StepCtl{nullptr, 0});
+  }
   g_gen_dbg = nullptr;
   if (trace_gen) {
     std::vector<unsigned long long> h(256);
@@ -1254,7 +1287,9 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
                    rel(h[128 + j]), rel(h[144 + j]), rel(h[160 + 2 * j]), rel(h[176 + 2 * j]), rel(h[161 + 2 * j]),
                    rel(h[177 + 2 * j]));
   }
-  launch_row_reduce(g.ms, g.tz, g.ti, n_parts, x.rows_pad, R, k, dl.as<float>(), dz.as<float>(), di.as<int>(), m->stream);
+  if (!gs)
+    launch_row_reduce(g.ms, g.tz, g.ti, n_parts, x.rows_pad, R, k, dl.as<float>(), dz.as<float>(), di.as<int>(),
+                      m->stream);
   ONMT_CUDA(cudaGetLastError());
   ONMT_CUDA(cudaMemcpyAsync(lse, dl.p, (size_t)R * 4, cudaMemcpyDeviceToHost, m->stream));
   ONMT_CUDA(cudaMemcpyAsync(top_z, dz.p, (size_t)R * k * 4, cudaMemcpyDeviceToHost, m->stream));

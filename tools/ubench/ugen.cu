@@ -1,0 +1,96 @@
+// Microbenchmark of the persistent generator step kernel (gen_step.cu), c2 shape
+// (R = 150 rows, H = 500, V = 50000, K = 5), phases A (+B), with per-CTA phase stamps.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DONMT_KTRACE -I../../paper_1805_11462_b200/csrc \
+//      -I../../include ugen.cu -lcuda -o ugen
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+#include "../../paper_1805_11462_b200/csrc/gen_step.cu"
+using namespace onmt;
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static CUtensorMap make_tmap(const void* base, int k_pad, int rows, int box_rows) {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) { void* p = nullptr; cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q)); fn = (PFN_encodeTiled_t)p; }
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)k_pad, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)k_pad * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("tmap\n"); exit(1); }
+  return m;
+}
+int main(int argc, char** argv) {
+  const int phases = argc > 1 ? atoi(argv[1]) : 1;
+  g_gs_dbg = argc > 2 ? atoi(argv[2]) : 0;
+  cudaStream_t st; CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const int R = 150, NP = 160, KP = 512, V = 50000, VP = 50048, K = 5, C = 148;
+  __nv_bfloat16 *W, *X; float* bias;
+  CK(cudaMalloc(&W, (size_t)VP * KP * 2)); CK(cudaMalloc(&X, (size_t)2 * NP * KP * 2)); CK(cudaMalloc(&bias, VP * 4));
+  {  // realistic values: W ~ U(-0.1, 0.1) bf16, activations tanh-like (hi plane; lo = 0), bias ~ U(-0.1, 0.1)
+    std::vector<__nv_bfloat16> hw((size_t)VP * KP), hx((size_t)2 * NP * KP);
+    std::vector<float> hb(VP);
+    unsigned long long st_ = 88172645463325252ull;
+    auto rnd = [&]() { st_ ^= st_ << 13; st_ ^= st_ >> 7; st_ ^= st_ << 17; return (st_ >> 11) * (1.0 / 9007199254740992.0); };
+    for (size_t i = 0; i < hw.size(); ++i) hw[i] = __float2bfloat16((i % KP) < 500 ? (float)(0.2 * rnd() - 0.1) : 0.f);
+    for (size_t i = 0; i < hx.size(); ++i) hx[i] = __float2bfloat16(i < (size_t)NP * KP && (i % KP) < 500 ? (float)tanh(3 * rnd() - 1.5) : 0.f);
+    for (int i = 0; i < VP; ++i) hb[i] = i < V ? (float)(0.2 * rnd() - 0.1) : 0.f;
+    CK(cudaMemcpy(W, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(X, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(bias, hb.data(), VP * 4, cudaMemcpyHostToDevice));
+  }
+  CUtensorMap tmW = make_tmap(W, KP, VP, 128), tmX = make_tmap(X, KP, 2 * NP, NP);
+  float2* ms; float *tz, *rl, *rz; int *ti, *ri; unsigned int* gbar;
+  CK(cudaMalloc(&ms, C * NP * 8)); CK(cudaMalloc(&tz, C * NP * K * 4)); CK(cudaMalloc(&ti, C * NP * K * 4));
+  CK(cudaMalloc(&rl, R * 4)); CK(cudaMalloc(&rz, R * K * 4)); CK(cudaMalloc(&ri, R * K * 4));
+  CK(cudaMalloc(&gbar, 64)); CK(cudaMemset(gbar, 0, 64));
+  unsigned long long* tr; CK(cudaMalloc(&tr, 4096 * 96)); CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
+  GenOut g{ms, tz, ti, bias, V, K, R, NP};
+  // beam state / gather operands for phase C (zeroed; slot 0 of every sentence live)
+  const int B = R / K, H = 500, E = 500, L = 2, MAXLEN = 100;
+  auto zalloc = [&](size_t bytes) { void* p; CK(cudaMalloc(&p, bytes)); CK(cudaMemset(p, 0, bytes)); return p; };
+  BeamState bs{};
+  bs.cum = (double*)zalloc(2 * R * 8); bs.live = (int*)zalloc(2 * R * 4); bs.y = (int*)zalloc(R * 4);
+  bs.prow = (int*)zalloc(R * 4); bs.done = (int*)zalloc(B * 4); bs.n_done = (int*)zalloc(4);
+  bs.best_t = (int*)zalloc(B * 4); bs.best_r = (int*)zalloc(B * 4); bs.best_raw = (double*)zalloc(B * 8);
+  bs.best_norm = (double*)zalloc(B * 8); bs.hist_parent = (int*)zalloc(MAXLEN * R * 4);
+  bs.hist_token = (int*)zalloc(MAXLEN * R * 4); bs.hist_logp = (float*)zalloc(MAXLEN * R * 4);
+  { std::vector<int> lv(2 * R, 0); for (int b = 0; b < B; ++b) { lv[b * K] = 1; lv[R + b * K] = 1; }
+    CK(cudaMemcpy(bs.live, lv.data(), 2 * R * 4, cudaMemcpyHostToDevice)); }
+  GatherArgs ga{};
+  ga.emb_tgt = (float*)zalloc((size_t)V * E * 4); ga.E = E; ga.H = H; ga.L = L;
+  ga.htilde = (float*)zalloc(NP * H * 4); ga.h = (float*)zalloc(L * NP * H * 4); ga.c = (float*)zalloc(L * NP * H * 4);
+  ga.cg = (float*)zalloc(L * NP * H * 4); ga.rows_pad = NP;
+  ga.x[0] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1536 * 2), NP, 1536};
+  ga.x[1] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1024 * 2), NP, 1024};
+  auto launch = [&]() {
+    CK(gen_step(tmW, tmX, VP / 128, NP, NP, KP / 64, 148, g, rl, rz, ri, phases, 5, MAXLEN, 1.0, bs, ga, gbar,
+                StepCtl{nullptr, 0}, st));
+  };
+  cudaGraph_t gr; cudaGraphExec_t ge;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < 20; ++i) launch();
+  CK(cudaStreamEndCapture(st, &gr)); CK(cudaGraphInstantiate(&ge, gr, 0));
+  for (int w = 0; w < 50; ++w) CK(cudaGraphLaunch(ge, st));
+  CK(cudaStreamSynchronize(st));
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  CK(cudaEventRecord(a, st)); CK(cudaGraphLaunch(ge, st)); CK(cudaEventRecord(b, st)); CK(cudaStreamSynchronize(st));
+  float ms_; cudaEventElapsedTime(&ms_, a, b);
+  CK(cudaMemset(tr, 0, 4096 * 96)); CK(cudaGraphLaunch(ge, st)); launch(); CK(cudaStreamSynchronize(st));
+  const int grid = C;
+  std::vector<unsigned long long> h(grid * 12);
+  CK(cudaMemcpy(h.data(), tr, grid * 96, cudaMemcpyDeviceToHost));
+  unsigned long long t0 = ~0ull; for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[c * 12]);
+  double avg[12] = {0}, mx[12] = {0}; int cnt[12] = {0};
+  for (int c = 0; c < grid; ++c) for (int i = 0; i < 12; ++i) if (h[c * 12 + i]) {
+    double d = (h[c * 12 + i] - t0) / 1e3; avg[i] += d; cnt[i]++; mx[i] = std::max(mx[i], d); }
+  printf("gen_step phases=%d dbg=%d: %.2f us/launch (graph of 20)\n", phases, g_gs_dbg, ms_ * 1000 / 20);
+  const char* nm[12] = {"entry", "pdl_wait", "mma done (epi)", "phase A end", "phase B start", "phase C start", "stager: tile2 buf free", "first data (mma)", "batch scanned", "partial write", "stager: tile0 staged", "phase C end"};
+  for (int i = 0; i < 12; ++i) if (cnt[i]) printf("   %-16s avg %7.2f  max %7.2f us (n=%d)\n", nm[i], avg[i] / cnt[i], mx[i], cnt[i]);
+  return 0;
+}
