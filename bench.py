@@ -235,7 +235,7 @@ def run_ours(args):
             "e2e": {"value": round(e2e_tokens / (e2e_t / 1e3), 1), "unit": "target tok/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
-            "roofline": {"kernel": "tc_gemm_kernel<MODE_GEN> (fused generator + log-softmax + top-k)",
+            "roofline": {"kernel": "gen_step_kernel (K-outer tcgen05 generator + log-softmax + per-CTA top-K; logits never in HBM)",
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
                          "peak_src": pk["src"],

@@ -4,6 +4,7 @@
 #include <math_constants.h>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace onmt {
 
@@ -100,6 +101,7 @@ __device__ __forceinline__ void select_gather_row(int r, int slice, int nslice, 
     }
   }
   __syncthreads();
+  KT(4);
   if (!s_cont) return;
   // ---- gather this CTA's column slice of row r (all loads first)
   const int p = s_prow, y = s_y;
@@ -132,6 +134,334 @@ __device__ __forceinline__ void select_gather_row(int r, int slice, int nslice, 
         ga.cg[((size_t)l * ga.rows_pad + r) * H + j] = cv[l];
       }
   }
+}
+
+// A10 + A5 for one whole sentence b per CTA (512 threads): the generator partials of its K
+// hypothesis rows are combined (one warp per row: log-sum-exp and row top-K), thread 0
+// selects the K survivors (raw desc, slot asc, token asc; fp64 scores) with EOS / max_len
+// banking, histories and the stop flag, then the CTA gathers all K rows' next-step decoder
+// inputs.  Partial (p, r) of the generator lives at index p * ps + r * rs (ms) and
+// (p * ps + r * rs) * K (tz, ti).  Replaces a row-reduce launch plus a select/gather launch.
+template <int KMAX>
+__device__ __forceinline__ void beam_step_sentence(int b, const float2* __restrict__ ms, const float* __restrict__ tz,
+                                                   const int* __restrict__ ti, int n_parts, int ps, int rs, int K,
+                                                   int R, int t, int max_len, double lp, const BeamState& bs,
+                                                   const GatherArgs& ga, float* gbuf, int gbuf_floats) {
+  KT(1);
+  const int dn = __ldcg(&bs.done[b]);
+  if (dn != 0 && dn < t) return;                                 // (uniform over the CTA)
+  const int* __restrict__ live_in = bs.live + (size_t)(t & 1) * R;
+  const double* __restrict__ cum_in = bs.cum + (size_t)(t & 1) * R;
+  int* live_out = bs.live + (size_t)((t + 1) & 1) * R;
+  double* cum_out = bs.cum + (size_t)((t + 1) & 1) * R;
+  __shared__ int s_live[KMAX];
+  __shared__ double s_cum[KMAX];
+  __shared__ float s_lse[KMAX];
+  __shared__ float s_z[KMAX][KMAX];
+  __shared__ int s_id[KMAX][KMAX];
+  __shared__ int s_prow[KMAX], s_y[KMAX], s_go[KMAX];
+  __shared__ int s_cont;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (threadIdx.x < K) {
+    s_live[threadIdx.x] = __ldcg(&live_in[b * K + threadIdx.x]);
+    s_cum[threadIdx.x] = __ldcg(&cum_in[b * K + threadIdx.x]);
+  }
+  __syncthreads();
+  KT(2);
+  // ---- row reduce: warp k -> row b*K + k (dead slots skipped)
+  for (int k = warp; k < K; k += nw) {
+    const int r = b * K + k;
+    if (!s_live[k]) {
+      if (lane < K) s_z[k][lane] = -INFINITY;
+      continue;
+    }
+    // (1) every partial's (max, sum) and best logit in one round trip
+    constexpr int PPL = 8;                                       // partials per lane (n_parts <= 256)
+    float2 v[PPL];
+    float hz[PPL];
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      const int p = lane + 32 * u;
+      const size_t ix = (size_t)p * ps + (size_t)r * rs;
+      v[u] = p < n_parts ? __ldcg(&ms[ix]) : make_float2(-INFINITY, 0.f);
+      hz[u] = p < n_parts ? __ldcg(&tz[ix * K]) : -INFINITY;
+    }
+    float m = -INFINITY, sm = 0.f;
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      if (v[u].x == -INFINITY) continue;
+      const float M = fmaxf(m, v[u].x);
+      sm = (m == -INFINITY ? 0.f : sm * __expf(m - M)) + v[u].y * __expf(v[u].x - M);
+      m = M;
+    }
+    // (2) theta = K-th largest partial maximum: a partial whose best logit is below it holds
+    //     no row top-K entry (K other entries beat all of its entries)
+    float theta = -INFINITY;
+    {
+      float hh[PPL];
+#pragma unroll
+      for (int u = 0; u < PPL; ++u) hh[u] = hz[u];
+      for (int c = 0; c < K; ++c) {
+        float lm = hh[0];
+#pragma unroll
+        for (int u = 1; u < PPL; ++u) lm = fmaxf(lm, hh[u]);
+        float wm = lm;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        theta = wm;
+        const unsigned own = __ballot_sync(0xffffffffu, lm == wm);
+        if (lane == __ffs(own) - 1) {                            // the first owner drops one copy
+          bool hit = false;
+#pragma unroll
+          for (int u = 0; u < PPL; ++u) {
+            const bool h = !hit && hh[u] == wm;
+            hh[u] = h ? -INFINITY : hh[u];
+            hit |= h;
+          }
+        }
+      }
+    }
+    // (3) full lists of the qualifying partials (one more round trip), sorted insertion
+    float lz[KMAX];
+    int li[KMAX];
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) { lz[i] = -INFINITY; li[i] = 0x7fffffff; }
+    unsigned qual = 0;                                           // qualifying partials of this lane
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) qual |= (hz[u] >= theta && hz[u] != -INFINITY) ? (1u << u) : 0u;
+    while (qual) {
+      const int u = __ffs(qual) - 1;
+      qual &= qual - 1;
+      const size_t base = ((size_t)(lane + 32 * u) * ps + (size_t)r * rs) * K;
+      float cz[KMAX];
+      int ci[KMAX];
+#pragma unroll
+      for (int c = 0; c < KMAX; ++c) {
+        cz[c] = c < K ? __ldcg(&tz[base + c]) : -INFINITY;
+        ci[c] = c < K ? __ldcg(&ti[base + c]) : 0x7fffffff;
+      }
+#pragma unroll 1
+      for (int c = 0; c < K; ++c) {
+        float z = cz[0];
+        int id = ci[0];
+#pragma unroll
+        for (int q = 0; q < KMAX - 1; ++q) { cz[q] = cz[q + 1]; ci[q] = ci[q + 1]; }   // pop the head
+        if (!better(z, id, lz[KMAX - 1], li[KMAX - 1])) break;      // (sorted: the rest is worse)
+        bool gt[KMAX];                                           // sorted (z desc, id asc) insertion
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q) gt[q] = better(z, id, lz[q], li[q]);
+#pragma unroll
+        for (int q = KMAX - 1; q >= 1; --q) {
+          const float nz = gt[q - 1] ? lz[q - 1] : z;
+          const int ni = gt[q - 1] ? li[q - 1] : id;
+          lz[q] = gt[q] ? nz : lz[q];
+          li[q] = gt[q] ? ni : li[q];
+        }
+        lz[0] = gt[0] ? z : lz[0];
+        li[0] = gt[0] ? id : li[0];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sm, o);
+      const float M = fmaxf(m, m2);
+      sm = (m == -INFINITY ? 0.f : sm * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
+      m = M;
+    }
+    if (lane == 0) s_lse[k] = m + logf(sm);
+    for (int c = 0; c < K; ++c) {                                // K rounds of warp arg-max over list heads
+      float bz = lz[0];
+      int bi = li[0];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float z2 = __shfl_xor_sync(0xffffffffu, bz, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (better(z2, i2, bz, bi)) { bz = z2; bi = i2; }
+      }
+      if (lane == 0) { s_z[k][c] = bz; s_id[k][c] = bi; }
+      if (li[0] == bi && lz[0] == bz) {
+#pragma unroll
+        for (int q = 0; q < KMAX - 1; ++q) { lz[q] = lz[q + 1]; li[q] = li[q + 1]; }
+        lz[KMAX - 1] = -INFINITY;
+        li[KMAX - 1] = 0x7fffffff;
+      }
+    }
+  }
+  __syncthreads();
+  KT(3);
+  // ---- selection (parallel ranks): candidate (k, j) = slot k's j-th row best; its raw score
+  //      cum_k + z - lse_k in fp64; order (score desc, slot asc, position asc) - the merge of
+  //      the slots' sorted lists (R13); the K best survive.
+  __shared__ double s_sc[KMAX * KMAX];
+  __shared__ int s_valid[KMAX * KMAX];
+  __shared__ int s_sel_k[KMAX], s_sel_w[KMAX];
+  __shared__ double s_sel_s[KMAX];
+  __shared__ float s_sel_lp[KMAX];
+  __shared__ int s_nsel;
+  const int KK = K * K;
+  if (threadIdx.x < KK) {
+    const int k = threadIdx.x / K, j = threadIdx.x % K;
+    const float z = s_z[k][j];
+    const bool ok = s_live[k] && z != -INFINITY;
+    s_valid[threadIdx.x] = ok;
+    s_sc[threadIdx.x] = ok ? s_cum[k] + ((double)z - (double)s_lse[k]) : -CUDART_INF;
+  }
+  __syncthreads();
+  if (threadIdx.x < KK) {
+    const int i = threadIdx.x;
+    int rank = 0, nvalid = 0;
+    if (s_valid[i]) {
+      const double sc = s_sc[i];
+      for (int c = 0; c < KK; ++c) {                             // (c < i: earlier slot, or same slot earlier position)
+        if (!s_valid[c]) continue;
+        ++nvalid;
+        const double o = s_sc[c];
+        rank += (o > sc) || (o == sc && c < i);
+      }
+      if (rank < K) {
+        const int k = i / K, j = i % K;
+        s_sel_k[rank] = k;
+        s_sel_w[rank] = s_id[k][j];
+        s_sel_s[rank] = sc;
+        s_sel_lp[rank] = (float)((double)s_z[k][j] - (double)s_lse[k]);
+      }
+      if (rank == 0) s_nsel = nvalid < K ? nvalid : K;
+    }
+    if (i == 0 && nvalid == 0) {
+      bool any = false;
+      for (int c = 0; c < KK; ++c) any |= s_valid[c] != 0;
+      if (!any) s_nsel = 0;
+    }
+  }
+  __syncthreads();
+  const int n_sel = s_nsel;
+  const bool stop = [&] {
+    bool any_live = false;
+    for (int q = 0; q < n_sel; ++q) any_live |= !(s_sel_w[q] == 3 || t == max_len);
+    return !any_live || t == max_len || (n_sel > 0 && s_sel_w[0] == 3);
+  }();
+  if (threadIdx.x < K) {                                         // slot kr of sentence b
+    const int kr = threadIdx.x;
+    const int r = b * K + kr;
+    const bool mine_sel = kr < n_sel;
+    const bool mine_live = mine_sel && !(s_sel_w[kr] == 3 || t == max_len);
+    s_prow[kr] = mine_live ? b * K + s_sel_k[kr] : r;
+    s_y[kr] = mine_live ? s_sel_w[kr] : 0;
+    s_go[kr] = mine_live && !stop;
+    const size_t hb = (size_t)(t - 1) * (size_t)R + (size_t)r;
+    live_out[r] = mine_live;
+    cum_out[r] = mine_live ? s_sel_s[kr] : -CUDART_INF;
+    bs.prow[r] = s_prow[kr];
+    bs.y[r] = s_y[kr];
+    bs.hist_parent[hb] = mine_sel ? s_sel_k[kr] : -1;
+    bs.hist_token[hb] = mine_sel ? s_sel_w[kr] : 0;
+    bs.hist_logp[hb] = mine_sel ? s_sel_lp[kr] : 0.f;
+    if (bs.sel_parent) { bs.sel_parent[hb] = mine_sel ? s_sel_k[kr] : -1; bs.sel_score[hb] = mine_sel ? s_sel_s[kr] : -CUDART_INF; }
+  }
+  if (threadIdx.x == 0) {
+    s_cont = !stop;
+    int bt = bs.best_t[b], br = bs.best_r[b];                    // sentence-level banking and stop flag
+    double braw = bs.best_raw[b], bnorm = bs.best_norm[b];
+    for (int q = 0; q < n_sel; ++q) {
+      if (s_sel_w[q] == 3 || t == max_len) {
+        const double norm = s_sel_s[q] / lp;
+        if (bt == 0 || norm > bnorm) { bt = t; br = q; braw = s_sel_s[q]; bnorm = norm; }
+      }
+    }
+    bs.best_t[b] = bt; bs.best_r[b] = br; bs.best_raw[b] = braw; bs.best_norm[b] = bnorm;
+    if (stop) { bs.done[b] = t; atomicAdd(bs.n_done, 1); }
+  }
+  __syncthreads();
+  KT(4);
+  if (!s_cont) return;
+  // ---- gather the next step's inputs of the K rows (x1 = [E_tgt[y]; h~[p]; h_0[p]],
+  //      x_l = [.; h_l[p]], c_l[p]); dead slots are not gathered
+  const int E = ga.E, H = ga.H, L = ga.L;
+  const int per_row = E + H * (1 + 2 * L);                       // emb | h~ | h_l, c_l (l < L)
+  const bool bulk = gbuf != nullptr && (E & 3) == 0 && (H & 3) == 0;
+  const int slot_f = (per_row + 3) & ~3;
+  const int spb = bulk ? max(1, min(K, gbuf_floats / slot_f)) : 1;   // slots per staged batch
+  __shared__ __align__(8) uint64_t s_bar;
+  if (bulk && threadIdx.x == 0) { mbar_init(&s_bar, 1); fence_mbar_init(); }
+  __syncthreads();
+  int phase = 0;
+  for (int k0 = 0; k0 < K; k0 += spb) {
+    const int k1 = min(K, k0 + spb);
+    if (bulk) {
+      // one bulk copy per source row into shared memory (one round trip for the batch)
+      if (threadIdx.x == 0) {
+        uint32_t bytes = 0;
+        for (int kr = k0; kr < k1; ++kr)
+          if (s_go[kr]) bytes += (uint32_t)per_row * 4;
+        mbar_arrive_expect_tx(&s_bar, bytes);
+        for (int kr = k0; kr < k1; ++kr) {
+          if (!s_go[kr]) continue;
+          const int p = s_prow[kr];
+          float* d = gbuf + (size_t)(kr - k0) * slot_f;
+          bulk_g2s(d, ga.emb_tgt + (size_t)s_y[kr] * E, E * 4, &s_bar);
+          bulk_g2s(d + E, ga.htilde + (size_t)p * H, H * 4, &s_bar);
+          for (int l = 0; l < L; ++l) {
+            bulk_g2s(d + E + H + 2 * l * H, ga.h + ((size_t)l * ga.rows_pad + p) * H, H * 4, &s_bar);
+            bulk_g2s(d + E + H + (2 * l + 1) * H, ga.c + ((size_t)l * ga.rows_pad + p) * H, H * 4, &s_bar);
+          }
+        }
+      }
+      mbar_wait(&s_bar, phase & 1);
+      ++phase;
+      KT(5);
+    }
+    if (bulk) {
+      // segments of each row: [0, E+H) -> x0 cols [0, E+H); h_l -> x0 [E+H, E+2H) or x_l [H, 2H);
+      // c_l -> cg[l]; 4 consecutive columns per thread (E, H multiples of 4)
+      // one warp per (slot, segment) pair, lanes over 4-column groups
+      const int nseg = 1 + 2 * L;
+      for (int pr = warp; pr < (k1 - k0) * nseg; pr += nw) {
+        const int kr = k0 + pr / nseg, seg = pr % nseg;
+        if (!s_go[kr]) continue;
+        const int r = b * K + kr;
+        const float* src = gbuf + (size_t)(kr - k0) * slot_f;
+        const int off = seg == 0 ? 0 : E + H + (seg - 1) * H;
+        const int len = seg == 0 ? E + H : H;
+        const int l = (seg - 1) >> 1;
+        const bool is_c = seg > 0 && ((seg - 1) & 1);
+        const XOut xo = seg == 0 || l == 0 ? ga.x[0] : ga.x[l];
+        const int cbase = seg == 0 ? 0 : (l == 0 ? E + H : H);
+        float* cdst = is_c ? ga.cg + ((size_t)l * ga.rows_pad + r) * H : nullptr;
+        for (int j4 = 4 * lane; j4 < len; j4 += 128) {
+          const float4 v = *reinterpret_cast<const float4*>(src + off + j4);
+          if (is_c) *reinterpret_cast<float4*>(cdst + j4) = v;
+          else store_x4(xo, r, cbase + j4, v);
+        }
+      }
+    } else {
+      for (int it = threadIdx.x; it < (k1 - k0) * per_row; it += blockDim.x) {
+        const int kr = k0 + it / per_row, col = it % per_row;
+        if (!s_go[kr]) continue;
+        const int r = b * K + kr;
+        const int p = s_prow[kr];
+        float v;
+        if (col < E) v = __ldg(&ga.emb_tgt[(size_t)s_y[kr] * E + col]);
+        else if (col < E + H) v = __ldcg(&ga.htilde[(size_t)p * H + col - E]);
+        else {
+          const int x = col - E - H, l = x / (2 * H), j = x % (2 * H);
+          v = __ldcg(&(j < H ? ga.h : ga.c)[((size_t)l * ga.rows_pad + p) * H + (j < H ? j : j - H)]);
+        }
+        if (col < E + H) {
+          store_x(ga.x[0], r, col, v);
+        } else {
+          const int x = col - E - H, l = x / (2 * H), j = x % (2 * H);
+          if (j < H) {
+            if (l == 0) store_x(ga.x[0], r, E + H + j, v);
+            else store_x(ga.x[l], r, H + j, v);
+          } else {
+            ga.cg[((size_t)l * ga.rows_pad + r) * H + j - H] = v;
+          }
+        }
+      }
+    }
+    __syncthreads();                                             // staging buffer reused by the next batch
+  }
+  KT(6);
 }
 
 }  // namespace onmt

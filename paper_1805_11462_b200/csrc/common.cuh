@@ -67,6 +67,26 @@ __device__ __forceinline__ void store_x(const XOut& x, int r, int c, float v) {
   }
 }
 
+// 4 consecutive columns (c multiple of 4, row starts 8-byte aligned in the bf16 planes:
+// k_pad is a multiple of 64)
+__device__ __forceinline__ void store_x4(const XOut& x, int r, int c, float4 v) {
+  size_t i = (size_t)r * x.k_pad + c;
+  if (x.hl) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(v.x), h1 = __float2bfloat16_rn(v.y), h2 = __float2bfloat16_rn(v.z),
+                        h3 = __float2bfloat16_rn(v.w);
+    __nv_bfloat162 hi01(h0, h1), hi23(h2, h3);
+    __nv_bfloat162 lo01(__float2bfloat16_rn(v.x - __bfloat162float(h0)), __float2bfloat16_rn(v.y - __bfloat162float(h1)));
+    __nv_bfloat162 lo23(__float2bfloat16_rn(v.z - __bfloat162float(h2)), __float2bfloat16_rn(v.w - __bfloat162float(h3)));
+    uint2 hu, lu;
+    hu.x = *reinterpret_cast<uint32_t*>(&hi01); hu.y = *reinterpret_cast<uint32_t*>(&hi23);
+    lu.x = *reinterpret_cast<uint32_t*>(&lo01); lu.y = *reinterpret_cast<uint32_t*>(&lo23);
+    *reinterpret_cast<uint2*>(x.hl + i) = hu;
+    *reinterpret_cast<uint2*>(x.hl + (size_t)x.rows_pad * x.k_pad + i) = lu;
+  } else {
+    *reinterpret_cast<float4*>(x.f32 + i) = v;
+  }
+}
+
 // Early-exit control: every decode-step kernel returns at once when all B sentences
 // have stopped (n_done written by the beam merge kernel).
 struct StepCtl {

@@ -48,6 +48,14 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, in
       : "memory");
 }
 
+// 1D bulk copy global -> shared (16-byte aligned, size a multiple of 16), completes tx bytes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // 2D tiled load multicast to every CTA in ctaMask (same smem / mbarrier offsets in each).
 __device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const void* tmap, int x, int y, uint64_t* bar,
                                                uint16_t mask) {

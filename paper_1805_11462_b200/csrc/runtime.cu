@@ -843,14 +843,14 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       EvPair pm = prof_begin(m, "merge");
       launch_beam_merge(g.ms, g.tz, g.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
                         m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
-      count(m, 2);
+      count(m, n_vt <= 256 ? 1 : 2);
       prof_end(m, "merge", pm);
     } else {
       gen(m, m->xg, g, ctl);
       EvPair pm = prof_begin(m, "merge");
       launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, 1, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
                         m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
-      count(m, 2);
+      count(m, n_vt <= 256 ? 1 : 2);
       prof_end(m, "merge", pm);
     }
     prof_end(m, "step", ev);

@@ -404,21 +404,45 @@ void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepC
   gather_kernel<<<R, 128, 0, st>>>(bs, g, K, ctl);
 }
 
+constexpr size_t kBeamStageBytes = 64 * 1024;   // shared staging of the gathered rows
+
+template <int KMAX>
+__global__ void __launch_bounds__(512) beam_step_kernel(const float2* __restrict__ ms, const float* __restrict__ tz,
+                                                        const int* __restrict__ ti, int n_parts, int ps, int rs, int K,
+                                                        int t, int max_len, double lp, BeamState bs, GatherArgs ga,
+                                                        StepCtl ctl) {
+  KT(0);
+  pdl_trigger();
+  pdl_wait();
+  (void)ctl;
+  extern __shared__ __align__(16) float gbuf_dyn[];
+  beam_step_sentence<KMAX>(blockIdx.x, ms, tz, ti, n_parts, ps, rs, K, gridDim.x * K, t, max_len, lp, bs, ga,
+                           gbuf_dyn, (int)(kBeamStageBytes / 4));
+}
+
 void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_parts, int ps, int rs, int B, int K,
                        int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga, float* row_lse,
                        float* row_z, int* row_i, StepCtl ctl, cudaStream_t st) {
   const int R = B * K;
-  const int nslice = 4;
-#define ONMT_MERGE(KM)                                                                                         \
-  launch_pdl(row_reduce_topk_kernel<KM>, dim3(R), dim3(128), 0, st, ms, tz, ti, n_parts, ps, rs, K,           \
-             bs.live + (size_t)(t & 1) * R, row_lse, row_z, row_i, ctl);                                       \
-  launch_pdl(beam_select_gather_kernel<KM>, dim3(R, nslice), dim3(128), 0, st, row_lse, row_z, row_i, K, t,    \
-             max_len, lp, bs, ga, nslice, ctl)
-  if (K <= 1) { ONMT_MERGE(1); }
-  else if (K <= 2) { ONMT_MERGE(2); }
-  else if (K <= 4) { ONMT_MERGE(4); }
-  else if (K <= 8) { ONMT_MERGE(8); }
-  else { ONMT_MERGE(16); }
+  // one CTA per sentence (row reduce + select + gather) when its lanes hold every partial;
+  // otherwise (SIMT generator over many tiles) a row-reduce launch + a select/gather launch
+#define ONMT_MERGE(KM)                                                                                            \
+  if (n_parts <= 256) {                                                                                           \
+    cudaFuncSetAttribute(beam_step_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBeamStageBytes); \
+    launch_pdl(beam_step_kernel<KM>, dim3(B), dim3(512), kBeamStageBytes, st, ms, tz, ti, n_parts, ps, rs, K, t,   \
+               max_len, lp, bs, ga, ctl);                                                                         \
+  } else {                                                                                                        \
+    launch_pdl(row_reduce_topk_kernel<KM>, dim3(R), dim3(128), 0, st, ms, tz, ti, n_parts, ps, rs, K,             \
+               bs.live + (size_t)(t & 1) * R, row_lse, row_z, row_i, ctl);                                        \
+    launch_pdl(beam_select_gather_kernel<KM>, dim3(R, 4), dim3(128), 0, st, row_lse, row_z, row_i, K, t, max_len, \
+               lp, bs, ga, 4, ctl);                                                                               \
+  }
+  if (K <= 1) { ONMT_MERGE(1) }
+  else if (K <= 2) { ONMT_MERGE(2) }
+  else if (K <= 4) { ONMT_MERGE(4) }
+  else if (K == 5) { ONMT_MERGE(5) }
+  else if (K <= 8) { ONMT_MERGE(8) }
+  else { ONMT_MERGE(16) }
 #undef ONMT_MERGE
 }
 
