@@ -47,6 +47,8 @@ struct GenStepArgs {
   BeamState bs;
   GatherArgs ga;
   unsigned int* gbar;                           // grid barrier {count, generation}
+  unsigned int* thr;                            // [2][rows_pad] shared top-K thresholds (ordered
+                                                // uint keys; buffer t & 1, the other one is reset)
   StepCtl ctl;
   int dbg;                                      // microbenchmark ablations (ONMT_KTRACE builds)
 };
@@ -63,6 +65,15 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar) {
   __syncthreads();
   if (threadIdx.x == 0) cta_group_barrier(bar, gridDim.x);
   __syncthreads();
+}
+
+// order-preserving float <-> uint keys (atomicMax on the key = max on the float)
+__device__ __forceinline__ unsigned int f2key(float f) {
+  const unsigned int u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(unsigned int k) {
+  return k == 0u ? -INFINITY : __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
 // sorted (z desc, id asc) insertion into a register list (branch-free network)
@@ -124,6 +135,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (a.thr && blockIdx.x == 0)                                    // next step's thresholds start empty
+    for (int i = threadIdx.x; i < a.rows_pad; i += blockDim.x) a.thr[(size_t)((a.t + 1) & 1) * a.rows_pad + i] = 0u;
   if (all_done(a.ctl)) {                                           // uniform over the grid
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
@@ -269,6 +282,12 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 #ifdef ONMT_KTRACE
         if (a.dbg == 2) { __syncwarp(); if (lane == 0) mbar_arrive_local(&sempty[buf]); continue; }
 #endif
+        // the row's shared threshold: the largest list tail any scanner of any CTA published
+        // so far - a K-th best of a subset of the row, so a lower bound of the row's K-th best
+        // logit; values below it cannot reach the row's top-K
+        // (step 1 does not read: its buffer may still hold the previous call's last step)
+        const float gth = (row_ok && a.thr && a.t != 1) ? key2f(__ldcg(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c))
+                                                        : -INFINITY;
         if (row_ok) {
           const float* col = stg + (size_t)buf * a.n_group * kGsSLD + (size_t)c * kGsSLD + part * nv;
           const int vbase = (t0 + j) * kTileM + part * nv;
@@ -308,52 +327,48 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
             // a subset - so nothing below it can enter).  The bound matters on the first
             // chunks, when the list is still cold.  Ids increase along the scan, so a value
             // compare decides every insertion (a tie never displaces an earlier id).
-            float th = tz[KMAX - 1];
-            if (cmax > th) {
-              if (th == -INFINITY || u0 == 0) {
-                float gk = -INFINITY;                              // K-th largest of g (K <= 16)
+            float th = fmaxf(tz[KMAX - 1], gth);
+            if (cmax >= th && cmax > tz[KMAX - 1]) {
+              if (tz[KMAX - 1] == -INFINITY) {                     // cold list: K-th largest group max
+                float gg[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) gg[k] = g[k];
+                float gk = -INFINITY;
 #pragma unroll
                 for (int rnd = 0; rnd < KMAX; ++rnd) {
                   if (rnd < a.K) {
-                    float mx = g[0];
+                    float mx = gg[0];
 #pragma unroll
-                    for (int k = 1; k < 16; ++k) mx = fmaxf(mx, g[k]);
+                    for (int k = 1; k < 16; ++k) mx = fmaxf(mx, gg[k]);
                     gk = mx;
                     bool hit = false;
 #pragma unroll
                     for (int k = 0; k < 16; ++k) {
-                      const bool h = !hit && g[k] == mx;
-                      g[k] = h ? -INFINITY : g[k];
+                      const bool h = !hit && gg[k] == mx;
+                      gg[k] = h ? -INFINITY : gg[k];
                       hit |= h;
                     }
                   }
                 }
                 th = fmaxf(th, gk);
               }
-              unsigned m0 = 0, m1 = 0;
+              unsigned gm = 0;                                     // groups holding a candidate
 #pragma unroll
-              for (int k = 0; k < 32; ++k) {
-                m0 |= (z[k] >= th) ? (1u << k) : 0u;
-                m1 |= (z[k + 32] >= th) ? (1u << k) : 0u;
-              }
+              for (int k = 0; k < 16; ++k) gm |= (g[k] >= th) ? (1u << k) : 0u;
+              while (gm) {                                         // candidates in id order
+                const int gi = __ffs(gm) - 1;
+                gm &= gm - 1;
+                const float4 w = *reinterpret_cast<const float4*>(col + u0 + 4 * gi);
+                const float wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                unsigned msk = h ? m1 : m0;
-                while (msk) {                                      // candidates in id order
-                  const int k = __ffs(msk) - 1 + 32 * h;
-                  msk &= msk - 1;
-                  const float zk = col[u0 + k];
-                  if (zk > tz[KMAX - 1]) gs_insert<KMAX>(tz, ti, zk, vbase + u0 + k);
-#ifdef ONMT_GS_DEBUG
-                  if (c == 0 && blockIdx.x == 0)
-                    printf("part %d cand id %d z %f -> [%f %f %f %f] [%d %d %d %d] th %f\n", part, vbase + u0 + k, zk,
-                           tz[0], tz[1 % KMAX], tz[2 % KMAX], tz[3 % KMAX], ti[0], ti[1 % KMAX], ti[2 % KMAX], ti[3 % KMAX], th);
-#endif
-                }
+                for (int e = 0; e < 4; ++e)
+                  if (wv[e] >= th && wv[e] > tz[KMAX - 1]) gs_insert<KMAX>(tz, ti, wv[e], vbase + u0 + 4 * gi + e);
               }
             }
           }
         }
+        if (row_ok && a.thr && tz[KMAX - 1] != -INFINITY)              // publish my list tail
+          atomicMax(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c, f2key(tz[KMAX - 1]));
         __syncwarp();
         if (lane == 0) mbar_arrive_local(&sempty[buf]);
       }
@@ -544,7 +559,7 @@ static cudaError_t launch_gs(const CUtensorMap& tmW, const CUtensorMap& tmX, con
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i,
                      int phases, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
-                     unsigned int* gbar, StepCtl ctl, cudaStream_t st) {
+                     unsigned int* gbar, unsigned int* thr, StepCtl ctl, cudaStream_t st) {
   const int groups = n_rows_pad / n_group;
   GsPlan p;
   if (!gs_plan(n_vt, n_group, groups, num_sms, p)) return cudaErrorInvalidConfiguration;
@@ -576,6 +591,7 @@ cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, i
   a.bs = bs;
   a.ga = ga;
   a.gbar = gbar;
+  a.thr = thr;
   a.ctl = ctl;
   a.dbg = g_gs_dbg;
   const int grid = p.C * groups;

@@ -26,6 +26,7 @@
 
 #include "../../include/onmt.h"
 #include "common.cuh"
+#include "dec_step.cuh"
 
 namespace onmt {
 // kernels / launchers defined in the other translation units
@@ -40,7 +41,7 @@ int gen_step_parts(int n_vt, int n_group, int groups, int num_sms);
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i,
                      int phases, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
-                     unsigned int* gbar, StepCtl ctl, cudaStream_t st);
+                     unsigned int* gbar, unsigned int* thr, StepCtl ctl, cudaStream_t st);
 int gen_cluster_size(int n_group, int n_vt, int n_groups, int num_sms);
 extern unsigned long long* g_gen_dbg;
 
@@ -282,7 +283,9 @@ struct onmt_model {
   bool gen_mc = false;         // generator activation multicast across 4-CTA clusters (measured slower on c2)
   bool fused = true;           // split-K GEMM with the reduction and the cell / tanh epilogue fused in
                                // (one launch per layer instead of GEMM + consumer kernel)
-  bool gen_step = true;        // generator + row reduce + beam step as one persistent kernel (gen_step.cu)
+  bool gen_step = true;        // K-outer persistent generator (gen_step.cu)
+  bool dec_fused = false;      // decoder cells + attention + W_out as one persistent kernel (dec_step.cu;
+                               // opt-in: measured slower than the per-layer kernels)
   bool use_graph = true;
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -308,6 +311,8 @@ struct onmt_model {
   DevBuf dec_p, st_h, st_c, st_cg, htilde, logits;
   DevBuf f_scratch, f_count;                 // fused GEMM partial tiles + per-tile arrival counters
   DevBuf g_bar;                              // grid barrier counter of the generator step kernel
+  DevBuf g_thr;                              // generator: shared per-row top-K thresholds [2][rows_pad]
+  DevBuf ds_part, ds_bar;                    // fused decoder step: attention chunk partials, grid barrier
   DevBuf g_ms, g_tz, g_ti;
   DevBuf row_lse, row_z, row_i;
   DevBuf b_cum, b_live, b_y, b_prow, b_done, b_ndone, b_bt, b_br, b_braw, b_bnorm;
@@ -720,10 +725,25 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
     for (int l = 0; l < L; ++l)
       fs = std::max(fs, fused_scratch_floats(m->dec_w[l]->m_pad, m->xdec[l]->rows_pad, m->xdec[l]->n_group,
                                              m->dec_w[l]->k_pad / kBK, m->num_sms));
+    int ng = m->xo.n_group;                          // fused decoder step: tiles * S <= #SMs
+    for (int l = 0; l < L; ++l) ng = std::max(ng, m->xdec[l]->n_group);
+    fs = std::max(fs, (size_t)m->num_sms * ng * kTileM);
     m->f_scratch.ensure(std::max<size_t>(fs, 1) * 4);
     if (!m->g_bar.p) {
       m->g_bar.ensure(256);
       ONMT_CUDA(cudaMemset(m->g_bar.p, 0, 256));
+    }
+    if (m->g_thr.bytes < (size_t)2 * m->xg.rows_pad * 4) {
+      m->g_thr.ensure((size_t)2 * m->xg.rows_pad * 4);
+      ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
+    }
+    if (!m->ds_bar.p) {
+      m->ds_bar.ensure(256);
+      ONMT_CUDA(cudaMemset(m->ds_bar.p, 0, 256));
+    }
+    {
+      const int nch = dec_step_att_chunks(B, S_max, m->num_sms);
+      m->ds_part.ensure((size_t)B * nch * K * (2 + H) * 4);
     }
     const size_t nc = (size_t)(L + 1) * 2048 * 4;
     if (m->f_count.bytes < nc) {
@@ -731,6 +751,55 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
       ONMT_CUDA(cudaMemset(m->f_count.p, 0, nc));
     }
   }
+}
+
+// Specs of the fused decoder step (dec_step.cu): L cell GEMMs + W_out, attention operands.
+static void dec_step_specs(onmt_model* m, const int* d_lens, int B, int S_max, int K, const BeamState& bs,
+                           std::vector<DsGemmSpec>& specs, DsAtt& att) {
+  const bool bf = m->use_tc;
+  const int R = B * K, H = m->H, L = m->L;
+  const int rp = m->xg.rows_pad;
+  float* hh = m->st_h.as<float>();
+  float* cc = m->st_c.as<float>();
+  float* cg = m->st_cg.as<float>();
+  specs.assign(L + 1, DsGemmSpec{});
+  for (int l = 0; l < L; ++l) {
+    const Mat& W = *m->dec_w[l];
+    const Act& X = *m->xdec[l];
+    DsGemmSpec& sp = specs[l];
+    sp.tmW = &W.tmap; sp.tmX = &X.tmap;
+    sp.m_pad = W.m_pad; sp.n_rows_pad = X.rows_pad; sp.n_group = X.n_group; sp.n_valid = R;
+    sp.k_blocks = W.k_pad / kBK; sp.M = 4 * H;
+    sp.scratch = m->f_scratch.as<float>();
+    sp.counters = m->f_count.as<unsigned int>() + (size_t)l * 2048;
+    sp.epi = 0;
+    sp.bias = m->dec_bias[l]->as<float>();
+    sp.cg = cg + (size_t)l * rp * H; sp.c_out = cc + (size_t)l * rp * H; sp.h_out = hh + (size_t)l * rp * H;
+    sp.H = H;
+    CellDst dst{};
+    if (l + 1 < L) { dst.x[0] = m->xdec[l + 1]->xo(bf); dst.col[0] = 0; dst.n = 1; }
+    else { dst.x[0] = m->xo.xo(bf); dst.col[0] = H; dst.n = 1; }
+    sp.dst = dst;
+  }
+  DsGemmSpec& so = specs[L];
+  so.tmW = &m->attn_wout.tmap; so.tmX = &m->xo.tmap;
+  so.m_pad = m->attn_wout.m_pad; so.n_rows_pad = m->xo.rows_pad; so.n_group = m->xo.n_group; so.n_valid = R;
+  so.k_blocks = m->attn_wout.k_pad / kBK; so.M = H;
+  so.scratch = m->f_scratch.as<float>();
+  so.counters = m->f_count.as<unsigned int>() + (size_t)L * 2048;
+  so.epi = 1;
+  so.htilde = m->htilde.as<float>();
+  so.xg = m->xg.xo(bf);
+  att = DsAtt{};
+  att.htop = hh + (size_t)(L - 1) * rp * H;
+  att.keys = m->general ? m->keys.as<float>() : m->mem.as<float>();
+  att.key_ld = m->general ? m->attn_win_t.m_pad : H;
+  att.mem = m->mem.as<float>();
+  att.lens = d_lens;
+  att.B = B; att.S_max = S_max; att.H = H; att.K = K;
+  att.xo = m->xo.xo(bf);
+  att.done = bs.done;
+  att.part = m->ds_part.as<float>();
 }
 
 static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int K, int max_len, float alpha,
@@ -765,9 +834,24 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
   g.rows_valid = R;
   g.rows_pad = rp;
   float* P = m->dec_p.as<float>();
+  std::vector<DsGemmSpec> ds_specs;
+  DsAtt ds_att;
+  bool ds_on = false;
+  if (m->use_tc && m->dec_fused) {
+    dec_step_specs(m, d_lens, B, S_max, K, bs, ds_specs, ds_att);
+    ds_on = dec_step(ds_specs.data(), L, ds_att, m->ds_bar.as<unsigned int>(), ctl, m->num_sms, nullptr, nullptr) ==
+            cudaSuccess;
+  }
   for (int t = 1; t <= max_len; ++t) {
     EvPair ev = prof_begin(m, "step");
-    for (int l = 0; l < L; ++l) {
+    if (ds_on) {
+      EvPair pd = prof_begin(m, "gemm");
+      ONMT_CUDA(dec_step(ds_specs.data(), L, ds_att, m->ds_bar.as<unsigned int>(), ctl, m->num_sms, nullptr,
+                         m->stream));
+      count(m);
+      prof_end(m, "gemm", pd);
+    }
+    for (int l = 0; l < L && !ds_on; ++l) {
       const Mat& W = *m->dec_w[l];
       CellDst dst{};
       if (l + 1 < L) {
@@ -800,7 +884,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       prof_end(m, "cell", pc);
     }
     const float* htop = hh + (size_t)(L - 1) * rp * H;
-    {
+    if (!ds_on) {
       EvPair pa = prof_begin(m, "attention");
       const float* keys = m->general ? m->keys.as<float>() : m->mem.as<float>();
       const int key_ld = m->general ? m->attn_win_t.m_pad : H;
@@ -809,8 +893,8 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       count(m);
       prof_end(m, "attention", pa);
     }
-    cudaError_t fe = cudaErrorInvalidConfiguration;
-    if (m->use_tc && m->fused) {
+    cudaError_t fe = ds_on ? cudaSuccess : cudaErrorInvalidConfiguration;
+    if (m->use_tc && m->fused && !ds_on) {
       EvPair pg = prof_begin(m, "gemm");
       fe = tc_gemm_tanh(m->attn_wout.tmap, m->xo.tmap, m->attn_wout.m_pad, m->xo.rows_pad, m->xo.n_group, R,
                         m->attn_wout.k_pad / kBK, H, m->htilde.as<float>(), m->xg.xo(bf), m->f_scratch.as<float>(),
@@ -837,7 +921,8 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       EvPair pgs = prof_begin(m, "gen");
       ONMT_CUDA(gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
                          m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
-                         m->row_i.as<int>(), 1, t, max_len, lp, bs, ga, m->g_bar.as<unsigned int>(), ctl, m->stream));
+                         m->row_i.as<int>(), 1, t, max_len, lp, bs, ga, m->g_bar.as<unsigned int>(),
+                         m->g_thr.as<unsigned int>(), ctl, m->stream));
       count(m);
       prof_end(m, "gen", pgs);
       EvPair pm = prof_begin(m, "merge");
@@ -860,6 +945,31 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
   ONMT_CUDA(cudaGetLastError());
 }
 
+// ONMT_KTRACE builds + env ONMT_PHASES=1: per-CTA phase stamps of the last fused decoder step
+static unsigned long long* g_phase_buf = nullptr;
+static void phase_trace_begin() {
+  if (!std::getenv("ONMT_PHASES")) return;
+  if (!g_phase_buf) cudaMalloc(&g_phase_buf, 4096 * 12 * 8);
+  cudaMemset(g_phase_buf, 0, 4096 * 12 * 8);
+  dec_step_set_trace(g_phase_buf);
+}
+static void phase_trace_end(int grid) {
+  if (!std::getenv("ONMT_PHASES") || !g_phase_buf) return;
+  cudaDeviceSynchronize();
+  std::vector<unsigned long long> h((size_t)grid * 12);
+  cudaMemcpy(h.data(), g_phase_buf, h.size() * 8, cudaMemcpyDeviceToHost);
+  unsigned long long t0 = ~0ull;
+  for (int c = 0; c < grid; ++c) if (h[c * 12]) t0 = std::min(t0, h[c * 12]);
+  const char* nm[12] = {"entry", "pdl_wait", "L1 done", "sync", "L2 done", "sync", "att chunks", "sync",
+                        "att combine", "sync", "W_out done", "exit"};
+  for (int i = 0; i < 12; ++i) {
+    double s = 0, mx = 0; int n = 0;
+    for (int c = 0; c < grid; ++c) if (h[c * 12 + i]) { double d = (h[c * 12 + i] - t0) / 1e3; s += d; mx = std::max(mx, d); ++n; }
+    std::fprintf(stderr, "  %-12s avg %7.2f max %7.2f us (n=%d)\n", nm[i], n ? s / n : 0.0, mx, n);
+  }
+  dec_step_set_trace(nullptr);
+}
+
 // The whole translation (encoder, decoder init, every decode step, finalize) as one CUDA
 // graph, cached per shape / pointer set: one cudaGraphLaunch per call, no host round trip.
 static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int K, int max_len,
@@ -871,7 +981,9 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     enqueue_decoder(m, d_lens, B, S_max, K, max_len, alpha, trace, out);
   };
   if (!m->use_graph) {
+    phase_trace_begin();
     enqueue();
+    phase_trace_end(m->num_sms);
     return;
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc,
@@ -963,6 +1075,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   if (const char* ev = std::getenv("ONMT_GEN_MULTICAST")) m->gen_mc = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_FUSED_GEMM")) m->fused = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_GEN_STEP")) m->gen_step = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_DEC_FUSED")) m->dec_fused = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
@@ -1000,6 +1113,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->gen_mc = v != 0;
   } else if (n == "gen_step") {
     m->gen_step = v != 0;
+  } else if (n == "dec_fused") {
+    m->dec_fused = v != 0;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
   } else {
@@ -1264,9 +1379,12 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
       m->g_bar.ensure(256);
       ONMT_CUDA(cudaMemset(m->g_bar.p, 0, 256));
     }
+    if (m->g_thr.bytes < (size_t)2 * x.rows_pad * 4) m->g_thr.ensure((size_t)2 * x.rows_pad * 4);
+    ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
     ONMT_CUDA(gen_step(m->gen_w.tmap, x.tmap, (m->Vt + kVTile - 1) / kVTile, x.rows_pad, x.n_group,
                        m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 2, 0, 0, 1.0,
-                       BeamState{}, GatherArgs{}, m->g_bar.as<unsigned int>(), StepCtl{nullptr, 0}, m->stream));
+                       BeamState{}, GatherArgs{}, m->g_bar.as<unsigned int>(), m->g_thr.as<unsigned int>(),
+                       StepCtl{nullptr, 0}, m->stream));
   } else {
     gen(m, x, g, StepCtl{nullptr, 0});
   }

@@ -49,6 +49,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&ms, C * NP * 8)); CK(cudaMalloc(&tz, C * NP * K * 4)); CK(cudaMalloc(&ti, C * NP * K * 4));
   CK(cudaMalloc(&rl, R * 4)); CK(cudaMalloc(&rz, R * K * 4)); CK(cudaMalloc(&ri, R * K * 4));
   CK(cudaMalloc(&gbar, 64)); CK(cudaMemset(gbar, 0, 64));
+  unsigned int* thr; CK(cudaMalloc(&thr, 2 * NP * 4)); CK(cudaMemset(thr, 0, 2 * NP * 4));
   unsigned long long* tr; CK(cudaMalloc(&tr, 4096 * 96)); CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
   GenOut g{ms, tz, ti, bias, V, K, R, NP};
   // beam state / gather operands for phase C (zeroed; slot 0 of every sentence live)
@@ -69,7 +70,7 @@ int main(int argc, char** argv) {
   ga.x[0] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1536 * 2), NP, 1536};
   ga.x[1] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1024 * 2), NP, 1024};
   auto launch = [&]() {
-    CK(gen_step(tmW, tmX, VP / 128, NP, NP, KP / 64, 148, g, rl, rz, ri, phases, 5, MAXLEN, 1.0, bs, ga, gbar,
+    CK(gen_step(tmW, tmX, VP / 128, NP, NP, KP / 64, 148, g, rl, rz, ri, phases, 5, MAXLEN, 1.0, bs, ga, gbar, thr,
                 StepCtl{nullptr, 0}, st));
   };
   cudaGraph_t gr; cudaGraphExec_t ge;
