@@ -14,6 +14,8 @@
 //   * parks (m_k, l_k, ctx_k) in its shared memory; after a cluster barrier CTA r combines
 //     column slice r over all nch chunks through distributed shared memory, in fixed chunk
 //     order (deterministic), and writes the context into the W_out operand (columns [0, H)).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -297,6 +299,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
 
 // chunks per sentence: fill the SMs with one wave of clusters (<= 8 CTAs, >= 4 positions each)
 static int att_nch(int B, int S_max, int num_sms) {
+  if (const char* e = std::getenv("ONMT_ATT_NCH")) return std::atoi(e);   // (tuning experiments)
   int nch = num_sms / (B > 0 ? B : 1);
   nch = nch > 8 ? 8 : nch < 1 ? 1 : nch;
   const int pos_cap = (S_max + 3) / 4;

@@ -148,9 +148,8 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
                                                    int R, int t, int max_len, double lp, const BeamState& bs,
                                                    const GatherArgs& ga, float* gbuf, int gbuf_floats) {
   KT(1);
-  const int dn = __ldcg(&bs.done[b]);
-  if (dn != 0 && dn < t) return;                                 // (uniform over the CTA)
-  const int* __restrict__ live_in = bs.live + (size_t)(t & 1) * R;
+  const int dn = __ldcg(&bs.done[b]);                            // (checked after the row reduce:
+  const int* __restrict__ live_in = bs.live + (size_t)(t & 1) * R;   //  its loads overlap these)
   const double* __restrict__ cum_in = bs.cum + (size_t)(t & 1) * R;
   int* live_out = bs.live + (size_t)((t + 1) & 1) * R;
   double* cum_out = bs.cum + (size_t)((t + 1) & 1) * R;
@@ -159,7 +158,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   __shared__ float s_lse[KMAX];
   __shared__ float s_z[KMAX][KMAX];
   __shared__ int s_id[KMAX][KMAX];
-  __shared__ int s_prow[KMAX], s_y[KMAX], s_go[KMAX];
+  __shared__ int s_prow[KMAX], s_y[KMAX], s_go[KMAX], s_src[KMAX];
   __shared__ int s_cont;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (threadIdx.x < K) {
@@ -168,13 +167,9 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   }
   __syncthreads();
   KT(2);
-  // ---- row reduce: warp k -> row b*K + k (dead slots skipped)
+  // ---- row reduce: warp k -> row b*K + k (dead slots are masked afterwards)
   for (int k = warp; k < K; k += nw) {
     const int r = b * K + k;
-    if (!s_live[k]) {
-      if (lane < K) s_z[k][lane] = -INFINITY;
-      continue;
-    }
     // (1) every partial's (max, sum) and best logit in one round trip
     constexpr int PPL = 8;                                       // partials per lane (n_parts <= 256)
     float2 v[PPL];
@@ -288,13 +283,56 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     }
   }
   __syncthreads();
+  if (dn != 0 && dn < t) return;                                 // finished earlier (uniform)
+  if (threadIdx.x < K * K && !s_live[threadIdx.x / K]) s_z[threadIdx.x / K][threadIdx.x % K] = -INFINITY;
+  // ---- prefetch every possible gather source into shared memory (it overlaps the selection):
+  //      the embedding rows of the K x K candidate tokens and the state rows of the K slots
+  const int E = ga.E, H = ga.H, L = ga.L;
+  const int state_f = H * (1 + 2 * L);                           // h~ | h_l, c_l (l < L)
+  const int emb_f = (E + 3) & ~3, st_f = (state_f + 3) & ~3;
+  const bool pre = gbuf != nullptr && (E & 3) == 0 && (H & 3) == 0 &&
+                   (K * K * emb_f + K * st_f) <= gbuf_floats;
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) { mbar_init(&s_bar, 1); fence_mbar_init(); }
+  __syncthreads();
+  if (pre) {
+    // copy c (one thread each): c < K*(1+2L) -> slot c / (1+2L), row kind c % (1+2L) (h~, h_l, c_l);
+    // then the K*K candidate embedding rows
+    const int nst = 1 + 2 * L;
+    if (threadIdx.x == 0) {
+      uint32_t bytes = 0;
+      for (int k = 0; k < K; ++k) {
+        if (!s_live[k]) continue;
+        bytes += (uint32_t)state_f * 4;
+        for (int j = 0; j < K; ++j)
+          if (s_z[k][j] != -INFINITY) bytes += (uint32_t)E * 4;
+      }
+      mbar_arrive_expect_tx(&s_bar, bytes);
+    }
+    __syncthreads();
+    const int c = threadIdx.x;
+    if (c < K * nst) {
+      const int k = c / nst, w = c % nst;
+      if (s_live[k]) {
+        const int p = b * K + k;
+        float* d = gbuf + (size_t)K * K * emb_f + (size_t)k * st_f + (size_t)w * H;
+        const float* src = w == 0 ? ga.htilde + (size_t)p * H
+                                  : (((w - 1) & 1) ? ga.c : ga.h) + ((size_t)((w - 1) >> 1) * ga.rows_pad + p) * H;
+        bulk_g2s(d, src, H * 4, &s_bar);
+      }
+    } else if (c < K * nst + K * K) {
+      const int i = c - K * nst, k = i / K, j = i % K;
+      if (s_live[k] && s_z[k][j] != -INFINITY)
+        bulk_g2s(gbuf + (size_t)i * emb_f, ga.emb_tgt + (size_t)s_id[k][j] * E, E * 4, &s_bar);
+    }
+  }
   KT(3);
   // ---- selection (parallel ranks): candidate (k, j) = slot k's j-th row best; its raw score
   //      cum_k + z - lse_k in fp64; order (score desc, slot asc, position asc) - the merge of
   //      the slots' sorted lists (R13); the K best survive.
   __shared__ double s_sc[KMAX * KMAX];
   __shared__ int s_valid[KMAX * KMAX];
-  __shared__ int s_sel_k[KMAX], s_sel_w[KMAX];
+  __shared__ int s_sel_k[KMAX], s_sel_w[KMAX], s_sel_c[KMAX];
   __shared__ double s_sel_s[KMAX];
   __shared__ float s_sel_lp[KMAX];
   __shared__ int s_nsel;
@@ -321,6 +359,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
       if (rank < K) {
         const int k = i / K, j = i % K;
         s_sel_k[rank] = k;
+        s_sel_c[rank] = i;
         s_sel_w[rank] = s_id[k][j];
         s_sel_s[rank] = sc;
         s_sel_lp[rank] = (float)((double)s_z[k][j] - (double)s_lse[k]);
@@ -348,6 +387,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     s_prow[kr] = mine_live ? b * K + s_sel_k[kr] : r;
     s_y[kr] = mine_live ? s_sel_w[kr] : 0;
     s_go[kr] = mine_live && !stop;
+    s_src[kr] = mine_live ? s_sel_c[kr] : 0;
     const size_t hb = (size_t)(t - 1) * (size_t)R + (size_t)r;
     live_out[r] = mine_live;
     cum_out[r] = mine_live ? s_sel_s[kr] : -CUDART_INF;
@@ -376,14 +416,44 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   if (!s_cont) return;
   // ---- gather the next step's inputs of the K rows (x1 = [E_tgt[y]; h~[p]; h_0[p]],
   //      x_l = [.; h_l[p]], c_l[p]); dead slots are not gathered
-  const int E = ga.E, H = ga.H, L = ga.L;
+  if (pre) {
+    mbar_wait(&s_bar, 0);
+    KT(5);
+    const float* pst = gbuf + (size_t)K * K * emb_f;
+    const int nseg = 2 + 2 * L;                                  // emb | h~ | (h_l, c_l)
+    for (int pr = warp; pr < K * nseg; pr += nw) {               // one warp per (slot, segment)
+      const int kr = pr / nseg, seg = pr % nseg;
+      if (!s_go[kr]) continue;
+      const int r = b * K + kr;
+      const int pk = s_prow[kr] - b * K;                         // parent slot
+      const float* src;
+      int len, cbase;
+      XOut xo = ga.x[0];
+      float* cdst = nullptr;
+      if (seg == 0) { src = gbuf + (size_t)s_src[kr] * emb_f; len = E; cbase = 0; }
+      else if (seg == 1) { src = pst + (size_t)pk * st_f; len = H; cbase = E; }
+      else {
+        const int l = (seg - 2) >> 1;
+        src = pst + (size_t)pk * st_f + H + (seg - 2) * H;
+        len = H;
+        if ((seg - 2) & 1) cdst = ga.cg + ((size_t)l * ga.rows_pad + r) * H;
+        else { xo = l == 0 ? ga.x[0] : ga.x[l]; cbase = l == 0 ? E + H : H; }
+      }
+      for (int j4 = 4 * lane; j4 < len; j4 += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(src + j4);
+        if (cdst) *reinterpret_cast<float4*>(cdst + j4) = v;
+        else store_x4(xo, r, cbase + j4, v);
+      }
+    }
+    KT(6);
+    return;
+  }
+  if (threadIdx.x == 0) { mbar_init(&s_bar, 1); fence_mbar_init(); }   // (fresh phase for the batches)
+  __syncthreads();
   const int per_row = E + H * (1 + 2 * L);                       // emb | h~ | h_l, c_l (l < L)
   const bool bulk = gbuf != nullptr && (E & 3) == 0 && (H & 3) == 0;
   const int slot_f = (per_row + 3) & ~3;
   const int spb = bulk ? max(1, min(K, gbuf_floats / slot_f)) : 1;   // slots per staged batch
-  __shared__ __align__(8) uint64_t s_bar;
-  if (bulk && threadIdx.x == 0) { mbar_init(&s_bar, 1); fence_mbar_init(); }
-  __syncthreads();
   int phase = 0;
   for (int k0 = 0; k0 < K; k0 += spb) {
     const int k1 = min(K, k0 + spb);

@@ -19,6 +19,8 @@
 //      order (deterministic) and the epilogue runs on them.
 // A DSMEM exchange inside a cluster was measured slower (~20 B/clk per SM) than this L2
 // round trip for 80 KB partial tiles.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -325,7 +327,9 @@ static bool fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, 
   a.k_blocks = k_blocks;
   const int tiles = m_tiles * (n_rows_pad / n_group);
   const size_t limit = 227 * 1024;
-  for (int S = 16; S >= 1; --S) {
+  int s_max = 16;
+  if (const char* e = std::getenv("ONMT_FUSED_SMAX")) s_max = std::atoi(e);   // (tuning experiments)
+  for (int S = s_max; S >= 1; --S) {
     const int kbps = (k_blocks + S - 1) / S;
     if ((k_blocks + kbps - 1) / kbps != S) continue;     // no empty split
     if (tiles * S > num_sms) continue;

@@ -525,7 +525,7 @@ static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, GsPlan& p) {
   p.C = num_sms / groups;
   if (p.C > n_vt) p.C = n_vt;
   if (p.C < 1) return false;
-  p.nt_max = 512 / ((n_group + 31) / 32 * 32);                      // accumulators in TMEM
+  p.nt_max = 512 / n_group;                                          // accumulators in TMEM
   if (p.nt_max > 4) p.nt_max = 4;                                    // (bias registers of the stagers)
   const int need = (n_vt + p.C - 1) / p.C;
   if (p.nt_max > need) p.nt_max = need;

@@ -1071,6 +1071,10 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   m->prec = prec;
   m->use_tc = prec == ONMT_PREC_BF16;
   m->num_sms = prop.multiProcessorCount;
+  if (const char* ev = std::getenv("ONMT_NUM_SMS")) {   // size every grid for a part of the GPU
+    const int n = std::atoi(ev);
+    if (n >= 8 && n < m->num_sms) m->num_sms = n;
+  }
   if (const char* ev = std::getenv("ONMT_USE_GRAPH")) m->use_graph = std::atoi(ev) != 0;   // ncu runs use 0
   if (const char* ev = std::getenv("ONMT_GEN_MULTICAST")) m->gen_mc = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_FUSED_GEMM")) m->fused = std::atoi(ev) != 0;

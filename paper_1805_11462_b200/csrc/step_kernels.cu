@@ -404,7 +404,7 @@ void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepC
   gather_kernel<<<R, 128, 0, st>>>(bs, g, K, ctl);
 }
 
-constexpr size_t kBeamStageBytes = 64 * 1024;   // shared staging of the gathered rows
+constexpr size_t kBeamStageBytes = 120 * 1024;  // shared staging of the gathered rows
 
 template <int KMAX>
 __global__ void __launch_bounds__(512) beam_step_kernel(const float2* __restrict__ ms, const float* __restrict__ tz,

@@ -255,3 +255,28 @@ def test_fused_cluster_gemm_matches_unfused(weight_cache):
     gm.set_option("fused_gemm", 1)
     np.testing.assert_array_equal(a["hyps"], b["hyps"])
     np.testing.assert_allclose(a["token_logp"], b["token_logp"], atol=2e-5)
+
+
+def test_fused_decoder_step_matches(weight_cache):
+    """The one-kernel decoder step (cells + attention + W_out behind grid barriers) equals the
+    per-layer kernels up to fp32 summation order (same split-K reduction orders)."""
+    gm, om, p = model_pair("c2", weight_cache)
+    ids, lens = synth.make_corpus("c2", 6)
+    gm.set_option("dec_fused", 1)
+    a = gm.translate(ids, lens, 5, 12, 0.0)
+    gm.set_option("dec_fused", 0)
+    b = gm.translate(ids, lens, 5, 12, 0.0)
+    np.testing.assert_array_equal(a["hyps"], b["hyps"])
+    np.testing.assert_allclose(a["token_logp"], b["token_logp"], atol=2e-5)
+
+
+def test_repeated_calls_odd_max_len(weight_cache):
+    """Consecutive calls with different inputs and odd max_len (per-step scratch buffers are
+    double-buffered by step parity) give the same result as fresh calls."""
+    gm, om, p = model_pair("c2", weight_cache)
+    ids, lens = synth.make_corpus("c2", 4)
+    first = gm.translate(ids, lens, 5, 7, 0.0)
+    gm.translate(ids[::-1].copy(), lens[::-1].copy(), 5, 9, 0.0)
+    again = gm.translate(ids, lens, 5, 7, 0.0)
+    np.testing.assert_array_equal(first["hyps"], again["hyps"])
+    np.testing.assert_array_equal(first["token_logp"], again["token_logp"])

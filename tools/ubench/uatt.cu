@@ -43,7 +43,7 @@ int main() {
   CK(cudaEventRecord(a, st)); CK(cudaGraphLaunch(ge, st)); CK(cudaEventRecord(b2, st)); CK(cudaStreamSynchronize(st));
   float ms; cudaEventElapsedTime(&ms, a, b2);
   CK(cudaMemset(tr, 0, 8192 * 96)); CK(cudaGraphLaunch(ge, st)); launch(); CK(cudaStreamSynchronize(st));
-  const int nch = 4, grid = nch * B;
+  const char* en = getenv("ONMT_ATT_NCH"); const int nch = en ? atoi(en) : 4, grid = nch * B;
   std::vector<unsigned long long> h(grid * 12);
   CK(cudaMemcpy(h.data(), tr, grid * 96, cudaMemcpyDeviceToHost));
   unsigned long long t0 = ~0ull; for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[c * 12]);
