@@ -328,6 +328,64 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_score(args):
+    """Secondary workload: teacher-forced scoring of synthetic target
+    sentences (Zipf ids, lengths uniform in [10, max_len]) for the workload's batch, through
+    onmt_score (host buffers: H2D/D2H inside the timed region, so value == e2e).  Metric:
+    target tokens scored per second."""
+    import torch
+    import paper_1805_11462_b200 as ob
+    w = synth.WORKLOADS[args.workload]
+    B, T = w.data.batch, w.decode.max_len
+    cache = os.environ.get("ONMT_WEIGHT_CACHE", os.path.join(tempfile.gettempdir(), "onmt_weights"))
+    path = synth.weights_file(args.workload, cache)
+    model = ob.Model(path, 0, w.decode.precision)
+    ids, lens = synth.make_corpus(args.workload)
+    S = int(lens.max())
+    ids = np.ascontiguousarray(ids[:, :S])
+    rng = np.random.default_rng(7)
+    tl = rng.integers(10, T + 1, B).astype(np.int32)
+    ranks = np.arange(1, model.info["v_tgt"] - 3, dtype=np.float64)
+    pz = ranks ** -1.1
+    pz /= pz.sum()
+    tgt = np.zeros((B, T), np.int32)
+    for b in range(B):
+        tgt[b, :tl[b]] = 3 + rng.choice(len(ranks), tl[b], p=pz) + 1
+    for _ in range(args.warmup):
+        model.score(ids, lens, tgt, tl)
+    model.set_option("profile", 1)
+    model.score(ids, lens, tgt, tl)
+    model.kernel_time("gen", reset=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        model.score(ids, lens, tgt, tl)
+    dt = time.perf_counter() - t0
+    gen_ms, gen_n = model.kernel_time("gen", reset=True)
+    model.set_option("profile", 0)
+    toks = int(tl.sum()) * args.steps
+    pk = peaks()
+    H, V = model.info["hidden"], model.info["v_tgt"]
+    rows = B * T
+    flops = 2.0 * rows * H * V                              # algorithmic (hi/lo split not counted)
+    gen_s = gen_ms / max(gen_n, 1) / 1e3
+    line = {"metric": "target tokens/sec scored (teacher-forced NLL, SURVEY §8(f) rank 1)",
+            "value": round(toks / dt, 1), "unit": "target tok/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if w.decode.precision == "bf16" else "f32",
+            "data": "synthetic (Zipf(1.1) target ids, lengths U[10, max_len])",
+            "config": {"workload": args.workload, "task": "score", "batch": B, "t_max": T},
+            "e2e": {"value": round(toks / dt, 1), "unit": "target tok/s", "h2d_bytes_per_step": int(ids.nbytes + tgt.nbytes),
+                    "d2h_bytes_per_step": int(B * T * 4)},
+            "roofline": {"kernel": "tc_gemm_kernel<MODE_GEN> over every (step, sentence) row (log-softmax + gold gather)",
+                         "bound": "tensor", "achieved": round(flops / gen_s / 1e12, 1),
+                         "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                         "frac": round(flops / gen_s / 1e12 / pk["bf16_tflops"], 4), "traffic": None,
+                         "avg_launch_us": round(gen_s * 1e6, 2), "flops_per_launch": flops}}
+    print(json.dumps(line), flush=True)
+    model.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -337,11 +395,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-sentences", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--task", default="translate", choices=["translate", "score"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.task == "score":
+        run_score(args)
     else:
         run_ours(args)
 

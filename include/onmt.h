@@ -134,6 +134,25 @@ ONMT_API onmt_status onmt_translate_trace(onmt_model* m, const int32_t* src_ids,
                                  int32_t* sel_parent, int32_t* sel_token, double* sel_score);
 
 /*
+ * onmt_score - teacher-forced scoring (PAPER.md P105-108: log p(Y|X) = sum_t log p(y_t | y_<t, X);
+ * SURVEY §8(f) rank 1).  The decoder is fed the GIVEN target tokens (y_0 = BOS, then
+ * y_1 .. y_{n-1}) instead of beam selections; the generator runs once over every
+ * (step, sentence) row.
+ *   src_ids / src_lens / B / S_max: as onmt_translate (host memory).
+ *   tgt_ids [B*T_max] row-major host int32: y_1 .. y_n of sentence b in row b (no BOS; an
+ *     EOS, if wanted, is part of Y); ids past tgt_lens[b] are ignored.
+ *   tgt_lens [B]: 1 <= n_b <= T_max.
+ *   out_token_logp [B*T_max] (caller-allocated host float): log p(y_t | ...) for t < n_b,
+ *     0 past the end.  out_nll [B] (host double, or NULL): -sum_t log p.
+ * Errors: as onmt_translate for the source; EMPTY_SOURCE if a tgt_len < 1; INVALID_ARG if
+ * tgt_len > T_max or T_max < 1; ID_RANGE for a target id outside [0, V_tgt); CUDA.
+ * B == 0 is a no-op.
+ */
+ONMT_API onmt_status onmt_score(onmt_model* m, const int32_t* src_ids, const int32_t* src_lens, int32_t B,
+                                int32_t S_max, const int32_t* tgt_ids, const int32_t* tgt_lens, int32_t T_max,
+                                float* out_token_logp, double* out_nll);
+
+/*
  * onmt_translate_dev - same as onmt_translate with every pointer a DEVICE pointer on
  * the model's device, and no host synchronisation: the work is enqueued on the
  * handle's stream (onmt_set_stream) and the outputs are valid once it completes.

@@ -24,7 +24,7 @@ K_MAX = 16
 
 EXPORTS = ["onmt_load_weights", "onmt_model_get_info", "onmt_set_stream", "onmt_encode", "onmt_translate",
            "onmt_translate_trace", "onmt_translate_dev", "onmt_set_option", "onmt_get_kernel_time",
-           "onmt_kernel_launches", "onmt_free", "onmt_last_error", "onmt_test_gemm", "onmt_test_gen"]
+           "onmt_kernel_launches", "onmt_free", "onmt_last_error", "onmt_test_gemm", "onmt_test_gen", "onmt_score"]
 
 
 class OnmtError(RuntimeError):
@@ -66,6 +66,7 @@ def lib():
     L.onmt_last_error.restype = ctypes.c_char_p
     L.onmt_test_gemm.argtypes = [VP, VP, VP, I32, I32, I32, I32, VP]
     L.onmt_test_gen.argtypes = [VP, VP, I32, I32, VP, VP, VP]
+    L.onmt_score.argtypes = [VP, VP, VP, I32, I32, VP, VP, I32, VP, VP]
     for n in EXPORTS:
         if n not in ("onmt_free", "onmt_last_error"):
             getattr(L, n).restype = ctypes.c_int
@@ -171,6 +172,18 @@ class Model:
                                         float(length_penalty), _ptr(hyps), _ptr(olens), _ptr(scores),
                                         _ptr(raw), _ptr(tlogp)))
         return out
+
+    def score(self, ids, lens, tgt, tgt_lens) -> Dict[str, np.ndarray]:
+        """Teacher-forced scoring: token_logp [B, T_max] (0 past each length) and nll [B]."""
+        ids, lens, tgt, tgt_lens = _i32(ids), _i32(lens), _i32(tgt), _i32(tgt_lens)
+        B = len(lens)
+        S = ids.shape[1] if ids.ndim == 2 and B > 0 else 1
+        T = tgt.shape[1] if tgt.ndim == 2 and B > 0 else 1
+        tlogp = np.zeros((B, T), np.float32)
+        nll = np.zeros(B, np.float64)
+        _check(lib().onmt_score(self._h, _ptr(ids), _ptr(lens), B, S, _ptr(tgt), _ptr(tgt_lens), T, _ptr(tlogp),
+                                _ptr(nll)))
+        return {"token_logp": tlogp, "nll": nll}
 
     def translate_dev(self, ids_dev, lens_dev, beam: int, max_len: int, length_penalty: float,
                       out: Dict, lens_host=None):

@@ -113,6 +113,8 @@ struct GenOut {
   int K;
   int rows_valid;
   int rows_pad;
+  const int* gold;    // teacher-forced scoring (optional): gold id of each row, or -1
+  float* zgold;       // [rows] the gold logit, written by the tile that holds the id
 };
 
 // Scan one tile column (n <= 128 logits of one row): online max / sum-exp plus an

@@ -82,6 +82,12 @@ void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, 
 void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int R, int K,
                        float* lse, float* oz, int* oi, cudaStream_t st);
 
+void launch_teacher_gather(const int* tgt, int T_max, int t, int B, const GatherArgs& g, cudaStream_t st);
+void launch_score_reduce(const float2* ms, int n_vt, int rows_pad, const float* zgold, const int* gold, int B,
+                         int T_max, float* out, cudaStream_t st);
+void launch_score_row(const float* logits, int v_pad, const float* bias, int V, const int* gold, int B, int T_max,
+                      int t, float* out, cudaStream_t st);
+
 static thread_local std::string g_err;
 
 struct Error {
@@ -322,9 +328,15 @@ struct onmt_model {
   std::map<std::string, EventPairs> evs;   // per kernel family ("gen", "step", "encode", ...)
   bool capturing = false;
   GraphCache graph;
+  GraphCache* cap_graph = nullptr;           // the graph being captured (profiling event nodes)
+  GraphCache score_graph;
+  // teacher-forced scoring workspace
+  Act xs_all;                                // generator operand of every (step, sentence) row
+  DevBuf s_tgt, s_gold, s_zgold, s_out, s_ms, s_tz, s_ti;
 
   ~onmt_model() {
     if (graph.exec) cudaGraphExecDestroy(graph.exec);
+    if (score_graph.exec) cudaGraphExecDestroy(score_graph.exec);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
@@ -374,7 +386,7 @@ static EvPair prof_begin(onmt_model* m, const char* name) {
 static void prof_end(onmt_model* m, const char* name, const EvPair& ev) {
   if (!prof_on(m, name)) return;
   ev_record(ev.b, m->stream, m->capturing);
-  if (m->capturing) m->graph.ev_nodes.push_back({name, ev});
+  if (m->capturing) m->cap_graph->ev_nodes.push_back({name, ev});
   else m->evs[name].pending.push_back({ev, true});
 }
 
@@ -802,6 +814,84 @@ static void dec_step_specs(onmt_model* m, const int* d_lens, int B, int S_max, i
   att.part = m->ds_part.as<float>();
 }
 
+// One decoder step up to h~ (A5 inputs already gathered): the L LSTM layers, attention and
+// h~ = tanh(W_out [c; h]); h~ goes to m->htilde (input feed) and to the generator operand
+// xg_dst.  Used by translation (per-layer path) and by teacher-forced scoring.
+static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_max, int K, const int* done,
+                               XOut xg_dst, StepCtl ctl) {
+  const bool bf = m->use_tc;
+  const int R = B * K, H = m->H, L = m->L;
+  const int rp = m->xg.rows_pad;
+  float* hh = m->st_h.as<float>();
+  float* cc = m->st_c.as<float>();
+  float* cg = m->st_cg.as<float>();
+  float* P = m->dec_p.as<float>();
+  for (int l = 0; l < L; ++l) {
+    const Mat& W = *m->dec_w[l];
+    CellDst dst{};
+    if (l + 1 < L) {
+      dst.x[0] = m->xdec[l + 1]->xo(bf); dst.col[0] = 0; dst.n = 1;
+    } else {
+      dst.x[0] = m->xo.xo(bf); dst.col[0] = H; dst.n = 1;
+    }
+    if (m->use_tc && m->fused) {
+      // gates GEMM + split-K cluster reduction + LSTM cell in one kernel
+      EvPair pg = prof_begin(m, "gemm");
+      const Act& X = *m->xdec[l];
+      cudaError_t e = tc_gemm_cell(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, R, W.k_pad / kBK,
+                                   m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H, cc + (size_t)l * rp * H,
+                                   hh + (size_t)l * rp * H, H, dst, m->f_scratch.as<float>(),
+                                   m->f_count.as<unsigned int>() + (size_t)l * 2048, m->num_sms, ctl, m->stream);
+      prof_end(m, "gemm", pg);
+      if (e != cudaErrorInvalidConfiguration) {   // (no cluster shape fits: unfused path below)
+        ONMT_CUDA(e);
+        count(m);
+        continue;
+      }
+    }
+    EvPair pg = prof_begin(m, "gemm");
+    int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
+    prof_end(m, "gemm", pg);
+    EvPair pc = prof_begin(m, "cell");
+    launch_dec_cell(P, s, m->xdec[l]->rows_pad, W.m_pad, m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H,
+                    cc + (size_t)l * rp * H, hh + (size_t)l * rp * H, H, R, dst, ctl, m->stream);
+    count(m);
+    prof_end(m, "cell", pc);
+  }
+  const float* htop = hh + (size_t)(L - 1) * rp * H;
+  {
+    EvPair pa = prof_begin(m, "attention");
+    const float* keys = m->general ? m->keys.as<float>() : m->mem.as<float>();
+    const int key_ld = m->general ? m->attn_win_t.m_pad : H;
+    ONMT_CUDA(launch_attention(htop, keys, key_ld, m->mem.as<float>(), d_lens, B, S_max, H, K, m->xo.xo(bf),
+                               done, m->num_sms, ctl, m->stream));
+    count(m);
+    prof_end(m, "attention", pa);
+  }
+  cudaError_t fe = cudaErrorInvalidConfiguration;
+  if (m->use_tc && m->fused) {
+    EvPair pg = prof_begin(m, "gemm");
+    fe = tc_gemm_tanh(m->attn_wout.tmap, m->xo.tmap, m->attn_wout.m_pad, m->xo.rows_pad, m->xo.n_group, R,
+                      m->attn_wout.k_pad / kBK, H, m->htilde.as<float>(), xg_dst, m->f_scratch.as<float>(),
+                      m->f_count.as<unsigned int>() + (size_t)L * 2048, m->num_sms, ctl, m->stream);
+    prof_end(m, "gemm", pg);
+    if (fe != cudaErrorInvalidConfiguration) {
+      ONMT_CUDA(fe);
+      count(m);
+    }
+  }
+  if (fe == cudaErrorInvalidConfiguration) {
+    EvPair pg = prof_begin(m, "gemm");
+    int s = gemm(m, m->attn_wout, m->xo, R, 0, P, ctl);
+    prof_end(m, "gemm", pg);
+    EvPair po = prof_begin(m, "attn_out");
+    launch_attn_out(P, s, m->xo.rows_pad, m->attn_wout.m_pad, m->htilde.as<float>(), H, R, xg_dst, ctl,
+                    m->stream);
+    count(m);
+    prof_end(m, "attn_out", po);
+  }
+}
+
 static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int K, int max_len, float alpha,
                             bool trace, const DecodeOut& out) {
   const bool bf = m->use_tc;
@@ -851,70 +941,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       count(m);
       prof_end(m, "gemm", pd);
     }
-    for (int l = 0; l < L && !ds_on; ++l) {
-      const Mat& W = *m->dec_w[l];
-      CellDst dst{};
-      if (l + 1 < L) {
-        dst.x[0] = m->xdec[l + 1]->xo(bf); dst.col[0] = 0; dst.n = 1;
-      } else {
-        dst.x[0] = m->xo.xo(bf); dst.col[0] = H; dst.n = 1;
-      }
-      if (m->use_tc && m->fused) {
-        // gates GEMM + split-K cluster reduction + LSTM cell in one kernel
-        EvPair pg = prof_begin(m, "gemm");
-        const Act& X = *m->xdec[l];
-        cudaError_t e = tc_gemm_cell(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, R, W.k_pad / kBK,
-                                     m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H, cc + (size_t)l * rp * H,
-                                     hh + (size_t)l * rp * H, H, dst, m->f_scratch.as<float>(),
-                                     m->f_count.as<unsigned int>() + (size_t)l * 2048, m->num_sms, ctl, m->stream);
-        prof_end(m, "gemm", pg);
-        if (e != cudaErrorInvalidConfiguration) {   // (no cluster shape fits: unfused path below)
-          ONMT_CUDA(e);
-          count(m);
-          continue;
-        }
-      }
-      EvPair pg = prof_begin(m, "gemm");
-      int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
-      prof_end(m, "gemm", pg);
-      EvPair pc = prof_begin(m, "cell");
-      launch_dec_cell(P, s, m->xdec[l]->rows_pad, W.m_pad, m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H,
-                      cc + (size_t)l * rp * H, hh + (size_t)l * rp * H, H, R, dst, ctl, m->stream);
-      count(m);
-      prof_end(m, "cell", pc);
-    }
-    const float* htop = hh + (size_t)(L - 1) * rp * H;
-    if (!ds_on) {
-      EvPair pa = prof_begin(m, "attention");
-      const float* keys = m->general ? m->keys.as<float>() : m->mem.as<float>();
-      const int key_ld = m->general ? m->attn_win_t.m_pad : H;
-      ONMT_CUDA(launch_attention(htop, keys, key_ld, m->mem.as<float>(), d_lens, B, S_max, H, K, m->xo.xo(bf),
-                                 bs.done, m->num_sms, ctl, m->stream));
-      count(m);
-      prof_end(m, "attention", pa);
-    }
-    cudaError_t fe = ds_on ? cudaSuccess : cudaErrorInvalidConfiguration;
-    if (m->use_tc && m->fused && !ds_on) {
-      EvPair pg = prof_begin(m, "gemm");
-      fe = tc_gemm_tanh(m->attn_wout.tmap, m->xo.tmap, m->attn_wout.m_pad, m->xo.rows_pad, m->xo.n_group, R,
-                        m->attn_wout.k_pad / kBK, H, m->htilde.as<float>(), m->xg.xo(bf), m->f_scratch.as<float>(),
-                        m->f_count.as<unsigned int>() + (size_t)L * 2048, m->num_sms, ctl, m->stream);
-      prof_end(m, "gemm", pg);
-      if (fe != cudaErrorInvalidConfiguration) {
-        ONMT_CUDA(fe);
-        count(m);
-      }
-    }
-    if (fe == cudaErrorInvalidConfiguration) {
-      EvPair pg = prof_begin(m, "gemm");
-      int s = gemm(m, m->attn_wout, m->xo, R, 0, P, ctl);
-      prof_end(m, "gemm", pg);
-      EvPair po = prof_begin(m, "attn_out");
-      launch_attn_out(P, s, m->xo.rows_pad, m->attn_wout.m_pad, m->htilde.as<float>(), H, R, m->xg.xo(bf), ctl,
-                      m->stream);
-      count(m);
-      prof_end(m, "attn_out", po);
-    }
+    if (!ds_on) enqueue_dec_layers(m, d_lens, B, S_max, K, bs.done, m->xg.xo(bf), ctl);
     const double lp = std::pow((5.0 + t) / 6.0, (double)alpha);
     if (use_gen_step(m, m->xg)) {
       // K-outer generator (phase A of gen_step.cu), partials [row][C]; then row reduce + beam step
@@ -970,6 +997,124 @@ static void phase_trace_end(int grid) {
   dec_step_set_trace(nullptr);
 }
 
+// Teacher-forced scoring: encoder, then T_max decoder steps fed with
+// the gold tokens (A5 with parent = self), then ONE generator pass over every (step,
+// sentence) row - a tensor-core GEMM of [T_max*B x H] by [H x V] with the log-softmax and
+// the gold-logit gather fused (tc_gemm_kernel MODE_GEN) - and log p = z_gold - LSE.
+// fp32 models run the generator per step (SIMT logits + score_row_kernel).
+static void enqueue_score(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int T_max) {
+  const bool bf = m->use_tc;
+  const int H = m->H, L = m->L;
+  const int rp = m->xg.rows_pad;
+  enqueue_encoder(m, d_ids, d_lens, B, S_max);
+  BeamState bs = beam_state(m, false);
+  float* hh = m->st_h.as<float>();
+  float* cc = m->st_c.as<float>();
+  launch_init_decode(bs, B, 1, m->enc_h.as<float>(), m->enc_c.as<float>(), L, H, hh, cc, rp, m->htilde.as<float>(),
+                     m->stream);
+  count(m);
+  GatherArgs ga{};
+  ga.emb_tgt = m->emb_tgt.as<float>();
+  ga.E = m->E; ga.H = H; ga.L = L;
+  ga.htilde = m->htilde.as<float>();
+  ga.h = hh; ga.c = cc; ga.cg = m->st_cg.as<float>(); ga.rows_pad = rp;
+  for (int l = 0; l < L; ++l) ga.x[l] = m->xdec[l]->xo(bf);
+  const StepCtl none{nullptr, 0};
+  for (int t = 1; t <= T_max; ++t) {
+    launch_teacher_gather(m->s_tgt.as<int>(), T_max, t, B, ga, m->stream);
+    count(m);
+    XOut dst = m->xg.xo(bf);
+    if (bf) {                                  // rows (t-1)*B .. of the all-steps operand
+      dst = m->xs_all.xo(true);
+      dst.hl += (size_t)(t - 1) * B * dst.k_pad;
+    }
+    enqueue_dec_layers(m, d_lens, B, S_max, 1, nullptr, dst, none);
+    if (!bf) {
+      ONMT_CUDA(simt_gemm_partial(m->gen_w.w.p, m->gen_w.bf16, m->gen_w.m_pad, m->gen_w.k_pad, m->xg.f32.as<float>(),
+                                  m->xg.rows_pad, B, 1, m->logits.as<float>(), none, m->stream));
+      launch_score_row(m->logits.as<float>(), m->gen_w.m_pad, m->gen_b.as<float>(), m->Vt, m->s_gold.as<int>(), B,
+                       T_max, t, m->s_out.as<float>(), m->stream);
+      count(m, 2);
+    }
+  }
+  if (bf) {
+    const Act& X = m->xs_all;
+    GenOut g{};
+    g.ms = m->s_ms.as<float2>();
+    g.tz = m->s_tz.as<float>();
+    g.ti = m->s_ti.as<int>();
+    g.bias = m->gen_b.as<float>();
+    g.V = m->Vt;
+    g.K = 1;
+    g.rows_valid = T_max * B;
+    g.rows_pad = X.rows_pad;
+    g.gold = m->s_gold.as<int>();
+    g.zgold = m->s_zgold.as<float>();
+    EvPair pg = prof_begin(m, "gen");
+    ONMT_CUDA(tc_gemm_gen(m->gen_w.tmap, X.tmap, m->gen_w.m_pad, X.rows_pad, X.n_group, m->gen_w.k_pad / kBK, g, none,
+                          m->stream));
+    prof_end(m, "gen", pg);
+    launch_score_reduce(g.ms, m->gen_w.m_pad / kTileM, X.rows_pad, g.zgold, g.gold, B, T_max, m->s_out.as<float>(),
+                        m->stream);
+    count(m, 2);
+  }
+  ONMT_CUDA(cudaGetLastError());
+}
+
+static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int T_max) {
+  prepare_encoder(m, B, S_max);
+  prepare_decoder(m, B, S_max, 1, T_max, false);
+  const bool bf = m->use_tc;
+  if (bf) {
+    m->xs_all.ensure(T_max * B, m->H, true);
+    const size_t n_vt = m->gen_w.m_pad / kTileM, rp = m->xs_all.rows_pad;
+    m->s_ms.ensure(n_vt * rp * 8);
+    m->s_tz.ensure(n_vt * rp * 4);
+    m->s_ti.ensure(n_vt * rp * 4);
+    m->s_zgold.ensure(rp * 4);
+  }
+  if (!m->use_graph) {
+    enqueue_score(m, d_ids, d_lens, B, S_max, T_max);
+    return;
+  }
+  std::vector<int64_t> key = {B, S_max, T_max, m->profile, m->use_tc, (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
+                              (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
+  GraphCache& gc = m->score_graph;
+  if (!gc.exec || gc.key != key) {
+    if (gc.exec) {
+      ONMT_CUDA(cudaStreamSynchronize(m->stream));
+      ONMT_CUDA(cudaGraphExecDestroy(gc.exec));
+      gc.exec = nullptr;
+      for (auto& pe : gc.ev_nodes) m->evs[pe.first].release({pe.second});
+      gc.ev_nodes.clear();
+    }
+    cudaGraph_t graph;
+    const int64_t before = m->launches;
+    ONMT_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+    m->capturing = true;
+    m->cap_graph = &gc;
+    try {
+      enqueue_score(m, d_ids, d_lens, B, S_max, T_max);
+    } catch (...) {
+      m->capturing = false;
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(m->stream, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      throw;
+    }
+    m->capturing = false;
+    ONMT_CUDA(cudaStreamEndCapture(m->stream, &graph));
+    ONMT_CUDA(cudaGraphInstantiate(&gc.exec, graph, 0));
+    ONMT_CUDA(cudaGraphDestroy(graph));
+    gc.kernels = m->launches - before;
+    m->launches = before;
+    gc.key = key;
+  }
+  ONMT_CUDA(cudaGraphLaunch(gc.exec, m->stream));
+  m->launches += gc.kernels;
+  for (auto& pe : gc.ev_nodes) m->evs[pe.first].pending.push_back({pe.second, false});
+}
+
 // The whole translation (encoder, decoder init, every decode step, finalize) as one CUDA
 // graph, cached per shape / pointer set: one cudaGraphLaunch per call, no host round trip.
 static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int K, int max_len,
@@ -1003,6 +1148,7 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     const int64_t before = m->launches;
     ONMT_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
     m->capturing = true;
+    m->cap_graph = &gc;
     try {
       enqueue();
     } catch (...) {
@@ -1235,6 +1381,49 @@ onmt_status onmt_translate_trace(onmt_model* m, const int32_t* ids, const int32_
   if (!sel_parent || !sel_token || !sel_score) return fail(ONMT_E_INVALID_ARG, "null trace pointer");
   return translate_impl(m, ids, lens, B, S_max, beam, max_len, alpha, hyps, olens, scores, raw, tlogp, sel_parent,
                         sel_token, sel_score);
+}
+
+onmt_status onmt_score(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
+                       const int32_t* tgt, const int32_t* tgt_lens, int32_t T_max, float* out_token_logp,
+                       double* out_nll) {
+  onmt_status s = validate(m, ids, lens, B, S_max, true);
+  if (s != ONMT_OK) return s;
+  if (B == 0) return ONMT_OK;
+  if (T_max < 1) return fail(ONMT_E_INVALID_ARG, "T_max < 1");
+  if (!tgt || !tgt_lens || !out_token_logp) return fail(ONMT_E_INVALID_ARG, "null target / output pointer");
+  for (int b = 0; b < B; ++b) {
+    if (tgt_lens[b] < 1) return fail(ONMT_E_EMPTY_SOURCE, "empty target sentence " + std::to_string(b));
+    if (tgt_lens[b] > T_max) return fail(ONMT_E_INVALID_ARG, "tgt_len > T_max");
+    for (int t = 0; t < tgt_lens[b]; ++t) {
+      const int v = tgt[(size_t)b * T_max + t];
+      if (v < 0 || v >= m->Vt) return fail(ONMT_E_ID_RANGE, "target id out of range");
+    }
+  }
+  ONMT_API_BEGIN
+  ONMT_CUDA(cudaSetDevice(m->device));
+  upload_src(m, ids, lens, B, S_max);
+  std::vector<int32_t> clean((size_t)B * T_max, 0), gold((size_t)T_max * B, -1);
+  for (int b = 0; b < B; ++b)
+    for (int t = 0; t < tgt_lens[b]; ++t) {
+      clean[(size_t)b * T_max + t] = tgt[(size_t)b * T_max + t];
+      gold[(size_t)t * B + b] = tgt[(size_t)b * T_max + t];
+    }
+  m->s_tgt.ensure(clean.size() * 4);
+  m->s_gold.ensure(gold.size() * 4);
+  m->s_out.ensure((size_t)B * T_max * 4);
+  ONMT_CUDA(cudaMemcpyAsync(m->s_tgt.p, clean.data(), clean.size() * 4, cudaMemcpyHostToDevice, m->stream));
+  ONMT_CUDA(cudaMemcpyAsync(m->s_gold.p, gold.data(), gold.size() * 4, cudaMemcpyHostToDevice, m->stream));
+  run_score(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max, T_max);
+  ONMT_CUDA(cudaMemcpyAsync(out_token_logp, m->s_out.p, (size_t)B * T_max * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaStreamSynchronize(m->stream));
+  if (out_nll)
+    for (int b = 0; b < B; ++b) {
+      double acc = 0.0;
+      for (int t = 0; t < tgt_lens[b]; ++t) acc -= (double)out_token_logp[(size_t)b * T_max + t];
+      out_nll[b] = acc;
+    }
+  return ONMT_OK;
+  ONMT_API_END
 }
 
 onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_ids, const int32_t* d_lens, const int32_t* lens_host,
