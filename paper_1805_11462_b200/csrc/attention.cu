@@ -53,11 +53,16 @@ __device__ __forceinline__ float4 ld_peer4(const float* local, uint32_t peer) {
   return v;
 }
 
+__device__ __forceinline__ float att_tanh(float x) {
+  const float e = __expf(-2.f * fabsf(x));
+  return copysignf(__fdividef(1.f - e, 1.f + e), x);
+}
+
 template <int KMAX, int JPT>
 __global__ void __launch_bounds__(kAttThreads)
 attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict__ keys, int key_ld,
-                         const float* __restrict__ mem, const int* __restrict__ lens, int S_max, int H, int K, int CH,
-                         int SC, XOut xo, const int* __restrict__ done, StepCtl ctl) {
+                         const float* __restrict__ mem, int val_ld, const int* __restrict__ lens, int S_max, int H,
+                         int K, int CH, int SC, XOut xo, const int* __restrict__ done, StepCtl ctl, AttFold fo) {
   KT(0);
   pdl_trigger();
   extern __shared__ __align__(16) float sh[];
@@ -65,8 +70,9 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   const uint32_t r = cluster_ctarank();
   const int b = blockIdx.y;
   const bool same = keys == mem;
-  const int kl = same ? H : key_ld;
-  const bool vec = (H & 3) == 0 && (kl & 3) == 0;
+  const int kl = same ? val_ld : key_ld;
+  const int vl = val_ld;                          // value rows: m_s, or W_out[:, :H] m_s when folded
+  const bool vec = (H & 3) == 0 && (kl & 3) == 0 && (vl & 3) == 0;
   auto r4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
   // layout: q [K][H] (later: partial context) | m, l, scale [KMAX] | e [KMAX][16] |
   //         2 x (mem [SC][H], keys [SC][kl])
@@ -76,8 +82,9 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   float* s_scale = s_l + kKMax;
   float* e = s_scale + kKMax;
   float* buf = e + kKMax * kSCMax;
-  const size_t mb = r4((size_t)SC * H), kb = same ? 0 : r4((size_t)SC * kl);
+  const size_t mb = r4((size_t)SC * vl), kb = same ? 0 : r4((size_t)SC * kl);
   auto mbuf = [&](int i) { return buf + (size_t)(i & 1) * (mb + kb); };
+  float* s_hp = buf + 2 * (mb + kb);                // folded W_out: the combine slice's tile shares
   auto kbuf = [&](int i) { return same ? mbuf(i) : mbuf(i) + mb; };
 
   // source rows [s_beg, s_lim) of this chunk, prefetched before griddepcontrol.wait without
@@ -88,7 +95,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   auto stage = [&](int i) {
     const int s0 = s_beg + i * SC;
     const int ns = min(SC, s_lim - s0);
-    cp_async_rows(mbuf(i), mem + ((size_t)b * S_max + s0) * H, ns * H);
+    cp_async_rows(mbuf(i), mem + ((size_t)b * S_max + s0) * vl, ns * vl);
     if (!same) cp_async_rows(kbuf(i), keys + ((size_t)b * S_max + s0) * key_ld, ns * key_ld);
     cp_async_commit();
   };
@@ -103,6 +110,21 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   }
   cp_async_rows(q, htop + (size_t)b * K * H, K * H);   // queries: the K beam rows of sentence b
   cp_async_commit();
+  // folded W_out: prefetch this CTA's combine slice of the top layer's W_out h shares
+  // [tile][k][column] (produced by the previous kernel) - they land while the scores run
+  const bool hpref = fo.wpart && fo.pref && vec;
+  const int cj0 = (int)((long long)(H >> 2) * r / nch), cwj = (int)((long long)(H >> 2) * (r + 1) / nch) - cj0;
+  if (hpref) {
+    const int nit = K * cwj;
+    for (int idx = threadIdx.x; idx < fo.n_wt * nit; idx += blockDim.x) {
+      const int t = idx / nit, it = idx % nit;
+      const int k = it / cwj, j = 4 * (cj0 + it % cwj);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s_hp + 4 * (size_t)idx)),
+                   "l"(fo.wpart + ((size_t)t * fo.rows_pad + b * K + k) * H + j)
+                   : "memory");
+    }
+    cp_async_commit();
+  }
   const int L = lens[b];
   const int s_end = min(L, s_lim);
   const int nsub = s_end > s_beg ? (s_end - s_beg + SC - 1) / SC : 0;
@@ -117,7 +139,11 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
     for (int u = 0; u < JPT; ++u) acc[k][u] = 0.f;
 
   for (int i = 0; i < nsub; ++i) {
-    if (i == 0 || i + 1 >= nsub_max) cp_async_wait<0>();   // (iteration 0 also needs q)
+    if (i + 1 >= nsub_max) cp_async_wait<0>();
+    else if (i == 0) {                                       // (iteration 0 also needs q; the
+      if (hpref) cp_async_wait<1>();                         //  W_out shares may stay in flight)
+      else cp_async_wait<0>();
+    }
     else cp_async_wait<1>();
     __syncthreads();
     if (i == 0) KT(3);
@@ -208,7 +234,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
       for (int k = 0; k < KMAX; ++k)
         if (k < K) acc[k][u] *= s_scale[k];
       for (int s = 0; s < ns; ++s) {
-        const float mv = ms[(size_t)s * H + j];
+        const float mv = ms[(size_t)s * vl + j];
 #pragma unroll
         for (int k = 0; k < KMAX; ++k)
           if (k < K) acc[k][u] = fmaf(e[k * kSCMax + s], mv, acc[k][u]);
@@ -272,10 +298,38 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
         const float w = coef[p * KMAX + k];
         c.x = fmaf(w, v[p].x, c.x); c.y = fmaf(w, v[p].y, c.y); c.z = fmaf(w, v[p].z, c.z); c.w = fmaf(w, v[p].w, c.w);
       }
-      store_x(xo, b * K + k, j, c.x);
-      store_x(xo, b * K + k, j + 1, c.y);
-      store_x(xo, b * K + k, j + 2, c.z);
-      store_x(xo, b * K + k, j + 3, c.w);
+      const int row = b * K + k;
+      if (fo.wpart) {
+        // folded W_out: c = W_out[:, :H] c_t (values were projected); add the top cell layer's
+        // W_out[:, H:2H] h_t shares (fixed tile order) and finish h~ = tanh(.)
+        float4 hs = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (hpref) {                                               // prefetched (fixed tile order)
+          for (int t = 0; t < fo.n_wt; ++t) {
+            const float4 pv = *reinterpret_cast<const float4*>(s_hp + 4 * ((size_t)t * K * wj + it));
+            hs.x += pv.x; hs.y += pv.y; hs.z += pv.z; hs.w += pv.w;
+          }
+        } else
+        for (int t0 = 0; t0 < fo.n_wt; t0 += 8) {                 // 8 loads in flight, fixed order
+          float4 pv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            pv[u] = t0 + u < fo.n_wt ? __ldcg(reinterpret_cast<const float4*>(fo.wpart + ((size_t)(t0 + u) * fo.rows_pad + row) * H + j))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) { hs.x += pv[u].x; hs.y += pv[u].y; hs.z += pv[u].z; hs.w += pv[u].w; }
+        }
+        const float4 ht = make_float4(att_tanh(c.x + hs.x), att_tanh(c.y + hs.y), att_tanh(c.z + hs.z), att_tanh(c.w + hs.w));
+        *reinterpret_cast<float4*>(fo.htilde + (size_t)row * H + j) = ht;
+        store_x(fo.xg, row, j, ht.x);
+        store_x(fo.xg, row, j + 1, ht.y);
+        store_x(fo.xg, row, j + 2, ht.z);
+        store_x(fo.xg, row, j + 3, ht.w);
+      } else {
+        store_x(xo, row, j, c.x);
+        store_x(xo, row, j + 1, c.y);
+        store_x(xo, row, j + 2, c.z);
+        store_x(xo, row, j + 3, c.w);
+      }
     }
   } else {
     const int j0 = (int)((long long)H * r / nch), j1 = (int)((long long)H * (r + 1) / nch);
@@ -288,7 +342,22 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
       float c = 0.f;
 #pragma unroll
       for (int p = 0; p < 8; ++p) c = fmaf(coef[p * KMAX + k], v[p], c);
-      store_x(xo, b * K + k, j, c);
+      const int row = b * K + k;
+      if (fo.wpart) {
+        float hs = 0.f;
+        for (int t0 = 0; t0 < fo.n_wt; t0 += 8) {
+          float pv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pv[u] = t0 + u < fo.n_wt ? __ldcg(fo.wpart + ((size_t)(t0 + u) * fo.rows_pad + row) * H + j) : 0.f;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) hs += pv[u];
+        }
+        const float ht = att_tanh(c + hs);
+        fo.htilde[(size_t)row * H + j] = ht;
+        store_x(fo.xg, row, j, ht);
+      } else {
+        store_x(xo, row, j, c);
+      }
     }
   }
   KT(7);
@@ -308,8 +377,8 @@ static int att_nch(int B, int S_max, int num_sms) {
 
 template <int KMAX, int JPT>
 static cudaError_t launch_att(dim3 grid, int nch, size_t smem, cudaStream_t st, const float* htop, const float* keys,
-                              int key_ld, const float* mem, const int* lens, int S_max, int H, int K, int CH, int SC,
-                              XOut xo, const int* done, StepCtl ctl) {
+                              int key_ld, const float* mem, int val_ld, const int* lens, int S_max, int H, int K,
+                              int CH, int SC, XOut xo, const int* done, StepCtl ctl, AttFold fo) {
   auto fn = attention_cluster_kernel<KMAX, JPT>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -327,30 +396,33 @@ static cudaError_t launch_att(dim3 grid, int nch, size_t smem, cudaStream_t st, 
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, fn, htop, keys, key_ld, mem, lens, S_max, H, K, CH, SC, xo, done, ctl);
+  return cudaLaunchKernelEx(&cfg, fn, htop, keys, key_ld, mem, val_ld, lens, S_max, H, K, CH, SC, xo, done, ctl, fo);
 }
 
-cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, const float* mem, const int* lens,
-                             int B, int S_max, int H, int K, XOut xo, const int* done, int num_sms, StepCtl ctl,
-                             cudaStream_t st) {
+cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, const float* mem, int val_ld,
+                             const int* lens, int B, int S_max, int H, int K, XOut xo, const int* done, int num_sms,
+                             StepCtl ctl, cudaStream_t st, AttFold fo) {
   if (H > 4 * kAttThreads || K > kKMax) return cudaErrorInvalidValue;
   const int nch = att_nch(B, S_max, num_sms);
   const int CH = (S_max + nch - 1) / nch;
   const bool same = keys == mem;
-  const int kl = same ? H : key_ld;
+  const int kl = same ? val_ld : key_ld;
   auto r4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
   auto bytes = [&](int SC) {
-    return (r4((size_t)K * H) + 3 * 16 + 16 * kSCMax + 2 * (r4((size_t)SC * H) + (same ? 0 : r4((size_t)SC * kl)))) * 4;
+    return (r4((size_t)K * H) + 3 * 16 + 16 * kSCMax + 2 * (r4((size_t)SC * val_ld) + (same ? 0 : r4((size_t)SC * kl)))) * 4;
   };
-  const int SC = bytes(16) <= 200 * 1024 ? 16 : 8;
-  const size_t smem = bytes(SC);
+  size_t extra = 0;                                // folded W_out: prefetched tile shares
+  if (fo.wpart) extra = (size_t)fo.n_wt * K * ((H / 4 + nch - 1) / nch) * 16;
+  const int SC = bytes(16) + extra <= 200 * 1024 ? 16 : 8;
+  fo.pref = bytes(SC) + extra <= 220 * 1024;
+  const size_t smem = bytes(SC) + (fo.pref ? extra : 0);
   const dim3 grid(nch, B);
 #define ONMT_ATT(KM)                                                                                              \
   return H <= 2 * kAttThreads                                                                                     \
-             ? launch_att<KM, 2>(grid, nch, smem, st, htop, keys, key_ld, mem, lens, S_max, H, K, CH, SC, xo, done, \
-                                 ctl)                                                                             \
-             : launch_att<KM, 4>(grid, nch, smem, st, htop, keys, key_ld, mem, lens, S_max, H, K, CH, SC, xo, done, \
-                                 ctl)
+             ? launch_att<KM, 2>(grid, nch, smem, st, htop, keys, key_ld, mem, val_ld, lens, S_max, H, K, CH, SC, xo, \
+                                 done, ctl, fo)                                                                             \
+             : launch_att<KM, 4>(grid, nch, smem, st, htop, keys, key_ld, mem, val_ld, lens, S_max, H, K, CH, SC, xo, \
+                                 done, ctl, fo)
   if (K <= 1) ONMT_ATT(1);
   if (K <= 2) ONMT_ATT(2);
   if (K <= 4) ONMT_ATT(4);

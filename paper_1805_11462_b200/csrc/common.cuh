@@ -55,6 +55,18 @@ struct XOut {
   int k_pad;
 };
 
+// W_out folded into attention: the context accumulates the projected
+// values W_out[:, :H] m_s, the top cell layer left W_out[:, H:2H] h_t in n_wt tile shares
+// wpart [n_wt][rows_pad][H], and the combine writes h~ = tanh(sum) to htilde and xg.
+struct AttFold {
+  const float* wpart;           // nullptr: plain attention (context -> xo)
+  int n_wt;
+  int rows_pad;
+  float* htilde;
+  XOut xg;
+  int pref;                     // (set by the launcher) shares prefetched into shared memory
+};
+
 __device__ __forceinline__ void store_x(const XOut& x, int r, int c, float v) {
   size_t i = (size_t)r * x.k_pad + c;
   if (x.hl) {

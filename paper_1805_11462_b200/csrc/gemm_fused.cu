@@ -44,6 +44,11 @@ struct FusedArgs {
   // EPI_TANH
   float* htilde;
   XOut xg;
+  // EPI_CELL of the top decoder layer with W_out folded into attention:
+  // woh = W_out[:, H:2H]^T in 32-unit tile slices (bf16 [m_tiles*32][H]); the CTA adds its
+  // units' share  W_out[:, units] h[units, cols]  to woh_part[m_tile][row][H] (fp32)
+  const __nv_bfloat16* woh;
+  float* woh_part;
   StepCtl ctl;
   int dbg;                 // microbenchmark ablations (ONMT_KTRACE builds only)
 };
@@ -78,7 +83,13 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   uint64_t* full = reinterpret_cast<uint64_t*>(tail + 32 * 16 + (size_t)a.NC * 32 * 4);
   uint64_t* done = full + a.stages;
   uint64_t* rbar = done + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + 1);
+  uint64_t* wbar = rbar + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
+  const int ncp = (a.NC + 7) & ~7;                                 // s_hc row stride
+  // (offsets from smem keep the shared address space visible to the compiler: LDS, not LD.E)
+  const size_t woh_off = ((size_t)(reinterpret_cast<uint8_t*>(tslot) - smem) + 16 + 127) & ~(size_t)127;
+  __nv_bfloat16* woh_s = reinterpret_cast<__nv_bfloat16*>(smem + woh_off);                          // [32][H]
+  float* s_hc = reinterpret_cast<float*>(woh_s + (size_t)32 * a.H);                                 // [32][ncp]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x / a.S;
@@ -101,10 +112,16 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
     for (int s = 0; s < a.stages; ++s) mbar_init(&full[s], 1);
     mbar_init(done, 1);
     mbar_init(rbar, 1);
+    mbar_init(wbar, 1);
     fence_mbar_init();
     for (int i = 0; i < nkb; ++i) {
       mbar_expect_tx(&full[i], a_bytes);
       tma_load_2d(smem + i * stage_bytes, &tmW, (kb0 + i) * kBK, m0, &full[i]);
+    }
+    if (EPI == EPI_CELL && a.woh) {                                // W_out[:, tile's units]^T (constant)
+      const uint32_t wb = (uint32_t)(32 * a.H * 2);
+      mbar_arrive_expect_tx(wbar, wb);
+      bulk_g2s(woh_s, a.woh + (size_t)mt * 32 * a.H, wb, wbar);
     }
   }
   if (warp == 0) tmem_alloc_dyn(tslot, a.tmem_cols);
@@ -169,6 +186,7 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   tc_fence_after();
   KT(2);
   if (quit) {                                    // every TMA landed (waited above); nothing else in flight
+    if (EPI == EPI_CELL && a.woh) mbar_wait(wbar, 0);
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, a.tmem_cols);
@@ -204,9 +222,8 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
     }
   }
   tc_fence_before();
-  __threadfence();
-  __syncthreads();
-  KT(3);
+  __syncthreads();        // (thread 0's gpu-scope fence in cta_group_barrier is cumulative over
+  KT(3);                  //  the CTA's stores ordered before it by the barrier: release pattern)
   if (threadIdx.x == 0) {
     cta_group_barrier(a.counters + 2 * tile, (unsigned)a.S);   // the tile's S splits are stored
     asm volatile("fence.proxy.async;" ::: "memory");
@@ -279,6 +296,7 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
                       g_ = tanhfast(gz[u].z + bb[u].z), o_ = sigmf(gz[u].w + bb[u].w);
           const float cn = f_ * cp[u] + i_ * g_;
           const float h = o_ * tanhfast(cn);
+          if (a.woh && it < nit) s_hc[ul * ncp + c] = (r < a.n_valid && j < a.H) ? h : 0.f;
           if (it >= nit || r >= a.n_valid || j >= a.H) continue;
 #ifdef ONMT_KTRACE
           if (a.dbg == 2) { if (h == 12345.f) a.c_out[0] = cn; continue; }
@@ -290,6 +308,41 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
           if (a.dbg == 1) continue;
 #endif
           for (int d = 0; d < a.dst.n; ++d) store_x(a.dst.x[d], r, a.dst.col[d] + j, h);
+        }
+      }
+      if (a.woh) {
+        // W_out[:, units] h[units, my columns] -> woh_part[mt][row][o]; fp32 FFMA on the
+        // bf16 weights (exact products), fixed unit order (deterministic)
+        mbar_wait(wbar, 0);
+        __syncthreads();
+        for (int c0 = 0; c0 < ncols; c0 += 8) {
+          for (int o0 = 0; o0 < a.H; o0 += 512) {
+            const int oa = o0 + threadIdx.x, ob = oa + 256;
+            float acc[2][8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) { acc[0][x] = 0.f; acc[1][x] = 0.f; }
+#pragma unroll 4
+            for (int ul = 0; ul < 32; ++ul) {
+              const float wa = oa < a.H ? __bfloat162float(woh_s[(size_t)ul * a.H + oa]) : 0.f;
+              const float wb = ob < a.H ? __bfloat162float(woh_s[(size_t)ul * a.H + ob]) : 0.f;
+              const float4 h0 = *reinterpret_cast<const float4*>(s_hc + ul * ncp + c0);
+              const float4 h1 = *reinterpret_cast<const float4*>(s_hc + ul * ncp + c0 + 4);
+              const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+#pragma unroll
+              for (int x = 0; x < 8; ++x) {
+                acc[0][x] = fmaf(wa, hv[x], acc[0][x]);
+                acc[1][x] = fmaf(wb, hv[x], acc[1][x]);
+              }
+            }
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+              const int c = c0 + x;
+              if (c >= ncols) break;
+              float* dst = a.woh_part + ((size_t)mt * a.n_rows_pad + n0 + c_own + c) * a.H;
+              if (oa < a.H) __stcg(dst + oa, acc[0][x]);
+              if (ob < a.H) __stcg(dst + ob, acc[1][x]);
+            }
+          }
         }
       }
     } else {
@@ -310,17 +363,18 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   KT(7);
 }
 
-static size_t fused_smem_bytes(int n_group, int stages, int S, int NC) {
+static size_t fused_smem_bytes(int n_group, int stages, int S, int NC, int fold_H) {
   const size_t ring = (size_t)stages * (kTileM * 128 + 2 * (size_t)n_group * 128);
   const size_t recv = (size_t)(S + 1) * kTileM * NC * 4;
-  return 1024 + (ring > recv ? ring : recv) + 32 * 16 + (size_t)NC * 32 * 4 + (stages + 2) * 8 + 16;
+  const size_t fold = fold_H ? 128 + (size_t)32 * fold_H * 2 + (size_t)32 * ((NC + 7) & ~7) * 4 : 0;
+  return 1024 + (ring > recv ? ring : recv) + 32 * 16 + (size_t)NC * 32 * 4 + (stages + 3) * 8 + 16 + fold;
 }
 
 // Split S: the largest S <= 16 such that every split has >= 1 K block, the split's whole
 // K-slice fits the shared-memory ring, and tiles * S <= #SMs (one co-resident wave: the
 // tile counter wait needs every split resident).  1 CTA per SM (smem > half an SM).
 static bool fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, int k_blocks, int M, int m_tiles,
-                        int num_sms) {
+                        int num_sms, int fold_H = 0) {
   a.n_rows_pad = n_rows_pad;
   a.n_group = n_group;
   a.n_valid = n_valid;
@@ -335,7 +389,7 @@ static bool fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, 
     if (tiles * S > num_sms) continue;
     int NC = (n_group + S - 1) / S;
     NC = (NC + 3) / 4 * 4;
-    const size_t sm = fused_smem_bytes(n_group, kbps, S, NC);
+    const size_t sm = fused_smem_bytes(n_group, kbps, S, NC, fold_H);
     if (sm > limit) continue;
     a.S = S;
     a.NC = NC;
@@ -355,7 +409,7 @@ static cudaError_t launch_fused(const CUtensorMap& tmW, const CUtensorMap& tmX, 
                                 cudaStream_t st) {
   // at least 116 KB of shared memory: never two CTAs of this kernel on one SM (the tile wait
   // relies on one CTA per SM with grid <= #SMs)
-  size_t smem = fused_smem_bytes(a.n_group, a.stages, a.S, a.NC);
+  size_t smem = fused_smem_bytes(a.n_group, a.stages, a.S, a.NC, a.woh ? a.H : 0);
   if (smem < 116 * 1024) smem = 116 * 1024;
   auto fn = tc_gemm_fused_kernel<EPI>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -376,11 +430,13 @@ int g_fused_dbg = 0;
 cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                          int n_valid, int k_blocks, const float* bias, const float* cg, float* c_out, float* h_out,
                          int H, CellDst dst, float* scratch, unsigned int* counters, int num_sms, StepCtl ctl,
-                         cudaStream_t st) {
+                         cudaStream_t st, const __nv_bfloat16* woh, float* woh_part) {
   FusedArgs a{};
   a.dbg = g_fused_dbg;
-  if (!fill_common(a, n_rows_pad, n_group, n_valid, k_blocks, 4 * H, m_pad / kTileM, num_sms))
+  if (!fill_common(a, n_rows_pad, n_group, n_valid, k_blocks, 4 * H, m_pad / kTileM, num_sms, woh ? H : 0))
     return cudaErrorInvalidConfiguration;
+  a.woh = woh;
+  a.woh_part = woh_part;
   a.scratch = scratch;
   a.counters = counters;
   a.bias = reinterpret_cast<const float4*>(bias);
@@ -406,6 +462,12 @@ cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_p
   a.xg = xg;
   a.ctl = ctl;
   return launch_fused<EPI_TANH>(tmW, tmX, a, m_pad / kTileM * (n_rows_pad / n_group), st);
+}
+
+// does the top-layer cell kernel with the folded W_out share fit (shared memory, co-residency)?
+bool tc_cell_fold_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms) {
+  FusedArgs a{};
+  return fill_common(a, n_rows_pad, n_group, n_group, k_blocks, 4 * H, m_pad / kTileM, num_sms, H);
 }
 
 // split the fused kernels use for a shape (tests / DESIGN numbers; 0 = unfused)

@@ -51,7 +51,8 @@ int simt_effective_splits(int k_pad, int splits);
 cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                          int n_valid, int k_blocks, const float* bias, const float* cg, float* c_out, float* h_out,
                          int H, CellDst dst, float* scratch, unsigned int* counters, int num_sms, StepCtl ctl,
-                         cudaStream_t st);
+                         cudaStream_t st, const __nv_bfloat16* woh = nullptr, float* woh_part = nullptr);
+bool tc_cell_fold_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms);
 cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                          int n_valid, int k_blocks, int H, float* htilde, XOut xg, float* scratch,
                          unsigned int* counters, int num_sms, StepCtl ctl, cudaStream_t st);
@@ -66,9 +67,9 @@ void launch_enc_cell(const float* Z, int z_ld, const float* P, int splits, int p
                      int mem_col, cudaStream_t st);
 void launch_dec_cell(const float* P, int splits, int p_rows_pad, int p_ld, const float* bias, const float* cg,
                      float* c_out, float* h_out, int H, int R, CellDst dst, StepCtl ctl, cudaStream_t st);
-cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, const float* mem, const int* lens,
-                             int B, int S_max, int H, int K, XOut xo, const int* done, int num_sms, StepCtl ctl,
-                             cudaStream_t st);
+cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, const float* mem, int val_ld,
+                             const int* lens, int B, int S_max, int H, int K, XOut xo, const int* done, int num_sms,
+                             StepCtl ctl, cudaStream_t st, AttFold fo);
 void launch_attn_out(const float* P, int splits, int p_rows_pad, int p_ld, float* htilde, int H, int R, XOut xg,
                      StepCtl ctl, cudaStream_t st);
 void launch_init_decode(const BeamState& bs, int B, int K, const float* enc_h, const float* enc_c, int L, int H,
@@ -79,7 +80,7 @@ void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_p
                        float* row_z, int* row_i, StepCtl ctl, cudaStream_t st);
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
                      float* tlogp, cudaStream_t st);
-void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int R, int K,
+void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int ps, int rs, int R, int K,
                        float* lse, float* oz, int* oi, cudaStream_t st);
 
 void launch_teacher_gather(const int* tgt, int T_max, int t, int B, const GatherArgs& g, cudaStream_t st);
@@ -290,6 +291,8 @@ struct onmt_model {
   bool fused = true;           // split-K GEMM with the reduction and the cell / tanh epilogue fused in
                                // (one launch per layer instead of GEMM + consumer kernel)
   bool gen_step = true;        // K-outer persistent generator (gen_step.cu)
+  bool fold_wout = true;       // W_out folded into the top cell layer + attention (no W_out launch)
+  bool fold_cur = false;       // ... for the call being enqueued (fold_on)
   bool dec_fused = false;      // decoder cells + attention + W_out as one persistent kernel (dec_step.cu;
                                // opt-in: measured slower than the per-layer kernels)
   bool use_graph = true;
@@ -305,12 +308,14 @@ struct onmt_model {
   std::vector<std::unique_ptr<DevBuf>> dec_bias;
   Mat attn_win, attn_win_t, attn_wout, gen_w;
   DevBuf gen_b;
+  Mat attn_woc;                              // W_out[:, :H] (value projection, folded W_out)
+  DevBuf woh_t;                              // W_out[:, H:2H]^T bf16 [top-layer tiles * 32][H]
 
   // encoder workspace
   DevBuf d_ids, d_lens;
   Act enc_in0, enc_mid[2], enc_rec[2];
-  DevBuf enc_z[2], enc_p, mem, enc_h, enc_c, keys;
-  Act mem_x;                                 // memory bank as a GEMM operand ('general' keys)
+  DevBuf enc_z[2], enc_p, mem, enc_h, enc_c, keys, vals;
+  Act mem_x;                                 // memory bank as a GEMM operand (keys / values GEMMs)
   // decoder workspace
   std::vector<std::unique_ptr<Act>> xdec;    // [L]
   Act xo, xg;
@@ -319,6 +324,7 @@ struct onmt_model {
   DevBuf g_bar;                              // grid barrier counter of the generator step kernel
   DevBuf g_thr;                              // generator: shared per-row top-K thresholds [2][rows_pad]
   DevBuf ds_part, ds_bar;                    // fused decoder step: attention chunk partials, grid barrier
+  DevBuf woh_part;                           // folded W_out: top-layer shares W_out[:, units] h [tiles][rows_pad][H]
   DevBuf g_ms, g_tz, g_ti;
   DevBuf row_lse, row_z, row_i;
   DevBuf b_cum, b_live, b_y, b_prow, b_done, b_ndone, b_bt, b_br, b_braw, b_bnorm;
@@ -590,12 +596,37 @@ static void load_model(onmt_model* m, const char* path) {
   }
   const auto& wo = get(t, "attn.w_out", {H, 2 * H}, seen);
   m->attn_wout.upload(plain_pad(wo), (int)H, 2 * (int)H, bf);
+  if (bf) {
+    // folded W_out: W_oc = W_out[:, :H] projects the memory bank once per
+    // batch (values); W_oh^T = W_out[:, H:2H]^T rows by unit, in the top layer's 32-unit tiles
+    HostTensor woc;
+    woc.dims = {H, H};
+    woc.v.resize(H * H);
+    for (uint64_t i = 0; i < H; ++i)
+      for (uint64_t j = 0; j < H; ++j) woc.v[i * H + j] = wo.v[i * 2 * H + j];
+    m->attn_woc.upload(plain_pad(woc), (int)H, (int)H, bf);
+    const size_t units = (size_t)m->dec_w[m->L - 1]->m_pad / 4;
+    std::vector<__nv_bfloat16> wt(units * H, __float2bfloat16_rn(0.f));
+    for (uint64_t j = 0; j < H; ++j)
+      for (uint64_t o = 0; o < H; ++o) wt[j * H + o] = __float2bfloat16_rn(wo.v[o * 2 * H + H + j]);
+    m->woh_t.ensure(wt.size() * 2);
+    ONMT_CUDA(cudaMemcpy(m->woh_t.p, wt.data(), wt.size() * 2, cudaMemcpyHostToDevice));
+  }
   const auto& gw = get(t, "gen.w", {Vt, H}, seen);
   m->gen_w.upload(plain_pad(gw), (int)Vt, (int)H, bf);
   const auto& gb = get(t, "gen.b", {Vt}, seen);
   upload_f32(m->gen_b, gb.v);
   if (seen.size() != t.size()) throw Error{ONMT_E_FORMAT, "unexpected extra tensors in file"};
   ONMT_CUDA(cudaDeviceSynchronize());
+}
+
+// W_out folded away: bf16 models on the fused cell-GEMM path whose top
+// layer kernel fits the extra W_out share
+static bool fold_on(onmt_model* m, int rows) {
+  if (!(m->use_tc && m->fused && !m->dec_fused && m->fold_wout && m->attn_woc.m > 0)) return false;
+  const Mat& W = *m->dec_w[m->L - 1];
+  const RowPlan rp = plan_rows(rows);
+  return tc_cell_fold_fits(W.m_pad, rp.rows_pad, rp.n_group, W.k_pad / kBK, m->H, m->num_sms);
 }
 
 // ------------------------------------------------------------------ encoder
@@ -609,7 +640,8 @@ static void prepare_encoder(onmt_model* m, int B, int S_max) {
   for (int d = 0; d < D; ++d) m->enc_z[d].ensure((size_t)zrows * zld * 4);
   m->enc_p.ensure((size_t)16 * m->enc_rec[0].rows_pad * m->enc_whh[0]->m_pad * 4);
   m->mem.ensure((size_t)rows * H * 4);
-  if (m->general) m->mem_x.ensure(rows, H, m->prec == ONMT_PREC_BF16);
+  if (m->general || m->fold_cur) m->mem_x.ensure(rows, H, m->prec == ONMT_PREC_BF16);
+  if (m->fold_cur) m->vals.ensure((size_t)m->mem_x.rows_pad * m->attn_woc.m_pad * 4);
   m->enc_h.ensure((size_t)m->L * B * H * 4);
   m->enc_c.ensure((size_t)m->L * B * H * 4);
   if (m->general) m->keys.ensure((size_t)m->mem_x.rows_pad * m->attn_win_t.m_pad * 4);
@@ -641,7 +673,7 @@ static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, 
         }
         XOut xn{};
         if (xnext) xn = xnext->xo(bf);
-        else if (m->general) xn = m->mem_x.xo(bf);          // top layer: memory as the keys-GEMM operand
+        else if (m->general || m->fold_cur) xn = m->mem_x.xo(bf);   // top layer: memory as a GEMM operand
         launch_enc_cell(m->enc_z[d].as<float>(), zld, P, splits, m->enc_rec[d].rows_pad, whh.m_pad,
                         m->enc_bias[l * D + d]->as<float>(), Hd, B, d_lens, S_max, t, d == 1,
                         m->enc_h.as<float>() + (size_t)l * B * H + d * Hd,
@@ -653,6 +685,8 @@ static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, 
   }
   if (m->general)    // keys k_s = W_in^T m_s for every source position (hoisted 'general' query GEMM)
     gemm(m, m->attn_win_t, m->mem_x, rows, 1, m->keys.as<float>(), none);
+  if (m->fold_cur)   // values W_out[:, :H] m_s (folded W_out: the step's context arrives projected)
+    gemm(m, m->attn_woc, m->mem_x, rows, 1, m->vals.as<float>(), none);
   prof_end(m, "encode", pe);
   ONMT_CUDA(cudaGetLastError());
 }
@@ -701,6 +735,7 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
   m->st_c.ensure((size_t)L * rp * H * 4);
   m->st_cg.ensure((size_t)L * rp * H * 4);
   m->htilde.ensure((size_t)rp * H * 4);
+  if (m->fold_cur) m->woh_part.ensure((size_t)(m->dec_w[L - 1]->m_pad / kTileM) * rp * H * 4);
   const int n_vt = gen_parts(m, m->xg);
   m->g_ms.ensure((size_t)n_vt * rp * 8);
   m->g_tz.ensure((size_t)n_vt * rp * K * 4);
@@ -838,10 +873,14 @@ static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_ma
       // gates GEMM + split-K cluster reduction + LSTM cell in one kernel
       EvPair pg = prof_begin(m, "gemm");
       const Act& X = *m->xdec[l];
+      const bool fold_l = m->fold_cur && l + 1 == L;        // top layer also leaves its W_out share
       cudaError_t e = tc_gemm_cell(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, R, W.k_pad / kBK,
                                    m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H, cc + (size_t)l * rp * H,
                                    hh + (size_t)l * rp * H, H, dst, m->f_scratch.as<float>(),
-                                   m->f_count.as<unsigned int>() + (size_t)l * 2048, m->num_sms, ctl, m->stream);
+                                   m->f_count.as<unsigned int>() + (size_t)l * 2048, m->num_sms, ctl, m->stream,
+                                   fold_l ? m->woh_t.as<__nv_bfloat16>() : nullptr,
+                                   fold_l ? m->woh_part.as<float>() : nullptr);
+      if (fold_l && e == cudaErrorInvalidConfiguration) throw Error{ONMT_E_CUDA, "internal: folded W_out does not fit"};
       prof_end(m, "gemm", pg);
       if (e != cudaErrorInvalidConfiguration) {   // (no cluster shape fits: unfused path below)
         ONMT_CUDA(e);
@@ -863,11 +902,21 @@ static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_ma
     EvPair pa = prof_begin(m, "attention");
     const float* keys = m->general ? m->keys.as<float>() : m->mem.as<float>();
     const int key_ld = m->general ? m->attn_win_t.m_pad : H;
-    ONMT_CUDA(launch_attention(htop, keys, key_ld, m->mem.as<float>(), d_lens, B, S_max, H, K, m->xo.xo(bf),
-                               done, m->num_sms, ctl, m->stream));
+    AttFold fo{};
+    if (m->fold_cur) {
+      fo.wpart = m->woh_part.as<float>();
+      fo.n_wt = m->dec_w[L - 1]->m_pad / kTileM;
+      fo.rows_pad = rp;
+      fo.htilde = m->htilde.as<float>();
+      fo.xg = xg_dst;
+    }
+    ONMT_CUDA(launch_attention(htop, keys, key_ld, m->fold_cur ? m->vals.as<float>() : m->mem.as<float>(),
+                               m->fold_cur ? m->attn_woc.m_pad : H, d_lens, B, S_max, H, K, m->xo.xo(bf), done,
+                               m->num_sms, ctl, m->stream, fo));
     count(m);
     prof_end(m, "attention", pa);
   }
+  if (m->fold_cur) return;                                   // h~ written by the attention combine
   cudaError_t fe = cudaErrorInvalidConfiguration;
   if (m->use_tc && m->fused) {
     EvPair pg = prof_begin(m, "gemm");
@@ -1062,6 +1111,7 @@ static void enqueue_score(onmt_model* m, const int* d_ids, const int* d_lens, in
 }
 
 static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int T_max) {
+  m->fold_cur = fold_on(m, B);
   prepare_encoder(m, B, S_max);
   prepare_decoder(m, B, S_max, 1, T_max, false);
   const bool bf = m->use_tc;
@@ -1077,7 +1127,8 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
     enqueue_score(m, d_ids, d_lens, B, S_max, T_max);
     return;
   }
-  std::vector<int64_t> key = {B, S_max, T_max, m->profile, m->use_tc, (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
+  std::vector<int64_t> key = {B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->dec_fused, m->fold_cur,
+                              (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
                               (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
   GraphCache& gc = m->score_graph;
   if (!gc.exec || gc.key != key) {
@@ -1119,6 +1170,7 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
 // graph, cached per shape / pointer set: one cudaGraphLaunch per call, no host round trip.
 static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int K, int max_len,
                           float alpha, bool trace, const DecodeOut& out) {
+  m->fold_cur = fold_on(m, B * K);
   prepare_encoder(m, B, S_max);
   prepare_decoder(m, B, S_max, K, max_len, trace);
   auto enqueue = [&]() {
@@ -1131,7 +1183,8 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     phase_trace_end(m->num_sms);
     return;
   }
-  std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc,
+  std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
+                              m->gen_step, m->dec_fused, m->fold_cur,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
                               (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp};
@@ -1226,6 +1279,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   if (const char* ev = std::getenv("ONMT_FUSED_GEMM")) m->fused = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_GEN_STEP")) m->gen_step = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_DEC_FUSED")) m->dec_fused = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_FOLD_WOUT")) m->fold_wout = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
@@ -1265,6 +1319,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->gen_step = v != 0;
   } else if (n == "dec_fused") {
     m->dec_fused = v != 0;
+  } else if (n == "fold_wout") {
+    m->fold_wout = v != 0;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
   } else {
@@ -1312,6 +1368,7 @@ onmt_status onmt_encode(onmt_model* m, const int32_t* ids, const int32_t* lens, 
   ONMT_API_BEGIN
   ONMT_CUDA(cudaSetDevice(m->device));
   upload_src(m, ids, lens, B, S_max);
+  m->fold_cur = false;
   prepare_encoder(m, B, S_max);
   enqueue_encoder(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max);
   if (out_memory)
@@ -1575,7 +1632,7 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
     if (m->g_thr.bytes < (size_t)2 * x.rows_pad * 4) m->g_thr.ensure((size_t)2 * x.rows_pad * 4);
     ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
     ONMT_CUDA(gen_step(m->gen_w.tmap, x.tmap, (m->Vt + kVTile - 1) / kVTile, x.rows_pad, x.n_group,
-                       m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 2, 0, 0, 1.0,
+                       m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 1, 0, 0, 1.0,
                        BeamState{}, GatherArgs{}, m->g_bar.as<unsigned int>(), m->g_thr.as<unsigned int>(),
                        StepCtl{nullptr, 0}, m->stream));
   } else {
@@ -1598,9 +1655,9 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
                    rel(h[128 + j]), rel(h[144 + j]), rel(h[160 + 2 * j]), rel(h[176 + 2 * j]), rel(h[161 + 2 * j]),
                    rel(h[177 + 2 * j]));
   }
-  if (!gs)
-    launch_row_reduce(g.ms, g.tz, g.ti, n_parts, x.rows_pad, R, k, dl.as<float>(), dz.as<float>(), di.as<int>(),
-                      m->stream);
+  // partials: [row][part] from the step generator, [part][row] from the others
+  launch_row_reduce(g.ms, g.tz, g.ti, n_parts, gs ? 1 : x.rows_pad, gs ? n_parts : 1, R, k, dl.as<float>(),
+                    dz.as<float>(), di.as<int>(), m->stream);
   ONMT_CUDA(cudaGetLastError());
   ONMT_CUDA(cudaMemcpyAsync(lse, dl.p, (size_t)R * 4, cudaMemcpyDeviceToHost, m->stream));
   ONMT_CUDA(cudaMemcpyAsync(top_z, dz.p, (size_t)R * k * 4, cudaMemcpyDeviceToHost, m->stream));

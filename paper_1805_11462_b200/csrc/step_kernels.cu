@@ -454,13 +454,13 @@ void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, 
 // Test helper (onmt_test_gen): per row, combine generator partials into the LSE and
 // the top-k (z, id), one thread per row, sequential over tiles.
 __global__ void row_reduce_kernel(const float2* __restrict__ ms, const float* __restrict__ tz,
-                                  const int* __restrict__ ti, int n_vt, int rows_pad, int R, int K, float* lse,
+                                  const int* __restrict__ ti, int n_vt, int ps, int rs, int R, int K, float* lse,
                                   float* oz, int* oi) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
   float m = -INFINITY, s = 0.f;
   for (int v = 0; v < n_vt; ++v) {
-    const float2 p = ms[(size_t)v * rows_pad + r];
+    const float2 p = ms[(size_t)v * ps + (size_t)r * rs];
     if (p.x > m) { s = s * expf(m - p.x) + p.y; m = p.x; }
     else s += p.y * expf(p.x - m);
   }
@@ -470,8 +470,8 @@ __global__ void row_reduce_kernel(const float2* __restrict__ ms, const float* __
   for (int i = 0; i < K; ++i) { bz[i] = -INFINITY; bi[i] = 0x7fffffff; }
   for (int v = 0; v < n_vt; ++v)
     for (int c = 0; c < K; ++c) {
-      float cz = tz[((size_t)v * rows_pad + r) * K + c];
-      int ci = ti[((size_t)v * rows_pad + r) * K + c];
+      float cz = tz[((size_t)v * ps + (size_t)r * rs) * K + c];
+      int ci = ti[((size_t)v * ps + (size_t)r * rs) * K + c];
       for (int i = 0; i < K; ++i)
         if (better(cz, ci, bz[i], bi[i])) {
           float t1 = bz[i]; int t2 = bi[i];
@@ -481,9 +481,9 @@ __global__ void row_reduce_kernel(const float2* __restrict__ ms, const float* __
   for (int i = 0; i < K; ++i) { oz[(size_t)r * K + i] = bz[i]; oi[(size_t)r * K + i] = bi[i]; }
 }
 
-void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int rows_pad, int R, int K,
+void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int ps, int rs, int R, int K,
                        float* lse, float* oz, int* oi, cudaStream_t st) {
-  row_reduce_kernel<<<(R + 127) / 128, 128, 0, st>>>(ms, tz, ti, n_vt, rows_pad, R, K, lse, oz, oi);
+  row_reduce_kernel<<<(R + 127) / 128, 128, 0, st>>>(ms, tz, ti, n_vt, ps, rs, R, K, lse, oz, oi);
 }
 
 }  // namespace onmt
