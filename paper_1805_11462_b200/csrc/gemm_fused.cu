@@ -64,6 +64,19 @@ __device__ __forceinline__ float tanhfast(float x) {
 
 
 
+// folded W_out slice: row stride (bf16 elements) of W_out[:, units]^T in shared memory -
+// 16-byte rows for ldmatrix, +8 so the 8 rows of an 8x8 matrix hit distinct banks
+__host__ __device__ __forceinline__ int fold_ld(int H) { return (H + 15) / 16 * 16 + 8; }
+
+// D += A B, m16n8k16, bf16 inputs, fp32 accumulate (A: 4 regs, B: 2 regs, row.col)
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
 template <int EPI>
 __global__ void __launch_bounds__(256, 1)
 tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -85,11 +98,11 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   uint64_t* rbar = done + 1;
   uint64_t* wbar = rbar + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
-  const int ncp = (a.NC + 7) & ~7;                                 // s_hc row stride
+  const int ncp = (a.NC + 23) / 24 * 24;                           // s_hc row stride
   // (offsets from smem keep the shared address space visible to the compiler: LDS, not LD.E)
   const size_t woh_off = ((size_t)(reinterpret_cast<uint8_t*>(tslot) - smem) + 16 + 127) & ~(size_t)127;
   __nv_bfloat16* woh_s = reinterpret_cast<__nv_bfloat16*>(smem + woh_off);                          // [32][H]
-  float* s_hc = reinterpret_cast<float*>(woh_s + (size_t)32 * a.H);                                 // [32][ncp]
+  float* s_hc = reinterpret_cast<float*>(woh_s + (size_t)32 * fold_ld(a.H));                       // [32][ncp]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x / a.S;
@@ -119,9 +132,9 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
       tma_load_2d(smem + i * stage_bytes, &tmW, (kb0 + i) * kBK, m0, &full[i]);
     }
     if (EPI == EPI_CELL && a.woh) {                                // W_out[:, tile's units]^T (constant)
-      const uint32_t wb = (uint32_t)(32 * a.H * 2);
+      const uint32_t wb = (uint32_t)(32 * fold_ld(a.H) * 2);
       mbar_arrive_expect_tx(wbar, wb);
-      bulk_g2s(woh_s, a.woh + (size_t)mt * 32 * a.H, wb, wbar);
+      bulk_g2s(woh_s, a.woh + (size_t)mt * 32 * fold_ld(a.H), wb, wbar);
     }
   }
   if (warp == 0) tmem_alloc_dyn(tslot, a.tmem_cols);
@@ -310,38 +323,57 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
           for (int d = 0; d < a.dst.n; ++d) store_x(a.dst.x[d], r, a.dst.col[d] + j, h);
         }
       }
-      if (a.woh) {
-        // W_out[:, units] h[units, my columns] -> woh_part[mt][row][o]; fp32 FFMA on the
-        // bf16 weights (exact products), fixed unit order (deterministic)
+      if (a.woh && a.dbg != 11) {
+        // W_out[:, units] h[units, my columns] -> woh_part[mt][row][o] on the tensor cores
+        // (mma.sync m16n8k16: A = the bf16 weight slice via ldmatrix.trans, B = h split into
+        // bf16 hi + lo like every activation operand, fp32 accumulate; fixed order).
+        // Warp w: output tiles of 16 units o = 16 mi (mi = w, w + 8, ...), 24 columns per pass.
         mbar_wait(wbar, 0);
         __syncthreads();
-        for (int c0 = 0; c0 < ncols; c0 += 8) {
-          for (int o0 = 0; o0 < a.H; o0 += 512) {
-            const int oa = o0 + threadIdx.x, ob = oa + 256;
-            float acc[2][8];
+        const int hs = fold_ld(a.H);
+        const int g = lane >> 2, tq = lane & 3;
+        for (int c0 = 0; c0 < ncols; c0 += 24) {
+          uint32_t bh[3][2][2], bl[3][2][2];                        // [n tile][k step][reg]
 #pragma unroll
-            for (int x = 0; x < 8; ++x) { acc[0][x] = 0.f; acc[1][x] = 0.f; }
-#pragma unroll 4
-            for (int ul = 0; ul < 32; ++ul) {
-              const float wa = oa < a.H ? __bfloat162float(woh_s[(size_t)ul * a.H + oa]) : 0.f;
-              const float wb = ob < a.H ? __bfloat162float(woh_s[(size_t)ul * a.H + ob]) : 0.f;
-              const float4 h0 = *reinterpret_cast<const float4*>(s_hc + ul * ncp + c0);
-              const float4 h1 = *reinterpret_cast<const float4*>(s_hc + ul * ncp + c0 + 4);
-              const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+          for (int ni = 0; ni < 3; ++ni)
 #pragma unroll
-              for (int x = 0; x < 8; ++x) {
-                acc[0][x] = fmaf(wa, hv[x], acc[0][x]);
-                acc[1][x] = fmaf(wb, hv[x], acc[1][x]);
+            for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+              for (int rr = 0; rr < 2; ++rr) {
+                const int k = ks * 16 + rr * 8 + tq * 2, c = c0 + ni * 8 + g;
+                const float x0 = s_hc[k * ncp + c], x1 = s_hc[(k + 1) * ncp + c];
+                const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
+                const __nv_bfloat16 l0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
+                const __nv_bfloat16 l1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
+                bh[ni][ks][rr] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+                bl[ni][ks][rr] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+              }
+          for (int mi = warp; mi * 16 < a.H; mi += 8) {
+            float acc[3][4];
+#pragma unroll
+            for (int ni = 0; ni < 3; ++ni) acc[ni][0] = acc[ni][1] = acc[ni][2] = acc[ni][3] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const int mat = lane >> 3, rw = lane & 7;
+              const __nv_bfloat16* ra = woh_s + (size_t)(ks * 16 + (mat >> 1) * 8 + rw) * hs + mi * 16 + (mat & 1) * 8;
+              uint32_t af[4];
+              asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
+                           : "r"(smem_u32(ra)));
+#pragma unroll
+              for (int ni = 0; ni < 3; ++ni) {
+                mma_bf16_16816(acc[ni], af, bh[ni][ks]);
+                mma_bf16_16816(acc[ni], af, bl[ni][ks]);
               }
             }
 #pragma unroll
-            for (int x = 0; x < 8; ++x) {
-              const int c = c0 + x;
-              if (c >= ncols) break;
-              float* dst = a.woh_part + ((size_t)mt * a.n_rows_pad + n0 + c_own + c) * a.H;
-              if (oa < a.H) __stcg(dst + oa, acc[0][x]);
-              if (ob < a.H) __stcg(dst + ob, acc[1][x]);
-            }
+            for (int ni = 0; ni < 3; ++ni)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int o = mi * 16 + g + (e >> 1) * 8, c = c0 + ni * 8 + tq * 2 + (e & 1);
+                if (o < a.H && c < ncols)
+                  __stcg(a.woh_part + ((size_t)mt * a.n_rows_pad + n0 + c_own + c) * a.H + o, acc[ni][e]);
+              }
           }
         }
       }
@@ -366,7 +398,7 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
 static size_t fused_smem_bytes(int n_group, int stages, int S, int NC, int fold_H) {
   const size_t ring = (size_t)stages * (kTileM * 128 + 2 * (size_t)n_group * 128);
   const size_t recv = (size_t)(S + 1) * kTileM * NC * 4;
-  const size_t fold = fold_H ? 128 + (size_t)32 * fold_H * 2 + (size_t)32 * ((NC + 7) & ~7) * 4 : 0;
+  const size_t fold = fold_H ? 128 + (size_t)32 * fold_ld(fold_H) * 2 + (size_t)32 * ((NC + 23) / 24 * 24) * 4 : 0;
   return 1024 + (ring > recv ? ring : recv) + 32 * 16 + (size_t)NC * 32 * 4 + (stages + 3) * 8 + 16 + fold;
 }
 
@@ -437,6 +469,7 @@ cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_p
     return cudaErrorInvalidConfiguration;
   a.woh = woh;
   a.woh_part = woh_part;
+  if (const char* e = std::getenv("ONMT_FUSED_DBG")) a.dbg = std::atoi(e);   // (ablations; wrong results)
   a.scratch = scratch;
   a.counters = counters;
   a.bias = reinterpret_cast<const float4*>(bias);

@@ -309,7 +309,7 @@ struct onmt_model {
   Mat attn_win, attn_win_t, attn_wout, gen_w;
   DevBuf gen_b;
   Mat attn_woc;                              // W_out[:, :H] (value projection, folded W_out)
-  DevBuf woh_t;                              // W_out[:, H:2H]^T bf16 [top-layer tiles * 32][H]
+  DevBuf woh_t;                              // W_out[:, H:2H]^T bf16 [top-layer tiles * 32][fold_ld(H)]
 
   // encoder workspace
   DevBuf d_ids, d_lens;
@@ -606,9 +606,10 @@ static void load_model(onmt_model* m, const char* path) {
       for (uint64_t j = 0; j < H; ++j) woc.v[i * H + j] = wo.v[i * 2 * H + j];
     m->attn_woc.upload(plain_pad(woc), (int)H, (int)H, bf);
     const size_t units = (size_t)m->dec_w[m->L - 1]->m_pad / 4;
-    std::vector<__nv_bfloat16> wt(units * H, __float2bfloat16_rn(0.f));
+    const size_t hs = (H + 15) / 16 * 16 + 8;                      // (gemm_fused.cu fold_ld)
+    std::vector<__nv_bfloat16> wt(units * hs, __float2bfloat16_rn(0.f));
     for (uint64_t j = 0; j < H; ++j)
-      for (uint64_t o = 0; o < H; ++o) wt[j * H + o] = __float2bfloat16_rn(wo.v[o * 2 * H + H + j]);
+      for (uint64_t o = 0; o < H; ++o) wt[j * hs + o] = __float2bfloat16_rn(wo.v[o * 2 * H + H + j]);
     m->woh_t.ensure(wt.size() * 2);
     ONMT_CUDA(cudaMemcpy(m->woh_t.p, wt.data(), wt.size() * 2, cudaMemcpyHostToDevice));
   }
