@@ -53,6 +53,30 @@ cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_p
                          int H, CellDst dst, float* scratch, unsigned int* counters, int num_sms, StepCtl ctl,
                          cudaStream_t st, const __nv_bfloat16* woh = nullptr, float* woh_part = nullptr);
 bool tc_cell_fold_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms);
+struct EncRecDir {
+  const float* Z;
+  int z_ld;
+  const float4* bias;
+  XOut xrec[2];
+  float* h_st;
+  float* c_st;
+  int st_ld;
+  XOut xnext;
+  int next_col;
+  float* mem;
+  int mem_ld, mem_col;
+  int backward;
+};
+struct EncRecArgs {
+  EncRecDir dir[2];
+  int T, Hd, B, N, S_max, kb;
+  const int* lens;
+  unsigned int* bar;
+  unsigned long long* trace;
+};
+bool enc_rec_fits(int kb, int N, int D, int T, int num_sms);
+cudaError_t launch_enc_rec(const CUtensorMap* tmW, const CUtensorMap* tmX0, const CUtensorMap* tmX1,
+                           const EncRecArgs& a, int D, cudaStream_t st);
 cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                          int n_valid, int k_blocks, int H, float* htilde, XOut xg, float* scratch,
                          unsigned int* counters, int num_sms, StepCtl ctl, cudaStream_t st);
@@ -292,6 +316,7 @@ struct onmt_model {
                                // (one launch per layer instead of GEMM + consumer kernel)
   bool gen_step = true;        // K-outer persistent generator (gen_step.cu)
   bool fold_wout = true;       // W_out folded into the top cell layer + attention (no W_out launch)
+  bool enc_persistent = true;  // encoder recurrence of a layer as one persistent kernel (enc_rec.cu)
   bool fold_cur = false;       // ... for the call being enqueued (fold_on)
   bool dec_fused = false;      // decoder cells + attention + W_out as one persistent kernel (dec_step.cu;
                                // opt-in: measured slower than the per-layer kernels)
@@ -313,7 +338,8 @@ struct onmt_model {
 
   // encoder workspace
   DevBuf d_ids, d_lens;
-  Act enc_in0, enc_mid[2], enc_rec[2];
+  Act enc_in0, enc_mid[2], enc_rec[2], enc_rec2[2];   // enc_rec2: 2nd parity (persistent recurrence)
+  DevBuf er_bar;                             // step barriers of the persistent encoder recurrence
   DevBuf enc_z[2], enc_p, mem, enc_h, enc_c, keys, vals;
   Act mem_x;                                 // memory bank as a GEMM operand (keys / values GEMMs)
   // decoder workspace
@@ -636,6 +662,13 @@ static void prepare_encoder(onmt_model* m, int B, int S_max) {
   m->enc_in0.ensure(rows, m->E, m->prec == ONMT_PREC_BF16);
   if (m->L > 1) { m->enc_mid[0].ensure(rows, H, m->prec == ONMT_PREC_BF16); m->enc_mid[1].ensure(rows, H, m->prec == ONMT_PREC_BF16); }
   for (int d = 0; d < D; ++d) m->enc_rec[d].ensure(B, Hd, m->prec == ONMT_PREC_BF16);
+  if (m->use_tc && m->enc_persistent) {
+    for (int d = 0; d < D; ++d) m->enc_rec2[d].ensure(B, Hd, true);
+    if (!m->er_bar.p) {
+      m->er_bar.ensure(64 * 4);
+      ONMT_CUDA(cudaMemset(m->er_bar.p, 0, 64 * 4));
+    }
+  }
   const int zrows = std::max(m->enc_in0.rows_pad, m->L > 1 ? m->enc_mid[0].rows_pad : 0);
   const int zld = m->enc_wih[0]->m_pad;
   for (int d = 0; d < D; ++d) m->enc_z[d].ensure((size_t)zrows * zld * 4);
@@ -663,6 +696,59 @@ static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, 
     const Act* xnext = l + 1 < m->L ? &m->enc_mid[l % 2] : nullptr;
     for (int d = 0; d < D; ++d)
       gemm(m, *m->enc_wih[l * D + d], *xin, rows, 1, m->enc_z[d].as<float>(), none);
+    {
+      const Mat& w0 = *m->enc_whh[l * D];
+      const Act& r0 = m->enc_rec[0];
+      const int T = w0.m_pad / kTileM, kb = w0.k_pad / kBK;
+      if (m->use_tc && m->enc_persistent && r0.n_group == r0.rows_pad && enc_rec_fits(kb, r0.rows_pad, D, T, m->num_sms)) {
+        // the whole recurrence of this layer (both directions) in one launch (enc_rec.cu)
+        EncRecArgs ea{};
+        CUtensorMap tw[2], tx0[2], tx1[2];
+        for (int d = 0; d < D; ++d) {
+          EncRecDir& dr = ea.dir[d];
+          dr.Z = m->enc_z[d].as<float>();
+          dr.z_ld = zld;
+          dr.bias = m->enc_bias[l * D + d]->as<float4>();
+          dr.xrec[0] = m->enc_rec[d].xo(bf);
+          dr.xrec[1] = m->enc_rec2[d].xo(bf);
+          dr.h_st = m->enc_h.as<float>() + (size_t)l * B * H + d * Hd;
+          dr.c_st = m->enc_c.as<float>() + (size_t)l * B * H + d * Hd;
+          dr.st_ld = H;
+          if (xnext) dr.xnext = xnext->xo(bf);
+          else if (m->general || m->fold_cur) dr.xnext = m->mem_x.xo(bf);
+          dr.next_col = d * Hd;
+          dr.mem = l + 1 == m->L ? m->mem.as<float>() : nullptr;
+          dr.mem_ld = H;
+          dr.mem_col = d * Hd;
+          dr.backward = d == 1;
+          tw[d] = m->enc_whh[l * D + d]->tmap;
+          tx0[d] = m->enc_rec[d].tmap;
+          tx1[d] = m->enc_rec2[d].tmap;
+        }
+        ea.T = T; ea.Hd = Hd; ea.B = B; ea.N = r0.rows_pad; ea.S_max = S_max; ea.kb = kb;
+        ea.lens = d_lens;
+        ea.bar = m->er_bar.as<unsigned int>();
+        static unsigned long long* er_trace = nullptr;            // (debug: ONMT_ENC_TRACE, no graph)
+        const bool trc = std::getenv("ONMT_ENC_TRACE") && !m->capturing;
+        if (trc && !er_trace) cudaMalloc(&er_trace, 64 * 8 * 8);
+        ea.trace = trc ? er_trace : nullptr;
+        ONMT_CUDA(launch_enc_rec(tw, tx0, tx1, ea, D, m->stream));
+        count(m);
+        if (trc) {
+          std::vector<unsigned long long> h(64 * 8);
+          ONMT_CUDA(cudaStreamSynchronize(m->stream));
+          ONMT_CUDA(cudaMemcpy(h.data(), er_trace, h.size() * 8, cudaMemcpyDeviceToHost));
+          for (int t = 8; t < 12; ++t)
+            std::fprintf(stderr, "enc_rec l%d t%d: bar %lld  mma_done %lld  transp %lld  zwait %lld  loop0 %lld  sync %lld  next %lld ns\n", l, t,
+                         (long long)(h[t * 8 + 1] - h[t * 8 + 0]), (long long)(h[t * 8 + 3] - h[t * 8 + 1]),
+                         (long long)(h[t * 8 + 6] - h[t * 8 + 3]), (long long)(h[t * 8 + 4] - h[t * 8 + 6]),
+                         (long long)(h[t * 8 + 7] - h[t * 8 + 4]), (long long)(h[t * 8 + 5] - h[t * 8 + 7]),
+                         (long long)(h[(t + 1) * 8 + 0] - h[t * 8 + 5]));
+        }
+        xin = xnext;
+        continue;
+      }
+    }
     for (int t = 0; t < S_max; ++t)
       for (int d = 0; d < D; ++d) {
         const Mat& whh = *m->enc_whh[l * D + d];
@@ -1129,6 +1215,7 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
     return;
   }
   std::vector<int64_t> key = {B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->dec_fused, m->fold_cur,
+                              m->enc_persistent,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
                               (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
   GraphCache& gc = m->score_graph;
@@ -1185,7 +1272,7 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     return;
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
-                              m->gen_step, m->dec_fused, m->fold_cur,
+                              m->gen_step, m->dec_fused, m->fold_cur, m->enc_persistent,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
                               (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp};
@@ -1281,6 +1368,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   if (const char* ev = std::getenv("ONMT_GEN_STEP")) m->gen_step = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_DEC_FUSED")) m->dec_fused = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_FOLD_WOUT")) m->fold_wout = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_ENC_PERSISTENT")) m->enc_persistent = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
@@ -1322,6 +1410,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->dec_fused = v != 0;
   } else if (n == "fold_wout") {
     m->fold_wout = v != 0;
+  } else if (n == "enc_persistent") {
+    m->enc_persistent = v != 0;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
   } else {
