@@ -14,8 +14,10 @@ What it computes, each function citing PAPER.md
                (P115-118, P133-136), Luong general/dot global attention
                (P119-122, P299-301), tanh(W_c[c;h]) (P69), generator log-softmax
                (P118-119)
-  * `beam`   - beam search (P136-139), length normalisation (P315-316),
-               greedy, brute-force enumeration, teacher-forced scoring, traces.
+  * `beam`   - beam search (P136-139), length and coverage normalisation
+               (P315-316, S436-439), n-best lists (S422), attention-based unknown
+               replacement (S445-448), greedy, brute-force enumeration,
+               teacher-forced scoring, traces.
 
 Parity pins: see tests/test_oracle_*.py and DESIGN.md §4.  Every function here
 is pinned by at least one check that does not re-derive it from itself (a
@@ -26,4 +28,4 @@ unpinned beyond the compositional pins").
 from .mnmt import read_mnmt, bf16_round, load_model_tensors  # noqa: F401
 from .model import OracleModel  # noqa: F401
 from .beam import (beam_search, greedy, brute_force, score_sequence,  # noqa: F401
-                   translate_batch, length_penalty)
+                   translate_batch, length_penalty, coverage_penalty, final_score, replace_unknowns)

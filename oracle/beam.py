@@ -13,7 +13,7 @@ from typing import Dict, List, Optional
 
 import numpy as np
 
-from .model import BOS, EOS, OracleModel
+from .model import BOS, EOS, UNK, OracleModel
 
 TRACE_MARGIN = 16
 
@@ -21,6 +21,28 @@ TRACE_MARGIN = 16
 def length_penalty(n: int, alpha: float) -> float:
     """GNMT lp(n) = ((5 + n) / 6)^alpha (S439; P315-316; AMB-17: n counts EOS)."""
     return ((5.0 + n) / 6.0) ** alpha
+
+
+def coverage_penalty(cum_attn: np.ndarray, beta: float) -> float:
+    """GNMT cp = beta * sum_s log(min(sum_t a_{t,s}, 1.0)) over the real source
+    positions (S439 final_score; P315-316 "attention coverage normalization", formula of
+    the cited GNMT reference, SPEC S489).  cum_attn = sum over the hypothesis's steps
+    (every emitted token, EOS included) of its attention weights.  beta = 0 -> 0."""
+    if beta == 0.0:
+        return 0.0
+    return float(beta * np.sum(np.log(np.minimum(cum_attn, 1.0))))
+
+
+def final_score(raw: float, n: int, cum_attn: np.ndarray, alpha: float, beta: float) -> float:
+    """S436-439 final_score(hyp, alpha, beta) = raw / lp(|Y|) + cp."""
+    return raw / length_penalty(n, alpha) + coverage_penalty(cum_attn, beta)
+
+
+def replace_unknowns(tokens: List[int], attn_argmax: List[int]) -> List[int]:
+    """S445-448 in id space: for every <unk> (id 1) emitted at step t, the source
+    POSITION argmax_s a_{t,s} (ties -> smallest s) whose word replaces it; -1 for every
+    other token (no phrase table: the caller copies the source word at that position)."""
+    return [int(j) if w == UNK else -1 for w, j in zip(tokens, attn_argmax)]
 
 
 def _select(cum: np.ndarray, live: np.ndarray, logp: np.ndarray, K: int, M: int):
@@ -44,8 +66,14 @@ def _select(cum: np.ndarray, live: np.ndarray, logp: np.ndarray, K: int, M: int)
 
 
 def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha: float = 0.0,
-                stop: str = "rank0", trace: bool = False) -> Dict:
+                stop: str = "rank0", trace: bool = False, beta: float = 0.0, n_best: int = 1) -> Dict:
     """O7-O11 for one sentence.
+
+    beta > 0: banked entries are scored by final_score (raw / lp + cp, S436-439); the
+    ranking inside a step stays by raw score (AMB-13).  n_best: the returned "nbest"
+    list holds the n best bank entries (S422-423, 1 <= n_best <= K) in final order.
+    Every hypothesis carries its cumulative attention and the per-token attention
+    argmax (for coverage and unknown-word replacement, S445-448).
 
     stop = "rank0": stop after step t if the rank-0 selection is EOS, or no slot
              is live, or t == max_len (O10, AMB-15) - the product rule.
@@ -56,6 +84,8 @@ def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha:
     """
     if K < 1 or max_len < 1:
         raise ValueError("beam and max_len must be >= 1")
+    if not 1 <= n_best <= K:
+        raise ValueError("1 <= n_best <= beam (S423)")
     memory, finals = model.encode(src)
     y0, ht0, st0 = model.init_decoder(finals, 1)
     H = model.H
@@ -70,11 +100,14 @@ def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha:
         states[l][1][0] = st0[l][1][0]
     hyps: List[List[int]] = [[] for _ in range(K)]
     lps: List[List[float]] = [[] for _ in range(K)]
-    bank = []      # (norm, t, r, raw, hyp, lps)
+    S = len(src)
+    catt = np.zeros((K, S))                                    # cumulative attention per slot
+    amax: List[List[int]] = [[] for _ in range(K)]             # per-token attention argmax
+    bank = []      # (norm, t, r, raw, hyp, lps, amax, cp)
     steps = []
     for t in range(1, max_len + 1):
         ks = np.nonzero(live)[0]
-        logp_l, _, ht_l, st_l = model.decode_step(
+        logp_l, att_l, ht_l, st_l = model.decode_step(
             y[ks], htilde[ks], [(h[ks], c[ks]) for (h, c) in states], memory)
         logp = np.full((K, model.V), -np.inf)
         logp[ks] = logp_l
@@ -89,14 +122,20 @@ def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha:
         n_states = [(np.zeros((K, H)), np.zeros((K, H))) for _ in range(model.L)]
         n_hyps: List[List[int]] = [[] for _ in range(K)]
         n_lps: List[List[float]] = [[] for _ in range(K)]
+        n_catt = np.zeros((K, S))
+        n_amax: List[List[int]] = [[] for _ in range(K)]
         pos = {int(k): i for i, k in enumerate(ks)}
         for r, (s, k, w) in enumerate(sel):
             i = pos[k]
             n_hyps[r] = hyps[k] + [w]
             n_lps[r] = lps[k] + [float(logp[k, w])]
+            n_catt[r] = catt[k] + att_l[i]                     # a_t of the parent's step-t state
+            n_amax[r] = amax[k] + [int(np.argmax(att_l[i]))]   # first maximum: ties -> smallest s
             if w == EOS or t == max_len:                       # O9 banking
                 n = t
-                bank.append((s / length_penalty(n, alpha), t, r, s, n_hyps[r], n_lps[r]))
+                cp = coverage_penalty(n_catt[r], beta)
+                bank.append((final_score(s, n, n_catt[r], alpha, beta), t, r, s, n_hyps[r], n_lps[r],
+                             n_amax[r], cp))
             else:
                 n_live[r] = True
                 n_cum[r] = s
@@ -109,6 +148,7 @@ def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha:
             steps.append({"t": t, "cand": cand, "sel": [(k, w, s) for (s, k, w) in sel],
                           "cum": cum.copy(), "live": live.copy()})
         live, cum, y, htilde, states, hyps, lps = n_live, n_cum, n_y, n_ht, n_states, n_hyps, n_lps
+        catt, amax = n_catt, n_amax
         # O10 stop
         if not live.any() or t == max_len:
             break
@@ -122,9 +162,13 @@ def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha:
     if not bank:
         raise RuntimeError("beam exhausted with empty bank (S431)")
     # O11: largest norm; ties -> smaller t, then smaller r (AMB-19)
-    best = sorted(bank, key=lambda b: (-b[0], b[1], b[2]))[0]
+    ranked = sorted(bank, key=lambda b: (-b[0], b[1], b[2]))
+    best = ranked[0]
     out = {"tokens": list(best[4]), "norm": best[0], "raw": best[3], "t": best[1], "r": best[2],
-           "token_logp": list(best[5]), "bank": bank}
+           "token_logp": list(best[5]), "attn_argmax": list(best[6]), "cp": best[7], "bank": bank,
+           "nbest": [{"tokens": list(e[4]), "norm": e[0], "raw": e[3], "t": e[1], "r": e[2],
+                      "token_logp": list(e[5]), "attn_argmax": list(e[6]), "cp": e[7]}
+                     for e in ranked[:n_best]]}
     if trace:
         out["steps"] = steps
     return out
@@ -145,22 +189,26 @@ def greedy(model: OracleModel, src: List[int], max_len: int) -> Dict:
     return {"tokens": toks, "raw": float(np.sum(lps)), "token_logp": lps}
 
 
-def score_sequence(model: OracleModel, src: List[int], Y: List[int]) -> List[float]:
-    """Teacher-forced log p(y_t | y_<t, x) of every token of Y (P105-108)."""
+def score_sequence(model: OracleModel, src: List[int], Y: List[int], with_attn: bool = False):
+    """Teacher-forced log p(y_t | y_<t, x) of every token of Y (P105-108); with_attn:
+    also the attention rows a_t [|Y| x S] of those steps."""
     memory, finals = model.encode(src)
     y, ht, st = model.init_decoder(finals, 1)
-    out = []
+    out, att = [], []
     for w in Y:
-        logp, _, ht, st = model.decode_step(y, ht, st, memory)
+        logp, a, ht, st = model.decode_step(y, ht, st, memory)
         out.append(float(logp[0, w]))
+        att.append(a[0])
         y = np.array([w])
-    return out
+    return (out, np.array(att)) if with_attn else out
 
 
-def brute_force(model: OracleModel, src: List[int], max_len: int, alpha: float = 0.0) -> List[Dict]:
+def brute_force(model: OracleModel, src: List[int], max_len: int, alpha: float = 0.0,
+                beta: float = 0.0) -> List[Dict]:
     """O12: enumerate Y = {sequences ending at their first EOS, length <= max_len}
     U {EOS-free sequences of length exactly max_len}; score each by teacher
-    forcing.  Returns all of them sorted by (norm desc, then token tuple)."""
+    forcing (final_score: raw / lp + cp).  Returns all of them sorted by (norm desc,
+    then token tuple)."""
     V = model.V
     out = []
     for n in range(1, max_len + 1):
@@ -168,9 +216,9 @@ def brute_force(model: OracleModel, src: List[int], max_len: int, alpha: float =
             tails = [EOS] if n < max_len else list(range(V))
             for last in tails:
                 Y = list(prefix) + [last]
-                lp = score_sequence(model, src, Y)
+                lp, att = score_sequence(model, src, Y, with_attn=True)
                 raw = float(np.sum(lp))
-                out.append({"tokens": Y, "raw": raw, "norm": raw / length_penalty(n, alpha),
+                out.append({"tokens": Y, "raw": raw, "norm": final_score(raw, n, att.sum(0), alpha, beta),
                             "token_logp": lp})
     out.sort(key=lambda d: (-d["norm"], d["tokens"]))
     return out
@@ -193,4 +241,5 @@ def model_from_file(path: str, precision: str) -> OracleModel:
 
 
 __all__ = ["beam_search", "greedy", "score_sequence", "brute_force", "translate_batch",
-           "length_penalty", "unpad", "model_from_file", "Optional"]
+           "length_penalty", "coverage_penalty", "final_score", "replace_unknowns", "unpad",
+           "model_from_file", "Optional"]
