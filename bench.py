@@ -386,6 +386,52 @@ def run_score(args):
     model.close()
 
 
+def run_translate_ex(args):
+    """Translation customisations on the workload's batch through
+    onmt_translate_ex (host buffers: H2D/D2H inside the timed region, so value == e2e):
+    GNMT coverage penalty beta = 0.2, 5-best lists, attention-based <unk> replacement.
+    The same call with the customisations off is timed beside it (their overhead)."""
+    import torch
+    import paper_1805_11462_b200 as ob
+    w = synth.WORKLOADS[args.workload]
+    K, ML, alpha = w.decode.beam, w.decode.max_len, w.decode.alpha
+    cache = os.environ.get("ONMT_WEIGHT_CACHE", os.path.join(tempfile.gettempdir(), "onmt_weights"))
+    path = synth.weights_file(args.workload, cache)
+    model = ob.Model(path, 0, w.decode.precision)
+    ids, lens = synth.make_corpus(args.workload)
+    S = int(lens.max())
+    ids = np.ascontiguousarray(ids[:, :S])
+
+    def timed(beta, nb, unk):
+        for _ in range(args.warmup):
+            model.translate_ex(ids, lens, K, ML, alpha, beta, nb, unk)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        toks = 0
+        for _ in range(args.steps):
+            r = model.translate_ex(ids, lens, K, ML, alpha, beta, nb, unk)
+            toks += int(r["lens"][:, 0].sum())
+        return toks / (time.perf_counter() - t0), r
+
+    v_ext, r = timed(0.2, K, True)
+    v_plain, _ = timed(0.0, 1, False)
+    B = len(lens)
+    line = {"metric": "target tokens/sec (1-best tokens), beam-5 translate with coverage penalty + n-best + "
+                      "unk replacement (SURVEY §8(f) rank 2)",
+            "value": round(v_ext, 1), "unit": "target tok/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (DESIGN.md §3)",
+            "config": {"workload": args.workload, "task": "translate_ex", "batch": B, "beam": K, "max_len": ML,
+                       "coverage_penalty": 0.2, "n_best": K, "replace_unk": True},
+            "e2e": {"value": round(v_ext, 1), "unit": "target tok/s", "h2d_bytes_per_step": int(ids.nbytes + lens.nbytes),
+                    "d2h_bytes_per_step": int(B * K * (ML * 4 * 3 + 4 * 3))},
+            "same_call_plain": {"value": round(v_plain, 1), "note": "onmt_translate_ex with beta = 0, n_best = 1, "
+                                                                   "no replacement (host API)"},
+            "unk_emitted": int((r["hyps"][:, 0] == 1).sum())}
+    print(json.dumps(line), flush=True)
+    model.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -395,7 +441,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-sentences", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--task", default="translate", choices=["translate", "score"])
+    ap.add_argument("--task", default="translate", choices=["translate", "score", "translate_ex"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -403,6 +449,8 @@ def main():
         run_reference(args)
     elif args.task == "score":
         run_score(args)
+    elif args.task == "translate_ex":
+        run_translate_ex(args)
     else:
         run_ours(args)
 

@@ -121,6 +121,37 @@ ONMT_API onmt_status onmt_translate(onmt_model* m, const int32_t* src_ids, const
                            float* out_scores, float* out_raw_scores, float* out_token_logp);
 
 /*
+ * onmt_translate_ex - onmt_translate with the paper's translation customisations
+ * (PAPER.md P313-316 "beam search with various normalizations including length and
+ * attention coverage normalization" and OOV handling; SPEC S421-448):
+ *   coverage_penalty = beta >= 0: banked hypotheses are ranked by the GNMT final score
+ *     raw / lp(n) + beta * sum_{s < len} log(min(sum_t a_{t,s}, 1)) over the hypothesis's
+ *     attention history (S439); the ranking inside a step stays by raw score.
+ *   n_best in [1, beam]: the n best bank entries per sentence, in final order
+ *     (score desc, then earlier step, then lower rank).  A sentence that banked fewer
+ *     entries reports len 0 and score -inf for the missing ranks.
+ *   replace_unk != 0: out_unk_pos [B*n_best*max_len] receives, for every emitted <unk>
+ *     (id 1), the source position argmax_s a_{t,s} (ties -> smallest s) whose word replaces
+ *     it (S448; no phrase table), and -1 for every other position.
+ *   Host outputs are [B][n_best][...]: out_hyps [B*n_best*max_len], out_lens,
+ *   out_scores (final score), out_raw_scores (or NULL), out_token_logp (or NULL).
+ *   With beta = 0, n_best = 1, replace_unk = 0 it equals onmt_translate.
+ * Errors: as onmt_translate, plus INVALID_ARG for n_best outside [1, beam], beta < 0 or
+ * NaN, out_unk_pos without replace_unk; UNSUPPORTED when coverage / unk replacement is
+ * requested for a model whose generator partials exceed the one-CTA-per-sentence beam
+ * step (fp32 models with V_tgt > 32768).
+ */
+typedef struct {
+  int32_t beam, max_len;
+  float length_penalty, coverage_penalty;
+  int32_t n_best, replace_unk;
+} onmt_decode_opts;
+ONMT_API onmt_status onmt_translate_ex(onmt_model* m, const int32_t* src_ids, const int32_t* src_lens,
+                              int32_t B, int32_t S_max, const onmt_decode_opts* opts, int32_t* out_hyps,
+                              int32_t* out_lens, float* out_scores, float* out_raw_scores,
+                              float* out_token_logp, int32_t* out_unk_pos);
+
+/*
  * onmt_translate_trace - onmt_translate plus the per-step beam selections, for the
  * parity protocol: for step t (0-based), sentence b, rank r:
  *   sel_parent [max_len*B*beam]: parent slot k, or -1 if nothing was selected;

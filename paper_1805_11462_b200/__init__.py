@@ -24,7 +24,8 @@ K_MAX = 16
 
 EXPORTS = ["onmt_load_weights", "onmt_model_get_info", "onmt_set_stream", "onmt_encode", "onmt_translate",
            "onmt_translate_trace", "onmt_translate_dev", "onmt_set_option", "onmt_get_kernel_time",
-           "onmt_kernel_launches", "onmt_free", "onmt_last_error", "onmt_test_gemm", "onmt_test_gen", "onmt_score"]
+           "onmt_kernel_launches", "onmt_free", "onmt_last_error", "onmt_test_gemm", "onmt_test_gen", "onmt_score",
+           "onmt_translate_ex"]
 
 
 class OnmtError(RuntimeError):
@@ -32,6 +33,12 @@ class OnmtError(RuntimeError):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
         self.status = status
         self.name = STATUS.get(status, str(status))
+
+
+class _DecodeOpts(ctypes.Structure):
+    """onmt_decode_opts (include/onmt.h)."""
+    _fields_ = [("beam", ctypes.c_int32), ("max_len", ctypes.c_int32), ("length_penalty", ctypes.c_float),
+                ("coverage_penalty", ctypes.c_float), ("n_best", ctypes.c_int32), ("replace_unk", ctypes.c_int32)]
 
 
 class _Info(ctypes.Structure):
@@ -67,6 +74,7 @@ def lib():
     L.onmt_test_gemm.argtypes = [VP, VP, VP, I32, I32, I32, I32, VP]
     L.onmt_test_gen.argtypes = [VP, VP, I32, I32, VP, VP, VP]
     L.onmt_score.argtypes = [VP, VP, VP, I32, I32, VP, VP, I32, VP, VP]
+    L.onmt_translate_ex.argtypes = [VP, VP, VP, I32, I32, P(_DecodeOpts), VP, VP, VP, VP, VP, VP]
     for n in EXPORTS:
         if n not in ("onmt_free", "onmt_last_error"):
             getattr(L, n).restype = ctypes.c_int
@@ -144,6 +152,27 @@ class Model:
         c = np.zeros((L, B, H), np.float32)
         _check(lib().onmt_encode(self._h, _ptr(ids), _ptr(lens), B, S, _ptr(mem), _ptr(h), _ptr(c)))
         return mem, h, c
+
+    def translate_ex(self, ids, lens, beam: int, max_len: int, length_penalty: float = 0.0,
+                     coverage_penalty: float = 0.0, n_best: int = 1, replace_unk: bool = False) -> Dict[str, np.ndarray]:
+        """onmt_translate_ex: outputs shaped [B, n_best, ...] (final order)."""
+        ids, lens = _i32(ids), _i32(lens)
+        B = len(lens)
+        S = ids.shape[1] if ids.ndim == 2 and B > 0 else 1
+        n = max(n_best, 1)
+        hyps = np.zeros((B, n, max_len), np.int32)
+        olens = np.zeros((B, n), np.int32)
+        scores = np.zeros((B, n), np.float32)
+        raw = np.zeros((B, n), np.float32)
+        tlogp = np.zeros((B, n, max_len), np.float32)
+        unk = np.full((B, n, max_len), -1, np.int32) if replace_unk else None
+        o = _DecodeOpts(beam, max_len, float(length_penalty), float(coverage_penalty), n_best, int(bool(replace_unk)))
+        _check(lib().onmt_translate_ex(self._h, _ptr(ids), _ptr(lens), B, S, ctypes.byref(o), _ptr(hyps), _ptr(olens),
+                                       _ptr(scores), _ptr(raw), _ptr(tlogp), _ptr(unk) if unk is not None else None))
+        out = {"hyps": hyps, "lens": olens, "scores": scores, "raw": raw, "token_logp": tlogp}
+        if unk is not None:
+            out["unk_pos"] = unk
+        return out
 
     def translate(self, ids, lens, beam: int, max_len: int, length_penalty: float = 0.0,
                   trace: bool = False) -> Dict[str, np.ndarray]:

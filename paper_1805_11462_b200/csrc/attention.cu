@@ -85,6 +85,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   const size_t mb = r4((size_t)SC * vl), kb = same ? 0 : r4((size_t)SC * kl);
   auto mbuf = [&](int i) { return buf + (size_t)(i & 1) * (mb + kb); };
   float* s_hp = buf + 2 * (mb + kb);                // folded W_out: the combine slice's tile shares
+  float* s_esave = s_hp + fo.hp_floats;             // attention output: my chunk's raw scores [K][CH]
   auto kbuf = [&](int i) { return same ? mbuf(i) : mbuf(i) + mb; };
 
   // source rows [s_beg, s_lim) of this chunk, prefetched before griddepcontrol.wait without
@@ -198,6 +199,10 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
             if (k < K) {
               e[k * kSCMax + pa] = da[k];
               if (hb) e[k * kSCMax + pb] = db[k];
+              if (fo.att_out) {
+                s_esave[k * CH + (s0 - s_beg) + pa] = da[k];
+                if (hb) s_esave[k * CH + (s0 - s_beg) + pb] = db[k];
+              }
             }
         }
       }
@@ -283,6 +288,15 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
     for (int p = 0; p < 8; ++p) coef[p * KMAX + k] = mp[p] * inv;
   }
   __syncthreads();
+  if (fo.att_out) {
+    // normalised weights of my chunk (coverage / unknown replacement, S436-448):
+    // a_s = exp(e_s - m_r) * exp(m_r - M) / l  (zero at padded positions)
+    for (int i = threadIdx.x; i < K * (s_lim - s_beg); i += blockDim.x) {
+      const int k = i / (s_lim - s_beg), s = s_beg + i % (s_lim - s_beg);
+      const float a = s < L ? expf(s_esave[k * CH + (s - s_beg)] - s_m[k]) * coef[r * KMAX + k] : 0.f;
+      fo.att_out[((size_t)b * K + k) * S_max + s] = a;
+    }
+  }
   if (vec) {
     const int H4 = H >> 2;
     const int j0 = (int)((long long)H4 * r / nch), j1 = (int)((long long)H4 * (r + 1) / nch);
@@ -413,9 +427,11 @@ cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, c
   };
   size_t extra = 0;                                // folded W_out: prefetched tile shares
   if (fo.wpart) extra = (size_t)fo.n_wt * K * ((H / 4 + nch - 1) / nch) * 16;
+  const size_t esave = fo.att_out ? (size_t)K * CH * 4 : 0;   // attention output: raw scores
   const int SC = bytes(16) + extra <= 200 * 1024 ? 16 : 8;
-  fo.pref = bytes(SC) + extra <= 220 * 1024;
-  const size_t smem = bytes(SC) + (fo.pref ? extra : 0);
+  fo.pref = bytes(SC) + extra + esave <= 220 * 1024;
+  fo.hp_floats = fo.pref ? (int)(extra / 4) : 0;
+  const size_t smem = bytes(SC) + (fo.pref ? extra : 0) + esave;
   const dim3 grid(nch, B);
 #define ONMT_ATT(KM)                                                                                              \
   return H <= 2 * kAttThreads                                                                                     \

@@ -398,17 +398,72 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     bs.hist_logp[hb] = mine_sel ? s_sel_lp[kr] : 0.f;
     if (bs.sel_parent) { bs.sel_parent[hb] = mine_sel ? s_sel_k[kr] : -1; bs.sel_score[hb] = mine_sel ? s_sel_s[kr] : -CUDART_INF; }
   }
-  if (threadIdx.x == 0) {
-    s_cont = !stop;
-    int bt = bs.best_t[b], br = bs.best_r[b];                    // sentence-level banking and stop flag
-    double braw = bs.best_raw[b], bnorm = bs.best_norm[b];
-    for (int q = 0; q < n_sel; ++q) {
-      if (s_sel_w[q] == 3 || t == max_len) {
-        const double norm = s_sel_s[q] / lp;
-        if (bt == 0 || norm > bnorm) { bt = t; br = q; braw = s_sel_s[q]; bnorm = norm; }
+  // ---- coverage / unknown replacement (S436-448): the new slot q inherits its parent's
+  //      cumulative attention plus the parent's step-t attention row; its token's attention
+  //      argmax (first maximum: ties -> smallest s) goes to the history
+  __shared__ double s_cp[KMAX];
+  if (bs.catt || bs.hist_amax) {
+    __syncthreads();                                             // (selection results visible)
+    const int Lb = __ldg(&bs.lens[b]);
+    const size_t RS = (size_t)R * bs.S_max;
+    if (bs.catt) {
+      const float* cin = bs.catt + (size_t)(t & 1) * RS;
+      float* cout = bs.catt + (size_t)((t + 1) & 1) * RS;
+      for (int i = threadIdx.x; i < n_sel * Lb; i += blockDim.x) {
+        const int q = i / Lb, s = i % Lb;
+        const size_t pr = (size_t)(b * K + s_sel_k[q]) * bs.S_max + s;
+        cout[(size_t)(b * K + q) * bs.S_max + s] = __ldcg(&cin[pr]) + __ldcg(&bs.att[pr]);
       }
     }
-    bs.best_t[b] = bt; bs.best_r[b] = br; bs.best_raw[b] = braw; bs.best_norm[b] = bnorm;
+    __syncthreads();
+    for (int q = warp; q < n_sel; q += nw) {
+      const size_t pbase = (size_t)(b * K + s_sel_k[q]) * bs.S_max;
+      float bv = -INFINITY;
+      int bi = 0x7fffffff;
+      double cp = 0.0;
+      for (int s = lane; s < Lb; s += 32) {
+        const float a = __ldcg(&bs.att[pbase + s]);
+        if (a > bv) { bv = a; bi = s; }                          // (s increases along a lane)
+        if (bs.catt && bs.beta != 0.0)
+          cp += log(fmin((double)__ldcg(&bs.catt[(size_t)((t + 1) & 1) * RS + (size_t)(b * K + q) * bs.S_max + s]), 1.0));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; }
+        cp += __shfl_xor_sync(0xffffffffu, cp, o);
+      }
+      if (lane == 0) {
+        s_cp[q] = bs.beta * cp;
+        if (bs.hist_amax) bs.hist_amax[(size_t)(t - 1) * R + b * K + q] = bi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    s_cont = !stop;
+    // sentence-level banking (final_score = raw / lp + cp, S436-439) into the n-best list
+    // (norm desc; an equal norm never displaces an earlier step / lower rank, AMB-19)
+    const int nb = bs.nbest > 0 ? bs.nbest : 1;
+    const int base = b * nb;
+    for (int q = 0; q < n_sel; ++q) {
+      if (s_sel_w[q] == 3 || t == max_len) {
+        const double norm = s_sel_s[q] / lp + ((bs.catt && bs.beta != 0.0) ? s_cp[q] : 0.0);
+        int pos = nb;
+        for (int i = nb - 1; i >= 0; --i)
+          if (bs.best_t[base + i] == 0 || norm > bs.best_norm[base + i]) pos = i;
+          else break;
+        if (pos < nb) {
+          for (int i = nb - 1; i > pos; --i) {
+            bs.best_t[base + i] = bs.best_t[base + i - 1]; bs.best_r[base + i] = bs.best_r[base + i - 1];
+            bs.best_raw[base + i] = bs.best_raw[base + i - 1]; bs.best_norm[base + i] = bs.best_norm[base + i - 1];
+          }
+          bs.best_t[base + pos] = t; bs.best_r[base + pos] = q;
+          bs.best_raw[base + pos] = s_sel_s[q]; bs.best_norm[base + pos] = norm;
+        }
+      }
+    }
     if (stop) { bs.done[b] = t; atomicAdd(bs.n_done, 1); }
   }
   __syncthreads();

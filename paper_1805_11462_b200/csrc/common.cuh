@@ -65,6 +65,8 @@ struct AttFold {
   float* htilde;
   XOut xg;
   int pref;                     // (set by the launcher) shares prefetched into shared memory
+  int hp_floats;                // (set by the launcher) size of that prefetch region
+  float* att_out;               // [B*K][S_max] normalised attention weights (coverage / unk), or nullptr
 };
 
 __device__ __forceinline__ void store_x(const XOut& x, int r, int c, float v) {
@@ -200,6 +202,14 @@ struct BeamState {
   float* hist_logp;   // [max_len][B*K]
   double* sel_score;  // [max_len][B*K] (trace)
   int* sel_parent;    // [max_len][B*K] (trace; -1 = none)
+  // coverage penalty / n-best / unknown replacement (S422-448)
+  const float* att;   // [B*K][S_max] attention weights of the current step (nullptr: off)
+  float* catt;        // [2][B*K][S_max] cumulative attention (step t reads buffer t & 1), or nullptr
+  int* hist_amax;     // [max_len][B*K] attention argmax of each history entry, or nullptr
+  const int* lens;    // [B] source lengths
+  int S_max;
+  double beta;        // coverage penalty weight (0: off)
+  int nbest;          // bank entries kept per sentence: best_* are [B][nbest] (norm desc, t asc, r asc)
 };
 
 // Operands of the parent gather (A5).

@@ -103,7 +103,7 @@ void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_p
                        int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga, float* row_lse,
                        float* row_z, int* row_i, StepCtl ctl, cudaStream_t st);
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
-                     float* tlogp, cudaStream_t st);
+                     float* tlogp, int* unk_pos, cudaStream_t st);
 void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int ps, int rs, int R, int K,
                        float* lse, float* oz, int* oi, cudaStream_t st);
 
@@ -355,7 +355,8 @@ struct onmt_model {
   DevBuf row_lse, row_z, row_i;
   DevBuf b_cum, b_live, b_y, b_prow, b_done, b_ndone, b_bt, b_br, b_braw, b_bnorm;
   DevBuf h_par, h_tok, h_lp, s_score, s_par;
-  DevBuf o_hyps, o_lens, o_scores, o_raw, o_tlogp;
+  DevBuf b_att, b_catt, h_amax;              // coverage / unknown replacement state
+  DevBuf o_hyps, o_lens, o_scores, o_raw, o_tlogp, o_unk;
 
   std::map<std::string, EventPairs> evs;   // per kernel family ("gen", "step", "encode", ...)
   bool capturing = false;
@@ -780,15 +781,35 @@ static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, 
 
 // ------------------------------------------------------------------ decoder
 struct DecodeOut {
-  int* hyps;
-  int* lens;
+  int* hyps;            // [B][nbest][max_len]
+  int* lens;            // [B][nbest]
   float* scores;
   float* raw;
   float* tlogp;
+  int* unk_pos = nullptr;   // [B][nbest][max_len] source position replacing an <unk>, else -1
 };
 
-static BeamState beam_state(onmt_model* m, bool trace) {
-  BeamState bs;
+// Decoding customisations (SPEC S421-424): coverage penalty beta,
+// n-best list size, attention-based unknown replacement.  Defaults = the plain path.
+struct DecodeOpts {
+  double beta = 0.0;
+  int nbest = 1;
+  bool unk = false;
+  bool att() const { return beta != 0.0 || unk; }
+};
+
+static BeamState beam_state(onmt_model* m, bool trace, const DecodeOpts& op = DecodeOpts{}, const int* d_lens = nullptr,
+                            int S_max = 0) {
+  BeamState bs{};
+  bs.nbest = op.nbest;
+  bs.beta = op.beta;
+  if (op.att()) {
+    bs.att = m->b_att.as<float>();
+    bs.catt = op.beta != 0.0 ? m->b_catt.as<float>() : nullptr;
+    bs.hist_amax = op.unk ? m->h_amax.as<int>() : nullptr;
+    bs.lens = d_lens;
+    bs.S_max = S_max;
+  }
   bs.cum = m->b_cum.as<double>();
   bs.live = m->b_live.as<int>();
   bs.y = m->b_y.as<int>();
@@ -807,7 +828,8 @@ static BeamState beam_state(onmt_model* m, bool trace) {
   return bs;
 }
 
-static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len, bool trace) {
+static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len, bool trace,
+                            const DecodeOpts& op = DecodeOpts{}) {
   const bool bfm = m->prec == ONMT_PREC_BF16;
   const int R = B * K, H = m->H, E = m->E, L = m->L;
   while ((int)m->xdec.size() < L) m->xdec.push_back(std::make_unique<Act>());
@@ -836,10 +858,15 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
   m->b_prow.ensure((size_t)R * 4);
   m->b_done.ensure((size_t)B * 4);
   m->b_ndone.ensure(4);
-  m->b_bt.ensure((size_t)B * 4);
-  m->b_br.ensure((size_t)B * 4);
-  m->b_braw.ensure((size_t)B * 8);
-  m->b_bnorm.ensure((size_t)B * 8);
+  m->b_bt.ensure((size_t)B * op.nbest * 4);
+  m->b_br.ensure((size_t)B * op.nbest * 4);
+  m->b_braw.ensure((size_t)B * op.nbest * 8);
+  m->b_bnorm.ensure((size_t)B * op.nbest * 8);
+  if (op.att()) {
+    m->b_att.ensure((size_t)R * S_max * 4);
+    if (op.beta != 0.0) m->b_catt.ensure((size_t)2 * R * S_max * 4);
+    if (op.unk) m->h_amax.ensure((size_t)max_len * R * 4);
+  }
   m->h_par.ensure((size_t)max_len * R * 4);
   m->h_tok.ensure((size_t)max_len * R * 4);
   m->h_lp.ensure((size_t)max_len * R * 4);
@@ -940,7 +967,7 @@ static void dec_step_specs(onmt_model* m, const int* d_lens, int B, int S_max, i
 // h~ = tanh(W_out [c; h]); h~ goes to m->htilde (input feed) and to the generator operand
 // xg_dst.  Used by translation (per-layer path) and by teacher-forced scoring.
 static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_max, int K, const int* done,
-                               XOut xg_dst, StepCtl ctl) {
+                               XOut xg_dst, StepCtl ctl, float* att_out = nullptr) {
   const bool bf = m->use_tc;
   const int R = B * K, H = m->H, L = m->L;
   const int rp = m->xg.rows_pad;
@@ -990,6 +1017,7 @@ static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_ma
     const float* keys = m->general ? m->keys.as<float>() : m->mem.as<float>();
     const int key_ld = m->general ? m->attn_win_t.m_pad : H;
     AttFold fo{};
+    fo.att_out = att_out;
     if (m->fold_cur) {
       fo.wpart = m->woh_part.as<float>();
       fo.n_wt = m->dec_w[L - 1]->m_pad / kTileM;
@@ -1029,12 +1057,14 @@ static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_ma
 }
 
 static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int K, int max_len, float alpha,
-                            bool trace, const DecodeOut& out) {
+                            bool trace, const DecodeOut& out, const DecodeOpts& op) {
   const bool bf = m->use_tc;
   const int R = B * K, H = m->H, E = m->E, L = m->L;
   const int rp = m->xg.rows_pad;
   const int n_vt = gen_parts(m, m->xg);
-  BeamState bs = beam_state(m, trace);
+  BeamState bs = beam_state(m, trace, op, d_lens, S_max);
+  if (op.att() && n_vt > 256)
+    throw Error{ONMT_E_UNSUPPORTED, "coverage / unk replacement need the one-CTA-per-sentence beam step (<= 256 generator partials)"};
   float* hh = m->st_h.as<float>();
   float* cc = m->st_c.as<float>();
   float* cg = m->st_cg.as<float>();
@@ -1063,7 +1093,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
   std::vector<DsGemmSpec> ds_specs;
   DsAtt ds_att;
   bool ds_on = false;
-  if (m->use_tc && m->dec_fused) {
+  if (m->use_tc && m->dec_fused && !op.att()) {
     dec_step_specs(m, d_lens, B, S_max, K, bs, ds_specs, ds_att);
     ds_on = dec_step(ds_specs.data(), L, ds_att, m->ds_bar.as<unsigned int>(), ctl, m->num_sms, nullptr, nullptr) ==
             cudaSuccess;
@@ -1077,7 +1107,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       count(m);
       prof_end(m, "gemm", pd);
     }
-    if (!ds_on) enqueue_dec_layers(m, d_lens, B, S_max, K, bs.done, m->xg.xo(bf), ctl);
+    if (!ds_on) enqueue_dec_layers(m, d_lens, B, S_max, K, bs.done, m->xg.xo(bf), ctl, op.att() ? m->b_att.as<float>() : nullptr);
     const double lp = std::pow((5.0 + t) / 6.0, (double)alpha);
     if (use_gen_step(m, m->xg)) {
       // K-outer generator (phase A of gen_step.cu), partials [row][C]; then row reduce + beam step
@@ -1103,7 +1133,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
     }
     prof_end(m, "step", ev);
   }
-  launch_finalize(bs, B, K, max_len, out.hyps, out.lens, out.scores, out.raw, out.tlogp, m->stream);
+  launch_finalize(bs, B, K, max_len, out.hyps, out.lens, out.scores, out.raw, out.tlogp, out.unk_pos, m->stream);
   count(m);
   ONMT_CUDA(cudaGetLastError());
 }
@@ -1257,13 +1287,13 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
 // The whole translation (encoder, decoder init, every decode step, finalize) as one CUDA
 // graph, cached per shape / pointer set: one cudaGraphLaunch per call, no host round trip.
 static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int K, int max_len,
-                          float alpha, bool trace, const DecodeOut& out) {
+                          float alpha, bool trace, const DecodeOut& out, const DecodeOpts& op = DecodeOpts{}) {
   m->fold_cur = fold_on(m, B * K);
   prepare_encoder(m, B, S_max);
-  prepare_decoder(m, B, S_max, K, max_len, trace);
+  prepare_decoder(m, B, S_max, K, max_len, trace, op);
   auto enqueue = [&]() {
     enqueue_encoder(m, d_ids, d_lens, B, S_max);
-    enqueue_decoder(m, d_lens, B, S_max, K, max_len, alpha, trace, out);
+    enqueue_decoder(m, d_lens, B, S_max, K, max_len, alpha, trace, out, op);
   };
   if (!m->use_graph) {
     phase_trace_begin();
@@ -1275,7 +1305,8 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
                               m->gen_step, m->dec_fused, m->fold_cur, m->enc_persistent,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
-                              (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp};
+                              (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp,
+                              (int64_t)(intptr_t)out.unk_pos, (int64_t)(op.beta * 1e9), op.nbest, op.unk};
   GraphCache& gc = m->graph;
   if (!gc.exec || gc.key != key) {
     if (gc.exec) {
@@ -1482,7 +1513,7 @@ static onmt_status check_decode_args(int32_t beam, int32_t max_len, float alpha)
 static onmt_status translate_impl(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
                                   int32_t beam, int32_t max_len, float alpha, int32_t* hyps, int32_t* olens,
                                   float* scores, float* raw, float* tlogp, int32_t* sel_parent, int32_t* sel_token,
-                                  double* sel_score) {
+                                  double* sel_score, const DecodeOpts& op = DecodeOpts{}, int32_t* unk_pos = nullptr) {
   onmt_status s = validate(m, ids, lens, B, S_max, true);
   if (s != ONMT_OK) return s;
   s = check_decode_args(beam, max_len, alpha);
@@ -1493,19 +1524,23 @@ static onmt_status translate_impl(onmt_model* m, const int32_t* ids, const int32
   ONMT_API_BEGIN
   ONMT_CUDA(cudaSetDevice(m->device));
   upload_src(m, ids, lens, B, S_max);
-  m->o_hyps.ensure((size_t)B * max_len * 4);
-  m->o_lens.ensure((size_t)B * 4);
-  m->o_scores.ensure((size_t)B * 4);
-  m->o_raw.ensure((size_t)B * 4);
-  m->o_tlogp.ensure((size_t)B * max_len * 4);
+  const size_t nb = (size_t)op.nbest;
+  m->o_hyps.ensure((size_t)B * nb * max_len * 4);
+  m->o_lens.ensure((size_t)B * nb * 4);
+  m->o_scores.ensure((size_t)B * nb * 4);
+  m->o_raw.ensure((size_t)B * nb * 4);
+  m->o_tlogp.ensure((size_t)B * nb * max_len * 4);
+  if (unk_pos) m->o_unk.ensure((size_t)B * nb * max_len * 4);
   DecodeOut o{m->o_hyps.as<int>(), m->o_lens.as<int>(), m->o_scores.as<float>(), m->o_raw.as<float>(),
-              m->o_tlogp.as<float>()};
-  run_translate(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max, beam, max_len, alpha, trace, o);
-  ONMT_CUDA(cudaMemcpyAsync(hyps, o.hyps, (size_t)B * max_len * 4, cudaMemcpyDeviceToHost, m->stream));
-  ONMT_CUDA(cudaMemcpyAsync(olens, o.lens, (size_t)B * 4, cudaMemcpyDeviceToHost, m->stream));
-  ONMT_CUDA(cudaMemcpyAsync(scores, o.scores, (size_t)B * 4, cudaMemcpyDeviceToHost, m->stream));
-  if (raw) ONMT_CUDA(cudaMemcpyAsync(raw, o.raw, (size_t)B * 4, cudaMemcpyDeviceToHost, m->stream));
-  if (tlogp) ONMT_CUDA(cudaMemcpyAsync(tlogp, o.tlogp, (size_t)B * max_len * 4, cudaMemcpyDeviceToHost, m->stream));
+              m->o_tlogp.as<float>(), unk_pos ? m->o_unk.as<int>() : nullptr};
+  run_translate(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max, beam, max_len, alpha, trace, o, op);
+  ONMT_CUDA(cudaMemcpyAsync(hyps, o.hyps, (size_t)B * nb * max_len * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaMemcpyAsync(olens, o.lens, (size_t)B * nb * 4, cudaMemcpyDeviceToHost, m->stream));
+  ONMT_CUDA(cudaMemcpyAsync(scores, o.scores, (size_t)B * nb * 4, cudaMemcpyDeviceToHost, m->stream));
+  if (raw) ONMT_CUDA(cudaMemcpyAsync(raw, o.raw, (size_t)B * nb * 4, cudaMemcpyDeviceToHost, m->stream));
+  if (tlogp) ONMT_CUDA(cudaMemcpyAsync(tlogp, o.tlogp, (size_t)B * nb * max_len * 4, cudaMemcpyDeviceToHost, m->stream));
+  if (unk_pos)
+    ONMT_CUDA(cudaMemcpyAsync(unk_pos, o.unk_pos, (size_t)B * nb * max_len * 4, cudaMemcpyDeviceToHost, m->stream));
   const size_t n = (size_t)max_len * B * beam;
   if (sel_parent) ONMT_CUDA(cudaMemcpyAsync(sel_parent, m->s_par.p, n * 4, cudaMemcpyDeviceToHost, m->stream));
   if (sel_token) ONMT_CUDA(cudaMemcpyAsync(sel_token, m->h_tok.p, n * 4, cudaMemcpyDeviceToHost, m->stream));
@@ -1520,6 +1555,21 @@ onmt_status onmt_translate(onmt_model* m, const int32_t* ids, const int32_t* len
                            float* raw, float* tlogp) {
   return translate_impl(m, ids, lens, B, S_max, beam, max_len, alpha, hyps, olens, scores, raw, tlogp, nullptr,
                         nullptr, nullptr);
+}
+
+onmt_status onmt_translate_ex(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
+                              const onmt_decode_opts* opts, int32_t* hyps, int32_t* olens, float* scores, float* raw,
+                              float* tlogp, int32_t* unk_pos) {
+  if (!opts) return fail(ONMT_E_INVALID_ARG, "null options");
+  if (opts->n_best < 1 || opts->n_best > opts->beam) return fail(ONMT_E_INVALID_ARG, "n_best must be in [1, beam]");
+  if (!(opts->coverage_penalty >= 0.f)) return fail(ONMT_E_INVALID_ARG, "coverage_penalty must be >= 0");
+  if (unk_pos && !opts->replace_unk) return fail(ONMT_E_INVALID_ARG, "unk_pos needs replace_unk");
+  DecodeOpts op;
+  op.beta = opts->coverage_penalty;
+  op.nbest = opts->n_best;
+  op.unk = opts->replace_unk != 0;
+  return translate_impl(m, ids, lens, B, S_max, opts->beam, opts->max_len, opts->length_penalty, hyps, olens, scores,
+                        raw, tlogp, nullptr, nullptr, nullptr, op, unk_pos);
 }
 
 onmt_status onmt_translate_trace(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,

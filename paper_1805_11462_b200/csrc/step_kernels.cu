@@ -158,13 +158,18 @@ __global__ void init_decode_kernel(BeamState bs, int B, int K, const float* __re
     bs.prow[r] = r;
     if (k == 0) {
       bs.done[b] = 0;
-      bs.best_t[b] = 0;
-      bs.best_r[b] = 0;
-      bs.best_raw[b] = -CUDART_INF;
-      bs.best_norm[b] = -CUDART_INF;
+      const int nb = bs.nbest > 0 ? bs.nbest : 1;
+      for (int i = 0; i < nb; ++i) {
+        bs.best_t[b * nb + i] = 0;
+        bs.best_r[b * nb + i] = 0;
+        bs.best_raw[b * nb + i] = -CUDART_INF;
+        bs.best_norm[b * nb + i] = -CUDART_INF;
+      }
       if (b == 0) *bs.n_done = 0;
     }
   }
+  if (bs.catt)                                       // step 1 reads buffer 1 (empty history)
+    for (int s = threadIdx.x; s < bs.S_max; s += blockDim.x) bs.catt[((size_t)gridDim.x + r) * bs.S_max + s] = 0.f;
   for (int l = 0; l < L; ++l) {
     for (int j = threadIdx.x; j < H; j += blockDim.x) {
       dec_h[((size_t)l * dec_rows_pad + r) * H + j] = enc_h[((size_t)l * B + b) * H + j];
@@ -343,24 +348,31 @@ __global__ void __launch_bounds__(128) beam_select_gather_kernel(const float* __
 
 // A11 + O11: backtrack the banked best entry of each sentence.
 __global__ void finalize_kernel(BeamState bs, int B, int K, int max_len, int* hyps, int* lens, float* scores,
-                                float* raw, float* tlogp) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const int T = bs.best_t[b];
-  int r = bs.best_r[b];
+                                float* raw, float* tlogp, int* unk_pos) {
+  // one thread per (sentence b, n-best rank i); output row o = b * nbest + i
+  const int nb = bs.nbest > 0 ? bs.nbest : 1;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= B * nb) return;
+  const int b = o / nb;
+  const int T = bs.best_t[o];                        // 0: fewer than i + 1 entries were banked
+  int r = bs.best_r[o];
   for (int t = max_len; t > T; --t) {
-    hyps[(size_t)b * max_len + t - 1] = 0;
-    if (tlogp) tlogp[(size_t)b * max_len + t - 1] = 0.f;
+    hyps[(size_t)o * max_len + t - 1] = 0;
+    if (tlogp) tlogp[(size_t)o * max_len + t - 1] = 0.f;
+    if (unk_pos) unk_pos[(size_t)o * max_len + t - 1] = -1;
   }
   for (int t = T; t >= 1; --t) {
     const size_t h = (size_t)(t - 1) * B * K + (size_t)b * K + r;
-    hyps[(size_t)b * max_len + t - 1] = bs.hist_token[h];
-    if (tlogp) tlogp[(size_t)b * max_len + t - 1] = bs.hist_logp[h];
+    const int w = bs.hist_token[h];
+    hyps[(size_t)o * max_len + t - 1] = w;
+    if (tlogp) tlogp[(size_t)o * max_len + t - 1] = bs.hist_logp[h];
+    // S448: an <unk> emitted at step t is replaced by the source word at argmax_s a_{t,s}
+    if (unk_pos) unk_pos[(size_t)o * max_len + t - 1] = (w == 1 && bs.hist_amax) ? bs.hist_amax[h] : -1;
     r = bs.hist_parent[h];
   }
-  lens[b] = T;
-  scores[b] = (float)bs.best_norm[b];
-  if (raw) raw[b] = (float)bs.best_raw[b];
+  lens[o] = T;
+  scores[o] = T ? (float)bs.best_norm[o] : -INFINITY;
+  if (raw) raw[o] = T ? (float)bs.best_raw[o] : -INFINITY;
 }
 
 // ------------------------------------------------------------------ host launchers
@@ -447,8 +459,9 @@ void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_p
 }
 
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
-                     float* tlogp, cudaStream_t st) {
-  finalize_kernel<<<(B + 127) / 128, 128, 0, st>>>(bs, B, K, max_len, hyps, lens, scores, raw, tlogp);
+                     float* tlogp, int* unk_pos, cudaStream_t st) {
+  const int n = B * (bs.nbest > 0 ? bs.nbest : 1);
+  finalize_kernel<<<(n + 127) / 128, 128, 0, st>>>(bs, B, K, max_len, hyps, lens, scores, raw, tlogp, unk_pos);
 }
 
 // Test helper (onmt_test_gen): per row, combine generator partials into the LSE and
