@@ -51,6 +51,9 @@ struct GenStepArgs {
                                                 // uint keys; buffer t & 1, the other one is reset)
   StepCtl ctl;
   int dbg;                                      // microbenchmark ablations (ONMT_KTRACE builds)
+  unsigned long long* arrive;                   // phases == 4: monotonic arrival counter (64-bit)
+  int B;                                        // phases == 4: sentences (one beam-step CTA each)
+  int gbuf_floats;                              // phases == 4: dynamic smem reusable as beam staging
 };
 
 __device__ __forceinline__ float gs_ex2(float x) {
@@ -416,6 +419,37 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
+  if (a.phases == 4) {
+    // ============================================================ fused beam step (A10 + A5)
+    // Every CTA counts itself in after its partials are stored (release); the LAST B CTAs
+    // to arrive stay: each waits for the whole grid (all co-resident) and runs the beam step
+    // of one sentence (beam_device.cuh) - the separate beam-step launch disappears.
+    __shared__ unsigned long long s_arr;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_arr = atomicAdd(a.arrive, 1ull);
+    }
+    __syncthreads();
+    const unsigned long long G = gridDim.x;
+    const unsigned long long idx = s_arr % G;
+    if (idx < G - (unsigned long long)a.B) return;
+    const int b = (int)(idx - (G - (unsigned long long)a.B));
+    if (threadIdx.x == 0) {
+      const unsigned long long target = (s_arr / G + 1ull) * G;   // this step's generation complete
+      while (true) {
+        unsigned long long v;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.arrive) : "memory");
+        if (v >= target) break;
+      }
+      __threadfence();
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging (generic) -> bulk copies
+    __syncthreads();
+    KT(4);
+    beam_step_sentence<KMAX>(b, a.ms, a.tz, a.ti, a.C, 1, a.C, a.K, a.R, a.t, a.max_len, a.lp, a.bs, a.ga,
+                             reinterpret_cast<float*>(smem), a.gbuf_floats);
+    return;
+  }
   if (a.phases < 2) return;
 
   // ================================================================ phase B
@@ -532,7 +566,8 @@ static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, GsPlan& p) {
   if (p.nt_max < 1) return false;
   p.P = 2 * n_group <= 32 * kGsScanWarps ? 2 : 1;
   if (n_group > 32 * kGsScanWarps) return false;
-  const size_t limit = 227 * 1024 - 6144;         // (static shared memory of phases B / C: <= 4.5 KB)
+  const size_t limit = 227 * 1024 - 12288;        // (static shared memory of phases B / C and the fused
+                                                  //  beam step: <= 11 KB)
   p.stages = 4;
   while (p.stages > 2 && gs_smem_bytes(n_group, p.nt_max, p.stages) > limit) --p.stages;
   while (p.nt_max > 1 && gs_smem_bytes(n_group, p.nt_max, p.stages) > limit) --p.nt_max;
@@ -559,7 +594,8 @@ static cudaError_t launch_gs(const CUtensorMap& tmW, const CUtensorMap& tmX, con
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i,
                      int phases, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
-                     unsigned int* gbar, unsigned int* thr, StepCtl ctl, cudaStream_t st) {
+                     unsigned int* gbar, unsigned int* thr, StepCtl ctl, cudaStream_t st,
+                     unsigned long long* arrive, int B) {
   const int groups = n_rows_pad / n_group;
   GsPlan p;
   if (!gs_plan(n_vt, n_group, groups, num_sms, p)) return cudaErrorInvalidConfiguration;
@@ -596,6 +632,10 @@ cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, i
   a.dbg = g_gs_dbg;
   const int grid = p.C * groups;
   const size_t smem = gs_smem_bytes(n_group, p.nt_max, p.stages);
+  a.arrive = arrive;
+  a.B = B;
+  a.gbuf_floats = (int)((smem - 1024 - (2 * (size_t)p.stages + 9) * 8 - 16) / 4);
+  if (phases == 4 && (!arrive || B > grid || p.C > 256)) return cudaErrorInvalidConfiguration;
   if (g.K <= 1) return launch_gs<1>(tmW, tmX, a, grid, smem, st);
   if (g.K <= 2) return launch_gs<2>(tmW, tmX, a, grid, smem, st);
   if (g.K <= 4) return launch_gs<4>(tmW, tmX, a, grid, smem, st);

@@ -41,7 +41,8 @@ int gen_step_parts(int n_vt, int n_group, int groups, int num_sms);
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i,
                      int phases, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
-                     unsigned int* gbar, unsigned int* thr, StepCtl ctl, cudaStream_t st);
+                     unsigned int* gbar, unsigned int* thr, StepCtl ctl, cudaStream_t st,
+                     unsigned long long* arrive = nullptr, int B = 0);
 int gen_cluster_size(int n_group, int n_vt, int n_groups, int num_sms);
 extern unsigned long long* g_gen_dbg;
 
@@ -317,6 +318,8 @@ struct onmt_model {
   bool gen_step = true;        // K-outer persistent generator (gen_step.cu)
   bool fold_wout = true;       // W_out folded into the top cell layer + attention (no W_out launch)
   bool enc_persistent = true;  // encoder recurrence of a layer as one persistent kernel (enc_rec.cu)
+  bool fuse_beam = false;      // beam step run by the generator's last-arriving CTAs (gen_step.cu phases 4;
+                               // opt-in: parity-tested but measured 3 us/step slower than the separate launch)
   bool fold_cur = false;       // ... for the call being enqueued (fold_on)
   bool dec_fused = false;      // decoder cells + attention + W_out as one persistent kernel (dec_step.cu;
                                // opt-in: measured slower than the per-layer kernels)
@@ -349,6 +352,7 @@ struct onmt_model {
   DevBuf f_scratch, f_count;                 // fused GEMM partial tiles + per-tile arrival counters
   DevBuf g_bar;                              // grid barrier counter of the generator step kernel
   DevBuf g_thr;                              // generator: shared per-row top-K thresholds [2][rows_pad]
+  DevBuf g_arrive;                           // generator + fused beam step: 64-bit arrival counter
   DevBuf ds_part, ds_bar;                    // fused decoder step: attention chunk partials, grid barrier
   DevBuf woh_part;                           // folded W_out: top-layer shares W_out[:, units] h [tiles][rows_pad][H]
   DevBuf g_ms, g_tz, g_ti;
@@ -894,6 +898,10 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
       m->g_bar.ensure(256);
       ONMT_CUDA(cudaMemset(m->g_bar.p, 0, 256));
     }
+    if (!m->g_arrive.p) {
+      m->g_arrive.ensure(256);
+      ONMT_CUDA(cudaMemset(m->g_arrive.p, 0, 256));
+    }
     if (m->g_thr.bytes < (size_t)2 * m->xg.rows_pad * 4) {
       m->g_thr.ensure((size_t)2 * m->xg.rows_pad * 4);
       ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
@@ -1112,12 +1120,27 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
     if (use_gen_step(m, m->xg)) {
       // K-outer generator (phase A of gen_step.cu), partials [row][C]; then row reduce + beam step
       EvPair pgs = prof_begin(m, "gen");
-      ONMT_CUDA(gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
-                         m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
-                         m->row_i.as<int>(), 1, t, max_len, lp, bs, ga, m->g_bar.as<unsigned int>(),
-                         m->g_thr.as<unsigned int>(), ctl, m->stream));
+      // generator + (fused) beam step: the generator's last B CTAs to finish run the beam step
+      cudaError_t ge = cudaErrorInvalidConfiguration;
+      if (m->fuse_beam)
+        ge = gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
+                      m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
+                      m->row_i.as<int>(), 4, t, max_len, lp, bs, ga, m->g_bar.as<unsigned int>(),
+                      m->g_thr.as<unsigned int>(), ctl, m->stream, m->g_arrive.as<unsigned long long>(), B);
+      const bool fused_beam = ge == cudaSuccess;
+      if (!fused_beam) {
+        if (ge != cudaErrorInvalidConfiguration) ONMT_CUDA(ge);
+        ONMT_CUDA(gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
+                           m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
+                           m->row_i.as<int>(), 1, t, max_len, lp, bs, ga, m->g_bar.as<unsigned int>(),
+                           m->g_thr.as<unsigned int>(), ctl, m->stream));
+      }
       count(m);
       prof_end(m, "gen", pgs);
+      if (fused_beam) {
+        prof_end(m, "step", ev);
+        continue;
+      }
       EvPair pm = prof_begin(m, "merge");
       launch_beam_merge(g.ms, g.tz, g.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
                         m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
@@ -1302,7 +1325,7 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     return;
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
-                              m->gen_step, m->dec_fused, m->fold_cur, m->enc_persistent,
+                              m->gen_step, m->dec_fused, m->fold_cur, m->enc_persistent, m->fuse_beam,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
                               (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp,
@@ -1400,6 +1423,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   if (const char* ev = std::getenv("ONMT_DEC_FUSED")) m->dec_fused = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_FOLD_WOUT")) m->fold_wout = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_PERSISTENT")) m->enc_persistent = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_FUSE_BEAM")) m->fuse_beam = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
@@ -1443,6 +1467,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->fold_wout = v != 0;
   } else if (n == "enc_persistent") {
     m->enc_persistent = v != 0;
+  } else if (n == "fuse_beam") {
+    m->fuse_beam = v != 0;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
   } else {
