@@ -121,3 +121,23 @@ def test_ex_errors(weight_cache):
         gm.translate_ex(ids, lens, 3, 10, 0.0, 0.0, 4)      # n_best > beam
     with pytest.raises(ob.OnmtError):
         gm.translate_ex(ids, lens, 3, 10, 0.0, -1.0, 1)     # beta < 0
+
+
+def test_fused_beam_step_option(weight_cache):
+    """The generator kernel's fused beam step (option fuse_beam) computes exactly what the
+    separate beam-step kernel does (same device function, same inputs)."""
+    cfg = synth.ModelConfig(2, 64, 128, 300, 2000, False, True)
+    gm, om, prec = toy_pair(cfg, 2, 0.1, weight_cache, "bf16")
+    ids, lens = synth.make_corpus("c1")
+    a = gm.translate(ids, lens, 5, 8, 0.6)
+    gm.set_option("fuse_beam", 1)
+    try:
+        b = gm.translate(ids, lens, 5, 8, 0.6)
+        c = gm.translate_ex(ids, lens, 5, 8, 0.6, 0.3, 3, True)
+    finally:
+        gm.set_option("fuse_beam", 0)
+    d = gm.translate_ex(ids, lens, 5, 8, 0.6, 0.3, 3, True)
+    for k in ("hyps", "lens", "scores", "token_logp"):
+        assert np.array_equal(a[k], b[k]), k
+        assert np.array_equal(c[k], d[k]), k
+    assert np.array_equal(c["unk_pos"], d["unk_pos"])
