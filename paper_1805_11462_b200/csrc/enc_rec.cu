@@ -7,14 +7,19 @@
 // per sentence over its own S_b tokens (packed semantics, R3: frozen for t >= S_b; the
 // backward direction runs pos = S_b-1-t), Z = W_ih x hoisted over all t by one GEMM before.
 //
-// Grid = D x T CTAs (direction, 128-row tile of the interleaved gate rows = 32 units), all
-// co-resident (one per SM).  Each CTA keeps its W_hh tile (128 x K bf16) resident in shared
-// memory for the whole sequence and its units' c state on chip; per step it TMA-loads
-// h_{t-1} of every sentence (bf16 hi/lo planes, written by all tiles of its direction in the
-// previous step), runs the tcgen05 MMAs (M = 128 gate rows, N = sentences), applies the cell
-// to its 32 units and stores h_t into the other parity buffer; a software barrier among the
-// direction's T CTAs separates the steps.  This replaces 2 launches per step (split-K GEMM +
-// cell kernel) by one launch per layer.
+// Grid = D x T x S CTAs: direction, 128-row tile of the interleaved gate rows (32 units),
+// split of the K = Hd reduction; the S splits of a tile form one thread-block cluster.  All
+// CTAs are co-resident (one per SM).  Each CTA keeps its W_hh tile's K-slice resident in
+// shared memory for the whole sequence.  Per step it TMA-loads its K-slice of h_{t-1}
+// (bf16 hi/lo planes, written in the previous step by the tiles owning those units), runs
+// the tcgen05 MMAs (M = 128 gate rows, N = sentences; 1/S of the MMAs a whole-K tile would
+// issue - small-N MMAs are issue-bound), then the cluster reduce-scatters the partial gate
+// tiles through distributed shared memory: split s owns sentence columns
+// [s*N/S, (s+1)*N/S), receives the other splits' partials of those columns, sums them in
+// fixed split order (deterministic), applies the cell to its 32 units x N/S sentences (their
+// c state stays on chip) and stores h_t into the other parity buffer.  A software barrier
+// among the direction's T*S CTAs separates the steps (h_t of every unit is needed by every
+// tile).  One launch per layer replaces 2 launches per step (split-K GEMM + cell kernel).
 #include <math_constants.h>
 
 #include "common.cuh"
@@ -39,7 +44,7 @@ struct EncRecDir {
 
 struct EncRecArgs {
   EncRecDir dir[2];
-  int T, Hd, B, N, S_max, kb;
+  int T, S, Hd, B, N, S_max, kb;   // kb: K blocks of the whole reduction (S divides it)
   const int* lens;
   unsigned int* bar;       // [2 x 32] step-barrier words (one per direction, self-resetting)
   unsigned long long* trace;   // (debug) per-step %globaltimer stamps of CTA 0, or nullptr
@@ -50,8 +55,6 @@ __device__ __forceinline__ unsigned long long er_now() {
   return t;
 }
 
-constexpr int kErTr = 132;                        // transpose buffer row stride (floats)
-
 // sigmoid / tanh via the fast exponential (rel. error ~2^-21, as the decoder's fused cell)
 __device__ __forceinline__ float er_sigm(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
 __device__ __forceinline__ float er_tanh(float x) {
@@ -59,9 +62,10 @@ __device__ __forceinline__ float er_tanh(float x) {
   return copysignf(__fdividef(1.f - e, 1.f + e), x);
 }
 
-static size_t er_smem_bytes(int kb, int N) {
-  return 1024 + (size_t)kb * 16384 + (size_t)kb * 2 * N * 128 + (size_t)N * 128 * 4 + (size_t)2 * 32 * N * 4 +
-         32 * 16 + (size_t)N * 4 + (2 + kb) * 8 + 32 + 16;
+static size_t er_smem_bytes(int kbs, int N, int S) {
+  const int NS = N / S;
+  return 1024 + (size_t)kbs * 16384 + (size_t)kbs * 2 * N * 128 + (size_t)S * 128 * NS * 4 + (size_t)NS * 128 * 4 +
+         (size_t)2 * 32 * NS * 4 + 32 * 16 + (size_t)NS * 4 + (2 + kbs) * 8 + 32 + 16;
 }
 
 __global__ void __launch_bounds__(256, 1)
@@ -71,26 +75,30 @@ enc_rec_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__
                EncRecArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int d = blockIdx.x / a.T, tile = blockIdx.x % a.T;
+  const int S = a.S;
+  const int s = (int)cluster_ctarank();                          // K split = my sentence-column group
+  const int ts = blockIdx.x / S;
+  const int d = ts / a.T, tile = ts % a.T;
   __shared__ EncRecDir dr;                                        // my direction's arguments (uniform)
   if (threadIdx.x == 0) dr = a.dir[d];
   const CUtensorMap* tmW = d ? &tmW1 : &tmW0;
   const CUtensorMap* tmXa = d ? &tmX10 : &tmX00;                 // parity 0 (h_{t-1} for even t)
   const CUtensorMap* tmXb = d ? &tmX11 : &tmX01;
-  const int N = a.N, kb = a.kb;
+  const int N = a.N, kbs = a.kb / S, NS = N / S;
+  const int kb0 = s * kbs;                                        // my first K block
   const uint32_t nb = (uint32_t)N * 128;                          // one operand plane, one K block
-  uint8_t* sW = smem;                                             // [kb][128 x 64] bf16 (SW128)
-  uint8_t* sX = sW + (size_t)kb * 16384;                          // [kb][hi, lo][N x 64]
-  float* Tr = reinterpret_cast<float*>(sX);                       // [N][132] gates (overlays sX)
-  float* Zs = reinterpret_cast<float*>(sX + (size_t)kb * 2 * nb); // [N][128] Z_t of my gate rows
-  float* cst = Zs + (size_t)N * 128;                              // [N][32] c of my units
-  float* hst = cst + 32 * N;                                      // [N][32] h of my units
-  float4* s_bias = reinterpret_cast<float4*>(hst + 32 * N);      // [32]
-  int* s_len = reinterpret_cast<int*>(s_bias + 32);               // [N]
-  uint64_t* wbar = reinterpret_cast<uint64_t*>(s_len + ((N + 3) & ~3));
+  uint8_t* sW = smem;                                             // [kbs][128 x 64] bf16 (SW128)
+  uint8_t* sX = sW + (size_t)kbs * 16384;                         // [kbs][hi, lo][N x 64]
+  float* recv = reinterpret_cast<float*>(sX + (size_t)kbs * 2 * nb);   // [S][NS][128] partials of my columns
+  float* Zs = recv + (size_t)S * 128 * NS;                        // [NS][128] Z_t of my gate rows
+  float* cst = Zs + (size_t)NS * 128;                             // [NS][32] c of my units, my sentences
+  float* hst = cst + 32 * NS;                                     // [NS][32] h
+  float4* s_bias = reinterpret_cast<float4*>(hst + 32 * NS);     // [32]
+  int* s_len = reinterpret_cast<int*>(s_bias + 32);               // [NS]
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(s_len + ((NS + 3) & ~3));
   uint64_t* mdone = wbar + 1;
-  uint64_t* xfull = wbar + 2;                                     // [kb] per K block (TMA -> MMA pipelining)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(xfull + kb);
+  uint64_t* xfull = wbar + 2;                                     // [kbs] per K block (TMA -> MMA pipelining)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xfull + kbs);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tcols = 32;
   while ((int)tcols < N) tcols <<= 1;
@@ -100,11 +108,11 @@ enc_rec_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__
     tma_prefetch_desc(tmXa);
     tma_prefetch_desc(tmXb);
     mbar_init(wbar, 1);
-    for (int i = 0; i < kb; ++i) mbar_init(&xfull[i], 1);
+    for (int i = 0; i < kbs; ++i) mbar_init(&xfull[i], 1);
     mbar_init(mdone, 1);
     fence_mbar_init();
-    mbar_arrive_expect_tx(wbar, (uint32_t)kb * 16384);            // W_hh tile, resident for all t
-    for (int i = 0; i < kb; ++i) tma_load_2d(sW + (size_t)i * 16384, tmW, i * kBK, tile * kTileM, wbar);
+    mbar_arrive_expect_tx(wbar, (uint32_t)kbs * 16384);           // my W_hh K-slice, resident for all t
+    for (int i = 0; i < kbs; ++i) tma_load_2d(sW + (size_t)i * 16384, tmW, (kb0 + i) * kBK, tile * kTileM, wbar);
   }
   if (warp == 1) tmem_alloc_dyn(tslot, tcols);
   __syncthreads();
@@ -112,20 +120,21 @@ enc_rec_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__
     const int j = tile * 32 + threadIdx.x;
     s_bias[threadIdx.x] = j < a.Hd ? dr.bias[j] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  for (int b = threadIdx.x; b < N; b += blockDim.x) s_len[b] = b < a.B ? a.lens[b] : 0;
-  for (int i = threadIdx.x; i < 32 * N; i += blockDim.x) { cst[i] = 0.f; hst[i] = 0.f; }
+  for (int j = threadIdx.x; j < NS; j += blockDim.x) s_len[j] = s * NS + j < a.B ? a.lens[s * NS + j] : 0;
+  for (int i = threadIdx.x; i < 32 * NS; i += blockDim.x) { cst[i] = 0.f; hst[i] = 0.f; }
   __syncthreads();
-  // Z_t of my gate rows for every live sentence (cp.async, 16 B chunks)
   const bool backward_ = dr.backward != 0;
   const float* const Zg = dr.Z;
   const int z_ld = dr.z_ld;
+  // Z_t of my gate rows for my live sentences (cp.async, 16 B chunks)
   auto prefetch_z = [&](int t) {
-    for (int i = threadIdx.x; i < N * 32; i += blockDim.x) {
-      const int b = i >> 5, ch = i & 31;
-      const int L = s_len[b];
+    for (int i = threadIdx.x; i < NS * 32; i += blockDim.x) {
+      const int j = i >> 5, ch = i & 31;
+      const int b = s * NS + j;
+      const int L = s_len[j];
       if (b >= a.B || t >= L) continue;
       const int pos = backward_ ? L - 1 - t : t;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(Zs + (size_t)b * 128 + 4 * ch)),
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(Zs + (size_t)j * 128 + 4 * ch)),
                    "l"(Zg + ((size_t)b * a.S_max + pos) * z_ld + (size_t)tile * 128 + 4 * ch)
                    : "memory");
     }
@@ -143,29 +152,30 @@ enc_rec_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__
   float* const c_st = dr.c_st;
   float* const mem = dr.mem;
   const int st_ld = dr.st_ld, next_col = dr.next_col, mem_ld = dr.mem_ld, mem_col = dr.mem_col;
-  const bool backward = dr.backward != 0, has_next = xnext.f32 || xnext.hl;
+  const bool has_next = xnext.f32 || xnext.hl;
+  const bool tr = a.trace && blockIdx.x == 0;
 
   for (int t = 0; t < a.S_max; ++t) {
     if (t > 0) {
-      // every tile of my direction has stored h_{t-1} (and finished reading h_{t-2}'s buffer)
+      // every CTA of my direction has stored h_{t-1} (and finished reading h_{t-2}'s buffer
+      // and its receive buffers of step t-1)
       __syncthreads();
       if (threadIdx.x == 0) {
-        if (a.trace && blockIdx.x == 0 && t < 64) a.trace[t * 8 + 0] = er_now();
-        cta_group_barrier(a.bar + 32 * d, (unsigned)a.T);
-        if (a.trace && blockIdx.x == 0 && t < 64) a.trace[t * 8 + 1] = er_now();
+        if (tr && t < 64) a.trace[t * 8 + 0] = er_now();
+        cta_group_barrier(a.bar + 32 * d, (unsigned)(a.T * S));
+        if (tr && t < 64) a.trace[t * 8 + 1] = er_now();
         asm volatile("fence.proxy.async;" ::: "memory");          // generic stores -> TMA reads
         const CUtensorMap* tx = (t & 1) ? tmXb : tmXa;            // buffer t & 1 holds h_{t-1}
-        for (int i = 0; i < kb; ++i) {
+        for (int i = 0; i < kbs; ++i) {
           mbar_arrive_expect_tx(&xfull[i], 2 * nb);
-          tma_load_2d(sX + (size_t)i * 2 * nb, tx, i * kBK, 0, &xfull[i]);
-          tma_load_2d(sX + (size_t)i * 2 * nb + nb, tx, i * kBK, N, &xfull[i]);
+          tma_load_2d(sX + (size_t)i * 2 * nb, tx, (kb0 + i) * kBK, 0, &xfull[i]);
+          tma_load_2d(sX + (size_t)i * 2 * nb + nb, tx, (kb0 + i) * kBK, N, &xfull[i]);
         }
       }
       if (warp == 1 && lane == 0) {
         if (t == 1) mbar_wait(wbar, 0);
-        if (a.trace && blockIdx.x == 0 && t < 64) a.trace[t * 8 + 2] = er_now();
         const uint32_t idesc = umma_idesc_bf16(kTileM, N);
-        for (int i = 0; i < kb; ++i) {
+        for (int i = 0; i < kbs; ++i) {
           mbar_wait(&xfull[i], (t - 1) & 1);
           tc_fence_after();
           const uint32_t sa = smem_u32(sW + (size_t)i * 16384);
@@ -181,84 +191,122 @@ enc_rec_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__
       }
       __syncwarp();
       mbar_wait(mdone, (t - 1) & 1);
-      if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 3] = er_now();
+      if (tr && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 3] = er_now();
       tc_fence_after();
-      // W_hh h_{t-1}: TMEM [gate row][sentence] -> Tr[sentence][gate row]
+      // reduce-scatter: my partial of split p's sentence columns -> p's recv[s] (DSMEM).
+      // Warp w: TMEM lane quarter w & 3, peers p = (w >> 2), (w >> 2) + 2, ...
       {
-        const int q = warp & 3, half = warp >> 2;
-        const int cb = half * (N >> 1), ce = cb + (N >> 1);
+        const int q = warp & 3;
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-        for (int c0 = cb; c0 < ce; c0 += 8) {
-          uint32_t r[8];
-          tmem_ld8_nw(trow + c0, r);
-          tmem_wait_ld();
-          tmem_fence_regs(r);
+        const int row = q * 32 + lane;
+        for (int p = warp >> 2; p < S; p += 2) {
+          for (int c0 = 0; c0 < NS; c0 += 8) {
+            uint32_t r[8];
+            tmem_ld8_nw(trow + p * NS + c0, r);
+            tmem_wait_ld();
+            tmem_fence_regs(r);
+            // recv[s][column][row]: a warp's store covers 32 consecutive rows (128 B)
+            float* dst = recv + ((size_t)s * NS + c0) * 128 + row;
+            if (p == s) {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) Tr[(size_t)(c0 + k) * kErTr + q * 32 + lane] = __uint_as_float(r[k]);
+              for (int k = 0; k < 8; ++k) dst[(size_t)k * 128] = __uint_as_float(r[k]);
+            } else {
+              const uint32_t pa = mapa_peer(smem_u32(dst), (uint32_t)p);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) st_cluster_b32(pa + (uint32_t)k * 512u, r[k]);
+            }
+          }
         }
       }
       tc_fence_before();
-      if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 6] = er_now();
+      cluster_arrive();                                           // (release: my DSMEM stores)
+      cluster_wait();                                             // every split's partial landed
+      if (tr && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 6] = er_now();
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");          // Z_t landed (my chunks)
     __syncthreads();
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 4] = er_now();
-    // ---- the cell for (unit u, sentence b); consecutive threads take consecutive units
+    if (tr && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 4] = er_now();
+    // ---- the cell for (unit u, my sentence j); consecutive threads take consecutive units
     const XOut xo = (t & 1) ? xrec0 : xrec1;                     // h_t for step t+1's MMA
-    for (int i = threadIdx.x; i < 32 * N; i += blockDim.x) {
-      const int u = i & 31, b = i >> 5;
-      const int j = tile * 32 + u;
-      if (b >= a.B || j >= a.Hd) continue;
-      const int L = s_len[b];
+    for (int i = threadIdx.x; i < 32 * NS; i += blockDim.x) {
+      const int u = i & 31, j = i >> 5;
+      const int b = s * NS + j, jj = tile * 32 + u;
+      if (b >= a.B || jj >= a.Hd) continue;
+      const int L = s_len[j];
       if (t >= L) {                                               // finished: carry h forward
-        store_x(xo, b, j, hst[b * 32 + u]);
+        store_x(xo, b, jj, hst[j * 32 + u]);
         continue;
       }
-      const int pos = backward ? L - 1 - t : t;
+      const int pos = backward_ ? L - 1 - t : t;
       const size_t row = (size_t)b * a.S_max + pos;
-      float4 g = *reinterpret_cast<const float4*>(Zs + (size_t)b * 128 + 4 * u);
+      float4 g = *reinterpret_cast<const float4*>(Zs + (size_t)j * 128 + 4 * u);
       const float4 bb = s_bias[u];
       g.x += bb.x; g.y += bb.y; g.z += bb.z; g.w += bb.w;
       if (t > 0) {
-        const float4 p = *reinterpret_cast<const float4*>(Tr + (size_t)b * kErTr + 4 * u);
-        g.x += p.x; g.y += p.y; g.z += p.z; g.w += p.w;
+        for (int p = 0; p < S; ++p) {                             // fixed split order
+          const float4 pv = *reinterpret_cast<const float4*>(recv + ((size_t)p * NS + j) * 128 + 4 * u);
+          g.x += pv.x; g.y += pv.y; g.z += pv.z; g.w += pv.w;
+        }
       }
       const float ig = er_sigm(g.x), fg = er_sigm(g.y), gg = er_tanh(g.z), og = er_sigm(g.w);
-      const float c = fg * cst[b * 32 + u] + ig * gg;
+      const float c = fg * cst[j * 32 + u] + ig * gg;
       const float h = og * er_tanh(c);
-      cst[b * 32 + u] = c;
-      hst[b * 32 + u] = h;
-      store_x(xo, b, j, h);
-      h_st[(size_t)b * st_ld + j] = h;
-      c_st[(size_t)b * st_ld + j] = c;
-      if (has_next) store_x(xnext, (int)row, next_col + j, h);
-      if (mem) mem[row * mem_ld + mem_col + j] = h;
+      cst[j * 32 + u] = c;
+      hst[j * 32 + u] = h;
+      if (tr && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 2] = er_now() + (unsigned long long)(h == 1234.5f);
+      store_x(xo, b, jj, h);
+      if (t == L - 1) {                                           // final state (R5: decoder init)
+        h_st[(size_t)b * st_ld + jj] = h;
+        c_st[(size_t)b * st_ld + jj] = c;
+      }
+      if (has_next) store_x(xnext, (int)row, next_col + jj, h);
+      if (mem) mem[row * mem_ld + mem_col + jj] = h;
     }
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 7] = er_now();
-    __syncthreads();                                              // Zs / Tr consumed
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 5] = er_now();
+    if (tr && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 7] = er_now();
+    __syncthreads();                                              // Zs / recv consumed
+    if (tr && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 5] = er_now();
     if (t + 1 < a.S_max) prefetch_z(t + 1);
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
+  cluster_arrive();                                               // (no peer still writes my smem)
+  cluster_wait();
   if (warp == 1) tmem_dealloc(tmem, tcols);
 }
 
-// can this layer run as one persistent kernel? (shared memory, co-residency)
-bool enc_rec_fits(int kb, int N, int D, int T, int num_sms) {
-  return N >= 16 && N <= 256 && (N % 16) == 0 && D * T <= num_sms && er_smem_bytes(kb, N) <= 227 * 1024 &&
-         (size_t)N * kErTr * 4 <= (size_t)kb * 2 * N * 128;
+// splits per tile for this layer (0 = the persistent kernel does not fit): the largest S in
+// {4, 2, 1} dividing the K blocks with N/S a multiple of 8, the grid co-resident and the
+// shared memory within 227 KB
+int enc_rec_splits(int kb, int N, int D, int T, int num_sms) {
+  if (N < 16 || N > 256 || (N % 16) != 0) return 0;
+  for (int S = 4; S >= 1; S >>= 1) {
+    if (kb % S != 0 || (N / S) % 8 != 0 || D * T * S > num_sms) continue;
+    if (er_smem_bytes(kb / S, N, S) > 227 * 1024) continue;
+    return S;
+  }
+  return 0;
 }
 
 cudaError_t launch_enc_rec(const CUtensorMap* tmW, const CUtensorMap* tmX0, const CUtensorMap* tmX1,
                            const EncRecArgs& a, int D, cudaStream_t st) {
-  const size_t smem = er_smem_bytes(a.kb, a.N);
+  const size_t smem = er_smem_bytes(a.kb / a.S, a.N, a.S);
   cudaError_t e = cudaFuncSetAttribute(enc_rec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int d1 = D > 1 ? 1 : 0;
-  enc_rec_kernel<<<D * a.T, 256, smem, st>>>(tmW[0], tmW[d1], tmX0[0], tmX1[0], tmX0[d1], tmX1[d1], a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(D * a.T * a.S);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, enc_rec_kernel, tmW[0], tmW[d1], tmX0[0], tmX1[0], tmX0[d1], tmX1[d1], a);
 }
 
 }  // namespace onmt

@@ -70,12 +70,12 @@ struct EncRecDir {
 };
 struct EncRecArgs {
   EncRecDir dir[2];
-  int T, Hd, B, N, S_max, kb;
+  int T, S, Hd, B, N, S_max, kb;
   const int* lens;
   unsigned int* bar;
   unsigned long long* trace;
 };
-bool enc_rec_fits(int kb, int N, int D, int T, int num_sms);
+int enc_rec_splits(int kb, int N, int D, int T, int num_sms);
 cudaError_t launch_enc_rec(const CUtensorMap* tmW, const CUtensorMap* tmX0, const CUtensorMap* tmX1,
                            const EncRecArgs& a, int D, cudaStream_t st);
 cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
@@ -705,7 +705,9 @@ static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, 
       const Mat& w0 = *m->enc_whh[l * D];
       const Act& r0 = m->enc_rec[0];
       const int T = w0.m_pad / kTileM, kb = w0.k_pad / kBK;
-      if (m->use_tc && m->enc_persistent && r0.n_group == r0.rows_pad && enc_rec_fits(kb, r0.rows_pad, D, T, m->num_sms)) {
+      const int S = (m->use_tc && m->enc_persistent && r0.n_group == r0.rows_pad)
+                        ? enc_rec_splits(kb, r0.rows_pad, D, T, m->num_sms) : 0;
+      if (S > 0) {
         // the whole recurrence of this layer (both directions) in one launch (enc_rec.cu)
         EncRecArgs ea{};
         CUtensorMap tw[2], tx0[2], tx1[2];
@@ -730,7 +732,7 @@ static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, 
           tx0[d] = m->enc_rec[d].tmap;
           tx1[d] = m->enc_rec2[d].tmap;
         }
-        ea.T = T; ea.Hd = Hd; ea.B = B; ea.N = r0.rows_pad; ea.S_max = S_max; ea.kb = kb;
+        ea.T = T; ea.S = S; ea.Hd = Hd; ea.B = B; ea.N = r0.rows_pad; ea.S_max = S_max; ea.kb = kb;
         ea.lens = d_lens;
         ea.bar = m->er_bar.as<unsigned int>();
         static unsigned long long* er_trace = nullptr;            // (debug: ONMT_ENC_TRACE, no graph)
@@ -744,10 +746,10 @@ static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, 
           ONMT_CUDA(cudaStreamSynchronize(m->stream));
           ONMT_CUDA(cudaMemcpy(h.data(), er_trace, h.size() * 8, cudaMemcpyDeviceToHost));
           for (int t = 8; t < 12; ++t)
-            std::fprintf(stderr, "enc_rec l%d t%d: bar %lld  mma_done %lld  transp %lld  zwait %lld  loop0 %lld  sync %lld  next %lld ns\n", l, t,
+            std::fprintf(stderr, "enc_rec l%d t%d: bar %lld  mma_done %lld  exch %lld  zwait %lld  math %lld  stores %lld  next %lld ns\n", l, t,
                          (long long)(h[t * 8 + 1] - h[t * 8 + 0]), (long long)(h[t * 8 + 3] - h[t * 8 + 1]),
                          (long long)(h[t * 8 + 6] - h[t * 8 + 3]), (long long)(h[t * 8 + 4] - h[t * 8 + 6]),
-                         (long long)(h[t * 8 + 7] - h[t * 8 + 4]), (long long)(h[t * 8 + 5] - h[t * 8 + 7]),
+                         (long long)(h[t * 8 + 2] - h[t * 8 + 4]), (long long)(h[t * 8 + 7] - h[t * 8 + 2]),
                          (long long)(h[(t + 1) * 8 + 0] - h[t * 8 + 5]));
         }
         xin = xnext;
