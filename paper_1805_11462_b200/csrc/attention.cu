@@ -248,7 +248,8 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
     __syncthreads();                               // buffer (i & 1) free for sub-chunk i + 2
     if (i + 2 < nsub_max) stage(i + 2);
   }
-  cp_async_wait<0>();                              // (q, and prefetches past S_b)
+  if (hpref) cp_async_wait<1>();                   // (q, and prefetches past S_b; the W_out shares
+  else cp_async_wait<0>();                         //  are waited for only by the combine)
   __syncthreads();
   // ---- park the unnormalised partial context in q's place (q is no longer read)
 #pragma unroll
@@ -287,6 +288,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
 #pragma unroll
     for (int p = 0; p < 8; ++p) coef[p * KMAX + k] = mp[p] * inv;
   }
+  if (hpref) cp_async_wait<0>();                   // my prefetched W_out shares (and any stage)
   __syncthreads();
   if (fo.att_out) {
     // normalised weights of my chunk (coverage / unknown replacement, S436-448):

@@ -32,7 +32,16 @@ int main() {
   CK(cudaMalloc(&xhl, 2 * 160 * 1024 * 2));
   unsigned long long* tr; CK(cudaMalloc(&tr, 8192 * 96)); CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
   XOut xo{nullptr, xhl, 160, 1024};
-  auto launch = [&]() { CK(launch_attention(htop, keys, KL, mem, dl, B, S, H, K, xo, nullptr, 148, StepCtl{nullptr, 0}, st)); };
+  // production configuration: folded W_out (values with ld 512, 16 top-layer tile shares)
+  const bool fold = !getenv("UATT_PLAIN");
+  float *wpart, *ht, *vals; __nv_bfloat16* xg;
+  CK(cudaMalloc(&wpart, (size_t)16 * 160 * H * 4)); CK(cudaMemset(wpart, 0, (size_t)16 * 160 * H * 4));
+  CK(cudaMalloc(&ht, 160 * H * 4)); CK(cudaMalloc(&xg, 2 * 160 * 512 * 2));
+  CK(cudaMalloc(&vals, (size_t)B * S * KL * 4)); CK(cudaMemset(vals, 0, (size_t)B * S * KL * 4));
+  AttFold fo{};
+  if (fold) { fo.wpart = wpart; fo.n_wt = 16; fo.rows_pad = 160; fo.htilde = ht; fo.xg = XOut{nullptr, xg, 160, 512}; }
+  auto launch = [&]() { CK(launch_attention(htop, keys, KL, fold ? vals : mem, fold ? KL : H, dl, B, S, H, K, xo, nullptr, 148,
+                                            StepCtl{nullptr, 0}, st, fo)); };
   cudaGraph_t g; cudaGraphExec_t ge;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   for (int i = 0; i < 50; ++i) launch();
