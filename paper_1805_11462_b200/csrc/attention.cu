@@ -14,6 +14,7 @@
 //   * parks (m_k, l_k, ctx_k) in its shared memory; after a cluster barrier CTA r combines
 //     column slice r over all nch chunks through distributed shared memory, in fixed chunk
 //     order (deterministic), and writes the context into the W_out operand (columns [0, H)).
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -415,38 +416,77 @@ static cudaError_t launch_att(dim3 grid, int nch, size_t smem, cudaStream_t st, 
   return cudaLaunchKernelEx(&cfg, fn, htop, keys, key_ld, mem, val_ld, lens, S_max, H, K, CH, SC, xo, done, ctl, fo);
 }
 
+struct AttPlan {
+  int nch, CH, SC;
+  size_t smem;
+};
+
+// Launch plan: the largest nch (<= att_nch) whose B clusters of nch CTAs are all co-resident
+// (cudaOccupancyMaxActiveClusters: clusters must fit inside a GPC, 1 CTA per SM at this shared
+// memory size) - a second wave of clusters would double the kernel time.
+template <int KMAX, int JPT>
+static AttPlan att_plan(int B, int S_max, int H, int K, int key_ld, int val_ld, bool same, int num_sms, AttFold& fo) {
+  auto fn = attention_cluster_kernel<KMAX, JPT>;
+  const char* forced = std::getenv("ONMT_ATT_NCH");
+  AttPlan p{};
+  for (int nch = att_nch(B, S_max, num_sms); nch >= 1; --nch) {
+    const int CH = (S_max + nch - 1) / nch;
+    const int kl = same ? val_ld : key_ld;
+    auto r4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
+    auto bytes = [&](int SC) {
+      return (r4((size_t)K * H) + 3 * 16 + 16 * kSCMax + 2 * (r4((size_t)SC * val_ld) + (same ? 0 : r4((size_t)SC * kl)))) * 4;
+    };
+    size_t extra = 0;                              // folded W_out: prefetched tile shares
+    if (fo.wpart) extra = (size_t)fo.n_wt * K * ((H / 4 + nch - 1) / nch) * 16;
+    const size_t esave = fo.att_out ? (size_t)K * CH * 4 : 0;   // attention output: raw scores
+    const int SC = bytes(16) + extra <= 200 * 1024 ? 16 : 8;
+    fo.pref = bytes(SC) + extra + esave <= 220 * 1024;
+    fo.hp_floats = fo.pref ? (int)(extra / 4) : 0;
+    p = AttPlan{nch, CH, SC, bytes(SC) + (fo.pref ? extra : 0) + esave};
+    if (forced || nch == 1) break;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess) break;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nch, B);
+    cfg.blockDim = dim3(kAttThreads);
+    cfg.dynamicSmemBytes = p.smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nch;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess) { cudaGetLastError(); break; }
+    if (std::getenv("ONMT_ATT_DEBUG"))
+      std::fprintf(stderr, "att_plan B=%d S=%d K=%d nch=%d smem=%zu -> %d co-resident clusters\n", B, S_max, K, nch,
+                   p.smem, ncl);
+    if (ncl >= B) break;
+  }
+  return p;
+}
+
 cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, const float* mem, int val_ld,
                              const int* lens, int B, int S_max, int H, int K, XOut xo, const int* done, int num_sms,
                              StepCtl ctl, cudaStream_t st, AttFold fo) {
   if (H > 4 * kAttThreads || K > kKMax) return cudaErrorInvalidValue;
-  const int nch = att_nch(B, S_max, num_sms);
-  const int CH = (S_max + nch - 1) / nch;
   const bool same = keys == mem;
-  const int kl = same ? val_ld : key_ld;
-  auto r4 = [](size_t n) { return (n + 3) & ~(size_t)3; };
-  auto bytes = [&](int SC) {
-    return (r4((size_t)K * H) + 3 * 16 + 16 * kSCMax + 2 * (r4((size_t)SC * val_ld) + (same ? 0 : r4((size_t)SC * kl)))) * 4;
-  };
-  size_t extra = 0;                                // folded W_out: prefetched tile shares
-  if (fo.wpart) extra = (size_t)fo.n_wt * K * ((H / 4 + nch - 1) / nch) * 16;
-  const size_t esave = fo.att_out ? (size_t)K * CH * 4 : 0;   // attention output: raw scores
-  const int SC = bytes(16) + extra <= 200 * 1024 ? 16 : 8;
-  fo.pref = bytes(SC) + extra + esave <= 220 * 1024;
-  fo.hp_floats = fo.pref ? (int)(extra / 4) : 0;
-  const size_t smem = bytes(SC) + (fo.pref ? extra : 0) + esave;
-  const dim3 grid(nch, B);
-#define ONMT_ATT(KM)                                                                                              \
-  return H <= 2 * kAttThreads                                                                                     \
-             ? launch_att<KM, 2>(grid, nch, smem, st, htop, keys, key_ld, mem, val_ld, lens, S_max, H, K, CH, SC, xo, \
-                                 done, ctl, fo)                                                                             \
-             : launch_att<KM, 4>(grid, nch, smem, st, htop, keys, key_ld, mem, val_ld, lens, S_max, H, K, CH, SC, xo, \
-                                 done, ctl, fo)
+#define ONMT_ATT_J(KM, J)                                                                                          \
+  {                                                                                                                \
+    const AttPlan p = att_plan<KM, J>(B, S_max, H, K, key_ld, val_ld, same, num_sms, fo);                         \
+    return launch_att<KM, J>(dim3(p.nch, B), p.nch, p.smem, st, htop, keys, key_ld, mem, val_ld, lens, S_max, H, K, \
+                             p.CH, p.SC, xo, done, ctl, fo);                                                       \
+  }
+#define ONMT_ATT(KM)                 \
+  if (H <= 2 * kAttThreads) ONMT_ATT_J(KM, 2) \
+  else ONMT_ATT_J(KM, 4)
   if (K <= 1) ONMT_ATT(1);
   if (K <= 2) ONMT_ATT(2);
   if (K <= 4) ONMT_ATT(4);
   if (K <= 8) ONMT_ATT(8);
   ONMT_ATT(16);
 #undef ONMT_ATT
+#undef ONMT_ATT_J
 }
 
 }  // namespace onmt

@@ -22,24 +22,26 @@ __global__ void calib(unsigned long long* out, float* sink) {
 int main() {
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  const int B = 30, S = 50, K = 5, H = 500, KL = 512;
+  auto envi = [](const char* n, int d) { const char* v = getenv(n); return v ? atoi(v) : d; };
+  const int B = envi("UATT_B", 30), S = envi("UATT_S", 50), K = envi("UATT_K", 5), H = envi("UATT_H", 500), KL = 512;
+  const int LO = envi("UATT_LO", 10), SPAN = envi("UATT_SPAN", 41);
   std::vector<int> lens(B);
-  for (int b = 0; b < B; ++b) lens[b] = 10 + (b * 37) % 41;
+  for (int b = 0; b < B; ++b) lens[b] = LO + (b * 37) % SPAN;
   int* dl; float *htop, *keys, *mem, *xf; __nv_bfloat16* xhl;
   CK(cudaMalloc(&dl, B * 4)); CK(cudaMemcpy(dl, lens.data(), B * 4, cudaMemcpyHostToDevice));
   CK(cudaMalloc(&htop, B * K * H * 4)); CK(cudaMalloc(&keys, (size_t)B * S * KL * 4)); CK(cudaMalloc(&mem, (size_t)B * S * H * 4));
   CK(cudaMemset(htop, 0, B * K * H * 4)); CK(cudaMemset(keys, 0, (size_t)B * S * KL * 4)); CK(cudaMemset(mem, 0, (size_t)B * S * H * 4));
-  CK(cudaMalloc(&xhl, 2 * 160 * 1024 * 2));
+  CK(cudaMalloc(&xhl, 2 * 256 * 1024 * 2));
   unsigned long long* tr; CK(cudaMalloc(&tr, 8192 * 96)); CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
-  XOut xo{nullptr, xhl, 160, 1024};
+  XOut xo{nullptr, xhl, 256, 1024};
   // production configuration: folded W_out (values with ld 512, 16 top-layer tile shares)
   const bool fold = !getenv("UATT_PLAIN");
   float *wpart, *ht, *vals; __nv_bfloat16* xg;
-  CK(cudaMalloc(&wpart, (size_t)16 * 160 * H * 4)); CK(cudaMemset(wpart, 0, (size_t)16 * 160 * H * 4));
-  CK(cudaMalloc(&ht, 160 * H * 4)); CK(cudaMalloc(&xg, 2 * 160 * 512 * 2));
+  CK(cudaMalloc(&wpart, (size_t)16 * 256 * H * 4)); CK(cudaMemset(wpart, 0, (size_t)16 * 256 * H * 4));
+  CK(cudaMalloc(&ht, 256 * H * 4)); CK(cudaMalloc(&xg, 2 * 256 * 512 * 2));
   CK(cudaMalloc(&vals, (size_t)B * S * KL * 4)); CK(cudaMemset(vals, 0, (size_t)B * S * KL * 4));
   AttFold fo{};
-  if (fold) { fo.wpart = wpart; fo.n_wt = 16; fo.rows_pad = 160; fo.htilde = ht; fo.xg = XOut{nullptr, xg, 160, 512}; }
+  if (fold) { fo.wpart = wpart; fo.n_wt = 16; fo.rows_pad = 256; fo.htilde = ht; fo.xg = XOut{nullptr, xg, 256, 512}; }
   auto launch = [&]() { CK(launch_attention(htop, keys, KL, fold ? vals : mem, fold ? KL : H, dl, B, S, H, K, xo, nullptr, 148,
                                             StepCtl{nullptr, 0}, st, fo)); };
   cudaGraph_t g; cudaGraphExec_t ge;
@@ -52,7 +54,8 @@ int main() {
   CK(cudaEventRecord(a, st)); CK(cudaGraphLaunch(ge, st)); CK(cudaEventRecord(b2, st)); CK(cudaStreamSynchronize(st));
   float ms; cudaEventElapsedTime(&ms, a, b2);
   CK(cudaMemset(tr, 0, 8192 * 96)); CK(cudaGraphLaunch(ge, st)); launch(); CK(cudaStreamSynchronize(st));
-  const char* en = getenv("ONMT_ATT_NCH"); const int nch = en ? atoi(en) : 4, grid = nch * B;
+  int nch = 148 / B; nch = nch > 8 ? 8 : nch; if (getenv("ONMT_ATT_NCH")) nch = atoi(getenv("ONMT_ATT_NCH"));
+  const int grid = nch * B;
   std::vector<unsigned long long> h(grid * 12);
   CK(cudaMemcpy(h.data(), tr, grid * 96, cudaMemcpyDeviceToHost));
   unsigned long long t0 = ~0ull; for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[c * 12]);
@@ -65,7 +68,7 @@ int main() {
     unsigned long long hh[2]; CK(cudaMemcpy(hh, o, 16, cudaMemcpyDeviceToHost));
     printf("calib: 100k dependent FMA: %.1f us, %llu cycles -> %.0f MHz\n", hh[0] / 1e3, hh[1], hh[1] / (hh[0] / 1e3));
   }
-  printf("attention c2: %.2f us/launch (graph of 50)\n", ms * 1000 / 50);
+  printf("attention B%d S%d K%d: %.2f us/launch (graph of 50)\n", B, S, K, ms * 1000 / 50);
   const char* nm[9] = {"entry", "prefetch issued", "pdl_wait", "sub0 staged", "scores", "parked", "cluster sync", "combined", "exit"};
   for (int i = 0; i < 9; ++i) printf("   %-16s avg %7.2f  max %7.2f us (n=%d)\n", nm[i], cnt[i] ? avg[i] / cnt[i] : 0, mx[i], cnt[i]);
   return 0;
