@@ -458,9 +458,84 @@ void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_p
 #undef ONMT_MERGE
 }
 
+// A11 with the sentence's history staged in shared memory: one CTA per sentence loads the
+// (token, parent, log p, attention argmax) entries of its K slots for every step (coalesced),
+// one thread per n-best rank walks the parent pointers on chip, then the CTA writes the
+// outputs in parallel.  The thread-per-sentence walk over global memory paid one dependent
+// L2 round trip per step (~144 us at max_len 100).
+__global__ void __launch_bounds__(256) finalize_smem_kernel(BeamState bs, int B, int K, int max_len, int* hyps,
+                                                            int* lens, float* scores, float* raw, float* tlogp,
+                                                            int* unk_pos) {
+  extern __shared__ int fz[];
+  const int nb = bs.nbest > 0 ? bs.nbest : 1;
+  const int b = blockIdx.x, R = B * K;
+  const int n_hist = max_len * K;
+  int* ptok = fz;
+  int* ppar = ptok + n_hist;
+  float* plp = reinterpret_cast<float*>(ppar + n_hist);
+  int* pam = reinterpret_cast<int*>(plp + n_hist);
+  int* path = pam + n_hist;                                      // [nb][max_len] slot per step
+  __shared__ int s_T;
+  if (threadIdx.x == 0) {
+    int T = 0;
+    for (int i = 0; i < nb; ++i) T = max(T, bs.best_t[b * nb + i]);
+    s_T = T;
+  }
+  __syncthreads();
+  const int T = s_T;
+  for (int i = threadIdx.x; i < T * K; i += blockDim.x) {
+    const int t = i / K, k = i % K;
+    const size_t h = (size_t)t * R + (size_t)b * K + k;
+    ptok[i] = bs.hist_token[h];
+    ppar[i] = bs.hist_parent[h];
+    plp[i] = bs.hist_logp[h];
+    pam[i] = bs.hist_amax ? bs.hist_amax[h] : -1;
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    const int o = b * nb + threadIdx.x;
+    const int Ti = bs.best_t[o];
+    int r = bs.best_r[o];
+    for (int t = Ti; t >= 1; --t) {
+      path[threadIdx.x * max_len + t - 1] = r;
+      r = ppar[(t - 1) * K + r];
+    }
+    lens[o] = Ti;
+    scores[o] = Ti ? (float)bs.best_norm[o] : -INFINITY;
+    if (raw) raw[o] = Ti ? (float)bs.best_raw[o] : -INFINITY;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb * max_len; i += blockDim.x) {
+    const int rank = i / max_len, t = i % max_len;
+    const int o = b * nb + rank;
+    const int Ti = bs.best_t[o];
+    const size_t oi = (size_t)o * max_len + t;
+    if (t < Ti) {
+      const int e = t * K + path[rank * max_len + t];
+      const int w = ptok[e];
+      hyps[oi] = w;
+      if (tlogp) tlogp[oi] = plp[e];
+      // S448: an <unk> emitted at step t is replaced by the source word at argmax_s a_{t,s}
+      if (unk_pos) unk_pos[oi] = (w == 1 && bs.hist_amax) ? pam[e] : -1;
+    } else {
+      hyps[oi] = 0;
+      if (tlogp) tlogp[oi] = 0.f;
+      if (unk_pos) unk_pos[oi] = -1;
+    }
+  }
+}
+
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
                      float* tlogp, int* unk_pos, cudaStream_t st) {
-  const int n = B * (bs.nbest > 0 ? bs.nbest : 1);
+  const int nb = bs.nbest > 0 ? bs.nbest : 1;
+  const size_t smem = ((size_t)4 * max_len * K + (size_t)nb * max_len) * 4;
+  if (smem <= 200 * 1024) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(finalize_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    finalize_smem_kernel<<<B, 256, smem, st>>>(bs, B, K, max_len, hyps, lens, scores, raw, tlogp, unk_pos);
+    return;
+  }
+  const int n = B * nb;
   finalize_kernel<<<(n + 127) / 128, 128, 0, st>>>(bs, B, K, max_len, hyps, lens, scores, raw, tlogp, unk_pos);
 }
 
