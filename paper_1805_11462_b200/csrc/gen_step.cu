@@ -2,12 +2,11 @@
 //
 //   phase A  generator + log-softmax statistics + per-CTA top-K (PAPER.md P118-119):
 //            z = W_gen h~ + b for every vocabulary id, logits never written to HBM.
-//   phase B  per hypothesis row: combine the CTA partials into log-sum-exp and row top-K.
-//   phase C  per sentence: beam selection / EOS banking / histories and the gather of the
-//            next step's decoder inputs (P136-139; beam_device.cuh).
+//   (option) the beam step of the decoder step (P136-139; beam_device.cuh), run by the
+//            last B CTAs to finish (phases == 4; off by default).
 //
-// Grid = groups x C CTAs, one per SM (grid <= #SMs), so software grid barriers between
-// the phases are safe.  Phase A is "K-outer": CTA (g, i) owns a contiguous run of nt
+// Grid = groups x C CTAs, one per SM (grid <= #SMs: all co-resident, which the optional
+// beam step's wait on the arrival counter relies on).  Phase A is "K-outer": CTA (g, i) owns a contiguous run of nt
 // vocabulary tiles (128 rows each) of N-group g and keeps all nt accumulators in TMEM
 // (nt * n_group <= 512 columns), so every activation K-block (hi/lo planes, the MMA B
 // operand) crosses L2 -> SM once per CTA instead of once per tile.
@@ -41,7 +40,7 @@ struct GenStepArgs {
   float* row_lse;                               // [R]
   float* row_z;                                 // [R][K]
   int* row_i;
-  int phases;                                   // 1 = A, 2 = A + B, 3 = A + B + C
+  int phases;                                   // 1 = phase A, 4 = phase A + the fused beam step
   int t, max_len;
   double lp;
   BeamState bs;
@@ -63,12 +62,6 @@ __device__ __forceinline__ float gs_ex2(float x) {
 }
 __device__ __forceinline__ void gs_named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// all CTAs of the grid (co-resident by construction) meet
-__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) cta_group_barrier(bar, gridDim.x);
-  __syncthreads();
-}
 
 // order-preserving float <-> uint keys (atomicMax on the key = max on the float)
 __device__ __forceinline__ unsigned int f2key(float f) {
@@ -450,100 +443,6 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
                              reinterpret_cast<float*>(smem), a.gbuf_floats);
     return;
   }
-  if (a.phases < 2) return;
-
-  // ================================================================ phase B
-  // CTA i reduces rows i, i + G, ...: its warps split the C partials of the row (one
-  // partial per lane, all loads in flight), then warp and CTA merges in fixed order.
-  grid_barrier(a.gbar);
-  KT(4);
-  {
-    __shared__ float sb_m[16], sb_s[16];
-    __shared__ float sb_z[16][kKMax];
-    __shared__ int sb_i[16][kKMax];
-    const int nw = blockDim.x >> 5;
-    const int per_w = (a.C + nw - 1) / nw;                          // partials per warp (<= 32)
-    for (int r = blockIdx.x; r < a.R; r += gridDim.x) {
-      const int p = warp * per_w + lane;
-      const bool ok = lane < per_w && p < a.C;
-      float2 v = ok ? __ldcg(&a.ms[(size_t)r * a.C + p]) : make_float2(-INFINITY, 0.f);
-      float lz[KMAX];
-      int li[KMAX];
-      const size_t base = ((size_t)r * a.C + p) * a.K;
-#pragma unroll
-      for (int k = 0; k < KMAX; ++k) {
-        const bool ck = ok && k < a.K;
-        lz[k] = ck ? __ldcg(&a.tz[base + k]) : -INFINITY;
-        li[k] = ck ? __ldcg(&a.ti[base + k]) : 0x7fffffff;
-      }
-      float m = v.x, sm = v.x == -INFINITY ? 0.f : v.y;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sm, o);
-        const float M = fmaxf(m, m2);
-        sm = (m == -INFINITY ? 0.f : sm * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
-        m = M;
-      }
-      // warp top-K: K rounds of arg-max over the lanes' sorted lists (heads at index 0)
-      for (int k = 0; k < a.K; ++k) {
-        float bz = lz[0];
-        int bi = li[0];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float z2 = __shfl_xor_sync(0xffffffffu, bz, o);
-          const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (better(z2, i2, bz, bi)) { bz = z2; bi = i2; }
-        }
-        if (lane == 0) { sb_z[warp][k] = bz; sb_i[warp][k] = bi; }
-        if (li[0] == bi && lz[0] == bz) {
-#pragma unroll
-          for (int i = 0; i < KMAX - 1; ++i) { lz[i] = lz[i + 1]; li[i] = li[i + 1]; }
-          lz[KMAX - 1] = -INFINITY;
-          li[KMAX - 1] = 0x7fffffff;
-        }
-      }
-      if (lane == 0) { sb_m[warp] = m; sb_s[warp] = sm; }
-      __syncthreads();
-      if (warp == 0) {                                              // CTA merge of the nw warp results
-        float M = lane < nw ? sb_m[lane] : -INFINITY;
-        float S = lane < nw ? sb_s[lane] : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float m2 = __shfl_xor_sync(0xffffffffu, M, o), s2 = __shfl_xor_sync(0xffffffffu, S, o);
-          const float Mx = fmaxf(M, m2);
-          S = (M == -INFINITY ? 0.f : S * __expf(M - Mx)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - Mx));
-          M = Mx;
-        }
-        if (lane == 0) a.row_lse[r] = M + logf(S);
-        int h = 0;                                                  // lane w walks warp w's sorted list
-        for (int k = 0; k < a.K; ++k) {
-          float bz = (lane < nw && h < a.K) ? sb_z[lane][h] : -INFINITY;
-          int bi = (lane < nw && h < a.K) ? sb_i[lane][h] : 0x7fffffff;
-          const float mz = bz;
-          const int mi = bi;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const float z2 = __shfl_xor_sync(0xffffffffu, bz, o);
-            const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (better(z2, i2, bz, bi)) { bz = z2; bi = i2; }
-          }
-          if (lane == 0) { a.row_z[(size_t)r * a.K + k] = bz; a.row_i[(size_t)r * a.K + k] = bi; }
-          if (mz == bz && mi == bi && lane < nw) ++h;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  if (a.phases < 3) return;
-
-  // ================================================================ phase C
-  grid_barrier(a.gbar);
-  KT(5);
-  for (int r = blockIdx.x; r < a.R; r += gridDim.x) {
-    select_gather_row<KMAX>(r, 0, 1, a.R, a.row_lse, a.row_z, a.row_i, a.K, a.t, a.max_len, a.lp, a.bs, a.ga);
-    __syncthreads();
-  }
-  KTX(11, threadIdx.x == 0);
 }
 
 static size_t gs_smem_bytes(int n_group, int nt_max, int stages) {
@@ -566,8 +465,7 @@ static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, GsPlan& p) {
   if (p.nt_max < 1) return false;
   p.P = 2 * n_group <= 32 * kGsScanWarps ? 2 : 1;
   if (n_group > 32 * kGsScanWarps) return false;
-  const size_t limit = 227 * 1024 - 12288;        // (static shared memory of phases B / C and the fused
-                                                  //  beam step: <= 11 KB)
+  const size_t limit = 227 * 1024 - 12288;        // (static shared memory incl. the fused beam step: <= 11 KB)
   p.stages = 4;
   while (p.stages > 2 && gs_smem_bytes(n_group, p.nt_max, p.stages) > limit) --p.stages;
   while (p.nt_max > 1 && gs_smem_bytes(n_group, p.nt_max, p.stages) > limit) --p.nt_max;
@@ -590,7 +488,7 @@ static cudaError_t launch_gs(const CUtensorMap& tmW, const CUtensorMap& tmX, con
   return launch_pdl(fn, dim3(grid), dim3(kGsThreads), smem, st, tmW, tmX, a);
 }
 
-// phases: 1 = generator partials, 2 = + row LSE / top-K, 3 = + beam step and gather
+// phases: 1 = generator partials, 4 = + the beam step by the last-arriving CTAs
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i,
                      int phases, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
