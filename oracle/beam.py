@@ -65,8 +65,21 @@ def _select(cum: np.ndarray, live: np.ndarray, logp: np.ndarray, K: int, M: int)
     return [(float(ss[i]), int(kk[i]), int(ww[i])) for i in order[:need]]
 
 
+def _step_log_probs(model: OracleModel, y, htilde, states, memory, src_ext):
+    """One decoder step for the hypotheses of one sentence: (log p over the vocabulary -
+    extended by the sentence's source-only ids for a copy model, S293-297 -, attention,
+    h~, states).  A copy model reads an emitted extended id >= V back as <unk> (R32)."""
+    y_in = np.where(np.asarray(y) < model.V, y, UNK)
+    logp, a, ht, st = model.decode_step(y_in, htilde, states, memory)
+    if model.copy:
+        v_ext = max(model.V, max(src_ext) + 1)
+        logp = model.extended_log_probs(logp, a, model.copy_gate(ht), src_ext, v_ext)
+    return logp, a, ht, st
+
+
 def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha: float = 0.0,
-                stop: str = "rank0", trace: bool = False, beta: float = 0.0, n_best: int = 1) -> Dict:
+                stop: str = "rank0", trace: bool = False, beta: float = 0.0, n_best: int = 1,
+                src_ext: Optional[List[int]] = None) -> Dict:
     """O7-O11 for one sentence.
 
     beta > 0: banked entries are scored by final_score (raw / lp + cp, S436-439); the
@@ -86,6 +99,8 @@ def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha:
         raise ValueError("beam and max_len must be >= 1")
     if not 1 <= n_best <= K:
         raise ValueError("1 <= n_best <= beam (S423)")
+    if model.copy and (src_ext is None or len(src_ext) != len(src)):
+        raise ValueError("a copy model needs src_ext: one extended id per source position (S293)")
     memory, finals = model.encode(src)
     y0, ht0, st0 = model.init_decoder(finals, 1)
     H = model.H
@@ -107,9 +122,9 @@ def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha:
     steps = []
     for t in range(1, max_len + 1):
         ks = np.nonzero(live)[0]
-        logp_l, att_l, ht_l, st_l = model.decode_step(
-            y[ks], htilde[ks], [(h[ks], c[ks]) for (h, c) in states], memory)
-        logp = np.full((K, model.V), -np.inf)
+        logp_l, att_l, ht_l, st_l = _step_log_probs(
+            model, y[ks], htilde[ks], [(h[ks], c[ks]) for (h, c) in states], memory, src_ext)
+        logp = np.full((K, logp_l.shape[1]), -np.inf)
         logp[ks] = logp_l
         cand = _select(cum, live, logp, K, TRACE_MARGIN)
         n_sel = min(K, int(live.sum()) * model.V)
@@ -174,13 +189,13 @@ def beam_search(model: OracleModel, src: List[int], K: int, max_len: int, alpha:
     return out
 
 
-def greedy(model: OracleModel, src: List[int], max_len: int) -> Dict:
+def greedy(model: OracleModel, src: List[int], max_len: int, src_ext: Optional[List[int]] = None) -> Dict:
     """O12: argmax with the lowest id on ties; stop at EOS or max_len."""
     memory, finals = model.encode(src)
     y, ht, st = model.init_decoder(finals, 1)
     toks, lps = [], []
     for t in range(1, max_len + 1):
-        logp, _, ht, st = model.decode_step(y, ht, st, memory)
+        logp, _, ht, st = _step_log_probs(model, y, ht, st, memory, src_ext)
         w = int(np.argmax(logp[0]))          # np.argmax returns the first maximum
         toks.append(w); lps.append(float(logp[0, w]))
         y = np.array([w])
@@ -189,14 +204,15 @@ def greedy(model: OracleModel, src: List[int], max_len: int) -> Dict:
     return {"tokens": toks, "raw": float(np.sum(lps)), "token_logp": lps}
 
 
-def score_sequence(model: OracleModel, src: List[int], Y: List[int], with_attn: bool = False):
+def score_sequence(model: OracleModel, src: List[int], Y: List[int], with_attn: bool = False,
+                   src_ext: Optional[List[int]] = None):
     """Teacher-forced log p(y_t | y_<t, x) of every token of Y (P105-108); with_attn:
     also the attention rows a_t [|Y| x S] of those steps."""
     memory, finals = model.encode(src)
     y, ht, st = model.init_decoder(finals, 1)
     out, att = [], []
     for w in Y:
-        logp, a, ht, st = model.decode_step(y, ht, st, memory)
+        logp, a, ht, st = _step_log_probs(model, y, ht, st, memory, src_ext)
         out.append(float(logp[0, w]))
         att.append(a[0])
         y = np.array([w])
@@ -204,19 +220,19 @@ def score_sequence(model: OracleModel, src: List[int], Y: List[int], with_attn: 
 
 
 def brute_force(model: OracleModel, src: List[int], max_len: int, alpha: float = 0.0,
-                beta: float = 0.0) -> List[Dict]:
+                beta: float = 0.0, src_ext: Optional[List[int]] = None) -> List[Dict]:
     """O12: enumerate Y = {sequences ending at their first EOS, length <= max_len}
     U {EOS-free sequences of length exactly max_len}; score each by teacher
     forcing (final_score: raw / lp + cp).  Returns all of them sorted by (norm desc,
     then token tuple)."""
-    V = model.V
+    V = max(model.V, max(src_ext) + 1) if model.copy else model.V
     out = []
     for n in range(1, max_len + 1):
         for prefix in itertools.product([w for w in range(V) if w != EOS], repeat=n - 1):
             tails = [EOS] if n < max_len else list(range(V))
             for last in tails:
                 Y = list(prefix) + [last]
-                lp, att = score_sequence(model, src, Y, with_attn=True)
+                lp, att = score_sequence(model, src, Y, with_attn=True, src_ext=src_ext)
                 raw = float(np.sum(lp))
                 out.append({"tokens": Y, "raw": raw, "norm": final_score(raw, n, att.sum(0), alpha, beta),
                             "token_logp": lp})

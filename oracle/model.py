@@ -66,6 +66,7 @@ class OracleModel:
         self.Hd = t["enc.l0.fwd.w_hh"].shape[1]
         self.general = "attn.w_in" in t
         self.V = t["gen.w"].shape[0]
+        self.copy = "copy.w" in t            # copy / pointer generator (SPEC S293-301)
         self.dirs = ["fwd", "bwd"] if self.bidir else ["fwd"]
         assert self.Hd * len(self.dirs) == self.H, "AMB-5: [fwd;bwd] must equal the decoder width"
 
@@ -153,6 +154,26 @@ class OracleModel:
         htilde = np.tanh(np.concatenate([ctx, h_top], axis=1) @ self.t["attn.w_out"].T)
         z = htilde @ self.t["gen.w"].T + self.t["gen.b"]
         return log_softmax(z), a, htilde, new_states
+
+    # ------------------------------------------------------------- copy model
+    def copy_gate(self, htilde: np.ndarray) -> np.ndarray:
+        """g = sigmoid(w_copy . h~ + b_copy) per hypothesis: the generator's share of the
+        extended distribution (SPEC S293-297 "copy_gate"; reading DESIGN.md §3 R31)."""
+        return sigmoid(htilde @ self.t["copy.w"][0] + self.t["copy.b"][0])
+
+    @staticmethod
+    def extended_log_probs(logp: np.ndarray, a: np.ndarray, g: np.ndarray, src_ext: List[int],
+                           v_ext: int) -> np.ndarray:
+        """S296: p(w) = g p_vocab(w) + (1 - g) sum_{s: src_s = w} a_s over the extended
+        vocabulary (target vocabulary, then this sentence's source-only ids).
+        logp [n x V] generator log-probs, a [n x S] attention, g [n], src_ext [S] ids."""
+        n, V = logp.shape
+        p = np.zeros((n, v_ext))
+        p[:, :V] = g[:, None] * np.exp(logp)
+        for s, w in enumerate(src_ext):                 # scatter-add of the copy attention
+            p[:, w] += (1.0 - g) * a[:, s]
+        with np.errstate(divide="ignore"):
+            return np.log(p)
 
     def init_decoder(self, finals, n: int):
         """O3: decoder layer l starts from the encoder layer-l final state,

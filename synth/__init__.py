@@ -37,6 +37,7 @@ class ModelConfig:
     v_tgt: int
     bidir: bool          # encoder bidirectional (per-direction width hidden/2)
     attn_general: bool   # 'general' (W_in present) vs 'dot'
+    copy: bool = False   # copy / pointer generator: copy.w [1,H], copy.b [1]
 
     @property
     def h_dir(self) -> int:
@@ -110,6 +111,8 @@ def tensor_specs(cfg: ModelConfig) -> List[Tuple[str, Tuple[int, ...]]]:
     if cfg.attn_general:
         specs.append(("attn.w_in", (H, H)))
     specs += [("attn.w_out", (H, 2 * H)), ("gen.w", (cfg.v_tgt, H)), ("gen.b", (cfg.v_tgt,))]
+    if cfg.copy:
+        specs += [("copy.w", (1, H)), ("copy.b", (1,))]
     return specs
 
 
@@ -195,3 +198,26 @@ def random_model_tensors(cfg: ModelConfig, seed: int, scale: float = 0.1) -> Dic
     """Toy models for tests: U(-scale, scale) in canonical order."""
     rng = np.random.Generator(np.random.PCG64(seed))
     return {n: rng.uniform(-scale, scale, size=s).astype(np.float32) for n, s in tensor_specs(cfg)}
+
+
+def make_src_ext(ids: np.ndarray, lens: np.ndarray, v_tgt: int, seed: int = 5, p_shared: float = 0.7) -> np.ndarray:
+    """Dynamic-dictionary input of the copy model (SPEC S293 "src_map: source-position ->
+    extended-vocab-id"), as synthetic DATA: a seeded table decides which source ids have a
+    target-vocabulary counterpart (the same id, when < v_tgt, with probability p_shared);
+    every other distinct source id of a sentence gets the next extended id v_tgt, v_tgt+1, ...
+    in order of first appearance.  Pads are 0."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    vmax = int(ids.max()) + 1 if ids.size else 1
+    shared = rng.uniform(0, 1, vmax) < p_shared
+    out = np.zeros_like(ids, dtype=np.int32)
+    for b in range(len(lens)):
+        extra: Dict[int, int] = {}
+        for s in range(int(lens[b])):
+            x = int(ids[b, s])
+            if x < v_tgt and shared[x]:
+                out[b, s] = x
+            else:
+                if x not in extra:
+                    extra[x] = v_tgt + len(extra)
+                out[b, s] = extra[x]
+    return out
