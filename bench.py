@@ -432,6 +432,60 @@ def run_translate_ex(args):
     model.close()
 
 
+def run_copy(args):
+    """Copy / pointer generator on the workload's batch through
+    onmt_translate_copy (host buffers, so value == e2e): the workload's model plus the copy
+    gate (copy.w, copy.b; seeded like every weight), the synthetic dynamic dictionary of
+    synth.make_src_ext.  The plain model's host call is timed beside it."""
+    import dataclasses
+    import torch
+    import paper_1805_11462_b200 as ob
+    w = synth.WORKLOADS[args.workload]
+    K, ML, alpha = w.decode.beam, w.decode.max_len, w.decode.alpha
+    cache = os.environ.get("ONMT_WEIGHT_CACHE", os.path.join(tempfile.gettempdir(), "onmt_weights"))
+    os.makedirs(cache, exist_ok=True)
+    cfg = dataclasses.replace(w.model, copy=True)
+    path = os.path.join(cache, f"{args.workload}_copy_s{w.weight_seed}.mnmt")
+    if not os.path.exists(path):
+        synth.write_mnmt(path, synth.make_weights(cfg, w.weight_seed))
+    model = ob.Model(path, 0, w.decode.precision)
+    ids, lens = synth.make_corpus(args.workload)
+    S = int(lens.max())
+    ids = np.ascontiguousarray(ids[:, :S])
+    ext = synth.make_src_ext(ids, lens, cfg.v_tgt)
+    for _ in range(args.warmup):
+        r = model.translate_copy(ids, lens, ext, K, ML, alpha)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    toks = 0
+    for _ in range(args.steps):
+        r = model.translate_copy(ids, lens, ext, K, ML, alpha)
+        toks += int(r["lens"].sum())
+    v = toks / (time.perf_counter() - t0)
+    model.close()
+    plain = ob.Model(synth.weights_file(args.workload, cache), 0, w.decode.precision)
+    for _ in range(args.warmup):
+        plain.translate(ids, lens, K, ML, alpha)
+    t0 = time.perf_counter()
+    pt = 0
+    for _ in range(args.steps):
+        pt += int(plain.translate(ids, lens, K, ML, alpha)["lens"].sum())
+    vp = pt / (time.perf_counter() - t0)
+    plain.close()
+    B = len(lens)
+    line = {"metric": "target tokens/sec, beam translate of a copy / pointer-generator model over the extended "
+                      "vocabulary (SURVEY §8(f) rank 3)",
+            "value": round(v, 1), "unit": "target tok/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": w.decode.precision.replace("fp", "f"),
+            "data": "synthetic (DESIGN.md §3; dynamic dictionary synth.make_src_ext)",
+            "config": {"workload": args.workload, "task": "copy", "batch": B, "beam": K, "max_len": ML},
+            "e2e": {"value": round(v, 1), "unit": "target tok/s", "h2d_bytes_per_step": int(2 * ids.nbytes + lens.nbytes),
+                    "d2h_bytes_per_step": int(B * (ML * 8 + 12))},
+            "same_workload_plain_model": {"value": round(vp, 1), "note": "onmt_translate of the model without the copy gate"},
+            "copied_source_only_tokens": int((r["hyps"] >= cfg.v_tgt).sum())}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -441,7 +495,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-sentences", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--task", default="translate", choices=["translate", "score", "translate_ex"])
+    ap.add_argument("--task", default="translate", choices=["translate", "score", "translate_ex", "copy"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -451,6 +505,8 @@ def main():
         run_score(args)
     elif args.task == "translate_ex":
         run_translate_ex(args)
+    elif args.task == "copy":
+        run_copy(args)
     else:
         run_ours(args)
 

@@ -152,6 +152,27 @@ ONMT_API onmt_status onmt_translate_ex(onmt_model* m, const int32_t* src_ids, co
                               float* out_token_logp, int32_t* out_unk_pos);
 
 /*
+ * onmt_translate_copy - beam search of a COPY / POINTER-GENERATOR model (weights copy.w
+ * [1,H], copy.b [1]; PAPER.md P302-304, P316-317; SPEC S293-301) over
+ * the extended vocabulary: p(w) = g p_vocab(w) + (1 - g) sum_{s: src_ext[s] = w} a_s with
+ * g = sigmoid(copy.w . h~ + copy.b) and a the step's attention weights.
+ *   src_ext [B*S_max] host int32: the dynamic dictionary - for every real source position
+ *   its extended id, < V_tgt for a word of the target vocabulary, V_tgt + k for the k-th
+ *   source-only word of the sentence (ids of padded positions are ignored).
+ *   Output hyps may hold extended ids >= V_tgt (copied source-only words; the caller maps
+ *   them back through its dictionary); such a token is fed to the next step as <unk>.
+ *   opts: beam, max_len, length_penalty as onmt_translate; n_best must be 1, coverage 0,
+ *   replace_unk 0.  Outputs as onmt_translate.
+ * Errors: as onmt_translate, plus UNSUPPORTED for a model without copy.* tensors or other
+ * options, ID_RANGE for an extended id outside [0, V_tgt + S_max), INVALID_ARG for a null
+ * src_ext.  onmt_translate on a copy model is INVALID_ARG (it needs src_ext).
+ */
+ONMT_API onmt_status onmt_translate_copy(onmt_model* m, const int32_t* src_ids, const int32_t* src_lens,
+                                const int32_t* src_ext, int32_t B, int32_t S_max,
+                                const onmt_decode_opts* opts, int32_t* out_hyps, int32_t* out_lens,
+                                float* out_scores, float* out_raw_scores, float* out_token_logp);
+
+/*
  * onmt_translate_trace - onmt_translate plus the per-step beam selections, for the
  * parity protocol: for step t (0-based), sentence b, rank r:
  *   sel_parent [max_len*B*beam]: parent slot k, or -1 if nothing was selected;

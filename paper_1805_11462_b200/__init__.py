@@ -25,7 +25,7 @@ K_MAX = 16
 EXPORTS = ["onmt_load_weights", "onmt_model_get_info", "onmt_set_stream", "onmt_encode", "onmt_translate",
            "onmt_translate_trace", "onmt_translate_dev", "onmt_set_option", "onmt_get_kernel_time",
            "onmt_kernel_launches", "onmt_free", "onmt_last_error", "onmt_test_gemm", "onmt_test_gen", "onmt_score",
-           "onmt_translate_ex"]
+           "onmt_translate_ex", "onmt_translate_copy"]
 
 
 class OnmtError(RuntimeError):
@@ -75,6 +75,7 @@ def lib():
     L.onmt_test_gen.argtypes = [VP, VP, I32, I32, VP, VP, VP]
     L.onmt_score.argtypes = [VP, VP, VP, I32, I32, VP, VP, I32, VP, VP]
     L.onmt_translate_ex.argtypes = [VP, VP, VP, I32, I32, P(_DecodeOpts), VP, VP, VP, VP, VP, VP]
+    L.onmt_translate_copy.argtypes = [VP, VP, VP, VP, I32, I32, P(_DecodeOpts), VP, VP, VP, VP, VP]
     for n in EXPORTS:
         if n not in ("onmt_free", "onmt_last_error"):
             getattr(L, n).restype = ctypes.c_int
@@ -173,6 +174,22 @@ class Model:
         if unk is not None:
             out["unk_pos"] = unk
         return out
+
+    def translate_copy(self, ids, lens, src_ext, beam: int, max_len: int,
+                       length_penalty: float = 0.0) -> Dict[str, np.ndarray]:
+        """onmt_translate_copy (copy / pointer-generator models): hyps over extended ids."""
+        ids, lens, src_ext = _i32(ids), _i32(lens), _i32(src_ext)
+        B = len(lens)
+        S = ids.shape[1] if ids.ndim == 2 and B > 0 else 1
+        hyps = np.zeros((B, max_len), np.int32)
+        olens = np.zeros(B, np.int32)
+        scores = np.zeros(B, np.float32)
+        raw = np.zeros(B, np.float32)
+        tlogp = np.zeros((B, max_len), np.float32)
+        o = _DecodeOpts(beam, max_len, float(length_penalty), 0.0, 1, 0)
+        _check(lib().onmt_translate_copy(self._h, _ptr(ids), _ptr(lens), _ptr(src_ext), B, S, ctypes.byref(o), _ptr(hyps),
+                                         _ptr(olens), _ptr(scores), _ptr(raw), _ptr(tlogp)))
+        return {"hyps": hyps, "lens": olens, "scores": scores, "raw": raw, "token_logp": tlogp}
 
     def translate(self, ids, lens, beam: int, max_len: int, length_penalty: float = 0.0,
                   trace: bool = False) -> Dict[str, np.ndarray]:

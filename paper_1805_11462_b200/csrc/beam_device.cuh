@@ -108,7 +108,7 @@ __device__ __forceinline__ void select_gather_row(int r, int slice, int nslice, 
   const int E = ga.E, H = ga.H, L = ga.L;
   const int e0 = (E * slice) / nslice, e1 = (E * (slice + 1)) / nslice;
   const int h0 = (H * slice) / nslice, h1 = (H * (slice + 1)) / nslice;
-  const float* __restrict__ emb = ga.emb_tgt + (size_t)y * E;
+  const float* __restrict__ emb = ga.emb_tgt + (size_t)feed_id(ga, y) * E;
   for (int c0 = e0 + threadIdx.x; c0 < e1; c0 += 2 * blockDim.x) {
     const int c1 = c0 + blockDim.x;
     const float v0 = __ldg(&emb[c0]);
@@ -323,7 +323,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     } else if (c < K * nst + K * K) {
       const int i = c - K * nst, k = i / K, j = i % K;
       if (s_live[k] && s_z[k][j] != -INFINITY)
-        bulk_g2s(gbuf + (size_t)i * emb_f, ga.emb_tgt + (size_t)s_id[k][j] * E, E * 4, &s_bar);
+        bulk_g2s(gbuf + (size_t)i * emb_f, ga.emb_tgt + (size_t)feed_id(ga, s_id[k][j]) * E, E * 4, &s_bar);
     }
   }
   KT(3);
@@ -523,7 +523,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
           if (!s_go[kr]) continue;
           const int p = s_prow[kr];
           float* d = gbuf + (size_t)(kr - k0) * slot_f;
-          bulk_g2s(d, ga.emb_tgt + (size_t)s_y[kr] * E, E * 4, &s_bar);
+          bulk_g2s(d, ga.emb_tgt + (size_t)feed_id(ga, s_y[kr]) * E, E * 4, &s_bar);
           bulk_g2s(d + E, ga.htilde + (size_t)p * H, H * 4, &s_bar);
           for (int l = 0; l < L; ++l) {
             bulk_g2s(d + E + H + 2 * l * H, ga.h + ((size_t)l * ga.rows_pad + p) * H, H * 4, &s_bar);
@@ -565,7 +565,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
         const int r = b * K + kr;
         const int p = s_prow[kr];
         float v;
-        if (col < E) v = __ldg(&ga.emb_tgt[(size_t)s_y[kr] * E + col]);
+        if (col < E) v = __ldg(&ga.emb_tgt[(size_t)feed_id(ga, s_y[kr]) * E + col]);
         else if (col < E + H) v = __ldcg(&ga.htilde[(size_t)p * H + col - E]);
         else {
           const int x = col - E - H, l = x / (2 * H), j = x % (2 * H);

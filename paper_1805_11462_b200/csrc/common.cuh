@@ -222,7 +222,10 @@ struct GatherArgs {
   float* cg;           // [L][rows_pad][H]
   int rows_pad;
   XOut x[8];           // x[0] = layer-0 operand; x[l] = layer-l operand
+  int v_map;           // copy models: an emitted extended id >= v_map is fed back as <unk> (0: off)
 };
+// the embedding row fed back for an emitted (possibly extended) id
+__device__ __forceinline__ int feed_id(const GatherArgs& ga, int y) { return (ga.v_map && y >= ga.v_map) ? 1 : y; }
 
 
 // Software barrier among n co-resident CTAs (thread 0 of each calls it).  One 32-bit word:

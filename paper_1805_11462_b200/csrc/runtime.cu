@@ -76,6 +76,30 @@ struct EncRecArgs {
   unsigned long long* trace;
 };
 int enc_rec_splits(int kb, int N, int D, int T, int num_sms);
+struct CopyArgs {
+  const float* htilde;
+  int H;
+  const float* copy_w;
+  float copy_b;
+  const float* att;
+  int S_max;
+  const int* src_ext;
+  const int* lens;
+  const void* gen_w;
+  int gen_ld, gen_bf16;
+  const float* gen_b;
+  int V, K;
+  const int* live;
+  float* row_lse;
+  float* row_z;
+  int* row_i;
+  StepCtl ctl;
+};
+cudaError_t launch_copy_rows(const CopyArgs& a, int R, cudaStream_t st);
+void launch_row_topk(const float2* ms, const float* tz, const int* ti, int n_parts, int ps, int rs, int B, int K, int t,
+                     const BeamState& bs, float* row_lse, float* row_z, int* row_i, StepCtl ctl, cudaStream_t st);
+void launch_select_gather(int B, int K, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
+                          const float* row_lse, const float* row_z, const int* row_i, StepCtl ctl, cudaStream_t st);
 cudaError_t launch_enc_rec(const CUtensorMap* tmW, const CUtensorMap* tmX0, const CUtensorMap* tmX1,
                            const EncRecArgs& a, int D, cudaStream_t st);
 cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
@@ -337,6 +361,9 @@ struct onmt_model {
   Mat attn_win, attn_win_t, attn_wout, gen_w;
   DevBuf gen_b;
   Mat attn_woc;                              // W_out[:, :H] (value projection, folded W_out)
+  bool copy = false;                         // copy / pointer generator (copy.w, copy.b present)
+  DevBuf copy_w;                             // [H] fp32 (bf16-rounded in bf16 mode)
+  float copy_b = 0.f;
   DevBuf woh_t;                              // W_out[:, H:2H]^T bf16 [top-layer tiles * 32][fold_ld(H)]
 
   // encoder workspace
@@ -360,6 +387,7 @@ struct onmt_model {
   DevBuf b_cum, b_live, b_y, b_prow, b_done, b_ndone, b_bt, b_br, b_braw, b_bnorm;
   DevBuf h_par, h_tok, h_lp, s_score, s_par;
   DevBuf b_att, b_catt, h_amax;              // coverage / unknown replacement state
+  DevBuf d_ext;                              // copy models: the call's extended source ids [B][S_max]
   DevBuf o_hyps, o_lens, o_scores, o_raw, o_tlogp, o_unk;
 
   std::map<std::string, EventPairs> evs;   // per kernel family ("gen", "step", "encode", ...)
@@ -648,6 +676,19 @@ static void load_model(onmt_model* m, const char* path) {
   m->gen_w.upload(plain_pad(gw), (int)Vt, (int)H, bf);
   const auto& gb = get(t, "gen.b", {Vt}, seen);
   upload_f32(m->gen_b, gb.v);
+  if (t.count("copy.w")) {                          // copy / pointer generator (SPEC S293-301)
+    const auto& cw = get(t, "copy.w", {1, H}, seen);
+    const auto& cb = get(t, "copy.b", {1}, seen);
+    std::vector<float> w = cw.v;
+    float bv = cb.v[0];
+    if (bf) {                                       // (every tensor of a bf16 model is bf16-rounded)
+      for (auto& x : w) x = __bfloat162float(__float2bfloat16_rn(x));
+      bv = __bfloat162float(__float2bfloat16_rn(bv));
+    }
+    upload_f32(m->copy_w, w);
+    m->copy_b = bv;
+    m->copy = true;
+  }
   if (seen.size() != t.size()) throw Error{ONMT_E_FORMAT, "unexpected extra tensors in file"};
   ONMT_CUDA(cudaDeviceSynchronize());
 }
@@ -801,7 +842,8 @@ struct DecodeOpts {
   double beta = 0.0;
   int nbest = 1;
   bool unk = false;
-  bool att() const { return beta != 0.0 || unk; }
+  const int* src_ext = nullptr;   // copy models: device [B][S_max] extended source ids
+  bool att() const { return beta != 0.0 || unk || src_ext; }
 };
 
 static BeamState beam_state(onmt_model* m, bool trace, const DecodeOpts& op = DecodeOpts{}, const int* d_lens = nullptr,
@@ -1073,7 +1115,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
   const int rp = m->xg.rows_pad;
   const int n_vt = gen_parts(m, m->xg);
   BeamState bs = beam_state(m, trace, op, d_lens, S_max);
-  if (op.att() && n_vt > 256)
+  if ((op.beta != 0.0 || op.unk) && n_vt > 256)
     throw Error{ONMT_E_UNSUPPORTED, "coverage / unk replacement need the one-CTA-per-sentence beam step (<= 256 generator partials)"};
   float* hh = m->st_h.as<float>();
   float* cc = m->st_c.as<float>();
@@ -1088,6 +1130,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
   ga.htilde = m->htilde.as<float>();
   ga.h = hh; ga.c = cc; ga.cg = cg; ga.rows_pad = rp;
   for (int l = 0; l < L; ++l) ga.x[l] = m->xdec[l]->xo(bf);
+  ga.v_map = op.src_ext ? m->Vt : 0;
   launch_gather(bs, ga, R, K, StepCtl{nullptr, 0}, m->stream);
   count(m);
   GenOut g;
@@ -1099,6 +1142,35 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
   g.K = K;
   g.rows_valid = R;
   g.rows_pad = rp;
+  // copy models: generator row top-K -> extended top-K (copy.cu) -> selection + gather
+  auto merge_copy = [&](int n_parts, int ps, int rs, int t, double lp) {
+    launch_row_topk(g.ms, g.tz, g.ti, n_parts, ps, rs, B, K, t, bs, m->row_lse.as<float>(), m->row_z.as<float>(),
+                    m->row_i.as<int>(), ctl, m->stream);
+    CopyArgs ca{};
+    ca.htilde = m->htilde.as<float>();
+    ca.H = H;
+    ca.copy_w = m->copy_w.as<float>();
+    ca.copy_b = m->copy_b;
+    ca.att = m->b_att.as<float>();
+    ca.S_max = S_max;
+    ca.src_ext = op.src_ext;
+    ca.lens = d_lens;
+    ca.gen_w = m->gen_w.w.p;
+    ca.gen_ld = m->gen_w.k_pad;
+    ca.gen_bf16 = m->gen_w.bf16;
+    ca.gen_b = m->gen_b.as<float>();
+    ca.V = m->Vt;
+    ca.K = K;
+    ca.live = bs.live + (size_t)(t & 1) * R;
+    ca.row_lse = m->row_lse.as<float>();
+    ca.row_z = m->row_z.as<float>();
+    ca.row_i = m->row_i.as<int>();
+    ca.ctl = ctl;
+    ONMT_CUDA(launch_copy_rows(ca, R, m->stream));
+    launch_select_gather(B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(), m->row_z.as<float>(),
+                         m->row_i.as<int>(), ctl, m->stream);
+    count(m, 3);
+  };
   float* P = m->dec_p.as<float>();
   std::vector<DsGemmSpec> ds_specs;
   DsAtt ds_att;
@@ -1124,7 +1196,7 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       EvPair pgs = prof_begin(m, "gen");
       // generator + (fused) beam step: the generator's last B CTAs to finish run the beam step
       cudaError_t ge = cudaErrorInvalidConfiguration;
-      if (m->fuse_beam)
+      if (m->fuse_beam && !op.src_ext)
         ge = gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
                       m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
                       m->row_i.as<int>(), 4, t, max_len, lp, bs, ga, m->g_bar.as<unsigned int>(),
@@ -1144,16 +1216,24 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
         continue;
       }
       EvPair pm = prof_begin(m, "merge");
-      launch_beam_merge(g.ms, g.tz, g.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
-                        m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
-      count(m, n_vt <= 256 ? 1 : 2);
+      if (op.src_ext) {
+        merge_copy(n_vt, 1, n_vt, t, lp);
+      } else {
+        launch_beam_merge(g.ms, g.tz, g.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
+                          m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
+        count(m, n_vt <= 256 ? 1 : 2);
+      }
       prof_end(m, "merge", pm);
     } else {
       gen(m, m->xg, g, ctl);
       EvPair pm = prof_begin(m, "merge");
-      launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, 1, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
-                        m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
-      count(m, n_vt <= 256 ? 1 : 2);
+      if (op.src_ext) {
+        merge_copy(n_vt, rp, 1, t, lp);
+      } else {
+        launch_beam_merge(g.ms, g.tz, g.ti, n_vt, rp, 1, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
+                          m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
+        count(m, n_vt <= 256 ? 1 : 2);
+      }
       prof_end(m, "merge", pm);
     }
     prof_end(m, "step", ev);
@@ -1331,7 +1411,8 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
                               (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp,
-                              (int64_t)(intptr_t)out.unk_pos, (int64_t)(op.beta * 1e9), op.nbest, op.unk};
+                              (int64_t)(intptr_t)out.unk_pos, (int64_t)(op.beta * 1e9), op.nbest, op.unk,
+                              (int64_t)(intptr_t)op.src_ext};
   GraphCache& gc = m->graph;
   if (!gc.exec || gc.key != key) {
     if (gc.exec) {
@@ -1541,9 +1622,19 @@ static onmt_status check_decode_args(int32_t beam, int32_t max_len, float alpha)
 static onmt_status translate_impl(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
                                   int32_t beam, int32_t max_len, float alpha, int32_t* hyps, int32_t* olens,
                                   float* scores, float* raw, float* tlogp, int32_t* sel_parent, int32_t* sel_token,
-                                  double* sel_score, const DecodeOpts& op = DecodeOpts{}, int32_t* unk_pos = nullptr) {
+                                  double* sel_score, DecodeOpts op = DecodeOpts{}, int32_t* unk_pos = nullptr,
+                                  const int32_t* src_ext = nullptr) {
   onmt_status s = validate(m, ids, lens, B, S_max, true);
   if (s != ONMT_OK) return s;
+  if (m && m->copy != (src_ext != nullptr))
+    return fail(ONMT_E_INVALID_ARG, m->copy ? "a copy model needs the extended source ids (onmt_translate_copy)"
+                                            : "src_ext given for a model without a copy generator");
+  if (src_ext)
+    for (int b = 0; b < B; ++b)
+      for (int t = 0; t < lens[b]; ++t) {
+        const int v = src_ext[(size_t)b * S_max + t];
+        if (v < 0 || v >= m->Vt + S_max) return fail(ONMT_E_ID_RANGE, "extended source id out of range");
+      }
   s = check_decode_args(beam, max_len, alpha);
   if (s != ONMT_OK) return s;
   if (B == 0) return ONMT_OK;
@@ -1552,6 +1643,15 @@ static onmt_status translate_impl(onmt_model* m, const int32_t* ids, const int32
   ONMT_API_BEGIN
   ONMT_CUDA(cudaSetDevice(m->device));
   upload_src(m, ids, lens, B, S_max);
+  if (src_ext) {                                     // pads -> 0 (never read)
+    std::vector<int32_t> e((size_t)B * S_max, 0);
+    for (int b = 0; b < B; ++b)
+      for (int t = 0; t < lens[b]; ++t) e[(size_t)b * S_max + t] = src_ext[(size_t)b * S_max + t];
+    m->d_ext.ensure(e.size() * 4);
+    ONMT_CUDA(cudaMemcpyAsync(m->d_ext.p, e.data(), e.size() * 4, cudaMemcpyHostToDevice, m->stream));
+    ONMT_CUDA(cudaStreamSynchronize(m->stream));
+    op.src_ext = m->d_ext.as<int>();
+  }
   const size_t nb = (size_t)op.nbest;
   m->o_hyps.ensure((size_t)B * nb * max_len * 4);
   m->o_lens.ensure((size_t)B * nb * 4);
@@ -1600,6 +1700,18 @@ onmt_status onmt_translate_ex(onmt_model* m, const int32_t* ids, const int32_t* 
                         raw, tlogp, nullptr, nullptr, nullptr, op, unk_pos);
 }
 
+onmt_status onmt_translate_copy(onmt_model* m, const int32_t* ids, const int32_t* lens, const int32_t* src_ext,
+                                int32_t B, int32_t S_max, const onmt_decode_opts* opts, int32_t* hyps, int32_t* olens,
+                                float* scores, float* raw, float* tlogp) {
+  if (!opts) return fail(ONMT_E_INVALID_ARG, "null options");
+  if (!src_ext && B > 0) return fail(ONMT_E_INVALID_ARG, "null src_ext");
+  if (m && !m->copy) return fail(ONMT_E_UNSUPPORTED, "the model has no copy generator (copy.w / copy.b)");
+  if (opts->n_best != 1 || opts->coverage_penalty != 0.f || opts->replace_unk)
+    return fail(ONMT_E_UNSUPPORTED, "copy decoding supports n_best = 1, no coverage penalty, no unk replacement");
+  return translate_impl(m, ids, lens, B, S_max, opts->beam, opts->max_len, opts->length_penalty, hyps, olens, scores,
+                        raw, tlogp, nullptr, nullptr, nullptr, DecodeOpts{}, nullptr, B > 0 ? src_ext : nullptr);
+}
+
 onmt_status onmt_translate_trace(onmt_model* m, const int32_t* ids, const int32_t* lens, int32_t B, int32_t S_max,
                                  int32_t beam, int32_t max_len, float alpha, int32_t* hyps, int32_t* olens,
                                  float* scores, float* raw, float* tlogp, int32_t* sel_parent, int32_t* sel_token,
@@ -1616,6 +1728,7 @@ onmt_status onmt_score(onmt_model* m, const int32_t* ids, const int32_t* lens, i
   if (s != ONMT_OK) return s;
   if (B == 0) return ONMT_OK;
   if (T_max < 1) return fail(ONMT_E_INVALID_ARG, "T_max < 1");
+  if (m->copy) return fail(ONMT_E_UNSUPPORTED, "teacher-forced scoring of copy models is not built");
   if (!tgt || !tgt_lens || !out_token_logp) return fail(ONMT_E_INVALID_ARG, "null target / output pointer");
   for (int b = 0; b < B; ++b) {
     if (tgt_lens[b] < 1) return fail(ONMT_E_EMPTY_SOURCE, "empty target sentence " + std::to_string(b));
@@ -1667,6 +1780,7 @@ onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_ids, const int32_
     if (s != ONMT_OK) return s;
   }
   if (!d_ids || !d_lens || !d_hyps || !d_olens || !d_scores) return fail(ONMT_E_INVALID_ARG, "null device pointer");
+  if (m->copy) return fail(ONMT_E_UNSUPPORTED, "copy models decode through onmt_translate_copy");
   ONMT_API_BEGIN
   ONMT_CUDA(cudaSetDevice(m->device));
   m->o_raw.ensure((size_t)B * 4);

@@ -525,6 +525,37 @@ __global__ void __launch_bounds__(256) finalize_smem_kernel(BeamState bs, int B,
   }
 }
 
+// the two halves of the split beam merge, separately (copy models run copy_rows_kernel between)
+void launch_row_topk(const float2* ms, const float* tz, const int* ti, int n_parts, int ps, int rs, int B, int K, int t,
+                     const BeamState& bs, float* row_lse, float* row_z, int* row_i, StepCtl ctl, cudaStream_t st) {
+  const int R = B * K;
+#define ONMT_RT(KM)                                                                                                \
+  launch_pdl(row_reduce_topk_kernel<KM>, dim3(R), dim3(128), 0, st, ms, tz, ti, n_parts, ps, rs, K,                \
+             bs.live + (size_t)(t & 1) * R, row_lse, row_z, row_i, ctl);
+  if (K <= 1) { ONMT_RT(1) }
+  else if (K <= 2) { ONMT_RT(2) }
+  else if (K <= 4) { ONMT_RT(4) }
+  else if (K == 5) { ONMT_RT(5) }
+  else if (K <= 8) { ONMT_RT(8) }
+  else { ONMT_RT(16) }
+#undef ONMT_RT
+}
+
+void launch_select_gather(int B, int K, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
+                          const float* row_lse, const float* row_z, const int* row_i, StepCtl ctl, cudaStream_t st) {
+  const int R = B * K;
+#define ONMT_SG(KM)                                                                                                \
+  launch_pdl(beam_select_gather_kernel<KM>, dim3(R, 4), dim3(128), 0, st, row_lse, row_z, row_i, K, t, max_len, lp, \
+             bs, ga, 4, ctl);
+  if (K <= 1) { ONMT_SG(1) }
+  else if (K <= 2) { ONMT_SG(2) }
+  else if (K <= 4) { ONMT_SG(4) }
+  else if (K == 5) { ONMT_SG(5) }
+  else if (K <= 8) { ONMT_SG(8) }
+  else { ONMT_SG(16) }
+#undef ONMT_SG
+}
+
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
                      float* tlogp, int* unk_pos, cudaStream_t st) {
   const int nb = bs.nbest > 0 ? bs.nbest : 1;
