@@ -83,6 +83,9 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   float* s_scale = s_l + kKMax;
   float* e = s_scale + kKMax;
   float* buf = e + kKMax * kSCMax;
+  constexpr int KP = (KMAX + 3) & ~3;
+  __shared__ __align__(16) float et[kSCMax * KP];   // softmax weights [position][row], rows >= K stay 0
+  for (int i = threadIdx.x; i < kSCMax * KP; i += blockDim.x) et[i] = 0.f;
   const size_t mb = r4((size_t)SC * vl), kb = same ? 0 : r4((size_t)SC * kl);
   auto mbuf = [&](int i) { return buf + (size_t)(i & 1) * (mb + kb); };
   float* s_hp = buf + 2 * (mb + kb);                // folded W_out: the combine slice's tile shares
@@ -222,7 +225,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
       float sum = w;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (lane < kSCMax) e[k * kSCMax + lane] = w;
+      if (lane < kSCMax) et[lane * KP + k] = w;   // (transposed: the context reads 4 rows at once)
       if (lane == 0) {
         const float sc = mo == -INFINITY ? 0.f : expf(mo - mn);
         s_scale[k] = sc;
@@ -241,9 +244,15 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
         if (k < K) acc[k][u] *= s_scale[k];
       for (int s = 0; s < ns; ++s) {
         const float mv = ms[(size_t)s * vl + j];
+        const float4* ev = reinterpret_cast<const float4*>(et + s * KP);
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k)
-          if (k < K) acc[k][u] = fmaf(e[k * kSCMax + s], mv, acc[k][u]);
+        for (int k4 = 0; k4 < KP / 4; ++k4) {              // (rows >= K hold weight 0)
+          const float4 w = ev[k4];
+          if (4 * k4 < KMAX) acc[4 * k4][u] = fmaf(w.x, mv, acc[4 * k4][u]);
+          if (4 * k4 + 1 < KMAX) acc[4 * k4 + 1][u] = fmaf(w.y, mv, acc[4 * k4 + 1][u]);
+          if (4 * k4 + 2 < KMAX) acc[4 * k4 + 2][u] = fmaf(w.z, mv, acc[4 * k4 + 2][u]);
+          if (4 * k4 + 3 < KMAX) acc[4 * k4 + 3][u] = fmaf(w.w, mv, acc[4 * k4 + 3][u]);
+        }
       }
     }
     __syncthreads();                               // buffer (i & 1) free for sub-chunk i + 2
@@ -483,7 +492,9 @@ cudaError_t launch_attention(const float* htop, const float* keys, int key_ld, c
   if (K <= 1) ONMT_ATT(1);
   if (K <= 2) ONMT_ATT(2);
   if (K <= 4) ONMT_ATT(4);
+  if (K == 5) ONMT_ATT(5);                         // (the paper's beam size: no predicated-off rows)
   if (K <= 8) ONMT_ATT(8);
+  if (K == 10) ONMT_ATT(10);                       // (BASELINE c5)
   ONMT_ATT(16);
 #undef ONMT_ATT
 #undef ONMT_ATT_J

@@ -539,6 +539,7 @@ cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, i
   if (g.K <= 4) return launch_gs<4>(tmW, tmX, a, grid, smem, st);
   if (g.K == 5) return launch_gs<5>(tmW, tmX, a, grid, smem, st);     // (the paper's beam size)
   if (g.K <= 8) return launch_gs<8>(tmW, tmX, a, grid, smem, st);
+  if (g.K == 10) return launch_gs<10>(tmW, tmX, a, grid, smem, st);   // (BASELINE c5)
   return launch_gs<16>(tmW, tmX, a, grid, smem, st);
 }
 

@@ -454,6 +454,7 @@ void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_p
   else if (K <= 4) { ONMT_MERGE(4) }
   else if (K == 5) { ONMT_MERGE(5) }
   else if (K <= 8) { ONMT_MERGE(8) }
+  else if (K == 10) { ONMT_MERGE(10) }
   else { ONMT_MERGE(16) }
 #undef ONMT_MERGE
 }
@@ -537,6 +538,7 @@ void launch_row_topk(const float2* ms, const float* tz, const int* ti, int n_par
   else if (K <= 4) { ONMT_RT(4) }
   else if (K == 5) { ONMT_RT(5) }
   else if (K <= 8) { ONMT_RT(8) }
+  else if (K == 10) { ONMT_RT(10) }
   else { ONMT_RT(16) }
 #undef ONMT_RT
 }
@@ -552,6 +554,7 @@ void launch_select_gather(int B, int K, int t, int max_len, double lp, const Bea
   else if (K <= 4) { ONMT_SG(4) }
   else if (K == 5) { ONMT_SG(5) }
   else if (K <= 8) { ONMT_SG(8) }
+  else if (K == 10) { ONMT_SG(10) }
   else { ONMT_SG(16) }
 #undef ONMT_SG
 }
