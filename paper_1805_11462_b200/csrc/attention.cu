@@ -59,6 +59,34 @@ __device__ __forceinline__ float att_tanh(float x) {
   return copysignf(__fdividef(1.f - e, 1.f + e), x);
 }
 
+// Transposed butterfly: lane-partial sums of NV values (NV a power of two <= 32) reduced over
+// the warp in log2(NV) halvings + the remaining pair sums; value index x ends on the lanes with
+// xpose_index(lane) == x.  31 shuffles for 32 values instead of 5 per value.
+template <int NV>
+__device__ __forceinline__ float xpose_reduce(float (&v)[NV], int lane) {
+#pragma unroll
+  for (int h = NV / 2, o = 16; h >= 1; h /= 2, o /= 2) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = up ? v[i] : v[i + h];
+      const float keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (int o = 16 / NV; o >= 1; o /= 2) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  return v[0];
+}
+template <int NV>
+__device__ __forceinline__ int xpose_index(int lane) {
+  int x = 0;
+#pragma unroll
+  for (int h = NV / 2, o = 16; h >= 1; h /= 2, o /= 2) x += (lane & o) ? h : 0;
+  return x;
+}
+__host__ __device__ constexpr int pow2_at_least(int n) { return n <= 1 ? 1 : 2 * pow2_at_least((n + 1) / 2); }
+
 template <int KMAX, int JPT>
 __global__ void __launch_bounds__(kAttThreads)
 attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict__ keys, int key_ld,
@@ -113,7 +141,22 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
     cp_async_wait<0>();
     return;
   }
-  cp_async_rows(q, htop + (size_t)b * K * H, K * H);   // queries: the K beam rows of sentence b
+  // queries: the K beam rows of sentence b - in registers for small K (each lane's 4 float4
+  // columns of every row, reused by every position), else staged in shared memory
+  constexpr bool QREG = KMAX <= 5 && JPT == 2;
+  float4 qr[QREG ? KMAX : 1][4];
+  if (QREG && vec) {
+#pragma unroll
+    for (int k = 0; k < (QREG ? KMAX : 1); ++k)
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int j = 4 * (threadIdx.x & 31) + 128 * it;
+        qr[k][it] = (k < K && j < H) ? __ldg(reinterpret_cast<const float4*>(htop + ((size_t)b * K + k) * H + j))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+  } else {
+    cp_async_rows(q, htop + (size_t)b * K * H, K * H);
+  }
   cp_async_commit();
   // folded W_out: prefetch this CTA's combine slice of the top layer's W_out h shares
   // [tile][k][column] (produced by the previous kernel) - they land while the scores run
@@ -166,7 +209,21 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
         for (int k = 0; k < KMAX; ++k) { da[k] = 0.f; db[k] = 0.f; }
         const float* kra = ks + (size_t)pa * kl;
         const float* krb = ks + (size_t)(hb ? pb : pa) * kl;
-        if (vec) {
+        if (QREG && vec) {
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int j = 4 * lane + 128 * it;
+            if (j >= H) break;
+            const float4 ka = *reinterpret_cast<const float4*>(kra + j);
+            const float4 kbv = *reinterpret_cast<const float4*>(krb + j);
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k) {
+              const float4 qv = qr[QREG ? k : 0][it];
+              da[k] = fmaf(qv.x, ka.x, fmaf(qv.y, ka.y, fmaf(qv.z, ka.z, fmaf(qv.w, ka.w, da[k]))));
+              db[k] = fmaf(qv.x, kbv.x, fmaf(qv.y, kbv.y, fmaf(qv.z, kbv.z, fmaf(qv.w, kbv.w, db[k]))));
+            }
+          }
+        } else if (vec) {
           for (int j = 4 * lane; j < H; j += 128) {
             const float4 ka = *reinterpret_cast<const float4*>(kra + j);
             const float4 kbv = *reinterpret_cast<const float4*>(krb + j);
@@ -190,24 +247,20 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
               }
           }
         }
+        // warp sums of the 2 x KMAX dot products (transposed butterfly)
+        constexpr int NV = pow2_at_least(2 * KMAX);
+        float v[NV];
 #pragma unroll
-        for (int k = 0; k < KMAX; ++k)
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            da[k] += __shfl_xor_sync(0xffffffffu, da[k], o);
-            db[k] += __shfl_xor_sync(0xffffffffu, db[k], o);
+        for (int x = 0; x < NV; ++x) v[x] = x < KMAX ? da[x] : x < 2 * KMAX ? db[x - KMAX] : 0.f;
+        const float sum = xpose_reduce<NV>(v, lane);
+        const int x = xpose_index<NV>(lane);
+        if ((lane & (32 / NV - 1)) == 0 && x < 2 * KMAX) {
+          const int k = x < KMAX ? x : x - KMAX;
+          const int p = x < KMAX ? pa : pb;
+          if (k < K && (x < KMAX || hb)) {
+            e[k * kSCMax + p] = sum;
+            if (fo.att_out) s_esave[k * CH + (s0 - s_beg) + p] = sum;
           }
-        if (lane == 0) {
-#pragma unroll
-          for (int k = 0; k < KMAX; ++k)
-            if (k < K) {
-              e[k * kSCMax + pa] = da[k];
-              if (hb) e[k * kSCMax + pb] = db[k];
-              if (fo.att_out) {
-                s_esave[k * CH + (s0 - s_beg) + pa] = da[k];
-                if (hb) s_esave[k * CH + (s0 - s_beg) + pb] = db[k];
-              }
-            }
         }
       }
     }
