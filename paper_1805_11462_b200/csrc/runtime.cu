@@ -76,6 +76,29 @@ struct EncRecArgs {
   unsigned long long* trace;
 };
 int enc_rec_splits(int kb, int N, int D, int T, int num_sms);
+struct EncWaveLayer {
+  int T, S, kb, kb_in;
+  int cta0;
+  const float* Z;
+  int z_ld;
+  const float4* bias;
+  XOut xrec[2];
+  float* h_st;
+  float* c_st;
+  int st_ld;
+  XOut xnext;
+  float* mem;
+  int mem_ld;
+};
+struct EncWaveArgs {
+  EncWaveLayer layer[4];
+  int L, Hd, B, N, S_max;
+  const int* lens;
+  unsigned long long* cnt;
+};
+int enc_wave_splits(int L, const int* kb, int N, int T, int num_sms);
+cudaError_t launch_enc_wave(const CUtensorMap* tw, const CUtensorMap (*tx)[2], const EncWaveArgs& a, int grid, int S,
+                            cudaStream_t st);
 struct CopyArgs {
   const float* htilde;
   int H;
@@ -355,6 +378,8 @@ struct onmt_model {
   // weights
   DevBuf emb_src, emb_tgt;                   // fp32 [V x E]
   std::vector<std::unique_ptr<Mat>> enc_wih, enc_whh;  // [l*D + d]
+  std::vector<std::unique_ptr<Mat>> enc_wcat;          // [l] (D == 1, bf16): [W_ih | W_hh] for the wavefront encoder
+  bool enc_wavefront = true;                           // unidirectional stacked encoder as a layer wavefront
   std::vector<std::unique_ptr<DevBuf>> enc_bias;
   std::vector<std::unique_ptr<Mat>> dec_w;
   std::vector<std::unique_ptr<DevBuf>> dec_bias;
@@ -370,6 +395,8 @@ struct onmt_model {
   DevBuf d_ids, d_lens;
   Act enc_in0, enc_mid[2], enc_rec[2], enc_rec2[2];   // enc_rec2: 2nd parity (persistent recurrence)
   DevBuf er_bar;                             // step barriers of the persistent encoder recurrence
+  Act wave_rec[4][2];                        // wavefront encoder: per-layer recurrent-operand parity buffers
+  DevBuf wave_cnt;                           // wavefront encoder: per-layer finished-CTA counters
   DevBuf enc_z[2], enc_p, mem, enc_h, enc_c, keys, vals;
   Act mem_x;                                 // memory bank as a GEMM operand (keys / values GEMMs)
   // decoder workspace
@@ -624,6 +651,27 @@ static void load_model(onmt_model* m, const char* path) {
       m->enc_wih.push_back(std::move(a));
       m->enc_whh.push_back(std::move(b));
       m->enc_bias.push_back(std::move(bb));
+      if (bf && m->D == 1) {
+        // wavefront encoder (enc_wave.cu): layer l >= 1 reduces [h_{l-1,t} ; h_{l,t-1}] against
+        // [W_ih | W_hh], each part padded to whole 64-column K blocks, gate rows interleaved
+        std::unique_ptr<Mat> wc;
+        if (l >= 1) {
+          const int kin = round_up((int)in, kBK), kown = round_up((int)Hd, kBK);
+          const int mp = round_up(4 * (int)Hd, kTileM);
+          std::vector<float> h((size_t)mp * (kin + kown), 0.f);
+          for (int g = 0; g < 4; ++g)
+            for (uint64_t j = 0; j < Hd; ++j) {
+              float* dst = h.data() + (size_t)(4 * j + g) * (kin + kown);
+              const float* wa = wih.v.data() + (size_t)(g * Hd + j) * in;
+              const float* wb = whh.v.data() + (size_t)(g * Hd + j) * Hd;
+              std::copy(wa, wa + in, dst);
+              std::copy(wb, wb + Hd, dst + kin);
+            }
+          wc = std::make_unique<Mat>();
+          wc->upload(h, 4 * (int)Hd, kin + kown, bf);
+        }
+        m->enc_wcat.push_back(std::move(wc));
+      }
     }
   const auto& et = get(t, "dec.emb", {Vt, E}, seen);
   upload_f32(m->emb_tgt, et.v);
@@ -703,11 +751,30 @@ static bool fold_on(onmt_model* m, int rows) {
 }
 
 // ------------------------------------------------------------------ encoder
+// splits of the wavefront encoder for this batch (0 = not used): unidirectional bf16 models
+// with 2..4 layers whose layers all fit the persistent kernel's shared memory
+static int wave_splits(onmt_model* m, int B) {
+  if (!(m->use_tc && m->enc_persistent && m->enc_wavefront && m->D == 1 && m->L >= 2 && m->L <= 4 &&
+        (int)m->enc_wcat.size() == m->L))
+    return 0;
+  const RowPlan rp = plan_rows(B);
+  if (rp.n_group != rp.rows_pad) return 0;
+  int kb[4];
+  kb[0] = m->enc_whh[0]->k_pad / kBK;
+  for (int l = 1; l < m->L; ++l) kb[l] = m->enc_wcat[l]->k_pad / kBK;
+  return enc_wave_splits(m->L, kb, rp.rows_pad, m->enc_whh[0]->m_pad / kTileM, m->num_sms);
+}
+
 static void prepare_encoder(onmt_model* m, int B, int S_max) {
   const int rows = B * S_max, H = m->H, Hd = m->Hd, D = m->D;
   m->enc_in0.ensure(rows, m->E, m->prec == ONMT_PREC_BF16);
   if (m->L > 1) { m->enc_mid[0].ensure(rows, H, m->prec == ONMT_PREC_BF16); m->enc_mid[1].ensure(rows, H, m->prec == ONMT_PREC_BF16); }
   for (int d = 0; d < D; ++d) m->enc_rec[d].ensure(B, Hd, m->prec == ONMT_PREC_BF16);
+  if (wave_splits(m, B) > 0) {
+    for (int l = 0; l < m->L; ++l)
+      for (int p = 0; p < 2; ++p) m->wave_rec[l][p].ensure(B, Hd, true);
+    m->wave_cnt.ensure(4 * 16 * 8);
+  }
   if (m->use_tc && m->enc_persistent) {
     for (int d = 0; d < D; ++d) m->enc_rec2[d].ensure(B, Hd, true);
     if (!m->er_bar.p) {
@@ -737,8 +804,48 @@ static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, 
 
   launch_embed_gather(m->emb_src.as<float>(), m->E, d_ids, d_lens, B, S_max, m->enc_in0.xo(bf), m->stream);
   count(m);
+  const int WS = wave_splits(m, B);
+  if (WS > 0) {
+    // unidirectional stack as one wavefront launch (enc_wave.cu): layer 0's input projection
+    // is hoisted as usual, every other layer reduces [h_{l-1,t} ; h_{l,t-1}] per step
+    gemm(m, *m->enc_wih[0], m->enc_in0, rows, 1, m->enc_z[0].as<float>(), none);
+    EncWaveArgs wa{};
+    CUtensorMap tw[4], tx[4][2];
+    int cta = 0;
+    const int T = m->enc_whh[0]->m_pad / kTileM;
+    for (int l = 0; l < m->L; ++l) {
+      EncWaveLayer& ly = wa.layer[l];
+      const Mat& W = l == 0 ? *m->enc_whh[0] : *m->enc_wcat[l];
+      ly.T = T;
+      ly.S = WS;
+      ly.kb = W.k_pad / kBK;
+      ly.kb_in = l == 0 ? 0 : round_up(H, kBK) / kBK;
+      ly.cta0 = cta;
+      cta += T * WS;
+      ly.Z = l == 0 ? m->enc_z[0].as<float>() : nullptr;
+      ly.z_ld = zld;
+      ly.bias = m->enc_bias[l]->as<float4>();
+      ly.xrec[0] = m->wave_rec[l][0].xo(true);
+      ly.xrec[1] = m->wave_rec[l][1].xo(true);
+      ly.h_st = m->enc_h.as<float>() + (size_t)l * B * H;
+      ly.c_st = m->enc_c.as<float>() + (size_t)l * B * H;
+      ly.st_ld = H;
+      const bool top = l + 1 == m->L;
+      if (top && (m->general || m->fold_cur)) ly.xnext = m->mem_x.xo(true);
+      ly.mem = top ? m->mem.as<float>() : nullptr;
+      ly.mem_ld = H;
+      tw[l] = W.tmap;
+      tx[l][0] = m->wave_rec[l][0].tmap;
+      tx[l][1] = m->wave_rec[l][1].tmap;
+    }
+    wa.L = m->L; wa.Hd = Hd; wa.B = B; wa.N = m->wave_rec[0][0].rows_pad; wa.S_max = S_max;
+    wa.lens = d_lens;
+    wa.cnt = m->wave_cnt.as<unsigned long long>();
+    ONMT_CUDA(launch_enc_wave(tw, tx, wa, cta, WS, m->stream));
+    count(m);
+  }
   const Act* xin = &m->enc_in0;
-  for (int l = 0; l < m->L; ++l) {
+  for (int l = 0; l < (WS > 0 ? 0 : m->L); ++l) {
     const Act* xnext = l + 1 < m->L ? &m->enc_mid[l % 2] : nullptr;
     for (int d = 0; d < D; ++d)
       gemm(m, *m->enc_wih[l * D + d], *xin, rows, 1, m->enc_z[d].as<float>(), none);
@@ -1408,6 +1515,7 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
                               m->gen_step, m->dec_fused, m->fold_cur, m->enc_persistent, m->fuse_beam,
+                              m->enc_wavefront,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
                               (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp,
@@ -1507,6 +1615,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   if (const char* ev = std::getenv("ONMT_FOLD_WOUT")) m->fold_wout = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_PERSISTENT")) m->enc_persistent = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_FUSE_BEAM")) m->fuse_beam = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_ENC_WAVE")) m->enc_wavefront = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
@@ -1552,6 +1661,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->enc_persistent = v != 0;
   } else if (n == "fuse_beam") {
     m->fuse_beam = v != 0;
+  } else if (n == "enc_wavefront") {
+    m->enc_wavefront = v != 0;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
   } else {

@@ -141,3 +141,27 @@ def test_fused_beam_step_option(weight_cache):
         assert np.array_equal(a[k], b[k]), k
         assert np.array_equal(c[k], d[k]), k
     assert np.array_equal(c["unk_pos"], d["unk_pos"])
+
+
+@pytest.mark.parametrize("layers,bidir", [(3, False), (2, False), (2, True)])
+def test_persistent_encoders_match_per_step_path(weight_cache, layers, bidir):
+    """The persistent encoders (enc_rec.cu; the unidirectional layer wavefront enc_wave.cu)
+    compute the same memory bank and final states as the per-step launches, and both agree
+    with the fp64 oracle."""
+    cfg = synth.ModelConfig(layers, 64, 128, 300, 500, bidir, True)
+    gm, om, prec = toy_pair(cfg, 21, 0.2, weight_cache, "bf16", name=f"enc{layers}{bidir}")
+    ids, lens = synth.make_corpus("c1")
+    ids = ids % 300
+    ids[ids < 4] += 4
+    mem1, h1, c1 = gm.encode(ids, lens)
+    gm.set_option("enc_persistent", 0)
+    try:
+        mem0, h0, c0 = gm.encode(ids, lens)
+    finally:
+        gm.set_option("enc_persistent", 1)
+    np.testing.assert_allclose(mem1, mem0, atol=5e-6)
+    np.testing.assert_allclose(h1, h0, atol=5e-6)
+    np.testing.assert_allclose(c1, c0, atol=5e-6)
+    for b in range(len(lens)):
+        ref_mem, finals = om.encode([int(v) for v in ids[b, :lens[b]]])
+        np.testing.assert_allclose(mem1[b, :lens[b]], ref_mem, atol=2e-4)
