@@ -143,16 +143,20 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   }
   // queries: the K beam rows of sentence b - in registers for small K (each lane's 4 float4
   // columns of every row, reused by every position), else staged in shared memory
+  // (5 < K <= 10: each half of the warps holds half of the rows, QSPLIT)
   constexpr bool QREG = KMAX <= 5 && JPT == 2;
-  float4 qr[QREG ? KMAX : 1][4];
-  if (QREG && vec) {
+  constexpr bool QSPLIT = KMAX > 5 && KMAX <= 10 && JPT == 2;
+  constexpr int QR = QREG ? KMAX : QSPLIT ? (KMAX + 1) / 2 : 1;   // rows held per warp
+  const int qrow0 = QSPLIT ? (threadIdx.x >> 7) * QR : 0;         // first row of this warp (half)
+  float4 qr[QR][4];
+  if ((QREG || QSPLIT) && vec) {
 #pragma unroll
-    for (int k = 0; k < (QREG ? KMAX : 1); ++k)
+    for (int kk = 0; kk < QR; ++kk)
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
-        const int j = 4 * (threadIdx.x & 31) + 128 * it;
-        qr[k][it] = (k < K && j < H) ? __ldg(reinterpret_cast<const float4*>(htop + ((size_t)b * K + k) * H + j))
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int j = 4 * (threadIdx.x & 31) + 128 * it, k = qrow0 + kk;
+        qr[kk][it] = (k < K && j < H) ? __ldg(reinterpret_cast<const float4*>(htop + ((size_t)b * K + k) * H + j))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
       }
   } else {
     cp_async_rows(q, htop + (size_t)b * K * H, K * H);
@@ -200,7 +204,48 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
     const float* ms = mbuf(i);
     const float* ks = kbuf(i);
     // ---- scores: warp w -> positions w and w + 8 (they share the q loads)
-    {
+    if (QSPLIT && vec) {
+      // row half h = warp / 4 holds rows [h*QR, h*QR + QR); its 4 warps take the position
+      // pairs (w, w + 8) and (w + 4, w + 12), w = warp % 4
+#pragma unroll 1
+      for (int pp = 0; pp < 2; ++pp) {
+        const int pa = (warp & 3) + 4 * pp, pb = pa + 8;
+        const bool ha = pa < ns, hb = pb < ns;
+        if (!ha) continue;
+        float da[QR], db[QR];
+#pragma unroll
+        for (int kk = 0; kk < QR; ++kk) { da[kk] = 0.f; db[kk] = 0.f; }
+        const float* kra = ks + (size_t)pa * kl;
+        const float* krb = ks + (size_t)(hb ? pb : pa) * kl;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int j = 4 * lane + 128 * it;
+          if (j >= H) break;
+          const float4 ka = *reinterpret_cast<const float4*>(kra + j);
+          const float4 kbv = *reinterpret_cast<const float4*>(krb + j);
+#pragma unroll
+          for (int kk = 0; kk < QR; ++kk) {
+            const float4 qv = qr[kk][it];
+            da[kk] = fmaf(qv.x, ka.x, fmaf(qv.y, ka.y, fmaf(qv.z, ka.z, fmaf(qv.w, ka.w, da[kk]))));
+            db[kk] = fmaf(qv.x, kbv.x, fmaf(qv.y, kbv.y, fmaf(qv.z, kbv.z, fmaf(qv.w, kbv.w, db[kk]))));
+          }
+        }
+        constexpr int NV = pow2_at_least(2 * QR);
+        float v[NV];
+#pragma unroll
+        for (int x = 0; x < NV; ++x) v[x] = x < QR ? da[x] : x < 2 * QR ? db[x - QR] : 0.f;
+        const float sum = xpose_reduce<NV>(v, lane);
+        const int x = xpose_index<NV>(lane);
+        if ((lane & (32 / NV - 1)) == 0 && x < 2 * QR) {
+          const int k = qrow0 + (x < QR ? x : x - QR);
+          const int p = x < QR ? pa : pb;
+          if (k < K && (x < QR || hb)) {
+            e[k * kSCMax + p] = sum;
+            if (fo.att_out) s_esave[k * CH + (s0 - s_beg) + p] = sum;
+          }
+        }
+      }
+    } else {
       const int pa = warp, pb = warp + 8;
       const bool ha = pa < ns, hb = pb < ns;
       if (ha) {
