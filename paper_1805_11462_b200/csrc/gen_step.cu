@@ -89,6 +89,42 @@ __device__ __forceinline__ void gs_insert(float (&tz)[KMAX], int (&ti)[KMAX], fl
   ti[0] = gt[0] ? xi : ti[0];
 }
 
+// same list, for the scan: every list entry has a smaller id than x (each thread scans its
+// vocabulary rows in increasing order), so "better" reduces to a value compare
+template <int KMAX>
+__device__ __forceinline__ void gs_insert_scan(float (&tz)[KMAX], int (&ti)[KMAX], float x, int xi) {
+  bool gt[KMAX];
+#pragma unroll
+  for (int q = 0; q < KMAX; ++q) gt[q] = x > tz[q];
+#pragma unroll
+  for (int q = KMAX - 1; q >= 1; --q) {
+    tz[q] = gt[q] ? (gt[q - 1] ? tz[q - 1] : x) : tz[q];
+    ti[q] = gt[q] ? (gt[q - 1] ? ti[q - 1] : xi) : ti[q];
+  }
+  tz[0] = gt[0] ? x : tz[0];
+  ti[0] = gt[0] ? xi : ti[0];
+}
+
+// packed fp32 pairs (FFMA2 / FADD2): same rounding as two scalar operations
+__device__ __forceinline__ unsigned long long gs_pk(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void gs_upk(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ unsigned long long gs_ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long gs_fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 template <int KMAX>
 __global__ void __launch_bounds__(kGsThreads, 1)
 gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GenStepArgs a) {
@@ -152,6 +188,18 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           const int s = it % a.stages;
           if (it >= a.stages) mbar_wait(&empty[s], ((it / a.stages) & 1) ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
+#ifdef ONMT_KTRACE
+          if (a.dbg == 11 || a.dbg == 12) {                        // ablations: activations / weights only
+            mbar_arrive_expect_tx(&full[s], a.dbg == 12 ? 2 * b_bytes : nt * a_bytes);
+            if (a.dbg == 12) {
+              tma_load_2d(st, &tmX, kb * kBK, n0, &full[s]);
+              tma_load_2d(st + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[s]);
+            } else {
+              for (int j = 0; j < nt; ++j) tma_load_2d(st + 2 * b_bytes + j * a_bytes, &tmW, kb * kBK, (t0 + j) * kTileM, &full[s]);
+            }
+            continue;
+          }
+#endif
           mbar_arrive_expect_tx(&full[s], 2 * b_bytes + nt * a_bytes);
           tma_load_2d(st, &tmX, kb * kBK, n0, &full[s]);
           tma_load_2d(st + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[s]);
@@ -223,9 +271,14 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
             else tmem_ld16_nw(trow + c0, r);
           };
           auto put = [&](int c0, uint32_t* r) {
+            float* d = dst + (size_t)c0 * kGsSLD;
+            if (c0 + 32 <= a.n_group) {                            // whole chunk: immediate offsets
 #pragma unroll
-            for (int k = 0; k < 32; ++k)
-              if (c0 + k < a.n_group) dst[(size_t)(c0 + k) * kGsSLD] = __uint_as_float(r[k]) + bias;
+              for (int k = 0; k < 32; ++k) d[k * kGsSLD] = __uint_as_float(r[k]) + bias;
+            } else {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) d[k * kGsSLD] = __uint_as_float(r[k]) + bias;
+            }
           };
           uint32_t ra[32], rb[32];
           issue(0, ra);
@@ -274,16 +327,23 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       const int nt = min(a.nt_max, te - t0);
       for (int j = 0; j < nt; ++j, ++jj) {
         const int buf = jj & 1;
+        // the row's shared threshold: the largest list tail any scanner of any CTA published
+        // so far - a K-th best of a subset of the row, so a lower bound of the row's K-th best
+        // logit; values below it cannot reach the row's top-K.  Loaded before
+        // the wait for the staged tile so the L2 round trip overlaps it.
+        // (step 1 does not read: its buffer may still hold the previous call's last step)
+#ifdef ONMT_KTRACE
+        const float gth = (row_ok && a.thr && a.t != 1 && a.dbg != 5) ? key2f(__ldcg(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c))
+                                                        : -INFINITY;
+#else
+        const float gth = (row_ok && a.thr && a.t != 1) ? key2f(__ldcg(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c))
+                                                        : -INFINITY;
+#endif
         mbar_wait(&sfull[buf], (jj >> 1) & 1);
+        KTX(4, et == 0 && jj == 0);
 #ifdef ONMT_KTRACE
         if (a.dbg == 2) { __syncwarp(); if (lane == 0) mbar_arrive_local(&sempty[buf]); continue; }
 #endif
-        // the row's shared threshold: the largest list tail any scanner of any CTA published
-        // so far - a K-th best of a subset of the row, so a lower bound of the row's K-th best
-        // logit; values below it cannot reach the row's top-K
-        // (step 1 does not read: its buffer may still hold the previous call's last step)
-        const float gth = (row_ok && a.thr && a.t != 1) ? key2f(__ldcg(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c))
-                                                        : -INFINITY;
         if (row_ok) {
           const float* col = stg + (size_t)buf * a.n_group * kGsSLD + (size_t)c * kGsSLD + part * nv;
           const int vbase = (t0 + j) * kTileM + part * nv;
@@ -306,12 +366,20 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 #endif
             if (mn != -INFINITY) {
               const float mo = mn * L2E;
-              float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+              // s0..s3 accumulate z[k], z[k+1], z[k+2], z[k+3] as packed pairs (FFMA2 / FADD2)
+              const unsigned long long l2 = gs_pk(L2E, L2E), mo2 = gs_pk(-mo, -mo);
+              unsigned long long s01 = gs_pk(0.f, 0.f), s23 = gs_pk(0.f, 0.f);
 #pragma unroll
               for (int k = 0; k < 64; k += 4) {
-                s0 += gs_ex2(fmaf(z[k], L2E, -mo)); s1 += gs_ex2(fmaf(z[k + 1], L2E, -mo));
-                s2 += gs_ex2(fmaf(z[k + 2], L2E, -mo)); s3 += gs_ex2(fmaf(z[k + 3], L2E, -mo));
+                float e0, e1, e2, e3;
+                gs_upk(gs_ffma2(gs_pk(z[k], z[k + 1]), l2, mo2), e0, e1);
+                gs_upk(gs_ffma2(gs_pk(z[k + 2], z[k + 3]), l2, mo2), e2, e3);
+                s01 = gs_fadd2(s01, gs_pk(gs_ex2(e0), gs_ex2(e1)));
+                s23 = gs_fadd2(s23, gs_pk(gs_ex2(e2), gs_ex2(e3)));
               }
+              float s0, s1, s2, s3;
+              gs_upk(s01, s0, s1);
+              gs_upk(s23, s2, s3);
               run_s = (run_m == -INFINITY ? 0.f : run_s * gs_ex2((run_m - mn) * L2E)) + ((s0 + s1) + (s2 + s3));
               run_m = mn;
             }
@@ -323,50 +391,66 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
             // a subset - so nothing below it can enter).  The bound matters on the first
             // chunks, when the list is still cold.  Ids increase along the scan, so a value
             // compare decides every insertion (a tie never displaces an earlier id).
-            float th = fmaxf(tz[KMAX - 1], gth);
+            const float th = fmaxf(tz[KMAX - 1], gth);
             if (cmax >= th && cmax > tz[KMAX - 1]) {
-              if (tz[KMAX - 1] == -INFINITY) {                     // cold list: K-th largest group max
+              if (tz[KMAX - 1] == -INFINITY) {
+                // cold list: extract the chunk's K best exactly - K rounds of (largest group
+                // maximum, its first element, the group's maximum without it) - uniform work
+                // instead of inserting every element of every group above the K-th group max
                 float gg[16];
 #pragma unroll
                 for (int k = 0; k < 16; ++k) gg[k] = g[k];
-                float gk = -INFINITY;
+                unsigned long long rm = 0ull;                      // extracted: bit 4 * group + element
 #pragma unroll
                 for (int rnd = 0; rnd < KMAX; ++rnd) {
                   if (rnd < a.K) {
                     float mx = gg[0];
 #pragma unroll
                     for (int k = 1; k < 16; ++k) mx = fmaxf(mx, gg[k]);
-                    gk = mx;
-                    bool hit = false;
+                    if (mx != -INFINITY) {
+                      int sel = 15;
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                      const bool h = !hit && gg[k] == mx;
-                      gg[k] = h ? -INFINITY : gg[k];
-                      hit |= h;
+                      for (int k = 14; k >= 0; --k) sel = gg[k] == mx ? k : sel;
+                      const float4 w = *reinterpret_cast<const float4*>(col + u0 + 4 * sel);
+                      const unsigned gone = (unsigned)(rm >> (4 * sel)) & 15u;
+                      const float v0 = (gone & 1u) ? -INFINITY : w.x, v1 = (gone & 2u) ? -INFINITY : w.y;
+                      const float v2 = (gone & 4u) ? -INFINITY : w.z, v3 = (gone & 8u) ? -INFINITY : w.w;
+                      const int e = v0 == mx ? 0 : v1 == mx ? 1 : v2 == mx ? 2 : 3;
+                      gs_insert_scan<KMAX>(tz, ti, mx, vbase + u0 + 4 * sel + e);
+                      rm |= 1ull << (4 * sel + e);
+                      const float nm = fmaxf(fmaxf(e == 0 ? -INFINITY : v0, e == 1 ? -INFINITY : v1),
+                                             fmaxf(e == 2 ? -INFINITY : v2, e == 3 ? -INFINITY : v3));
+#pragma unroll
+                      for (int k = 0; k < 16; ++k) gg[k] = k == sel ? nm : gg[k];
                     }
                   }
                 }
-                th = fmaxf(th, gk);
-              }
-              unsigned gm = 0;                                     // groups holding a candidate
+              } else {
+                unsigned gm = 0;                                   // groups holding a candidate
 #pragma unroll
-              for (int k = 0; k < 16; ++k) gm |= (g[k] >= th) ? (1u << k) : 0u;
-              while (gm) {                                         // candidates in id order
-                const int gi = __ffs(gm) - 1;
-                gm &= gm - 1;
-                const float4 w = *reinterpret_cast<const float4*>(col + u0 + 4 * gi);
-                const float wv[4] = {w.x, w.y, w.z, w.w};
+                for (int k = 0; k < 16; ++k) gm |= (g[k] >= th) ? (1u << k) : 0u;
+                while (gm) {                                       // candidates in id order
+                  const int gi = __ffs(gm) - 1;
+                  gm &= gm - 1;
+                  const float4 w = *reinterpret_cast<const float4*>(col + u0 + 4 * gi);
+                  const float wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  if (wv[e] >= th && wv[e] > tz[KMAX - 1]) gs_insert<KMAX>(tz, ti, wv[e], vbase + u0 + 4 * gi + e);
+                  for (int e = 0; e < 4; ++e)
+                    if (wv[e] >= th && wv[e] > tz[KMAX - 1]) gs_insert_scan<KMAX>(tz, ti, wv[e], vbase + u0 + 4 * gi + e);
+                }
               }
             }
           }
         }
+#ifdef ONMT_KTRACE
+        if (a.dbg != 6)
+#endif
         if (row_ok && a.thr && tz[KMAX - 1] != -INFINITY)              // publish my list tail
           atomicMax(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c, f2key(tz[KMAX - 1]));
         __syncwarp();
         if (lane == 0) mbar_arrive_local(&sempty[buf]);
+        KTX(5, et == 0 && jj == 0);
+        KTX(11, et == 0 && jj == 1);
       }
     }
     KTX(8, et == 0);

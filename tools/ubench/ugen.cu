@@ -69,9 +69,11 @@ int main(int argc, char** argv) {
   ga.cg = (float*)zalloc(L * NP * H * 4); ga.rows_pad = NP;
   ga.x[0] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1536 * 2), NP, 1536};
   ga.x[1] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1024 * 2), NP, 1024};
+  int tstep = 2;  // alternate t: each launch clears the other threshold buffer, as in a decode
   auto launch = [&]() {
-    CK(gen_step(tmW, tmX, VP / 128, NP, NP, KP / 64, 148, g, rl, rz, ri, phases, 5, MAXLEN, 1.0, bs, ga, gbar, thr,
-                StepCtl{nullptr, 0}, st));
+    tstep = tstep == 2 ? 3 : 2;
+    CK(gen_step(tmW, tmX, VP / 128, NP, NP, KP / 64, 148, g, rl, rz, ri, phases, tstep, MAXLEN, 1.0, bs, ga, gbar, thr,
+                StepCtl{nullptr, 0}, st, nullptr, B));
   };
   cudaGraph_t gr; cudaGraphExec_t ge;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -91,7 +93,7 @@ int main(int argc, char** argv) {
   for (int c = 0; c < grid; ++c) for (int i = 0; i < 12; ++i) if (h[c * 12 + i]) {
     double d = (h[c * 12 + i] - t0) / 1e3; avg[i] += d; cnt[i]++; mx[i] = std::max(mx[i], d); }
   printf("gen_step phases=%d dbg=%d: %.2f us/launch (graph of 20)\n", phases, g_gs_dbg, ms_ * 1000 / 20);
-  const char* nm[12] = {"entry", "pdl_wait", "mma done (epi)", "phase A end", "phase B start", "phase C start", "stager: tile2 buf free", "first data (mma)", "batch scanned", "partial write", "stager: tile0 staged", "phase C end"};
+  const char* nm[12] = {"entry", "pdl_wait", "mma done (epi)", "phase A end", "scan0 start (w6)", "scan0 end (w6)", "stager: tile2 buf free", "first data (mma)", "batch scanned", "partial write", "stager: tile0 staged", "scan1 end (w6)"};
   for (int i = 0; i < 12; ++i) if (cnt[i]) printf("   %-16s avg %7.2f  max %7.2f us (n=%d)\n", nm[i], avg[i] / cnt[i], mx[i], cnt[i]);
   return 0;
 }
