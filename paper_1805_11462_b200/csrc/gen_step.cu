@@ -53,6 +53,12 @@ struct GenStepArgs {
   unsigned long long* arrive;                   // phases == 4: monotonic arrival counter (64-bit)
   int B;                                        // phases == 4: sentences (one beam-step CTA each)
   int gbuf_floats;                              // phases == 4: dynamic smem reusable as beam staging
+  int ovl;                                      // 1: staging has its own smem and odd batches their own
+                                                //    TMEM columns (from tcol_b), so batch b+1's MMAs
+                                                //    overlap batch b's epilogue
+  int tcol_b;
+  int nbuf;                                     // staging buffers (1 or 2)
+  int srows_alloc;                              // staging rows per buffer (min(n_group, R))
 };
 
 __device__ __forceinline__ float gs_ex2(float x) {
@@ -135,9 +141,9 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   const uint32_t a_bytes = kTileM * 128, b_bytes = a.n_group * 128;
   const uint32_t stage_bytes = 2 * b_bytes + a.nt_max * a_bytes;
   const size_t ring = (size_t)a.stages * stage_bytes;
-  const size_t stg_bytes = (size_t)a.n_group * kGsSLD * 4;
-  const size_t body = ring > 2 * stg_bytes ? ring : 2 * stg_bytes;
-  float* stg = reinterpret_cast<float*>(smem);                     // 2 x [n_group][132], overlays the ring
+  const size_t stg_bytes = (size_t)a.nbuf * a.srows_alloc * kGsSLD * 4;
+  const size_t body = a.ovl ? ring + stg_bytes : (ring > stg_bytes ? ring : stg_bytes);
+  float* stg = reinterpret_cast<float*>(a.ovl ? smem + ring : smem);  // nbuf x [srows][132] (overlays the ring unless ovl)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + body);
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
@@ -183,7 +189,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       for (int bt = 0; bt < nbatch; ++bt) {
         const int t0 = tb + bt * a.nt_max;
         const int nt = min(a.nt_max, te - t0);
-        if (bt > 0) mbar_wait(tempty, (bt - 1) & 1);              // staging (ring overlay) finished
+        if (bt > 0 && !a.ovl) mbar_wait(tempty, (bt - 1) & 1);   // staging (ring overlay) finished
         for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
           const int s = it % a.stages;
           if (it >= a.stages) mbar_wait(&empty[s], ((it / a.stages) & 1) ^ 1);
@@ -222,7 +228,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           const uint32_t sb = smem_u32(smem + (size_t)s * stage_bytes);
           for (int j = 0; j < nt; ++j) {
             const uint32_t sa = sb + 2 * b_bytes + j * a_bytes;
-            const uint32_t d = tmem + j * a.n_group;
+            const uint32_t d = tmem + ((a.ovl && (bt & 1)) ? a.tcol_b : 0) + j * a.n_group;
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {
               const uint64_t da = umma_desc_sw128(sa + kk * 32);
@@ -240,6 +246,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     // ---------------- stagers: accumulator j -> (+bias) -> smem buf[j & 1][c][v] (transposed)
     const int q = warp & 3;                                        // TMEM lane quarter of this warp
     const int vr = q * 32 + lane;                                  // vocabulary row this thread stages
+    const int srows = min(a.n_group, a.R - n0);                    // staged hypothesis rows (valid ones)
+    const int ncols = (srows + 15) & ~15;                          // TMEM columns loaded (x32 / x16)
     for (int bt = 0; bt < nbatch; ++bt) {
       const int t0 = tb + bt * a.nt_max;
       const int nt = min(a.nt_max, te - t0);
@@ -254,43 +262,46 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       KTX(2, threadIdx.x == 64 && bt == 0);
       for (int j = 0; j < nt; ++j) {
         const int jj = bt * a.nt_max + j;                          // staging sequence number
-        const int buf = jj & 1;
-        if (jj >= 2) mbar_wait(&sempty[buf], ((jj >> 1) - 1) & 1);
+        const int buf = jj % a.nbuf;
+        if (jj >= a.nbuf) mbar_wait(&sempty[buf], ((jj / a.nbuf) - 1) & 1);
         KTX(6, threadIdx.x == 64 && jj == 2);
 #ifdef ONMT_KTRACE
         if (a.dbg != 1)
 #endif
         {
           const float bias = j == 0 ? bias_r[0] : j == 1 ? bias_r[1] : j == 2 ? bias_r[2] : bias_r[3];
-          const uint32_t trow = tmem + j * a.n_group + ((uint32_t)(q * 32) << 16);
-          float* dst = stg + (size_t)buf * a.n_group * kGsSLD + vr;
+          const uint32_t trow = tmem + ((a.ovl && (bt & 1)) ? a.tcol_b : 0) + j * a.n_group + ((uint32_t)(q * 32) << 16);
+          float* dst = stg + (size_t)buf * a.srows_alloc * kGsSLD + vr;
           // 32-column chunks, software-pipelined: the load of chunk i+1 is in flight while
-          // chunk i is stored (n_group is a multiple of 16: a last half chunk uses x16)
+          // chunk i is stored (ncols is a multiple of 16: a last half chunk uses x16)
           auto issue = [&](int c0, uint32_t* r) {
-            if (c0 + 32 <= a.n_group) tmem_ld32_nw(trow + c0, r);
+            if (c0 + 32 <= ncols) tmem_ld32_nw(trow + c0, r);
             else tmem_ld16_nw(trow + c0, r);
           };
           auto put = [&](int c0, uint32_t* r) {
             float* d = dst + (size_t)c0 * kGsSLD;
-            if (c0 + 32 <= a.n_group) {                            // whole chunk: immediate offsets
+            if (c0 + 32 <= srows) {                                // whole chunk: immediate offsets
 #pragma unroll
               for (int k = 0; k < 32; ++k) d[k * kGsSLD] = __uint_as_float(r[k]) + bias;
             } else {
 #pragma unroll
-              for (int k = 0; k < 16; ++k) d[k * kGsSLD] = __uint_as_float(r[k]) + bias;
+              for (int k = 0; k < 32; ++k)
+                if (c0 + k < srows) d[k * kGsSLD] = __uint_as_float(r[k]) + bias;
             }
           };
           uint32_t ra[32], rb[32];
-          issue(0, ra);
-          tmem_wait_ld();
-          tmem_fence_regs(ra);
-          for (int c0 = 0; c0 < a.n_group; c0 += 64) {
-            if (c0 + 32 < a.n_group) issue(c0 + 32, rb);
+          if (ncols > 0) {
+            issue(0, ra);
+            tmem_wait_ld();
+            tmem_fence_regs(ra);
+          }
+          for (int c0 = 0; c0 < ncols; c0 += 64) {
+            if (c0 + 32 < ncols) issue(c0 + 32, rb);
             put(c0, ra);
             tmem_wait_ld();
             tmem_fence_regs(rb);
-            if (c0 + 32 >= a.n_group) break;
-            if (c0 + 64 < a.n_group) issue(c0 + 64, ra);
+            if (c0 + 32 >= ncols) break;
+            if (c0 + 64 < ncols) issue(c0 + 64, ra);
             put(c0 + 32, rb);
             tmem_wait_ld();
             tmem_fence_regs(ra);
@@ -326,7 +337,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       const int t0 = tb + bt * a.nt_max;
       const int nt = min(a.nt_max, te - t0);
       for (int j = 0; j < nt; ++j, ++jj) {
-        const int buf = jj & 1;
+        const int buf = jj % a.nbuf;
         // the row's shared threshold: the largest list tail any scanner of any CTA published
         // so far - a K-th best of a subset of the row, so a lower bound of the row's K-th best
         // logit; values below it cannot reach the row's top-K.  Loaded before
@@ -339,13 +350,13 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         const float gth = (row_ok && a.thr && a.t != 1) ? key2f(__ldcg(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c))
                                                         : -INFINITY;
 #endif
-        mbar_wait(&sfull[buf], (jj >> 1) & 1);
+        mbar_wait(&sfull[buf], (jj / a.nbuf) & 1);
         KTX(4, et == 0 && jj == 0);
 #ifdef ONMT_KTRACE
         if (a.dbg == 2) { __syncwarp(); if (lane == 0) mbar_arrive_local(&sempty[buf]); continue; }
 #endif
         if (row_ok) {
-          const float* col = stg + (size_t)buf * a.n_group * kGsSLD + (size_t)c * kGsSLD + part * nv;
+          const float* col = stg + (size_t)buf * a.srows_alloc * kGsSLD + (size_t)c * kGsSLD + part * nv;
           const int vbase = (t0 + j) * kTileM + part * nv;
           for (int u0 = 0; u0 < nv; u0 += 64) {                    // 64 logits per chunk, in registers
             float z[64];
@@ -529,38 +540,83 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   }
 }
 
-static size_t gs_smem_bytes(int n_group, int nt_max, int stages) {
+static size_t gs_body_bytes(int n_group, int nt_max, int stages, int ovl, int nbuf, int srows) {
   const size_t ring = (size_t)stages * (2 * (size_t)n_group * 128 + (size_t)nt_max * kTileM * 128);
-  const size_t stg = 2 * (size_t)n_group * kGsSLD * 4;
-  return 1024 + (ring > stg ? ring : stg) + (2 * stages + 6) * 8 + 16;
+  const size_t stg = (size_t)nbuf * srows * kGsSLD * 4;
+  return ovl ? ring + stg : (ring > stg ? ring : stg);
 }
+static size_t gs_smem_bytes(size_t body, int stages) { return 1024 + body + (2 * stages + 6) * 8 + 16; }
 
 struct GsPlan {
-  int C, nt_max, stages, P;
+  int C, nt_max, stages, P, ovl, nbuf, srows;
+  size_t body;
 };
-static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, GsPlan& p) {
+// static shared memory of the kernel instance for beam width K (the fused beam step's arrays):
+// the dynamic part gets the rest
+template <int KMAX>
+static size_t gs_static_of() {
+  cudaFuncAttributes fa;
+  return cudaFuncGetAttributes(&fa, gen_step_kernel<KMAX>) == cudaSuccess ? fa.sharedSizeBytes : 12288;
+}
+static size_t gs_static_smem(int K) {
+  static size_t v[7] = {0, 0, 0, 0, 0, 0, 0};
+  const int i = K <= 1 ? 0 : K <= 2 ? 1 : K <= 4 ? 2 : K == 5 ? 3 : K <= 8 ? 4 : K == 10 ? 5 : 6;
+  if (!v[i]) {
+    switch (i) {
+      case 0: v[i] = gs_static_of<1>(); break;
+      case 1: v[i] = gs_static_of<2>(); break;
+      case 2: v[i] = gs_static_of<4>(); break;
+      case 3: v[i] = gs_static_of<5>(); break;
+      case 4: v[i] = gs_static_of<8>(); break;
+      case 5: v[i] = gs_static_of<10>(); break;
+      default: v[i] = gs_static_of<16>(); break;
+    }
+  }
+  return v[i];
+}
+static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, int R, int K, GsPlan& p) {
   p.C = num_sms / groups;
   if (p.C > n_vt) p.C = n_vt;
   if (p.C < 1) return false;
+  if (n_group > 32 * kGsScanWarps) return false;
+  p.P = 2 * n_group <= 32 * kGsScanWarps ? 2 : 1;
+  p.srows = n_group < R ? n_group : R;
+  if (p.srows < 1) p.srows = 1;
+  const size_t limit = 227 * 1024 - gs_static_smem(K);
+  const int need = (n_vt + p.C - 1) / p.C;                          // most tiles of a CTA
+  // overlapped batches: the CTA's tiles in two K-outer batches, the second
+  // batch's MMAs (own TMEM columns, own ring) run while the first batch is staged and scanned
+  static const int ovl_env = getenv("ONMT_GEN_OVL") ? atoi(getenv("ONMT_GEN_OVL")) : 1;
+  if (ovl_env && need >= 2 && need * n_group <= 512) {
+    p.ovl = 1;
+    p.nt_max = (need + 1) / 2;
+    p.stages = 2;
+    for (p.nbuf = 2; p.nbuf >= 1; --p.nbuf) {
+      p.body = gs_body_bytes(n_group, p.nt_max, p.stages, 1, p.nbuf, p.srows);
+      if (gs_smem_bytes(p.body, p.stages) <= limit && p.nt_max <= 4) return true;
+    }
+  }
+  p.ovl = 0;
+  p.nbuf = 2;
   p.nt_max = 512 / n_group;                                          // accumulators in TMEM
   if (p.nt_max > 4) p.nt_max = 4;                                    // (bias registers of the stagers)
-  const int need = (n_vt + p.C - 1) / p.C;
   if (p.nt_max > need) p.nt_max = need;
   if (p.nt_max < 1) return false;
-  p.P = 2 * n_group <= 32 * kGsScanWarps ? 2 : 1;
-  if (n_group > 32 * kGsScanWarps) return false;
-  const size_t limit = 227 * 1024 - 12288;        // (static shared memory incl. the fused beam step: <= 11 KB)
   p.stages = 4;
-  while (p.stages > 2 && gs_smem_bytes(n_group, p.nt_max, p.stages) > limit) --p.stages;
-  while (p.nt_max > 1 && gs_smem_bytes(n_group, p.nt_max, p.stages) > limit) --p.nt_max;
-  return gs_smem_bytes(n_group, p.nt_max, p.stages) <= limit;
+  auto fits = [&]() {
+    p.body = gs_body_bytes(n_group, p.nt_max, p.stages, 0, p.nbuf, p.srows);
+    return gs_smem_bytes(p.body, p.stages) <= limit;
+  };
+  while (p.stages > 2 && !fits()) --p.stages;
+  while (p.nt_max > 1 && !fits()) --p.nt_max;
+  return fits();
 }
 
 // parts per row written by the step kernel's phase A (0 = not applicable)
 int g_gs_dbg = 0;
 int gen_step_parts(int n_vt, int n_group, int groups, int num_sms) {
   GsPlan p;
-  return gs_plan(n_vt, n_group, groups, num_sms, p) ? p.C : 0;
+  return gs_plan(n_vt, n_group, groups, num_sms, n_group * groups, 16, p) ? p.C : 0;
 }
 
 template <int KMAX>
@@ -580,7 +636,7 @@ cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, i
                      unsigned long long* arrive, int B) {
   const int groups = n_rows_pad / n_group;
   GsPlan p;
-  if (!gs_plan(n_vt, n_group, groups, num_sms, p)) return cudaErrorInvalidConfiguration;
+  if (!gs_plan(n_vt, n_group, groups, num_sms, g.rows_valid, g.K, p)) return cudaErrorInvalidConfiguration;
   GenStepArgs a{};
   a.n_rows_pad = n_rows_pad;
   a.n_group = n_group;
@@ -613,10 +669,14 @@ cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, i
   a.ctl = ctl;
   a.dbg = g_gs_dbg;
   const int grid = p.C * groups;
-  const size_t smem = gs_smem_bytes(n_group, p.nt_max, p.stages);
+  const size_t smem = gs_smem_bytes(p.body, p.stages);
   a.arrive = arrive;
   a.B = B;
-  a.gbuf_floats = (int)((smem - 1024 - (2 * (size_t)p.stages + 9) * 8 - 16) / 4);
+  a.gbuf_floats = (int)(p.body / 4);
+  a.ovl = p.ovl;
+  a.tcol_b = p.nt_max * n_group;
+  a.nbuf = p.nbuf;
+  a.srows_alloc = p.srows;
   if (phases == 4 && (!arrive || B > grid || p.C > 256)) return cudaErrorInvalidConfiguration;
   if (g.K <= 1) return launch_gs<1>(tmW, tmX, a, grid, smem, st);
   if (g.K <= 2) return launch_gs<2>(tmW, tmX, a, grid, smem, st);
