@@ -28,6 +28,7 @@ constexpr int kGsStageWarps = 4;               // TMEM -> smem stagers (one per 
 constexpr int kGsScanWarps = 10;                // scanners (2 threads x 160 hypothesis rows)
 constexpr int kGsThreads = 32 * (2 + kGsStageWarps + kGsScanWarps);
 constexpr int kGsSLD = 132;                     // staging row stride (floats)
+constexpr int kGsMaxCh = 10;                    // 32-row staging chunks per buffer (n_group <= 320)
 
 struct GenStepArgs {
   int n_rows_pad, n_group, groups, k_blocks, n_vt, C, nt_max, stages;
@@ -47,7 +48,8 @@ struct GenStepArgs {
   GatherArgs ga;
   unsigned int* gbar;                           // grid barrier {count, generation}
   unsigned int* thr;                            // [2][rows_pad] shared top-K thresholds (ordered
-                                                // uint keys; buffer t & 1, the other one is reset)
+                                                // uint keys; buffer t & 1, the other one is reset),
+                                                // then [2][rows_pad][16] running-max slots
   StepCtl ctl;
   int dbg;                                      // microbenchmark ablations (ONMT_KTRACE builds)
   unsigned long long* arrive;                   // phases == 4: monotonic arrival counter (64-bit)
@@ -148,15 +150,20 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
   uint64_t* tempty = tfull + 1;
-  uint64_t* sfull = tempty + 1;                                    // [2] staging buffer filled (stagers)
-  uint64_t* sempty = sfull + 2;                                    // [2] staging buffer scanned (scanners)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + 2);
+  uint64_t* sfull = tempty + 1;                                    // [2][kGsMaxCh] staged chunk filled (stagers)
+  uint64_t* sempty = sfull + 2 * kGsMaxCh;                         // [2][kGsMaxCh] staged chunk scanned (scanners)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + 2 * kGsMaxCh);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = blockIdx.x / a.C, ci = blockIdx.x % a.C;
   const int tb = (int)((long long)ci * a.n_vt / a.C), te = (int)((long long)(ci + 1) * a.n_vt / a.C);
   const int n0 = grp * a.n_group;
   const int nbatch = (te - tb + a.nt_max - 1) / a.nt_max;
+  // staging is split into 32-hypothesis-row chunks with their own full/empty barriers: the
+  // scanners of a chunk start as soon as it is staged and the stagers refill a chunk as soon
+  // as its scanners are done (instead of whole-tile hand-offs)
+  const int srows = min(a.n_group, a.R - n0);                      // staged hypothesis rows (valid ones)
+  const int ncols = srows > 0 ? (srows + 15) & ~15 : 0;            // TMEM columns staged (x32 / x16 loads)
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmW);
@@ -164,17 +171,29 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     mbar_init(tempty, kGsStageWarps);
-    for (int b = 0; b < 2; ++b) { mbar_init(&sfull[b], kGsStageWarps); mbar_init(&sempty[b], kGsScanWarps); }
-    fence_mbar_init();
   }
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kGsMaxCh) {      // chunk barriers (warp 1)
+    const int i = threadIdx.x - 32, k = i % kGsMaxCh;
+    int cnt = 0;                                                   // scanner warps of chunk k
+    for (int sw = 0; sw < kGsScanWarps; ++sw) {
+      const int r0 = 32 * sw / a.P;
+      cnt += (r0 < ncols && (r0 >> 5) == k) ? 1 : 0;
+    }
+    mbar_init(&sfull[i], kGsStageWarps);
+    mbar_init(&sempty[i], cnt > 0 ? cnt : 1);
+  }
+  if (threadIdx.x == 0 || threadIdx.x == 32) fence_mbar_init();
   if (warp == 1) tmem_alloc<512>(tslot);
   tc_fence_before();
   pdl_wait();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  if (a.thr && blockIdx.x == 0)                                    // next step's thresholds start empty
+  if (a.thr && blockIdx.x == 0) {                                  // next step's thresholds start empty
     for (int i = threadIdx.x; i < a.rows_pad; i += blockDim.x) a.thr[(size_t)((a.t + 1) & 1) * a.rows_pad + i] = 0u;
+    uint4* sl = reinterpret_cast<uint4*>(a.thr + (size_t)2 * a.rows_pad + (size_t)((a.t + 1) & 1) * a.rows_pad * 16);
+    for (int i = threadIdx.x; i < a.rows_pad * 4; i += blockDim.x) sl[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
   if (all_done(a.ctl)) {                                           // uniform over the grid
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
@@ -246,8 +265,6 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     // ---------------- stagers: accumulator j -> (+bias) -> smem buf[j & 1][c][v] (transposed)
     const int q = warp & 3;                                        // TMEM lane quarter of this warp
     const int vr = q * 32 + lane;                                  // vocabulary row this thread stages
-    const int srows = min(a.n_group, a.R - n0);                    // staged hypothesis rows (valid ones)
-    const int ncols = (srows + 15) & ~15;                          // TMEM columns loaded (x32 / x16)
     for (int bt = 0; bt < nbatch; ++bt) {
       const int t0 = tb + bt * a.nt_max;
       const int nt = min(a.nt_max, te - t0);
@@ -262,12 +279,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       KTX(2, threadIdx.x == 64 && bt == 0);
       for (int j = 0; j < nt; ++j) {
         const int jj = bt * a.nt_max + j;                          // staging sequence number
-        const int buf = jj % a.nbuf;
-        if (jj >= a.nbuf) mbar_wait(&sempty[buf], ((jj / a.nbuf) - 1) & 1);
+        const int buf = jj % a.nbuf, use = jj / a.nbuf;
         KTX(6, threadIdx.x == 64 && jj == 2);
-#ifdef ONMT_KTRACE
-        if (a.dbg != 1)
-#endif
         {
           const float bias = j == 0 ? bias_r[0] : j == 1 ? bias_r[1] : j == 2 ? bias_r[2] : bias_r[3];
           const uint32_t trow = tmem + ((a.ovl && (bt & 1)) ? a.tcol_b : 0) + j * a.n_group + ((uint32_t)(q * 32) << 16);
@@ -278,7 +291,9 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
             if (c0 + 32 <= ncols) tmem_ld32_nw(trow + c0, r);
             else tmem_ld16_nw(trow + c0, r);
           };
-          auto put = [&](int c0, uint32_t* r) {
+          auto put = [&](int c0, uint32_t* r) {                    // c0: a multiple of 32 (one chunk)
+            const int ch = buf * kGsMaxCh + (c0 >> 5);
+            if (use > 0) mbar_wait(&sempty[ch], (use - 1) & 1);     // its scanners are done with it
             float* d = dst + (size_t)c0 * kGsSLD;
             if (c0 + 32 <= srows) {                                // whole chunk: immediate offsets
 #pragma unroll
@@ -288,6 +303,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
               for (int k = 0; k < 32; ++k)
                 if (c0 + k < srows) d[k * kGsSLD] = __uint_as_float(r[k]) + bias;
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_local(&sfull[ch]);
           };
           uint32_t ra[32], rb[32];
           if (ncols > 0) {
@@ -307,8 +324,6 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
             tmem_fence_regs(ra);
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_local(&sfull[buf]);
         KTX(10, threadIdx.x == 64 && bt == 0 && j == 0);
       }
       tc_fence_before();                                           // batch's accumulators drained
@@ -322,6 +337,9 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     const int c = et / P, part = et % P;                           // hypothesis row (column) and part
     const int nv = kTileM / P;                                     // vocabulary rows scanned per tile
     const bool row_ok = c < a.n_group && n0 + c < a.R;
+    const int wrow0 = 32 * (warp - 2 - kGsStageWarps) / P;         // first row of this warp
+    const bool wact = wrow0 < ncols;                               // its chunk is staged at all
+    const int wch = wrow0 >> 5;
     constexpr float L2E = 1.4426950408889634f;
     float run_m = -INFINITY, run_s = 0.f;
     float tz[KMAX];
@@ -337,23 +355,39 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       const int t0 = tb + bt * a.nt_max;
       const int nt = min(a.nt_max, te - t0);
       for (int j = 0; j < nt; ++j, ++jj) {
-        const int buf = jj % a.nbuf;
+        const int buf = jj % a.nbuf, use = jj / a.nbuf;
         // the row's shared threshold: the largest list tail any scanner of any CTA published
         // so far - a K-th best of a subset of the row, so a lower bound of the row's K-th best
         // logit; values below it cannot reach the row's top-K.  Loaded before
         // the wait for the staged tile so the L2 round trip overlaps it.
         // (step 1 does not read: its buffer may still hold the previous call's last step)
+        // A second bound: slot s of the row holds the running maximum of the scanners of the
+        // CTAs ci with ci % K == s - disjoint element sets, so the K slots are K distinct
+        // elements and their minimum is a lower bound of the row's K-th best (an empty slot
+        // reads as -inf).  It is far tighter than the largest list tail once every CTA has
+        // scanned one tile.
+        float gth = -INFINITY;
+        const unsigned int* slot = a.thr + (size_t)2 * a.rows_pad + ((size_t)(a.t & 1) * a.rows_pad + n0 + c) * 16;
+        if (row_ok && a.thr && a.t != 1
 #ifdef ONMT_KTRACE
-        const float gth = (row_ok && a.thr && a.t != 1 && a.dbg != 5) ? key2f(__ldcg(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c))
-                                                        : -INFINITY;
-#else
-        const float gth = (row_ok && a.thr && a.t != 1) ? key2f(__ldcg(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c))
-                                                        : -INFINITY;
+            && a.dbg != 5
 #endif
-        mbar_wait(&sfull[buf], (jj / a.nbuf) & 1);
+        ) {
+          unsigned int kmin = 0xffffffffu;
+#pragma unroll
+          for (int q = 0; q < (KMAX + 3) / 4; ++q) {
+            const uint4 v = __ldcg(reinterpret_cast<const uint4*>(slot) + q);
+            if (4 * q < a.K) kmin = min(kmin, v.x);
+            if (4 * q + 1 < a.K) kmin = min(kmin, v.y);
+            if (4 * q + 2 < a.K) kmin = min(kmin, v.z);
+            if (4 * q + 3 < a.K) kmin = min(kmin, v.w);
+          }
+          gth = fmaxf(key2f(__ldcg(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c)), key2f(kmin));
+        }
+        if (wact) mbar_wait(&sfull[buf * kGsMaxCh + wch], use & 1);
         KTX(4, et == 0 && jj == 0);
 #ifdef ONMT_KTRACE
-        if (a.dbg == 2) { __syncwarp(); if (lane == 0) mbar_arrive_local(&sempty[buf]); continue; }
+        if (a.dbg == 2) { __syncwarp(); if (wact && lane == 0) mbar_arrive_local(&sempty[buf * kGsMaxCh + wch]); continue; }
 #endif
         if (row_ok) {
           const float* col = stg + (size_t)buf * a.srows_alloc * kGsSLD + (size_t)c * kGsSLD + part * nv;
@@ -456,10 +490,12 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 #ifdef ONMT_KTRACE
         if (a.dbg != 6)
 #endif
-        if (row_ok && a.thr && tz[KMAX - 1] != -INFINITY)              // publish my list tail
-          atomicMax(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c, f2key(tz[KMAX - 1]));
+        if (row_ok && a.thr) {                                     // publish my list tail and running max
+          if (tz[KMAX - 1] != -INFINITY) atomicMax(a.thr + (size_t)(a.t & 1) * a.rows_pad + n0 + c, f2key(tz[KMAX - 1]));
+          if (run_m != -INFINITY) atomicMax(const_cast<unsigned int*>(slot) + ci % a.K, f2key(run_m));
+        }
         __syncwarp();
-        if (lane == 0) mbar_arrive_local(&sempty[buf]);
+        if (wact && lane == 0) mbar_arrive_local(&sempty[buf * kGsMaxCh + wch]);
         KTX(5, et == 0 && jj == 0);
         KTX(11, et == 0 && jj == 1);
       }
@@ -545,7 +581,7 @@ static size_t gs_body_bytes(int n_group, int nt_max, int stages, int ovl, int nb
   const size_t stg = (size_t)nbuf * srows * kGsSLD * 4;
   return ovl ? ring + stg : (ring > stg ? ring : stg);
 }
-static size_t gs_smem_bytes(size_t body, int stages) { return 1024 + body + (2 * stages + 6) * 8 + 16; }
+static size_t gs_smem_bytes(size_t body, int stages) { return 1024 + body + (2 * stages + 2 + 4 * kGsMaxCh) * 8 + 16; }
 
 struct GsPlan {
   int C, nt_max, stages, P, ovl, nbuf, srows;

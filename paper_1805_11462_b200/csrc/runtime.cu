@@ -405,7 +405,7 @@ struct onmt_model {
   DevBuf dec_p, st_h, st_c, st_cg, htilde, logits;
   DevBuf f_scratch, f_count;                 // fused GEMM partial tiles + per-tile arrival counters
   DevBuf g_bar;                              // grid barrier counter of the generator step kernel
-  DevBuf g_thr;                              // generator: shared per-row top-K thresholds [2][rows_pad]
+  DevBuf g_thr;                              // generator: shared per-row top-K thresholds [2][rows_pad] + slots [2][rows_pad][16]
   DevBuf g_arrive;                           // generator + fused beam step: 64-bit arrival counter
   DevBuf ds_part, ds_bar;                    // fused decoder step: attention chunk partials, grid barrier
   DevBuf woh_part;                           // folded W_out: top-layer shares W_out[:, units] h [tiles][rows_pad][H]
@@ -1053,8 +1053,8 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
       m->g_arrive.ensure(256);
       ONMT_CUDA(cudaMemset(m->g_arrive.p, 0, 256));
     }
-    if (m->g_thr.bytes < (size_t)2 * m->xg.rows_pad * 4) {
-      m->g_thr.ensure((size_t)2 * m->xg.rows_pad * 4);
+    if (m->g_thr.bytes < (size_t)2 * m->xg.rows_pad * 17 * 4) {
+      m->g_thr.ensure((size_t)2 * m->xg.rows_pad * 17 * 4);
       ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
     }
     if (!m->ds_bar.p) {
@@ -2023,7 +2023,7 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
       m->g_bar.ensure(256);
       ONMT_CUDA(cudaMemset(m->g_bar.p, 0, 256));
     }
-    if (m->g_thr.bytes < (size_t)2 * x.rows_pad * 4) m->g_thr.ensure((size_t)2 * x.rows_pad * 4);
+    if (m->g_thr.bytes < (size_t)2 * x.rows_pad * 17 * 4) m->g_thr.ensure((size_t)2 * x.rows_pad * 17 * 4);
     ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
     ONMT_CUDA(gen_step(m->gen_w.tmap, x.tmap, (m->Vt + kVTile - 1) / kVTile, x.rows_pad, x.n_group,
                        m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 1, 0, 0, 1.0,

@@ -49,7 +49,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&ms, C * NP * 8)); CK(cudaMalloc(&tz, C * NP * K * 4)); CK(cudaMalloc(&ti, C * NP * K * 4));
   CK(cudaMalloc(&rl, R * 4)); CK(cudaMalloc(&rz, R * K * 4)); CK(cudaMalloc(&ri, R * K * 4));
   CK(cudaMalloc(&gbar, 64)); CK(cudaMemset(gbar, 0, 64));
-  unsigned int* thr; CK(cudaMalloc(&thr, 2 * NP * 4)); CK(cudaMemset(thr, 0, 2 * NP * 4));
+  unsigned int* thr; CK(cudaMalloc(&thr, 2 * NP * 17 * 4)); CK(cudaMemset(thr, 0, 2 * NP * 17 * 4));
   unsigned long long* tr; CK(cudaMalloc(&tr, 4096 * 96)); CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
   GenOut g{ms, tz, ti, bias, V, K, R, NP};
   // beam state / gather operands for phase C (zeroed; slot 0 of every sentence live)
