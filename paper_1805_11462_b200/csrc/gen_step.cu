@@ -55,10 +55,9 @@ struct GenStepArgs {
   unsigned long long* arrive;                   // phases == 4: monotonic arrival counter (64-bit)
   int B;                                        // phases == 4: sentences (one beam-step CTA each)
   int gbuf_floats;                              // phases == 4: dynamic smem reusable as beam staging
-  int ovl;                                      // 1: staging has its own smem and odd batches their own
-                                                //    TMEM columns (from tcol_b), so batch b+1's MMAs
-                                                //    overlap batch b's epilogue
-  int tcol_b;
+  int ovl;                                      // 1: staging has its own smem and every tile of the
+                                                //    CTA its own TMEM columns, so batch b+1's MMAs
+                                                //    overlap batch b's epilogue (batches of nt_max)
   int nbuf;                                     // staging buffers (1 or 2)
   int srows_alloc;                              // staging rows per buffer (min(n_group, R))
 };
@@ -158,7 +157,12 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   const int grp = blockIdx.x / a.C, ci = blockIdx.x % a.C;
   const int tb = (int)((long long)ci * a.n_vt / a.C), te = (int)((long long)(ci + 1) * a.n_vt / a.C);
   const int n0 = grp * a.n_group;
+  // batch bt = tiles [bfirst(bt), bfirst(bt) + bsize(bt)) of this CTA's run, staged from sequence
+  // number bfirst(bt) - tb.  ovl: two batches, the first one smaller (its epilogue starts early)
   const int nbatch = (te - tb + a.nt_max - 1) / a.nt_max;
+  auto bfirst = [&](int bt) { return tb + bt * a.nt_max; };
+  auto bsize = [&](int bt) { return min(a.nt_max, te - bfirst(bt)); };
+  auto tcol = [&](int bt, int j) { return (uint32_t)((a.ovl ? bt * a.nt_max + j : j) * a.n_group); };
   // staging is split into 32-hypothesis-row chunks with their own full/empty barriers: the
   // scanners of a chunk start as soon as it is staged and the stagers refill a chunk as soon
   // as its scanners are done (instead of whole-tile hand-offs)
@@ -206,8 +210,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     if (lane == 0) {
       int it = 0;
       for (int bt = 0; bt < nbatch; ++bt) {
-        const int t0 = tb + bt * a.nt_max;
-        const int nt = min(a.nt_max, te - t0);
+        const int t0 = bfirst(bt);
+        const int nt = bsize(bt);
         if (bt > 0 && !a.ovl) mbar_wait(tempty, (bt - 1) & 1);   // staging (ring overlay) finished
         for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
           const int s = it % a.stages;
@@ -238,7 +242,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_group);
       int it = 0;
       for (int bt = 0; bt < nbatch; ++bt) {
-        const int nt = min(a.nt_max, te - (tb + bt * a.nt_max));
+        const int nt = bsize(bt);
         for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
           const int s = it % a.stages;
           mbar_wait(&full[s], (it / a.stages) & 1);
@@ -247,7 +251,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           const uint32_t sb = smem_u32(smem + (size_t)s * stage_bytes);
           for (int j = 0; j < nt; ++j) {
             const uint32_t sa = sb + 2 * b_bytes + j * a_bytes;
-            const uint32_t d = tmem + ((a.ovl && (bt & 1)) ? a.tcol_b : 0) + j * a.n_group;
+            const uint32_t d = tmem + tcol(bt, j);
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {
               const uint64_t da = umma_desc_sw128(sa + kk * 32);
@@ -266,8 +270,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     const int q = warp & 3;                                        // TMEM lane quarter of this warp
     const int vr = q * 32 + lane;                                  // vocabulary row this thread stages
     for (int bt = 0; bt < nbatch; ++bt) {
-      const int t0 = tb + bt * a.nt_max;
-      const int nt = min(a.nt_max, te - t0);
+      const int t0 = bfirst(bt);
+      const int nt = bsize(bt);
       float bias_r[4];                                             // bias of my vocabulary row, loaded
 #pragma unroll                                                     // while the MMAs run
       for (int j = 0; j < 4; ++j) {
@@ -278,12 +282,12 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       tc_fence_after();
       KTX(2, threadIdx.x == 64 && bt == 0);
       for (int j = 0; j < nt; ++j) {
-        const int jj = bt * a.nt_max + j;                          // staging sequence number
+        const int jj = t0 - tb + j;                                // staging sequence number
         const int buf = jj % a.nbuf, use = jj / a.nbuf;
         KTX(6, threadIdx.x == 64 && jj == 2);
         {
           const float bias = j == 0 ? bias_r[0] : j == 1 ? bias_r[1] : j == 2 ? bias_r[2] : bias_r[3];
-          const uint32_t trow = tmem + ((a.ovl && (bt & 1)) ? a.tcol_b : 0) + j * a.n_group + ((uint32_t)(q * 32) << 16);
+          const uint32_t trow = tmem + tcol(bt, j) + ((uint32_t)(q * 32) << 16);
           float* dst = stg + (size_t)buf * a.srows_alloc * kGsSLD + vr;
           // 32-column chunks, software-pipelined: the load of chunk i+1 is in flight while
           // chunk i is stored (ncols is a multiple of 16: a last half chunk uses x16)
@@ -352,8 +356,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     }
     int jj = 0;
     for (int bt = 0; bt < nbatch; ++bt) {
-      const int t0 = tb + bt * a.nt_max;
-      const int nt = min(a.nt_max, te - t0);
+      const int t0 = bfirst(bt);
+      const int nt = bsize(bt);
       for (int j = 0; j < nt; ++j, ++jj) {
         const int buf = jj % a.nbuf, use = jj / a.nbuf;
         // the row's shared threshold: the largest list tail any scanner of any CTA published
@@ -620,12 +624,13 @@ static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, int R, int K
   if (p.srows < 1) p.srows = 1;
   const size_t limit = 227 * 1024 - gs_static_smem(K);
   const int need = (n_vt + p.C - 1) / p.C;                          // most tiles of a CTA
-  // overlapped batches: the CTA's tiles in two K-outer batches, the second
-  // batch's MMAs (own TMEM columns, own ring) run while the first batch is staged and scanned
-  static const int ovl_env = getenv("ONMT_GEN_OVL") ? atoi(getenv("ONMT_GEN_OVL")) : 1;
-  if (ovl_env && need >= 2 && need * n_group <= 512) {
+  // overlapped batches: the CTA's tiles in K-outer batches of ONMT_GEN_OVL tiles
+  // (every tile its own TMEM columns, staging outside the ring): batch b+1's MMAs run while
+  // batch b is staged and scanned
+  static const int ovl_env = getenv("ONMT_GEN_OVL") ? atoi(getenv("ONMT_GEN_OVL")) : 2;
+  if (ovl_env > 0 && need >= 2 && need * n_group <= 512) {
     p.ovl = 1;
-    p.nt_max = (need + 1) / 2;
+    p.nt_max = ovl_env < need ? ovl_env : need - 1;                  // tiles per batch
     p.stages = 2;
     for (p.nbuf = 2; p.nbuf >= 1; --p.nbuf) {
       p.body = gs_body_bytes(n_group, p.nt_max, p.stages, 1, p.nbuf, p.srows);
@@ -710,7 +715,6 @@ cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, i
   a.B = B;
   a.gbuf_floats = (int)(p.body / 4);
   a.ovl = p.ovl;
-  a.tcol_b = p.nt_max * n_group;
   a.nbuf = p.nbuf;
   a.srows_alloc = p.srows;
   if (phases == 4 && (!arrive || B > grid || p.C > 256)) return cudaErrorInvalidConfiguration;
