@@ -161,11 +161,36 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   __shared__ int s_prow[KMAX], s_y[KMAX], s_go[KMAX], s_src[KMAX];
   __shared__ int s_cont;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int E = ga.E, H = ga.H, L = ga.L;
+  const int state_f = H * (1 + 2 * L);                           // h~ | h_l, c_l (l < L)
+  const int emb_f = (E + 3) & ~3, st_f = (state_f + 3) & ~3;
+  // Every possible gather source is prefetched into shared memory while the rows are reduced
+  // and the survivors selected: the state rows of the live slots (issued by the last warp,
+  // idle during the row reduce) and, as soon as a row's top-K is known, the embedding rows of
+  // its K candidates (issued by that row's warp).  Each issuer raises the expected bytes of
+  // s_bar before its copies; thread 0 arrives once all rows are reduced.
+  const bool pre = gbuf != nullptr && (E & 3) == 0 && (H & 3) == 0 &&
+                   (K * K * emb_f + K * st_f) <= gbuf_floats && !(dn != 0 && dn < t);
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) { mbar_init(&s_bar, 1); fence_mbar_init(); }
   if (threadIdx.x < K) {
     s_live[threadIdx.x] = __ldcg(&live_in[b * K + threadIdx.x]);
     s_cum[threadIdx.x] = __ldcg(&cum_in[b * K + threadIdx.x]);
   }
   __syncthreads();
+  if (pre && warp == nw - 1) {
+    const int nst = 1 + 2 * L;
+    for (int c = lane; c < K * nst; c += 32) {                   // c -> slot c / nst, row kind c % nst
+      const int k = c / nst, w = c % nst;
+      if (!s_live[k]) continue;
+      const int p = b * K + k;
+      float* d = gbuf + (size_t)K * K * emb_f + (size_t)k * st_f + (size_t)w * H;
+      const float* src = w == 0 ? ga.htilde + (size_t)p * H
+                                : (((w - 1) & 1) ? ga.c : ga.h) + ((size_t)((w - 1) >> 1) * ga.rows_pad + p) * H;
+      mbar_expect_tx(&s_bar, (uint32_t)H * 4);
+      bulk_g2s(d, src, H * 4, &s_bar);
+    }
+  }
   KT(2);
   // ---- row reduce: warp k -> row b*K + k (dead slots are masked afterwards)
   for (int k = warp; k < K; k += nw) {
@@ -274,6 +299,10 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
         if (better(z2, i2, bz, bi)) { bz = z2; bi = i2; }
       }
       if (lane == 0) { s_z[k][c] = bz; s_id[k][c] = bi; }
+      if (pre && lane == c && s_live[k] && bz != -INFINITY) {   // candidate (k, c): prefetch its embedding
+        mbar_expect_tx(&s_bar, (uint32_t)E * 4);
+        bulk_g2s(gbuf + (size_t)(k * K + c) * emb_f, ga.emb_tgt + (size_t)feed_id(ga, bi) * E, E * 4, &s_bar);
+      }
       if (li[0] == bi && lz[0] == bz) {
 #pragma unroll
         for (int q = 0; q < KMAX - 1; ++q) { lz[q] = lz[q + 1]; li[q] = li[q + 1]; }
@@ -285,47 +314,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   __syncthreads();
   if (dn != 0 && dn < t) return;                                 // finished earlier (uniform)
   if (threadIdx.x < K * K && !s_live[threadIdx.x / K]) s_z[threadIdx.x / K][threadIdx.x % K] = -INFINITY;
-  // ---- prefetch every possible gather source into shared memory (it overlaps the selection):
-  //      the embedding rows of the K x K candidate tokens and the state rows of the K slots
-  const int E = ga.E, H = ga.H, L = ga.L;
-  const int state_f = H * (1 + 2 * L);                           // h~ | h_l, c_l (l < L)
-  const int emb_f = (E + 3) & ~3, st_f = (state_f + 3) & ~3;
-  const bool pre = gbuf != nullptr && (E & 3) == 0 && (H & 3) == 0 &&
-                   (K * K * emb_f + K * st_f) <= gbuf_floats;
-  __shared__ __align__(8) uint64_t s_bar;
-  if (threadIdx.x == 0) { mbar_init(&s_bar, 1); fence_mbar_init(); }
-  __syncthreads();
-  if (pre) {
-    // copy c (one thread each): c < K*(1+2L) -> slot c / (1+2L), row kind c % (1+2L) (h~, h_l, c_l);
-    // then the K*K candidate embedding rows
-    const int nst = 1 + 2 * L;
-    if (threadIdx.x == 0) {
-      uint32_t bytes = 0;
-      for (int k = 0; k < K; ++k) {
-        if (!s_live[k]) continue;
-        bytes += (uint32_t)state_f * 4;
-        for (int j = 0; j < K; ++j)
-          if (s_z[k][j] != -INFINITY) bytes += (uint32_t)E * 4;
-      }
-      mbar_arrive_expect_tx(&s_bar, bytes);
-    }
-    __syncthreads();
-    const int c = threadIdx.x;
-    if (c < K * nst) {
-      const int k = c / nst, w = c % nst;
-      if (s_live[k]) {
-        const int p = b * K + k;
-        float* d = gbuf + (size_t)K * K * emb_f + (size_t)k * st_f + (size_t)w * H;
-        const float* src = w == 0 ? ga.htilde + (size_t)p * H
-                                  : (((w - 1) & 1) ? ga.c : ga.h) + ((size_t)((w - 1) >> 1) * ga.rows_pad + p) * H;
-        bulk_g2s(d, src, H * 4, &s_bar);
-      }
-    } else if (c < K * nst + K * K) {
-      const int i = c - K * nst, k = i / K, j = i % K;
-      if (s_live[k] && s_z[k][j] != -INFINITY)
-        bulk_g2s(gbuf + (size_t)i * emb_f, ga.emb_tgt + (size_t)feed_id(ga, s_id[k][j]) * E, E * 4, &s_bar);
-    }
-  }
+  if (pre && threadIdx.x == 0) mbar_arrive_local(&s_bar);       // every issuer raised its bytes
   KT(3);
   // ---- selection (parallel ranks): candidate (k, j) = slot k's j-th row best; its raw score
   //      cum_k + z - lse_k in fp64; order (score desc, slot asc, position asc) - the merge of
@@ -468,7 +457,10 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   }
   __syncthreads();
   KT(4);
-  if (!s_cont) return;
+  if (!s_cont) {
+    if (pre) mbar_wait(&s_bar, 0);                               // (no copy may land after exit)
+    return;
+  }
   // ---- gather the next step's inputs of the K rows (x1 = [E_tgt[y]; h~[p]; h_0[p]],
   //      x_l = [.; h_l[p]], c_l[p]); dead slots are not gathered
   if (pre) {
