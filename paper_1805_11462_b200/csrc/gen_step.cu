@@ -187,6 +187,25 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     mbar_init(&sempty[i], cnt > 0 ? cnt : 1);
   }
   if (threadIdx.x == 0 || threadIdx.x == 32) fence_mbar_init();
+  // the weight tiles of the first ring stages are constants of the translation: their TMA loads
+  // are issued before griddepcontrol.wait (the activation halves follow after it)
+  int npre = nbatch > 0 ? min(a.stages, a.k_blocks) : 0;
+#ifdef ONMT_KTRACE
+  if (a.dbg == 11 || a.dbg == 12) npre = 0;
+#endif
+  auto load_act = [&](int it, int kb) {
+    uint8_t* st = smem + (size_t)(it % a.stages) * stage_bytes;
+    tma_load_2d(st, &tmX, kb * kBK, n0, &full[it % a.stages]);
+    tma_load_2d(st + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[it % a.stages]);
+  };
+  if (threadIdx.x == 0) {
+    const int nt0 = bsize(0), t00 = bfirst(0);
+    for (int it = 0; it < npre; ++it) {
+      uint8_t* st = smem + (size_t)it * stage_bytes;
+      mbar_arrive_expect_tx(&full[it], 2 * b_bytes + nt0 * a_bytes);
+      for (int j = 0; j < nt0; ++j) tma_load_2d(st + 2 * b_bytes + j * a_bytes, &tmW, it * kBK, (t00 + j) * kTileM, &full[it]);
+    }
+  }
   if (warp == 1) tmem_alloc<512>(tslot);
   tc_fence_before();
   pdl_wait();
@@ -199,6 +218,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     for (int i = threadIdx.x; i < a.rows_pad * 4; i += blockDim.x) sl[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (all_done(a.ctl)) {                                           // uniform over the grid
+    if (threadIdx.x == 0)                                          // (no TMA may land after exit)
+      for (int it = 0; it < npre; ++it) { load_act(it, it); mbar_wait(&full[it], 0); }
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
     return;
@@ -229,6 +250,10 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
             continue;
           }
 #endif
+          if (it < npre) {                                         // weights already in flight
+            load_act(it, kb);
+            continue;
+          }
           mbar_arrive_expect_tx(&full[s], 2 * b_bytes + nt * a_bytes);
           tma_load_2d(st, &tmX, kb * kBK, n0, &full[s]);
           tma_load_2d(st + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[s]);
