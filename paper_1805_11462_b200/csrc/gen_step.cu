@@ -27,7 +27,9 @@ namespace onmt {
 constexpr int kGsStageWarps = 4;               // TMEM -> smem stagers (one per TMEM lane quarter)
 constexpr int kGsScanWarps = 10;                // scanners (2 threads x 160 hypothesis rows)
 constexpr int kGsThreads = 32 * (2 + kGsStageWarps + kGsScanWarps);
-constexpr int kGsSLD = 132;                     // staging row stride (floats)
+constexpr int kGsSLD = 136;                     // staging row stride (floats; = 8 mod 32 banks: with the
+                                                // scanners' interleaved groups a quarter warp's float4
+                                                // reads hit distinct banks)
 constexpr int kGsMaxCh = 10;                    // 32-row staging chunks per buffer (n_group <= 320)
 
 struct GenStepArgs {
@@ -419,13 +421,15 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         if (a.dbg == 2) { __syncwarp(); if (wact && lane == 0) mbar_arrive_local(&sempty[buf * kGsMaxCh + wch]); continue; }
 #endif
         if (row_ok) {
-          const float* col = stg + (size_t)buf * a.srows_alloc * kGsSLD + (size_t)c * kGsSLD + part * nv;
-          const int vbase = (t0 + j) * kTileM + part * nv;
+          // part p of the row owns the tile's float4 groups p, p + P, p + 2P, ... (interleaved, ids
+          // increasing along the scan); chunk u0 / 64 covers 16 of them
+          const float* col = stg + (size_t)buf * a.srows_alloc * kGsSLD + (size_t)c * kGsSLD + 4 * part;
+          const int vbase = (t0 + j) * kTileM + 4 * part;
           for (int u0 = 0; u0 < nv; u0 += 64) {                    // 64 logits per chunk, in registers
             float z[64];
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-              const float4 w = *reinterpret_cast<const float4*>(col + u0 + 4 * k);
+              const float4 w = *reinterpret_cast<const float4*>(col + P * (u0 + 4 * k));
               z[4 * k] = w.x; z[4 * k + 1] = w.y; z[4 * k + 2] = w.z; z[4 * k + 3] = w.w;
             }
             float g[16];                                           // group maxima (groups of 4)
@@ -485,12 +489,12 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
                       int sel = 15;
 #pragma unroll
                       for (int k = 14; k >= 0; --k) sel = gg[k] == mx ? k : sel;
-                      const float4 w = *reinterpret_cast<const float4*>(col + u0 + 4 * sel);
+                      const float4 w = *reinterpret_cast<const float4*>(col + P * (u0 + 4 * sel));
                       const unsigned gone = (unsigned)(rm >> (4 * sel)) & 15u;
                       const float v0 = (gone & 1u) ? -INFINITY : w.x, v1 = (gone & 2u) ? -INFINITY : w.y;
                       const float v2 = (gone & 4u) ? -INFINITY : w.z, v3 = (gone & 8u) ? -INFINITY : w.w;
                       const int e = v0 == mx ? 0 : v1 == mx ? 1 : v2 == mx ? 2 : 3;
-                      gs_insert_scan<KMAX>(tz, ti, mx, vbase + u0 + 4 * sel + e);
+                      gs_insert_scan<KMAX>(tz, ti, mx, vbase + P * (u0 + 4 * sel) + e);
                       rm |= 1ull << (4 * sel + e);
                       const float nm = fmaxf(fmaxf(e == 0 ? -INFINITY : v0, e == 1 ? -INFINITY : v1),
                                              fmaxf(e == 2 ? -INFINITY : v2, e == 3 ? -INFINITY : v3));
@@ -506,11 +510,11 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
                 while (gm) {                                       // candidates in id order
                   const int gi = __ffs(gm) - 1;
                   gm &= gm - 1;
-                  const float4 w = *reinterpret_cast<const float4*>(col + u0 + 4 * gi);
+                  const float4 w = *reinterpret_cast<const float4*>(col + P * (u0 + 4 * gi));
                   const float wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                   for (int e = 0; e < 4; ++e)
-                    if (wv[e] >= th && wv[e] > tz[KMAX - 1]) gs_insert_scan<KMAX>(tz, ti, wv[e], vbase + u0 + 4 * gi + e);
+                    if (wv[e] >= th && wv[e] > tz[KMAX - 1]) gs_insert_scan<KMAX>(tz, ti, wv[e], vbase + P * (u0 + 4 * gi) + e);
                 }
               }
             }
