@@ -118,6 +118,15 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   auto mbuf = [&](int i) { return buf + (size_t)(i & 1) * (mb + kb); };
   float* s_hp = buf + 2 * (mb + kb);                // folded W_out: the combine slice's tile shares
   float* s_esave = s_hp + fo.hp_floats;             // attention output: my chunk's raw scores [K][CH]
+  // push combine (vec): every chunk stores its partial context slices into the owners' receive
+  // buffers [source chunk][K][4 * wjm] and its (m, l) into every rank's s_rbm / s_rbl before the
+  // cluster barrier; the combine then reads only local shared memory and no CTA reads a peer's
+  // memory after the barrier (no trailing cluster barrier)
+  // (measured: faster at c5 - 8 chunks, K = 10: 36 -> 28 us - slightly slower at c2 - 4 chunks, K = 5)
+  const bool push = vec && (nch >= 8 || K >= 8);
+  const int wjm = ((H >> 2) + nch - 1) / nch;
+  float* rb = s_esave + (fo.att_out ? r4((size_t)K * CH) : 0);
+  __shared__ float s_rbm[8 * KMAX], s_rbl[8 * KMAX];
   auto kbuf = [&](int i) { return same ? mbuf(i) : mbuf(i) + mb; };
 
   // source rows [s_beg, s_lim) of this chunk, prefetched before griddepcontrol.wait without
@@ -359,14 +368,39 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   if (hpref) cp_async_wait<1>();                   // (q, and prefetches past S_b; the W_out shares
   else cp_async_wait<0>();                         //  are waited for only by the combine)
   __syncthreads();
-  // ---- park the unnormalised partial context in q's place (q is no longer read)
+  if (push) {
+    // ---- push my unnormalised partial context: column j goes to the chunk that owns it
+    const int H4 = H >> 2;
 #pragma unroll
-  for (int u = 0; u < JPT; ++u) {
-    const int j = threadIdx.x + u * kAttThreads;
-    if (j >= H) continue;
+    for (int u = 0; u < JPT; ++u) {
+      const int j = threadIdx.x + u * kAttThreads;
+      if (j >= H) continue;
+      const int j4 = j >> 2;
+      int o = nch - 1;
+      while (o > 0 && (int)((long long)H4 * o / nch) > j4) --o;
+      const int j0o = (int)((long long)H4 * o / nch);
+      const uint32_t base = mapa_peer(smem_u32(rb + ((size_t)r * K) * 4 * wjm + (j - 4 * j0o)), (uint32_t)o);
 #pragma unroll
-    for (int k = 0; k < KMAX; ++k)
-      if (k < K) q[(size_t)k * H + j] = acc[k][u];
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) st_cluster_b32(base + (uint32_t)(k * 4 * wjm) * 4u, __float_as_uint(acc[k][u]));
+    }
+    if (threadIdx.x < K) {
+      const int k = threadIdx.x;
+      for (int p = 0; p < nch; ++p) {
+        st_cluster_b32(mapa_peer(smem_u32(s_rbm + r * KMAX + k), (uint32_t)p), __float_as_uint(s_m[k]));
+        st_cluster_b32(mapa_peer(smem_u32(s_rbl + r * KMAX + k), (uint32_t)p), __float_as_uint(s_l[k]));
+      }
+    }
+  } else {
+    // ---- park the unnormalised partial context in q's place (q is no longer read)
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) {
+      const int j = threadIdx.x + u * kAttThreads;
+      if (j >= H) continue;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) q[(size_t)k * H + j] = acc[k][u];
+    }
   }
   KT(5);
   cluster_arrive();
@@ -379,8 +413,8 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
     float mp[8], lp[8];
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
-      mp[p] = p < nch ? ld_peer(s_m + k, p) : -INFINITY;
-      lp[p] = p < nch ? ld_peer(s_l + k, p) : 0.f;
+      mp[p] = p < nch ? (push ? s_rbm[p * KMAX + k] : ld_peer(s_m + k, p)) : -INFINITY;
+      lp[p] = p < nch ? (push ? s_rbl[p * KMAX + k] : ld_peer(s_l + k, p)) : 0.f;
     }
     float M = -INFINITY;
 #pragma unroll
@@ -415,7 +449,10 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
       const int k = it / wj, j = 4 * (j0 + it % wj);
       float4 v[8];
 #pragma unroll
-      for (int p = 0; p < 8; ++p) v[p] = p < nch ? ld_peer4(q + (size_t)k * H + j, p) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int p = 0; p < 8; ++p)
+        v[p] = p >= nch ? make_float4(0.f, 0.f, 0.f, 0.f)
+               : push ? *reinterpret_cast<const float4*>(rb + ((size_t)p * K + k) * 4 * wjm + (j - 4 * j0))
+                      : ld_peer4(q + (size_t)k * H + j, p);
       float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
@@ -485,8 +522,10 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
     }
   }
   KT(7);
-  cluster_arrive();                                // peers may still be reading my partial
-  cluster_wait();
+  if (!push) {
+    cluster_arrive();                              // peers may still be reading my partial
+    cluster_wait();
+  }
   KT(8);
 }
 
@@ -545,11 +584,12 @@ static AttPlan att_plan(int B, int S_max, int H, int K, int key_ld, int val_ld, 
     };
     size_t extra = 0;                              // folded W_out: prefetched tile shares
     if (fo.wpart) extra = (size_t)fo.n_wt * K * ((H / 4 + nch - 1) / nch) * 16;
-    const size_t esave = fo.att_out ? (size_t)K * CH * 4 : 0;   // attention output: raw scores
+    const size_t esave = fo.att_out ? r4((size_t)K * CH) * 4 : 0;   // attention output: raw scores
+    const size_t rbb = (size_t)nch * K * 16 * ((H / 4 + nch - 1) / nch);   // push-combine receive buffer
     const int SC = bytes(16) + extra <= 200 * 1024 ? 16 : 8;
-    fo.pref = bytes(SC) + extra + esave <= 220 * 1024;
+    fo.pref = bytes(SC) + extra + esave + rbb <= 220 * 1024;
     fo.hp_floats = fo.pref ? (int)(extra / 4) : 0;
-    p = AttPlan{nch, CH, SC, bytes(SC) + (fo.pref ? extra : 0) + esave};
+    p = AttPlan{nch, CH, SC, bytes(SC) + (fo.pref ? extra : 0) + esave + rbb};
     if (forced || nch == 1) break;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess) break;
     cudaLaunchConfig_t cfg = {};
