@@ -333,15 +333,17 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     s_valid[threadIdx.x] = ok;
     s_sc[threadIdx.x] = ok ? s_cum[k] + ((double)z - (double)s_lse[k]) : -CUDART_INF;
   }
-  __syncthreads();
+  // (invalid candidates carry score -inf and never outrank a valid one, whose score is finite:
+  //  the rank loop needs no validity test and its loads pipeline)
+  const int nvalid = __syncthreads_count(threadIdx.x < KK && s_valid[threadIdx.x]);
+  KTX(7, threadIdx.x == 0);
   if (threadIdx.x < KK) {
     const int i = threadIdx.x;
-    int rank = 0, nvalid = 0;
     if (s_valid[i]) {
       const double sc = s_sc[i];
-      for (int c = 0; c < KK; ++c) {                             // (c < i: earlier slot, or same slot earlier position)
-        if (!s_valid[c]) continue;
-        ++nvalid;
+      int rank = 0;                                              // (c < i: earlier slot, or same slot earlier position)
+#pragma unroll 5
+      for (int c = 0; c < KK; ++c) {
         const double o = s_sc[c];
         rank += (o > sc) || (o == sc && c < i);
       }
@@ -355,13 +357,10 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
       }
       if (rank == 0) s_nsel = nvalid < K ? nvalid : K;
     }
-    if (i == 0 && nvalid == 0) {
-      bool any = false;
-      for (int c = 0; c < KK; ++c) any |= s_valid[c] != 0;
-      if (!any) s_nsel = 0;
-    }
+    if (i == 0 && nvalid == 0) s_nsel = 0;
   }
   __syncthreads();
+  KTX(8, threadIdx.x == 0);
   const int n_sel = s_nsel;
   const bool stop = [&] {
     bool any_live = false;
@@ -430,6 +429,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     }
     __syncthreads();
   }
+  KTX(9, threadIdx.x == 0);
   if (threadIdx.x == 0) {
     s_cont = !stop;
     // sentence-level banking (final_score = raw / lp + cp, S436-439) into the n-best list

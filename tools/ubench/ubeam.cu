@@ -58,7 +58,7 @@ int main() {
   for (int c = 0; c < B; ++c) for (int i = 0; i < 12; ++i) if (h[c * 12 + i]) {
     double d = (h[c * 12 + i] - t0) / 1e3; avg[i] += d; cnt[i]++; mx[i] = std::max(mx[i], d); }
   printf("beam_step: %.2f us/launch (graph of 20)\n", ms_ * 1000 / 20);
-  const char* nm[12] = {"entry", "after pdl/done", "live/cum loaded", "rows reduced", "selected", "gather staged", "exit", "rr: loaded", "rr: theta", "rr: lists", "rr: lse+argmax", "all rows (sync)"};
+  const char* nm[12] = {"entry", "after pdl/done", "live/cum loaded", "rows reduced", "selected", "gather staged", "exit", "sc ready", "ranked", "owners done", "", ""};
   for (int i = 0; i < 12; ++i) if (cnt[i]) printf("   %-16s avg %7.2f  max %7.2f us (n=%d)\n", nm[i], avg[i] / cnt[i], mx[i], cnt[i]);
   return 0;
 }
