@@ -206,14 +206,16 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
       v[u] = p < n_parts ? __ldcg(&ms[ix]) : make_float2(-INFINITY, 0.f);
       hz[u] = p < n_parts ? __ldcg(&tz[ix * K]) : -INFINITY;
     }
-    float m = -INFINITY, sm = 0.f;
+    // LSE: the row maximum first (warp), then every partial's sum rescaled to it - independent
+    // terms instead of a running (max, sum) chain
+    float m = -INFINITY;
 #pragma unroll
-    for (int u = 0; u < PPL; ++u) {
-      if (v[u].x == -INFINITY) continue;
-      const float M = fmaxf(m, v[u].x);
-      sm = (m == -INFINITY ? 0.f : sm * __expf(m - M)) + v[u].y * __expf(v[u].x - M);
-      m = M;
-    }
+    for (int u = 0; u < PPL; ++u) m = fmaxf(m, v[u].x);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float sm = 0.f;
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) sm += v[u].x == -INFINITY ? 0.f : v[u].y * __expf(v[u].x - m);
     // (2) theta = K-th largest partial maximum: a partial whose best logit is below it holds
     //     no row top-K entry (K other entries beat all of its entries)
     float theta = -INFINITY;
@@ -282,12 +284,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sm, o);
-      const float M = fmaxf(m, m2);
-      sm = (m == -INFINITY ? 0.f : sm * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
-      m = M;
-    }
+    for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
     if (lane == 0) s_lse[k] = m + logf(sm);
     for (int c = 0; c < K; ++c) {                                // K rounds of warp arg-max over list heads
       float bz = lz[0];
