@@ -585,7 +585,7 @@ static AttPlan att_plan(int B, int S_max, int H, int K, int key_ld, int val_ld, 
     size_t extra = 0;                              // folded W_out: prefetched tile shares
     if (fo.wpart) extra = (size_t)fo.n_wt * K * ((H / 4 + nch - 1) / nch) * 16;
     const size_t esave = fo.att_out ? r4((size_t)K * CH) * 4 : 0;   // attention output: raw scores
-    const size_t rbb = (size_t)nch * K * 16 * ((H / 4 + nch - 1) / nch);   // push-combine receive buffer
+    const size_t rbb = (nch >= 8 || K >= 8) ? (size_t)nch * K * 16 * ((H / 4 + nch - 1) / nch) : 0;   // push combine
     const int SC = bytes(16) + extra <= 200 * 1024 ? 16 : 8;
     fo.pref = bytes(SC) + extra + esave + rbb <= 220 * 1024;
     fo.hp_floats = fo.pref ? (int)(extra / 4) : 0;
