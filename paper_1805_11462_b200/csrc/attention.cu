@@ -481,15 +481,9 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
         }
         const float4 ht = make_float4(att_tanh(c.x + hs.x), att_tanh(c.y + hs.y), att_tanh(c.z + hs.z), att_tanh(c.w + hs.w));
         *reinterpret_cast<float4*>(fo.htilde + (size_t)row * H + j) = ht;
-        store_x(fo.xg, row, j, ht.x);
-        store_x(fo.xg, row, j + 1, ht.y);
-        store_x(fo.xg, row, j + 2, ht.z);
-        store_x(fo.xg, row, j + 3, ht.w);
+        store_x4(fo.xg, row, j, ht);                               // (8-byte hi / lo stores)
       } else {
-        store_x(xo, row, j, c.x);
-        store_x(xo, row, j + 1, c.y);
-        store_x(xo, row, j + 2, c.z);
-        store_x(xo, row, j + 3, c.w);
+        store_x4(xo, row, j, c);
       }
     }
   } else {
