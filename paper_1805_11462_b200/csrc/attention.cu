@@ -411,10 +411,18 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   if (threadIdx.x < K) {
     const int k = threadIdx.x;
     float mp[8], lp[8];
+    if (push) {
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      mp[p] = p < nch ? (push ? s_rbm[p * KMAX + k] : ld_peer(s_m + k, p)) : -INFINITY;
-      lp[p] = p < nch ? (push ? s_rbl[p * KMAX + k] : ld_peer(s_l + k, p)) : 0.f;
+      for (int p = 0; p < 8; ++p) {
+        mp[p] = p < nch ? s_rbm[p * KMAX + k] : -INFINITY;
+        lp[p] = p < nch ? s_rbl[p * KMAX + k] : 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        mp[p] = p < nch ? ld_peer(s_m + k, p) : -INFINITY;
+        lp[p] = p < nch ? ld_peer(s_l + k, p) : 0.f;
+      }
     }
     float M = -INFINITY;
 #pragma unroll
@@ -448,11 +456,15 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
     for (int it = threadIdx.x; it < K * wj; it += blockDim.x) {
       const int k = it / wj, j = 4 * (j0 + it % wj);
       float4 v[8];
+      if (push) {                                  // (separate loops: the DSMEM loads stay back to back)
 #pragma unroll
-      for (int p = 0; p < 8; ++p)
-        v[p] = p >= nch ? make_float4(0.f, 0.f, 0.f, 0.f)
-               : push ? *reinterpret_cast<const float4*>(rb + ((size_t)p * K + k) * 4 * wjm + (j - 4 * j0))
-                      : ld_peer4(q + (size_t)k * H + j, p);
+        for (int p = 0; p < 8; ++p)
+          v[p] = p < nch ? *reinterpret_cast<const float4*>(rb + ((size_t)p * K + k) * 4 * wjm + (j - 4 * j0))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+#pragma unroll
+        for (int p = 0; p < 8; ++p) v[p] = p < nch ? ld_peer4(q + (size_t)k * H + j, p) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
