@@ -230,8 +230,6 @@ ONMT_API onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_src_ids,
  *                   same kernel (L2 round trip + per-tile arrival counter) and apply the
  *                   LSTM cell / tanh there (default); 0 = separate partial GEMM + consumer
  *                   kernels.  Both give the same result up to fp32 summation order.
- *   "gen_multicast" 1 = share the generator's activation tiles across 4-CTA clusters by
- *                   TMA multicast; 0 = off (default; measured slower at c2).
  * INVALID_ARG on an unknown name or value.
  */
 ONMT_API onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t value);

@@ -49,7 +49,6 @@ struct FusedArgs {
   // units' share  W_out[:, units] h[units, cols]  to woh_part[m_tile][row][H] (fp32)
   const __nv_bfloat16* woh;
   float* woh_part;
-  int cl4;                 // split-K exchange: 1 = two 4-CTA clusters per tile (DSMEM + L2 pair), 0 = L2
   StepCtl ctl;
   int dbg;                 // microbenchmark ablations (ONMT_KTRACE builds only)
 };
@@ -90,7 +89,6 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   const uint32_t stage_bytes = a_bytes + 2 * b_bytes;
   const size_t ring = (size_t)a.stages * stage_bytes;
   size_t recv_bytes = (size_t)(a.S + 1) * a.NC * kTileM * 4;         // recv [S][NC][128] + red [NC][128]
-  if (a.cl4) recv_bytes = (size_t)(a.n_group + 2 * a.NC) * kTileM * 4;   // recv4 [4][n/4][128] + part + red
   float* recv = reinterpret_cast<float*>(smem);                  // [S][NC][128], overlays the ring
   uint8_t* tail = smem + (ring > recv_bytes ? ring : recv_bytes);
   float4* s_bias = reinterpret_cast<float4*>(tail);               // [32] (cell)
@@ -117,8 +115,7 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   int nkb = a.k_blocks - kb0;
   if (nkb > a.kb_per_split) nkb = a.kb_per_split;
   if (nkb < 0) nkb = 0;
-  // first hypothesis column I own (cluster exchange: block 2 * rank + cluster of the tile)
-  const int c_own = (a.cl4 ? 2 * (split & 3) + (split >> 2) : split) * a.NC;
+  const int c_own = split * a.NC;                                  // first hypothesis column I own
   const int ncols = max(0, min(a.NC, a.n_group - c_own));
 
   // ---- prologue (overlaps the predecessor under PDL): barriers, TMEM, weight prefetch
@@ -209,77 +206,7 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
     return;
   }
   float* red;
-  if (a.cl4) {
-    // ---- (3') split-K exchange in two 4-CTA clusters per tile: a DSMEM reduce-scatter of the
-    //      partial tiles inside each cluster (rank p owns column block p of n/4 columns), then
-    //      a pairwise exchange of half blocks with the same rank of the tile's other cluster
-    //      through L2.  Fixed summation order (deterministic).
-    const int W4 = a.n_group >> 2, rho = split & 3, cpar = split >> 2;
-    float* recv4 = reinterpret_cast<float*>(smem);                 // [4 src][W4][128], overlays the ring
-    float* part = recv4 + (size_t)4 * W4 * kTileM;                 // partner's half [NC][128]
-    red = part + (size_t)a.NC * kTileM;                            // [NC][128]
-    tc_fence_before();
-    cluster_arrive();                                              // every split's MMAs retired: the
-    cluster_wait();                                                // rings may be overwritten
-    tc_fence_after();
-    {
-      const int q = warp & 3, hh = warp >> 2;
-      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-      const int row = q * 32 + lane;
-      for (int p = hh; p < 4; p += 2) {
-        for (int c0 = 0; c0 < W4; c0 += 8) {
-          uint32_t r[8];
-          if (nkb > 0) {
-            tmem_ld8_nw(trow + p * W4 + c0, r);
-            tmem_wait_ld();
-            tmem_fence_regs(r);
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) r[k] = 0u;
-          }
-          float* dst = recv4 + ((size_t)rho * W4 + c0) * kTileM + row;
-          if (p == rho) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) dst[(size_t)k * kTileM] = __uint_as_float(r[k]);
-          } else {
-            const uint32_t pa = mapa_peer(smem_u32(dst), (uint32_t)p);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) st_cluster_b32(pa + (uint32_t)k * kTileM * 4u, r[k]);
-          }
-        }
-      }
-    }
-    tc_fence_before();
-    cluster_arrive();                                              // my block of all 4 splits landed
-    cluster_wait();
-    KT(3);
-    // cluster sum of my block; the half I own stays (in slot 0), the other half goes to the
-    // partner CTA through L2
-    float* out = a.scratch + (size_t)(tile * a.S + split) * a.NC * kTileM;   // [NC][128]
-    for (int i = threadIdx.x; i < W4 * kTileM; i += blockDim.x) {
-      float v = recv4[i];
-      v += recv4[(size_t)W4 * kTileM + i];
-      v += recv4[(size_t)2 * W4 * kTileM + i];
-      v += recv4[(size_t)3 * W4 * kTileM + i];
-      const int c = i / kTileM, hc = c / a.NC;
-      if (hc == cpar) recv4[i] = v;
-      else __stcg(out + (size_t)(c - hc * a.NC) * kTileM + (i % kTileM), v);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      cta_group_barrier(a.counters + 2 * (tile * 4 + rho), 2u);   // both halves stored
-      asm volatile("fence.proxy.async;" ::: "memory");
-      KT(4);
-      const uint32_t bytes = (uint32_t)a.NC * kTileM * 4;
-      mbar_arrive_expect_tx(rbar, bytes);
-      bulk_g2s(part, a.scratch + (size_t)(tile * a.S + (split ^ 4)) * a.NC * kTileM, bytes, rbar);
-    }
-    mbar_wait(rbar, 0);
-    KT(5);
-    const float* mine = recv4 + (size_t)cpar * a.NC * kTileM;
-    for (int i = threadIdx.x; i < a.NC * kTileM; i += blockDim.x)
-      red[i] = cpar == 0 ? mine[i] + part[i] : part[i] + mine[i];   // cluster 0 + cluster 1
-  } else {
+  {
   // ---- (3) partial tile: TMEM -> registers -> global scratch [tile][split][n/4][128][4]
     //      (each thread stores float4 = 4 consecutive columns of its row: a warp writes 512
     //      contiguous bytes), then release the tile counter
@@ -471,10 +398,9 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   KT(7);
 }
 
-static size_t fused_smem_bytes(int n_group, int stages, int S, int NC, int fold_H, int cl4 = 0) {
+static size_t fused_smem_bytes(int n_group, int stages, int S, int NC, int fold_H) {
   const size_t ring = (size_t)stages * (kTileM * 128 + 2 * (size_t)n_group * 128);
-  size_t recv = (size_t)(S + 1) * kTileM * NC * 4;
-  if (cl4) recv = (size_t)(n_group + 2 * NC) * kTileM * 4;
+  const size_t recv = (size_t)(S + 1) * kTileM * NC * 4;
   const size_t fold = fold_H ? 128 + (size_t)32 * fold_ld(fold_H) * 2 + (size_t)32 * ((NC + 23) / 24 * 24) * 4 : 0;
   return 1024 + (ring > recv ? ring : recv) + 32 * 16 + (size_t)NC * 32 * 4 + (stages + 3) * 8 + 16 + fold;
 }
@@ -504,13 +430,6 @@ static bool fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, 
     a.NC = NC;
     a.kb_per_split = kbps;
     a.stages = kbps;
-    // cluster exchange: 8 splits as two 4-CTA clusters (n_group a multiple of 32 so every block
-    // and half block is a whole number of 8- and 4-column chunks)
-    // (opt-in, ONMT_GEMM_CL4=1: parity-tested but measured 3 us slower per kernel at c2 - the
-    //  DSMEM reduce-scatter moves 60 KB per CTA at ~20 B/clk)
-    const char* ce = std::getenv("ONMT_GEMM_CL4");
-    a.cl4 = (S == 8 && n_group % 32 == 0 && NC * 8 == n_group && ce && std::atoi(ce) != 0 &&
-             fused_smem_bytes(n_group, kbps, S, NC, fold_H, 1) <= limit) ? 1 : 0;
     int tc = 32;
     while (tc < n_group) tc <<= 1;
     a.tmem_cols = tc;
@@ -525,35 +444,12 @@ static cudaError_t launch_fused(const CUtensorMap& tmW, const CUtensorMap& tmX, 
                                 cudaStream_t st) {
   // at least 116 KB of shared memory: never two CTAs of this kernel on one SM (the tile wait
   // relies on one CTA per SM with grid <= #SMs)
-  size_t smem = fused_smem_bytes(a.n_group, a.stages, a.S, a.NC, a.woh ? a.H : 0, a.cl4);
+  size_t smem = fused_smem_bytes(a.n_group, a.stages, a.S, a.NC, a.woh ? a.H : 0);
   if (smem < 116 * 1024) smem = 116 * 1024;
   auto fn = tc_gemm_fused_kernel<EPI>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (!a.cl4) return launch_pdl(fn, dim3(tiles * a.S), dim3(256), smem, st, tmW, tmX, a);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(tiles * a.S);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 4;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int ncl = 0;                                   // every cluster co-resident (the pair exchange waits)
-  if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl < tiles * 2) {
-    cudaGetLastError();
-    FusedArgs b = a;
-    b.cl4 = 0;
-    return launch_pdl(fn, dim3(tiles * a.S), dim3(256), smem, st, tmW, tmX, b);
-  }
-  cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, fn, tmW, tmX, a);
+  return launch_pdl(fn, dim3(tiles * a.S), dim3(256), smem, st, tmW, tmX, a);
 }
 
 // scratch floats a fused call needs (0 = no fused configuration fits)

@@ -602,14 +602,6 @@ static size_t genp_smem_bytes(int n_group, int stages, int kmax) {
          (size_t)n_group * (2 + 2 * kmax) * 4 + (2 * stages + 4) * 8 + 16;
 }
 
-// cluster size for the activation multicast (1 = off): needs n_group % (8*CS) == 0
-int gen_cluster_size(int n_group, int n_vt, int n_groups, int num_sms) {
-  const int cs = 4;
-  if (n_group % (8 * cs) != 0) return 1;
-  if (num_sms / n_groups < cs || n_vt < cs) return 1;
-  return cs;
-}
-
 // number of partials per row the persistent generator writes (C = CTAs per N-group)
 int gen_persistent_parts(int n_vt, int n_groups, int num_sms, int cs) {
   int C = num_sms / n_groups;
@@ -656,6 +648,7 @@ cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, in
   a.k_blocks = k_blocks;
   a.n_vt = n_vt;
   const int groups = n_rows_pad / n_group;
+  if (cs != 1) return cudaErrorInvalidValue;                 // (the multicast variant was removed)
   a.C = gen_persistent_parts(n_vt, groups, num_sms, cs);
   a.ctl = ctl;
   const size_t limit = 227 * 1024;
@@ -668,7 +661,7 @@ cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, in
   if (genp_smem_bytes(n_group, stages, kmax) > limit) return cudaErrorInvalidConfiguration;
   const int grid = a.C * groups;
 #define ONMT_GENP(KM)                                                     \
-  return cs == 4 ? launch_genp<KM, 4>(tmW, tmX, a, g, grid, st) : launch_genp<KM, 1>(tmW, tmX, a, g, grid, st)
+  return launch_genp<KM, 1>(tmW, tmX, a, g, grid, st)
   if (g.K <= 1) ONMT_GENP(1);
   if (g.K <= 2) ONMT_GENP(2);
   if (g.K <= 4) ONMT_GENP(4);

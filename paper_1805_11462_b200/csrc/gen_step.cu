@@ -2,11 +2,8 @@
 //
 //   phase A  generator + log-softmax statistics + per-CTA top-K (PAPER.md P118-119):
 //            z = W_gen h~ + b for every vocabulary id, logits never written to HBM.
-//   (option) the beam step of the decoder step (P136-139; beam_device.cuh), run by the
-//            last B CTAs to finish (phases == 4; off by default).
 //
-// Grid = groups x C CTAs, one per SM (grid <= #SMs: all co-resident, which the optional
-// beam step's wait on the arrival counter relies on).  Phase A is "K-outer": CTA (g, i) owns a contiguous run of nt
+// Grid = groups x C CTAs, one per SM.  Phase A is "K-outer": CTA (g, i) owns a contiguous run of nt
 // vocabulary tiles (128 rows each) of N-group g and keeps all nt accumulators in TMEM
 // (nt * n_group <= 512 columns), so every activation K-block (hi/lo planes, the MMA B
 // operand) crosses L2 -> SM once per CTA instead of once per tile.
@@ -43,20 +40,12 @@ struct GenStepArgs {
   float* row_lse;                               // [R]
   float* row_z;                                 // [R][K]
   int* row_i;
-  int phases;                                   // 1 = phase A, 4 = phase A + the fused beam step
-  int t, max_len;
-  double lp;
-  BeamState bs;
-  GatherArgs ga;
-  unsigned int* gbar;                           // grid barrier {count, generation}
+  int t;
   unsigned int* thr;                            // [2][rows_pad] shared top-K thresholds (ordered
                                                 // uint keys; buffer t & 1, the other one is reset),
                                                 // then [2][rows_pad][16] running-max slots
   StepCtl ctl;
   int dbg;                                      // microbenchmark ablations (ONMT_KTRACE builds)
-  unsigned long long* arrive;                   // phases == 4: monotonic arrival counter (64-bit)
-  int B;                                        // phases == 4: sentences (one beam-step CTA each)
-  int gbuf_floats;                              // phases == 4: dynamic smem reusable as beam staging
   int ovl;                                      // 1: staging has its own smem and every tile of the
                                                 //    CTA its own TMEM columns, so batch b+1's MMAs
                                                 //    overlap batch b's epilogue (batches of nt_max)
@@ -576,37 +565,6 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
-  if (a.phases == 4) {
-    // ============================================================ fused beam step (A10 + A5)
-    // Every CTA counts itself in after its partials are stored (release); the LAST B CTAs
-    // to arrive stay: each waits for the whole grid (all co-resident) and runs the beam step
-    // of one sentence (beam_device.cuh) - the separate beam-step launch disappears.
-    __shared__ unsigned long long s_arr;
-    if (threadIdx.x == 0) {
-      __threadfence();
-      s_arr = atomicAdd(a.arrive, 1ull);
-    }
-    __syncthreads();
-    const unsigned long long G = gridDim.x;
-    const unsigned long long idx = s_arr % G;
-    if (idx < G - (unsigned long long)a.B) return;
-    const int b = (int)(idx - (G - (unsigned long long)a.B));
-    if (threadIdx.x == 0) {
-      const unsigned long long target = (s_arr / G + 1ull) * G;   // this step's generation complete
-      while (true) {
-        unsigned long long v;
-        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.arrive) : "memory");
-        if (v >= target) break;
-      }
-      __threadfence();
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging (generic) -> bulk copies
-    __syncthreads();
-    KT(4);
-    beam_step_sentence<KMAX>(b, a.ms, a.tz, a.ti, a.C, 1, a.C, a.K, a.R, a.t, a.max_len, a.lp, a.bs, a.ga,
-                             reinterpret_cast<float*>(smem), a.gbuf_floats);
-    return;
-  }
 }
 
 static size_t gs_body_bytes(int n_group, int nt_max, int stages, int ovl, int nbuf, int srows) {
@@ -620,8 +578,7 @@ struct GsPlan {
   int C, nt_max, stages, P, ovl, nbuf, srows;
   size_t body;
 };
-// static shared memory of the kernel instance for beam width K (the fused beam step's arrays):
-// the dynamic part gets the rest
+// static shared memory of the kernel instance for beam width K: the dynamic part gets the rest
 template <int KMAX>
 static size_t gs_static_of() {
   cudaFuncAttributes fa;
@@ -698,12 +655,10 @@ static cudaError_t launch_gs(const CUtensorMap& tmW, const CUtensorMap& tmX, con
   return launch_pdl(fn, dim3(grid), dim3(kGsThreads), smem, st, tmW, tmX, a);
 }
 
-// phases: 1 = generator partials, 4 = + the beam step by the last-arriving CTAs
+// generator partials of decode step t (t selects the threshold buffers)
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
-                     int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i,
-                     int phases, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
-                     unsigned int* gbar, unsigned int* thr, StepCtl ctl, cudaStream_t st,
-                     unsigned long long* arrive, int B) {
+                     int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i, int t,
+                     unsigned int* thr, StepCtl ctl, cudaStream_t st) {
   const int groups = n_rows_pad / n_group;
   GsPlan p;
   if (!gs_plan(n_vt, n_group, groups, num_sms, g.rows_valid, g.K, p)) return cudaErrorInvalidConfiguration;
@@ -728,25 +683,15 @@ cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, i
   a.row_lse = row_lse;
   a.row_z = row_z;
   a.row_i = row_i;
-  a.phases = phases;
   a.t = t;
-  a.max_len = max_len;
-  a.lp = lp;
-  a.bs = bs;
-  a.ga = ga;
-  a.gbar = gbar;
   a.thr = thr;
   a.ctl = ctl;
   a.dbg = g_gs_dbg;
   const int grid = p.C * groups;
   const size_t smem = gs_smem_bytes(p.body, p.stages);
-  a.arrive = arrive;
-  a.B = B;
-  a.gbuf_floats = (int)(p.body / 4);
   a.ovl = p.ovl;
   a.nbuf = p.nbuf;
   a.srows_alloc = p.srows;
-  if (phases == 4 && (!arrive || B > grid || p.C > 256)) return cudaErrorInvalidConfiguration;
   if (g.K <= 1) return launch_gs<1>(tmW, tmX, a, grid, smem, st);
   if (g.K <= 2) return launch_gs<2>(tmW, tmX, a, grid, smem, st);
   if (g.K <= 4) return launch_gs<4>(tmW, tmX, a, grid, smem, st);

@@ -26,7 +26,6 @@
 
 #include "../../include/onmt.h"
 #include "common.cuh"
-#include "dec_step.cuh"
 
 namespace onmt {
 // kernels / launchers defined in the other translation units
@@ -39,11 +38,8 @@ cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, in
 int gen_persistent_parts(int n_vt, int n_groups, int num_sms, int cs);
 int gen_step_parts(int n_vt, int n_group, int groups, int num_sms);
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
-                     int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i,
-                     int phases, int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga,
-                     unsigned int* gbar, unsigned int* thr, StepCtl ctl, cudaStream_t st,
-                     unsigned long long* arrive = nullptr, int B = 0);
-int gen_cluster_size(int n_group, int n_vt, int n_groups, int num_sms);
+                     int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i, int t,
+                     unsigned int* thr, StepCtl ctl, cudaStream_t st);
 extern unsigned long long* g_gen_dbg;
 
 cudaError_t simt_gemm_partial(const void* W, bool w_bf16, int m_pad, int k_pad, const float* X, int n_rows_pad,
@@ -271,7 +267,7 @@ struct Act {
   int rows = 0, rows_pad = 0, n_group = 0, k = 0, k_pad = 0;
   bool bf16 = false;
   DevBuf f32, hl;
-  CUtensorMap tmap, tmap_q;   // box rows n_group / box rows n_group/4 (generator multicast slices)
+  CUtensorMap tmap;           // box {64, n_group}
   void ensure(int rows_, int k_, bool bf) {
     RowPlan rp = plan_rows(rows_);
     int kp = round_up(k_, kBK);
@@ -283,7 +279,6 @@ struct Act {
       hl.ensure((size_t)2 * rows_pad * k_pad * 2);
       ONMT_CUDA(cudaMemset(hl.p, 0, (size_t)2 * rows_pad * k_pad * 2));
       tmap = make_tmap(hl.p, k_pad, 2 * rows_pad, n_group);
-      if (n_group % 32 == 0) tmap_q = make_tmap(hl.p, k_pad, 2 * rows_pad, n_group / 4);
     }
   }
   XOut xo(bool use_tc) const {
@@ -359,17 +354,12 @@ struct onmt_model {
   bool bidir = false, general = false;
   bool use_tc = false;       // tcgen05 GEMM backend (bf16 models)
   int profile = 0;             // 0 off, 1 generator launches only, 2 every kernel family
-  bool gen_mc = false;         // generator activation multicast across 4-CTA clusters (measured slower on c2)
   bool fused = true;           // split-K GEMM with the reduction and the cell / tanh epilogue fused in
                                // (one launch per layer instead of GEMM + consumer kernel)
   bool gen_step = true;        // K-outer persistent generator (gen_step.cu)
   bool fold_wout = true;       // W_out folded into the top cell layer + attention (no W_out launch)
   bool enc_persistent = true;  // encoder recurrence of a layer as one persistent kernel (enc_rec.cu)
-  bool fuse_beam = false;      // beam step run by the generator's last-arriving CTAs (gen_step.cu phases 4;
-                               // opt-in: parity-tested but measured 3 us/step slower than the separate launch)
   bool fold_cur = false;       // ... for the call being enqueued (fold_on)
-  bool dec_fused = false;      // decoder cells + attention + W_out as one persistent kernel (dec_step.cu;
-                               // opt-in: measured slower than the per-layer kernels)
   bool use_graph = true;
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -404,10 +394,7 @@ struct onmt_model {
   Act xo, xg;
   DevBuf dec_p, st_h, st_c, st_cg, htilde, logits;
   DevBuf f_scratch, f_count;                 // fused GEMM partial tiles + per-tile arrival counters
-  DevBuf g_bar;                              // grid barrier counter of the generator step kernel
   DevBuf g_thr;                              // generator: shared per-row top-K thresholds [2][rows_pad] + slots [2][rows_pad][16]
-  DevBuf g_arrive;                           // generator + fused beam step: 64-bit arrival counter
-  DevBuf ds_part, ds_bar;                    // fused decoder step: attention chunk partials, grid barrier
   DevBuf woh_part;                           // folded W_out: top-layer shares W_out[:, units] h [tiles][rows_pad][H]
   DevBuf g_ms, g_tz, g_ti;
   DevBuf row_lse, row_z, row_i;
@@ -482,11 +469,6 @@ static void prof_end(onmt_model* m, const char* name, const EvPair& ev) {
   else m->evs[name].pending.push_back({ev, true});
 }
 
-// partials per row written by the generator for operand X
-static int gen_cs(onmt_model* m, const Act& X) {
-  const int n_vt = (m->Vt + kVTile - 1) / kVTile;
-  return m->gen_mc ? gen_cluster_size(X.n_group, n_vt, X.rows_pad / X.n_group, m->num_sms) : 1;
-}
 static bool use_gen_step(onmt_model* m, const Act& X) {
   const int n_vt = (m->Vt + kVTile - 1) / kVTile;
   return m->use_tc && m->gen_step && gen_step_parts(n_vt, X.n_group, X.rows_pad / X.n_group, m->num_sms) > 0;
@@ -494,15 +476,14 @@ static bool use_gen_step(onmt_model* m, const Act& X) {
 static int gen_parts(onmt_model* m, const Act& X) {
   const int n_vt = (m->Vt + kVTile - 1) / kVTile;
   if (use_gen_step(m, X)) return gen_step_parts(n_vt, X.n_group, X.rows_pad / X.n_group, m->num_sms);
-  return m->use_tc ? gen_persistent_parts(n_vt, X.rows_pad / X.n_group, m->num_sms, gen_cs(m, X)) : n_vt;
+  return m->use_tc ? gen_persistent_parts(n_vt, X.rows_pad / X.n_group, m->num_sms, 1) : n_vt;
 }
 
 static void gen(onmt_model* m, const Act& X, const GenOut& g, StepCtl ctl) {
   EvPair ev = prof_begin(m, "gen");
   if (m->use_tc) {
-    const int cs = gen_cs(m, X);
-    ONMT_CUDA(tc_gen_persistent(m->gen_w.tmap, cs > 1 ? X.tmap_q : X.tmap, m->gen_w.m_pad / kTileM, X.rows_pad,
-                                X.n_group, m->gen_w.k_pad / kBK, m->num_sms, cs, g, ctl, m->stream));
+    ONMT_CUDA(tc_gen_persistent(m->gen_w.tmap, X.tmap, m->gen_w.m_pad / kTileM, X.rows_pad, X.n_group,
+                                m->gen_w.k_pad / kBK, m->num_sms, 1, g, ctl, m->stream));
     count(m);
   } else {
     m->logits.ensure((size_t)X.rows_pad * m->gen_w.m_pad * 4);
@@ -744,7 +725,7 @@ static void load_model(onmt_model* m, const char* path) {
 // W_out folded away: bf16 models on the fused cell-GEMM path whose top
 // layer kernel fits the extra W_out share
 static bool fold_on(onmt_model* m, int rows) {
-  if (!(m->use_tc && m->fused && !m->dec_fused && m->fold_wout && m->attn_woc.m > 0)) return false;
+  if (!(m->use_tc && m->fused && m->fold_wout && m->attn_woc.m > 0)) return false;
   const Mat& W = *m->dec_w[m->L - 1];
   const RowPlan rp = plan_rows(rows);
   return tc_cell_fold_fits(W.m_pad, rp.rows_pad, rp.n_group, W.k_pad / kBK, m->H, m->num_sms);
@@ -1041,29 +1022,10 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
     for (int l = 0; l < L; ++l)
       fs = std::max(fs, fused_scratch_floats(m->dec_w[l]->m_pad, m->xdec[l]->rows_pad, m->xdec[l]->n_group,
                                              m->dec_w[l]->k_pad / kBK, m->num_sms));
-    int ng = m->xo.n_group;                          // fused decoder step: tiles * S <= #SMs
-    for (int l = 0; l < L; ++l) ng = std::max(ng, m->xdec[l]->n_group);
-    fs = std::max(fs, (size_t)m->num_sms * ng * kTileM);
     m->f_scratch.ensure(std::max<size_t>(fs, 1) * 4);
-    if (!m->g_bar.p) {
-      m->g_bar.ensure(256);
-      ONMT_CUDA(cudaMemset(m->g_bar.p, 0, 256));
-    }
-    if (!m->g_arrive.p) {
-      m->g_arrive.ensure(256);
-      ONMT_CUDA(cudaMemset(m->g_arrive.p, 0, 256));
-    }
     if (m->g_thr.bytes < (size_t)2 * m->xg.rows_pad * 17 * 4) {
       m->g_thr.ensure((size_t)2 * m->xg.rows_pad * 17 * 4);
       ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
-    }
-    if (!m->ds_bar.p) {
-      m->ds_bar.ensure(256);
-      ONMT_CUDA(cudaMemset(m->ds_bar.p, 0, 256));
-    }
-    {
-      const int nch = dec_step_att_chunks(B, S_max, m->num_sms);
-      m->ds_part.ensure((size_t)B * nch * K * (2 + H) * 4);
     }
     const size_t nc = (size_t)(L + 1) * 2048 * 4;
     if (m->f_count.bytes < nc) {
@@ -1071,55 +1033,6 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
       ONMT_CUDA(cudaMemset(m->f_count.p, 0, nc));
     }
   }
-}
-
-// Specs of the fused decoder step (dec_step.cu): L cell GEMMs + W_out, attention operands.
-static void dec_step_specs(onmt_model* m, const int* d_lens, int B, int S_max, int K, const BeamState& bs,
-                           std::vector<DsGemmSpec>& specs, DsAtt& att) {
-  const bool bf = m->use_tc;
-  const int R = B * K, H = m->H, L = m->L;
-  const int rp = m->xg.rows_pad;
-  float* hh = m->st_h.as<float>();
-  float* cc = m->st_c.as<float>();
-  float* cg = m->st_cg.as<float>();
-  specs.assign(L + 1, DsGemmSpec{});
-  for (int l = 0; l < L; ++l) {
-    const Mat& W = *m->dec_w[l];
-    const Act& X = *m->xdec[l];
-    DsGemmSpec& sp = specs[l];
-    sp.tmW = &W.tmap; sp.tmX = &X.tmap;
-    sp.m_pad = W.m_pad; sp.n_rows_pad = X.rows_pad; sp.n_group = X.n_group; sp.n_valid = R;
-    sp.k_blocks = W.k_pad / kBK; sp.M = 4 * H;
-    sp.scratch = m->f_scratch.as<float>();
-    sp.counters = m->f_count.as<unsigned int>() + (size_t)l * 2048;
-    sp.epi = 0;
-    sp.bias = m->dec_bias[l]->as<float>();
-    sp.cg = cg + (size_t)l * rp * H; sp.c_out = cc + (size_t)l * rp * H; sp.h_out = hh + (size_t)l * rp * H;
-    sp.H = H;
-    CellDst dst{};
-    if (l + 1 < L) { dst.x[0] = m->xdec[l + 1]->xo(bf); dst.col[0] = 0; dst.n = 1; }
-    else { dst.x[0] = m->xo.xo(bf); dst.col[0] = H; dst.n = 1; }
-    sp.dst = dst;
-  }
-  DsGemmSpec& so = specs[L];
-  so.tmW = &m->attn_wout.tmap; so.tmX = &m->xo.tmap;
-  so.m_pad = m->attn_wout.m_pad; so.n_rows_pad = m->xo.rows_pad; so.n_group = m->xo.n_group; so.n_valid = R;
-  so.k_blocks = m->attn_wout.k_pad / kBK; so.M = H;
-  so.scratch = m->f_scratch.as<float>();
-  so.counters = m->f_count.as<unsigned int>() + (size_t)L * 2048;
-  so.epi = 1;
-  so.htilde = m->htilde.as<float>();
-  so.xg = m->xg.xo(bf);
-  att = DsAtt{};
-  att.htop = hh + (size_t)(L - 1) * rp * H;
-  att.keys = m->general ? m->keys.as<float>() : m->mem.as<float>();
-  att.key_ld = m->general ? m->attn_win_t.m_pad : H;
-  att.mem = m->mem.as<float>();
-  att.lens = d_lens;
-  att.B = B; att.S_max = S_max; att.H = H; att.K = K;
-  att.xo = m->xo.xo(bf);
-  att.done = bs.done;
-  att.part = m->ds_part.as<float>();
 }
 
 // One decoder step up to h~ (A5 inputs already gathered): the L LSTM layers, attention and
@@ -1279,49 +1192,18 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
     count(m, 3);
   };
   float* P = m->dec_p.as<float>();
-  std::vector<DsGemmSpec> ds_specs;
-  DsAtt ds_att;
-  bool ds_on = false;
-  if (m->use_tc && m->dec_fused && !op.att()) {
-    dec_step_specs(m, d_lens, B, S_max, K, bs, ds_specs, ds_att);
-    ds_on = dec_step(ds_specs.data(), L, ds_att, m->ds_bar.as<unsigned int>(), ctl, m->num_sms, nullptr, nullptr) ==
-            cudaSuccess;
-  }
   for (int t = 1; t <= max_len; ++t) {
     EvPair ev = prof_begin(m, "step");
-    if (ds_on) {
-      EvPair pd = prof_begin(m, "gemm");
-      ONMT_CUDA(dec_step(ds_specs.data(), L, ds_att, m->ds_bar.as<unsigned int>(), ctl, m->num_sms, nullptr,
-                         m->stream));
-      count(m);
-      prof_end(m, "gemm", pd);
-    }
-    if (!ds_on) enqueue_dec_layers(m, d_lens, B, S_max, K, bs.done, m->xg.xo(bf), ctl, op.att() ? m->b_att.as<float>() : nullptr);
+    enqueue_dec_layers(m, d_lens, B, S_max, K, bs.done, m->xg.xo(bf), ctl, op.att() ? m->b_att.as<float>() : nullptr);
     const double lp = std::pow((5.0 + t) / 6.0, (double)alpha);
     if (use_gen_step(m, m->xg)) {
       // K-outer generator (phase A of gen_step.cu), partials [row][C]; then row reduce + beam step
       EvPair pgs = prof_begin(m, "gen");
-      // generator + (fused) beam step: the generator's last B CTAs to finish run the beam step
-      cudaError_t ge = cudaErrorInvalidConfiguration;
-      if (m->fuse_beam && !op.src_ext)
-        ge = gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
-                      m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
-                      m->row_i.as<int>(), 4, t, max_len, lp, bs, ga, m->g_bar.as<unsigned int>(),
-                      m->g_thr.as<unsigned int>(), ctl, m->stream, m->g_arrive.as<unsigned long long>(), B);
-      const bool fused_beam = ge == cudaSuccess;
-      if (!fused_beam) {
-        if (ge != cudaErrorInvalidConfiguration) ONMT_CUDA(ge);
-        ONMT_CUDA(gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
+      ONMT_CUDA(gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
                            m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
-                           m->row_i.as<int>(), 1, t, max_len, lp, bs, ga, m->g_bar.as<unsigned int>(),
-                           m->g_thr.as<unsigned int>(), ctl, m->stream));
-      }
+                           m->row_i.as<int>(), t, m->g_thr.as<unsigned int>(), ctl, m->stream));
       count(m);
       prof_end(m, "gen", pgs);
-      if (fused_beam) {
-        prof_end(m, "step", ev);
-        continue;
-      }
       EvPair pm = prof_begin(m, "merge");
       if (op.src_ext) {
         merge_copy(n_vt, 1, n_vt, t, lp);
@@ -1348,31 +1230,6 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
   launch_finalize(bs, B, K, max_len, out.hyps, out.lens, out.scores, out.raw, out.tlogp, out.unk_pos, m->stream);
   count(m);
   ONMT_CUDA(cudaGetLastError());
-}
-
-// ONMT_KTRACE builds + env ONMT_PHASES=1: per-CTA phase stamps of the last fused decoder step
-static unsigned long long* g_phase_buf = nullptr;
-static void phase_trace_begin() {
-  if (!std::getenv("ONMT_PHASES")) return;
-  if (!g_phase_buf) cudaMalloc(&g_phase_buf, 4096 * 12 * 8);
-  cudaMemset(g_phase_buf, 0, 4096 * 12 * 8);
-  dec_step_set_trace(g_phase_buf);
-}
-static void phase_trace_end(int grid) {
-  if (!std::getenv("ONMT_PHASES") || !g_phase_buf) return;
-  cudaDeviceSynchronize();
-  std::vector<unsigned long long> h((size_t)grid * 12);
-  cudaMemcpy(h.data(), g_phase_buf, h.size() * 8, cudaMemcpyDeviceToHost);
-  unsigned long long t0 = ~0ull;
-  for (int c = 0; c < grid; ++c) if (h[c * 12]) t0 = std::min(t0, h[c * 12]);
-  const char* nm[12] = {"entry", "pdl_wait", "L1 done", "sync", "L2 done", "sync", "att chunks", "sync",
-                        "att combine", "sync", "W_out done", "exit"};
-  for (int i = 0; i < 12; ++i) {
-    double s = 0, mx = 0; int n = 0;
-    for (int c = 0; c < grid; ++c) if (h[c * 12 + i]) { double d = (h[c * 12 + i] - t0) / 1e3; s += d; mx = std::max(mx, d); ++n; }
-    std::fprintf(stderr, "  %-12s avg %7.2f max %7.2f us (n=%d)\n", nm[i], n ? s / n : 0.0, mx, n);
-  }
-  dec_step_set_trace(nullptr);
 }
 
 // Teacher-forced scoring: encoder, then T_max decoder steps fed with
@@ -1456,7 +1313,7 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
     enqueue_score(m, d_ids, d_lens, B, S_max, T_max);
     return;
   }
-  std::vector<int64_t> key = {B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->dec_fused, m->fold_cur,
+  std::vector<int64_t> key = {B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->fold_cur,
                               m->enc_persistent,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
                               (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
@@ -1508,13 +1365,11 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     enqueue_decoder(m, d_lens, B, S_max, K, max_len, alpha, trace, out, op);
   };
   if (!m->use_graph) {
-    phase_trace_begin();
     enqueue();
-    phase_trace_end(m->num_sms);
     return;
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
-                              m->gen_step, m->dec_fused, m->fold_cur, m->enc_persistent, m->fuse_beam,
+                              m->gen_step, m->fold_cur, m->enc_persistent,
                               m->enc_wavefront,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
@@ -1608,13 +1463,10 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
     if (n >= 8 && n < m->num_sms) m->num_sms = n;
   }
   if (const char* ev = std::getenv("ONMT_USE_GRAPH")) m->use_graph = std::atoi(ev) != 0;   // ncu runs use 0
-  if (const char* ev = std::getenv("ONMT_GEN_MULTICAST")) m->gen_mc = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_FUSED_GEMM")) m->fused = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_GEN_STEP")) m->gen_step = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("ONMT_DEC_FUSED")) m->dec_fused = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_FOLD_WOUT")) m->fold_wout = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_PERSISTENT")) m->enc_persistent = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("ONMT_FUSE_BEAM")) m->fuse_beam = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_WAVE")) m->enc_wavefront = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
@@ -1649,18 +1501,12 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->profile = (int)v;
   } else if (n == "fused_gemm") {
     m->fused = v != 0;
-  } else if (n == "gen_multicast") {
-    m->gen_mc = v != 0;
   } else if (n == "gen_step") {
     m->gen_step = v != 0;
-  } else if (n == "dec_fused") {
-    m->dec_fused = v != 0;
   } else if (n == "fold_wout") {
     m->fold_wout = v != 0;
   } else if (n == "enc_persistent") {
     m->enc_persistent = v != 0;
-  } else if (n == "fuse_beam") {
-    m->fuse_beam = v != 0;
   } else if (n == "enc_wavefront") {
     m->enc_wavefront = v != 0;
   } else if (n == "use_graph") {
@@ -2019,16 +1865,11 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
   }
   const bool gs = use_gen_step(m, x);
   if (gs) {
-    if (!m->g_bar.p) {
-      m->g_bar.ensure(256);
-      ONMT_CUDA(cudaMemset(m->g_bar.p, 0, 256));
-    }
     if (m->g_thr.bytes < (size_t)2 * x.rows_pad * 17 * 4) m->g_thr.ensure((size_t)2 * x.rows_pad * 17 * 4);
     ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
     ONMT_CUDA(gen_step(m->gen_w.tmap, x.tmap, (m->Vt + kVTile - 1) / kVTile, x.rows_pad, x.n_group,
-                       m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 1, 0, 0, 1.0,
-                       BeamState{}, GatherArgs{}, m->g_bar.as<unsigned int>(), m->g_thr.as<unsigned int>(),
-                       StepCtl{nullptr, 0}, m->stream));
+                       m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 0,
+                       m->g_thr.as<unsigned int>(), StepCtl{nullptr, 0}, m->stream));
   } else {
     gen(m, x, g, StepCtl{nullptr, 0});
   }

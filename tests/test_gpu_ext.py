@@ -123,26 +123,6 @@ def test_ex_errors(weight_cache):
         gm.translate_ex(ids, lens, 3, 10, 0.0, -1.0, 1)     # beta < 0
 
 
-def test_fused_beam_step_option(weight_cache):
-    """The generator kernel's fused beam step (option fuse_beam) computes exactly what the
-    separate beam-step kernel does (same device function, same inputs)."""
-    cfg = synth.ModelConfig(2, 64, 128, 300, 2000, False, True)
-    gm, om, prec = toy_pair(cfg, 2, 0.1, weight_cache, "bf16")
-    ids, lens = synth.make_corpus("c1")
-    a = gm.translate(ids, lens, 5, 8, 0.6)
-    gm.set_option("fuse_beam", 1)
-    try:
-        b = gm.translate(ids, lens, 5, 8, 0.6)
-        c = gm.translate_ex(ids, lens, 5, 8, 0.6, 0.3, 3, True)
-    finally:
-        gm.set_option("fuse_beam", 0)
-    d = gm.translate_ex(ids, lens, 5, 8, 0.6, 0.3, 3, True)
-    for k in ("hyps", "lens", "scores", "token_logp"):
-        assert np.array_equal(a[k], b[k]), k
-        assert np.array_equal(c[k], d[k]), k
-    assert np.array_equal(c["unk_pos"], d["unk_pos"])
-
-
 @pytest.mark.parametrize("layers,bidir", [(3, False), (2, False), (2, True)])
 def test_persistent_encoders_match_per_step_path(weight_cache, layers, bidir):
     """The persistent encoders (enc_rec.cu; the unidirectional layer wavefront enc_wave.cu)
