@@ -94,18 +94,6 @@ def test_bf16_parity_subset(workload, n, max_len, weight_cache):
     assert res["match"] + res["excused"] == n
 
 
-def test_c2_full_length_sentence(weight_cache):
-    """One c2 sentence decoded to BASELINE's max_len = 100 (full-size launch config)."""
-    gm, om, prec = model_pair("c2", weight_cache)
-    ids, lens = synth.make_corpus("c2", 30)
-    gpu = gm.translate(ids, lens, 5, 100, 0.0, trace=True)
-    assert (gpu["lens"] == 100).all()          # random weights: every sentence runs to max_len
-    sub = [0]
-    res = compare_batch(om, ids[sub], lens[sub], {k: (v[:, sub] if k.startswith("sel_") else v[sub])
-                                                  for k, v in gpu.items()}, 5, 100, 0.0, prec)
-    assert res["fail"] == 0, res["details"]
-
-
 def test_fp32_mode_c2_model_subset(weight_cache):
     """fp32 mode on the c2 model (SIMT path): token log p within 1e-5."""
     gm, om, prec = model_pair("c2", weight_cache, precision="fp32")
@@ -135,6 +123,31 @@ def test_toy_models_peaky(prec, cfg, K, alpha, eos_bias, weight_cache):
     assert res["match"] + res["excused"] == 6
     if K > 1:
         assert (gpu["sel_token"] == synth.EOS).any()     # the EOS banking path really ran
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("cfg", [TOY, TOY_BI])
+@pytest.mark.parametrize("K,alpha", [(3, 0.6), (5, 0.0)])
+def test_toy_models_large_weights(prec, cfg, K, alpha, weight_cache):
+    """The round-1 toy models at their original scale, U(-1.5, 1.5) (no peaky output layer):
+    chaotic recurrences that amplify rounding.  Bars: reading R34 - max(north_star bar, 10 x the
+    oracle's own change under a unit-roundoff perturbation of the weights), per sentence; the
+    derived bars are printed.  EOS finishes happen naturally at this scale."""
+    from parity import compare_sentence, derived_tolerances
+    gm, om, p = toy_pair(cfg, 11, 1.5, weight_cache, prec, name="toy15")
+    rng = np.random.default_rng(100 + K)
+    lens = rng.integers(1, 12, 6).astype(np.int32)
+    ids = np.zeros((6, 12), np.int32)
+    for b in range(6):
+        ids[b, :lens[b]] = rng.integers(4, 60, lens[b])
+    gpu = gm.translate(ids, lens, K, 15, alpha, trace=True)
+    for b in range(6):
+        src = [int(v) for v in ids[b, :lens[b]]]
+        hyp = [int(v) for v in gpu["hyps"][b, :gpu["lens"][b]]]
+        tie, ltol, d_tok, d_cum = derived_tolerances(om, src, hyp, p)
+        st, det = compare_sentence(om, src, gpu, b, K, 15, alpha, p, tie=tie, logp_tol=ltol)
+        print(f"{p} b={b}: {st} logp_err={det['logp_err']:.2e} (bar {ltol:.2e}; sensitivity tok {d_tok:.2e} cum {d_cum:.2e})")
+        assert st != "fail", det
 
 
 def test_beam1_equals_oracle_greedy(weight_cache):

@@ -89,3 +89,49 @@ def test_extended_id_fed_back_as_unk():
     y2 = score_sequence(m, src, [4, 1, 6, 3], src_ext=ext)
     np.testing.assert_allclose(y1[2:], y2[2:], atol=1e-14)
     assert y1[1] != y2[1]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_copy_gate_reads_attentional_vector(seed):
+    """copy_gate with w != 0 (reading R31: g = sigmoid(copy.w . h~ + copy.b), h~ the attentional
+    vector, SPEC S293-297).  Closed-form model: W_in = 0 (uniform attention a_s = 1/S, S273-style),
+    W_out = [0 | kappa I] (h~ = tanh(kappa h_1)), W_gen = 0, b_gen = 0 (p_vocab = 1/V), so
+    p(w) = g / V + (1 - g) n_w / S (S296).  h_1 comes from torch.nn.LSTM / LSTMCell (library),
+    not from the oracle; feeding h_1 instead of h~ to the gate, a wrong sign or a dropped bias
+    fails it."""
+    import torch
+    cfg = synth.ModelConfig(1, 5, 6, 12, 9, False, True, copy=True)
+    t = {k: v.astype(np.float64) for k, v in synth.random_model_tensors(cfg, 70 + seed, 1.0).items()}
+    H, V, kappa = 6, 9, 2.0
+    t["attn.w_in"] = np.zeros((H, H))
+    t["attn.w_out"] = np.concatenate([np.zeros((H, H)), kappa * np.eye(H)], axis=1)
+    t["gen.w"] = np.zeros((V, H))
+    t["gen.b"] = np.zeros(V)
+    rng = np.random.default_rng(seed)
+    t["copy.w"] = rng.uniform(-2, 2, (1, H))
+    t["copy.b"] = np.array([rng.uniform(-1, 1)])
+    m = OracleModel(t)
+    src = [5, 9, 5, 11]
+    ext = [5, 9 + 0, 5, 10]                 # id 5 shared twice, 9 and 10 source-only (V = 9)
+    with torch.no_grad():
+        enc = torch.nn.LSTM(5, H, 1, batch_first=True).double()
+        enc.weight_ih_l0.copy_(torch.from_numpy(t["enc.l0.fwd.w_ih"]))
+        enc.weight_hh_l0.copy_(torch.from_numpy(t["enc.l0.fwd.w_hh"]))
+        enc.bias_ih_l0.copy_(torch.from_numpy(t["enc.l0.fwd.b_ih"]))
+        enc.bias_hh_l0.copy_(torch.from_numpy(t["enc.l0.fwd.b_hh"]))
+        x = torch.from_numpy(t["enc.emb"][src])[None]
+        _, (h0, c0) = enc(x)
+        cell = torch.nn.LSTMCell(5 + H, H).double()
+        cell.weight_ih.copy_(torch.from_numpy(t["dec.l0.w_ih"]))
+        cell.weight_hh.copy_(torch.from_numpy(t["dec.l0.w_hh"]))
+        cell.bias_ih.copy_(torch.from_numpy(t["dec.l0.b_ih"]))
+        cell.bias_hh.copy_(torch.from_numpy(t["dec.l0.b_hh"]))
+        u = torch.cat([torch.from_numpy(t["dec.emb"][2]), torch.zeros(H, dtype=torch.float64)])[None]
+        h1, _ = cell(u, (h0[0], c0[0]))
+        ht = torch.tanh(kappa * h1[0]).numpy()
+    g = 1.0 / (1.0 + math.exp(-(float(t["copy.w"][0] @ ht) + float(t["copy.b"][0]))))
+    S = len(src)
+    want = {5: g / V + (1 - g) * 2 / S, 9: (1 - g) / S, 10: (1 - g) / S, 4: g / V}
+    for w, p in want.items():
+        got = score_sequence(m, src, [w], src_ext=ext)[0]
+        assert abs(got - math.log(p)) <= 1e-12, (w, got, math.log(p))
