@@ -101,6 +101,52 @@ def gen_roofline_terms(w: synth.Workload, R: int):
 
 
 # ---------------------------------------------------------------------------- ours
+def corpus_run(model, args, w, ws, rank, dev):
+    """Corpus mode (SURVEY §8(d) timing corpus; PAPER.md P233-235 "translating a large set of
+    sentences"): the workload's corpus (c2: 30 x 8 x 16 = 3840 sentences) cut into batches of
+    the workload's size in corpus order, dealt round-robin to the ranks, each batch trimmed to
+    its own longest source and translated through the host API (onmt_translate: H2D of its
+    ids / lengths and D2H of every output inside the timed region), then one gather of every
+    output with the original indices.  Whole-corpus tokens / the max over ranks of the wall
+    time of the (barrier-bracketed) pass; one untimed pass first captures the few graphs the
+    bucketed source lengths need."""
+    import torch
+    import torch.distributed as dist
+    from paper_1805_11462_b200.parallel import deal_batches, gather_results, make_batches, translate_batches
+    B, K, ML, alpha = w.data.batch, w.decode.beam, w.decode.max_len, w.decode.alpha
+    n = CORPUS[args.workload]
+    ids, lens = synth.make_corpus(args.workload, n)
+    batches = make_batches(n, B)
+    mine = deal_batches(len(batches), ws, rank)
+    model.set_stream(None)
+    translate_batches(model, ids, lens, batches, mine, K, ML, alpha)      # warm-up: graphs captured
+    cap0 = model.graph_captures()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    local, idx = translate_batches(model, ids, lens, batches, mine, K, ML, alpha)
+    if ws > 1:
+        g = gather_results({k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in local.items()},
+                           torch.from_numpy(idx).to(dev), n_total=n)
+        total_tokens = int(g["lens"].sum().item())
+    else:
+        total_tokens = int(local["lens"].sum())
+    dt = time.perf_counter() - t0
+    recaptures = model.graph_captures() - cap0
+    if ws > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": round(total_tokens / dt, 1), "unit": "target tok/s", "sentences": n, "batches": len(batches),
+            "batch": B, "tokens": total_tokens, "wall_s": round(dt, 4), "graph_captures_in_timed_pass": int(recaptures),
+            "graphs_cached": int(cap0), "timing": "host wall clock, barrier-bracketed, max over ranks; host API "
+            "(H2D/D2H per batch inside); batches dealt round-robin, one gather of every output + indices"}
+
+
+CORPUS = {"c1": 2, "c2": 3840, "c3": 64 * 8, "c4": 128 * 8, "c5": 16 * 8}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -112,7 +158,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     w = synth.WORKLOADS[args.workload]
-    B, K, ML, alpha = w.data.batch, w.decode.beam, w.decode.max_len, w.decode.alpha
+    B_wl, K, ML, alpha = w.data.batch, w.decode.beam, w.decode.max_len, w.decode.alpha
     cache = os.environ.get("ONMT_WEIGHT_CACHE", os.path.join(tempfile.gettempdir(), "onmt_weights"))
     if rank == 0 or ws == 1:
         path = synth.weights_file(args.workload, cache)
@@ -120,10 +166,16 @@ def run_ours(args):
         dist.barrier()
         path = synth.weights_file(args.workload, cache)
     model = ob.Model(path, local, w.decode.precision)
-    # weak scaling: rank r translates sentences [r*B, (r+1)*B) of one seeded corpus
     from paper_1805_11462_b200.parallel import gather_results, rank_slice
-    ids_all, lens_all = synth.make_corpus(args.workload, B * ws)
-    b0, b1 = rank_slice(B * ws, ws, rank)
+    if args.scaling == "weak":
+        # weak scaling: rank r translates its own full batch, sentences [r*B, (r+1)*B) of one corpus
+        ids_all, lens_all = synth.make_corpus(args.workload, B_wl * ws)
+        b0, b1 = rank_slice(B_wl * ws, ws, rank)
+    else:
+        # strong scaling: the workload's one batch sharded by sentence over the ranks
+        ids_all, lens_all = synth.make_corpus(args.workload)
+        b0, b1 = rank_slice(B_wl, ws, rank)
+    B = b1 - b0
     ids = np.ascontiguousarray(ids_all[b0:b1])
     lens = np.ascontiguousarray(lens_all[b0:b1])
     S = int(lens.max())
@@ -134,6 +186,7 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         ids_d = torch.from_numpy(ids).to(dev)
         lens_d = torch.from_numpy(lens).to(dev)
+        index_d = torch.arange(b0, b1, dtype=torch.int64, device=dev)
         out = {"hyps": torch.zeros((B, ML), dtype=torch.int32, device=dev),
                "lens": torch.zeros(B, dtype=torch.int32, device=dev),
                "scores": torch.zeros(B, dtype=torch.float32, device=dev),
@@ -143,38 +196,47 @@ def run_ours(args):
     def step():
         model.translate_dev(ids_d, lens_d, K, ML, alpha, out, lens)
         if ws > 1:
-            gather_results(out)                  # the path's only collective (NCCL all-gather)
+            gather_results(out, index_d)        # the path's only collective (NCCL all-gather)
 
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            step()
-        stream.synchronize()
-        model.launches(reset=True)
-        model.set_option("profile", 1)         # events around the generator launches only
-        step()                                  # (re)capture the profiled decode graph outside timing
+    def timed_pass(profile):
+        model.set_option("profile", profile)
+        step()                                  # (re)capture this variant's graph outside timing
         stream.synchronize()
         model.launches(reset=True)
         for fam in FAMILIES:
             model.kernel_time(fam, reset=True)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        clk = ClockSampler(local)
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        clk.start()
-        tokens = 0
         for i in range(args.steps):
-            flush.zero_()                                   # L2 flush between timed steps
+            flush.zero_()                       # L2 flush between timed steps
             evs[i][0].record(stream)
             step()
             evs[i][1].record(stream)
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
+        return sum(a.elapsed_time(b) for a, b in evs), model.launches(reset=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        stream.synchronize()
+        # (1) THE timed region: uninstrumented graph (no event nodes between kernels)
+        model.set_option("profile", 0)
+        step()
+        stream.synchronize()
+        clk = ClockSampler(local)
+        clk.start()
+        t_ms, launches = timed_pass(0)
         clocks = clk.stop()
-        launches = model.launches(reset=True)
+        tokens = int(out["lens"].sum().item()) * args.steps
+        # (2) same steps again with CUDA events around every generator launch (the roofline's
+        #     per-launch duration; the events serialise the generator with its neighbours)
+        t_ms_gen_pass, _ = timed_pass(1)
         gen_ms, gen_n = model.kernel_time("gen", reset=True)
-        # untimed pass with every kernel family instrumented, for the per-family breakdown
+        # (3) one untimed call with every kernel family instrumented, for the breakdown
         model.set_option("profile", 2)
         step()
         stream.synchronize()
@@ -183,8 +245,6 @@ def run_ours(args):
         step()
         fam_t = {fam: model.kernel_time(fam, reset=True) for fam in FAMILIES}
         model.set_option("profile", 0)
-    tokens = int(out["lens"].sum().item()) * args.steps
-    t_ms = sum(a.elapsed_time(b) for a, b in evs)
     if ws > 1:
         tt = torch.tensor([t_ms, float(tokens)], dtype=torch.float64, device=dev)
         tmax = tt.clone()
@@ -197,6 +257,8 @@ def run_ours(args):
     model.set_stream(None)
     model.translate(ids, lens, K, ML, alpha)        # warm-up: capture the host-API graph untimed
     e2e_ms = []
+    if ws > 1:
+        dist.barrier()
     for i in range(max(1, args.steps)):
         flush.zero_()
         torch.cuda.synchronize()
@@ -213,6 +275,7 @@ def run_ours(args):
         e2e_t, e2e_tokens = float(tm[0].item()), int(tt[1].item())
     h2d = ids.nbytes + lens.nbytes
     d2h = B * ML * 4 * 2 + B * 4 * 3
+    corpus = corpus_run(model, args, w, ws, rank, dev) if not args.no_corpus else None
 
     if rank == 0:
         pk = peaks()
@@ -227,15 +290,17 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "target tok/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded U(-0.1,0.1) weights, Zipf(1.1) ids; DESIGN.md §3)",
             "config": {"workload": args.workload, "model": "2x500 LSTM enc-dec, general attn, input feed, V=50k"
                        if args.workload == "c2" else args.workload,
-                       "global_batch": B * ws, "batch_per_gpu": B, "beam": K, "max_len": ML,
+                       "global_batch": B_wl * ws if args.scaling == "weak" else B_wl, "batch_per_gpu": B,
+                       "beam": K, "max_len": ML,
                        "length_penalty": alpha, "src_len": [w.data.len_lo, w.data.len_hi],
-                       "parallelism": f"dp{ws} (sentence-sharded, NCCL all-gather of hypotheses)",
+                       "parallelism": f"dp{ws} (sentence-sharded, NCCL all-gather of every output + indices)",
                        "l2": "flushed (512 MB write) between timed steps; weights stay L2-resident "
-                             "across the decode steps of one step"},
+                             "across the decode steps of one step",
+                       "timed_graph": "uninstrumented (no CUDA-event nodes inside the call)"},
             "e2e": {"value": round(e2e_tokens / (e2e_t / 1e3), 1), "unit": "target tok/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
@@ -245,8 +310,10 @@ def run_ours(args):
                          "peak_src": pk["src"],
                          "algorithmic_bytes_per_launch": gbytes, "flops_per_launch": gflops,
                          "avg_launch_us": round(gen_avg_s * 1e6, 3), "launches": gen_n,
+                         "timing": "CUDA events around every generator launch in a second timed pass of the "
+                                   "same steps (ms_per_step of that pass: %.4f)" % (t_ms_gen_pass / args.steps),
                          "tensor_tflops_algorithmic": round(gflops / gen_avg_s / 1e12, 1),
-                         "gen_share_of_step": round(gen_ms / (t_ms * 1.0), 4) if t_ms else None},
+                         "gen_share_of_step": round(gen_ms / t_ms_gen_pass, 4) if t_ms_gen_pass else None},
             "breakdown_profiled_pass": {
                 "note": "one extra untimed call with CUDA events around every kernel family (events add a few "
                         "us per kernel)",
@@ -257,6 +324,8 @@ def run_ours(args):
             "clocks": clocks,
             "tokens_per_step": tokens // args.steps,
         }
+        if corpus is not None:
+            line["corpus"] = corpus
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.workload, path, args.cpu_sample_sentences)
         print(json.dumps(line), flush=True)
@@ -275,14 +344,18 @@ def oracle_cores():
         return 1
 
 
-def cpu_baseline(workload: str, path: str, n_sent: int, budget_s: float = 20.0):
-    """The fp64 oracle (as it stands) on a bounded sample of the same workload: the first
-    sentences of the batch, each translated in full (beam, max_len as the workload), until
-    n_sent sentences or ~budget_s seconds of CPU work."""
-    from oracle import OracleModel, beam_search, load_model_tensors
-    w = synth.WORKLOADS[workload]
-    om = OracleModel(load_model_tensors(path, w.decode.precision))
-    ids, lens = synth.make_corpus(workload)
+def cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _oracle_sample(om, w, ids, lens, n_sent, budget_s):
+    from oracle import beam_search
     t0 = time.perf_counter()
     toks, done = 0, 0
     for b in range(min(n_sent, len(lens))):
@@ -291,11 +364,28 @@ def cpu_baseline(workload: str, path: str, n_sent: int, budget_s: float = 20.0):
         done += 1
         if time.perf_counter() - t0 > budget_s:
             break
-    dt = time.perf_counter() - t0
+    return toks, done, time.perf_counter() - t0
+
+
+def cpu_baseline(workload: str, path: str, n_sent: int, budget_s: float = 20.0):
+    """The fp64 oracle (as it stands) on a bounded sample of the same workload: the first
+    sentences of the batch, each translated in full (beam, max_len as the workload), until
+    n_sent sentences or ~budget_s seconds of CPU work - with the BLAS pool at all host cores
+    (the reported value) and again at 1 thread (SURVEY §8(d) oracle timing, settings ii / i)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import OracleModel, load_model_tensors
+    w = synth.WORKLOADS[workload]
+    om = OracleModel(load_model_tensors(path, w.decode.precision))
+    ids, lens = synth.make_corpus(workload)
+    toks, done, dt = _oracle_sample(om, w, ids, lens, n_sent, budget_s)
+    with threadpool_limits(1):
+        t1, d1, s1 = _oracle_sample(om, w, ids, lens, n_sent, budget_s / 2)
     return {"value": round(toks / dt, 3), "unit": "target tok/s", "cores": oracle_cores(), "kind": "oracle",
             "sample": f"first {done} sentences of the {workload} batch, full decode (beam {w.decode.beam}, "
                       f"max_len {w.decode.max_len}), fp64 numpy per sentence, {dt:.1f} s",
-            "host_cpus": os.cpu_count()}
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_model(),
+            "single_thread": {"value": round(t1 / s1, 3), "cores": 1,
+                              "sample": f"first {d1} sentences, BLAS pool limited to 1 thread, {s1:.1f} s"}}
 
 
 def run_reference(args):
@@ -327,6 +417,7 @@ def run_reference(args):
             "config": {"workload": args.workload, "beam": w.decode.beam, "max_len": per,
                        "sample": "1 sentence of the batch per step (fp64 oracle on host cores)"},
             "cpu_baseline": {"value": round(v, 3), "unit": "target tok/s", "cores": cores, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"per step: 1 sentence of the {args.workload} batch, full decode to max_len {per}"},
             "e2e": {"value": round(v, 3), "unit": "target tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -499,6 +590,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-sentences", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-corpus", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: a full batch per GPU (c2, c4); strong: the workload's batch sharded (c3, c5)")
     ap.add_argument("--task", default="translate", choices=["translate", "score", "translate_ex", "copy"])
     args = ap.parse_args()
     if args.warmup < 3:

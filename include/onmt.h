@@ -23,8 +23,14 @@
  *  - Ownership: the caller owns every buffer it passes; the library copies host
  *    inputs in once per call and results out once per call, and owns all device
  *    memory of a model handle (released by onmt_free).
- *  - Threading: at most one in-flight call per model handle; distinct handles may be
- *    used concurrently (also on different devices).
+ *  - Threading: at most one in-flight call per model handle.  Handles on DIFFERENT
+ *    devices may run concurrently.  On one device, calls of distinct handles must not
+ *    overlap in time (serialise them on one stream or with events): several kernels of a
+ *    call are persistent grids whose CTAs (or thread-block clusters) wait for one another,
+ *    planned so that the whole grid is co-resident on an otherwise idle device
+ *    (cudaOccupancyMaxActiveClusters); if another grid holds the SMs such a wait times
+ *    out after 4 s, the kernel traps and the call fails with ONMT_E_CUDA instead of
+ *    hanging.
  */
 #ifndef ONMT_H_
 #define ONMT_H_
@@ -246,6 +252,13 @@ ONMT_API onmt_status onmt_get_kernel_time(onmt_model* m, const char* name, int32
 /* onmt_kernel_launches - number of this library's kernels launched by the handle since
  * the last call with reset != 0 (counted on the host at launch time). */
 ONMT_API onmt_status onmt_kernel_launches(onmt_model* m, int32_t reset, int64_t* launches);
+
+/* onmt_graph_captures - number of whole-call CUDA graphs the handle captured since load.
+ * Every call replays a cached graph (LRU, 8 entries keyed by shape and buffer set); the
+ * host-API calls pad S_max to a multiple of 8, so a corpus of batches with different
+ * source lengths captures a few graphs once and then only replays (a corpus benchmark
+ * reports this count).  INVALID_ARG on NULL. */
+ONMT_API onmt_status onmt_graph_captures(onmt_model* m, int64_t* captures);
 
 /* onmt_free - release every device/host resource of the handle (NULL is a no-op). */
 ONMT_API void onmt_free(onmt_model* m);

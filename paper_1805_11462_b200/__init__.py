@@ -25,7 +25,7 @@ K_MAX = 16
 EXPORTS = ["onmt_load_weights", "onmt_model_get_info", "onmt_set_stream", "onmt_encode", "onmt_translate",
            "onmt_translate_trace", "onmt_translate_dev", "onmt_set_option", "onmt_get_kernel_time",
            "onmt_kernel_launches", "onmt_free", "onmt_last_error", "onmt_test_gemm", "onmt_test_gen", "onmt_score",
-           "onmt_translate_ex", "onmt_translate_copy"]
+           "onmt_translate_ex", "onmt_translate_copy", "onmt_graph_captures"]
 
 
 class OnmtError(RuntimeError):
@@ -68,6 +68,7 @@ def lib():
     L.onmt_set_option.argtypes = [VP, ctypes.c_char_p, I64]
     L.onmt_get_kernel_time.argtypes = [VP, ctypes.c_char_p, I32, P(ctypes.c_double), P(I64)]
     L.onmt_kernel_launches.argtypes = [VP, I32, P(I64)]
+    L.onmt_graph_captures.argtypes = [VP, P(I64)]
     L.onmt_free.argtypes = [VP]
     L.onmt_free.restype = None
     L.onmt_last_error.restype = ctypes.c_char_p
@@ -140,6 +141,11 @@ class Model:
     def launches(self, reset: bool = True) -> int:
         n = ctypes.c_int64()
         _check(lib().onmt_kernel_launches(self._h, int(reset), ctypes.byref(n)))
+        return n.value
+
+    def graph_captures(self) -> int:
+        n = ctypes.c_int64()
+        _check(lib().onmt_graph_captures(self._h, ctypes.byref(n)))
         return n.value
 
     # --------------------------------------------------------------- compute

@@ -123,7 +123,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   // cluster barrier; the combine then reads only local shared memory and no CTA reads a peer's
   // memory after the barrier (no trailing cluster barrier)
   // (measured: faster at c5 - 8 chunks, K = 10: 36 -> 28 us - slightly slower at c2 - 4 chunks, K = 5)
-  const bool push = vec && (nch >= 8 || K >= 8);
+  const bool push = vec && fo.push;                // host plan: 8 chunks or K >= 8, and the buffer fits
   const int wjm = ((H >> 2) + nch - 1) / nch;
   float* rb = s_esave + (fo.att_out ? r4((size_t)K * CH) : 0);
   __shared__ float s_rbm[8 * KMAX], s_rbl[8 * KMAX];
@@ -144,10 +144,12 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   if (nsub_max > 0) stage(0);
   if (nsub_max > 1) stage(1);
   KT(1);
+  if (push) cluster_arrive_relaxed();              // (waited for before the first DSMEM store)
   pdl_wait();                                      // h_top, done flags of this step now visible
   const bool quit = all_done(ctl) || (done && done[b]);   // uniform over the cluster
   if (quit) {
     cp_async_wait<0>();
+    if (push) cluster_wait();                      // (complete the barrier phase opened above)
     return;
   }
   // queries: the K beam rows of sentence b - in registers for small K (each lane's 4 float4
@@ -370,6 +372,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   __syncthreads();
   if (push) {
     // ---- push my unnormalised partial context: column j goes to the chunk that owns it
+    cluster_wait();                                // every peer CTA has started (DSMEM targets exist)
     const int H4 = H >> 2;
 #pragma unroll
     for (int u = 0; u < JPT; ++u) {
@@ -591,8 +594,13 @@ static AttPlan att_plan(int B, int S_max, int H, int K, int key_ld, int val_ld, 
     size_t extra = 0;                              // folded W_out: prefetched tile shares
     if (fo.wpart) extra = (size_t)fo.n_wt * K * ((H / 4 + nch - 1) / nch) * 16;
     const size_t esave = fo.att_out ? r4((size_t)K * CH) * 4 : 0;   // attention output: raw scores
-    const size_t rbb = (nch >= 8 || K >= 8) ? (size_t)nch * K * 16 * ((H / 4 + nch - 1) / nch) : 0;   // push combine
     const int SC = bytes(16) + extra <= 200 * 1024 ? 16 : 8;
+    // push combine (8 chunks or K >= 8) only when its receive buffer fits next to the rest;
+    // otherwise the pull combine (no receive buffer)
+    const bool vec = (H & 3) == 0 && (kl & 3) == 0 && (val_ld & 3) == 0;
+    size_t rbb = (vec && (nch >= 8 || K >= 8)) ? (size_t)nch * K * 16 * ((H / 4 + nch - 1) / nch) : 0;
+    if (bytes(SC) + esave + rbb > 220 * 1024) rbb = 0;
+    fo.push = rbb > 0;
     fo.pref = bytes(SC) + extra + esave + rbb <= 220 * 1024;
     fo.hp_floats = fo.pref ? (int)(extra / 4) : 0;
     p = AttPlan{nch, CH, SC, bytes(SC) + (fo.pref ? extra : 0) + esave + rbb};

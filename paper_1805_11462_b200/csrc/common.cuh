@@ -67,6 +67,7 @@ struct AttFold {
   int pref;                     // (set by the launcher) shares prefetched into shared memory
   int hp_floats;                // (set by the launcher) size of that prefetch region
   float* att_out;               // [B*K][S_max] normalised attention weights (coverage / unk), or nullptr
+  int push;                     // (set by the launcher) push combine: its receive buffer fits shared memory
 };
 
 __device__ __forceinline__ void store_x(const XOut& x, int r, int c, float v) {
@@ -233,6 +234,20 @@ __device__ __forceinline__ int feed_id(const GatherArgs& ga, int y) { return (ga
 // and bumps the generation with a single atomic, so consecutive episodes may use a
 // different n (grids of different shapes sharing a counter).  Every participant must be
 // resident (callers guarantee grid <= #SMs at one CTA per SM, or a cluster).
+// Every cross-CTA spin is bounded: the host plans grids whose CTAs (clusters) are all
+// co-resident (occupancy-checked), so a wait longer than kSpinTimeoutNs means that promise
+// was broken (e.g. another context holding SMs) - the kernel traps (the call then fails with
+// a CUDA error) instead of hanging the GPU.
+constexpr unsigned long long kSpinTimeoutNs = 4000000000ull;
+__device__ __forceinline__ unsigned long long spin_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void spin_check(unsigned long long t0, unsigned int& it) {
+  if ((++it & 1023u) == 0u && spin_clock() - t0 > kSpinTimeoutNs) __trap();
+}
+
 __device__ __forceinline__ void cta_group_barrier(unsigned int* b, unsigned int n) {
   __threadfence();
   const unsigned int old = atomicAdd(b, 1u);
@@ -240,10 +255,13 @@ __device__ __forceinline__ void cta_group_barrier(unsigned int* b, unsigned int 
     atomicAdd(b, 0x10000u - n);
   } else {
     const unsigned int gen = old >> 16;
+    const unsigned long long t0 = spin_clock();
+    unsigned int it = 0;
     while (true) {
       unsigned int v;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(b) : "memory");
       if ((v >> 16) != gen) break;
+      spin_check(t0, it);
     }
   }
   __threadfence();

@@ -278,11 +278,37 @@ enc_rec_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__
 // splits per tile for this layer (0 = the persistent kernel does not fit): the largest S in
 // {4, 2, 1} dividing the K blocks with N/S a multiple of 8, the grid co-resident and the
 // shared memory within 227 KB
+// every CTA of the grid resident at once as clusters of S (the step barrier waits for all)
+static bool er_coresident(int grid, int S, size_t smem) {
+  if (cudaFuncSetAttribute(enc_rec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, enc_rec_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return ncl * S >= grid;
+}
+
 int enc_rec_splits(int kb, int N, int D, int T, int num_sms) {
   if (N < 16 || N > 256 || (N % 16) != 0) return 0;
   for (int S = 4; S >= 1; S >>= 1) {
     if (kb % S != 0 || (N / S) % 8 != 0 || D * T * S > num_sms) continue;
     if (er_smem_bytes(kb / S, N, S) > 227 * 1024) continue;
+    if (!er_coresident(D * T * S, S, er_smem_bytes(kb / S, N, S))) continue;
     return S;
   }
   return 0;

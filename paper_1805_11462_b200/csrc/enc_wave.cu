@@ -18,6 +18,8 @@
 //       overwrites - two parity buffers per layer).
 #include <math_constants.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -53,10 +55,13 @@ __device__ __forceinline__ float ew_tanh(float x) {
   return copysignf(__fdividef(1.f - e, 1.f + e), x);
 }
 __device__ __forceinline__ void ew_wait_count(const unsigned long long* c, unsigned long long target) {
+  const unsigned long long t0 = spin_clock();
+  unsigned int it = 0;
   while (true) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(c) : "memory");
     if (v >= target) break;
+    spin_check(t0, it);
   }
 }
 
@@ -146,6 +151,8 @@ enc_wave_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant__
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  cluster_arrive_relaxed();                                      // every peer CTA of the cluster has
+  cluster_wait();                                                // started before any DSMEM store
   const uint32_t tmem = *tslot;
   const XOut xrec0 = ly.xrec[0], xrec1 = ly.xrec[1], xnext = ly.xnext;
   float* const h_st = ly.h_st;
@@ -286,14 +293,43 @@ enc_wave_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant__
   if (warp == 1) tmem_dealloc(tmem, tcols);
 }
 
+// co-residency of the whole grid as clusters of S CTAs (clusters must fit inside a GPC):
+// the layers' counter waits need every CTA resident at once
+static bool ew_coresident(int grid, int S, size_t smem) {
+  if (cudaFuncSetAttribute(enc_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, enc_wave_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return ncl * S >= grid;
+}
+
 // splits per tile (uniform over the layers: one cluster shape per launch), 0 = does not fit
 int enc_wave_splits(int L, const int* kb, int N, int T, int num_sms) {
   if (L < 2 || L > kWaveMaxL || N < 16 || N > 256 || (N % 16) != 0) return 0;
   for (int S = 4; S >= 1; S >>= 1) {
     bool ok = (N / S) % 8 == 0 && L * T * S <= num_sms;
-    for (int l = 0; l < L && ok; ++l)
+    size_t smem = 0;
+    for (int l = 0; l < L && ok; ++l) {
       ok = kb[l] % S == 0 && ew_smem_bytes(kb[l] / S, N, S) <= 227 * 1024;
-    if (ok) return S;
+      if (ok) smem = std::max(smem, ew_smem_bytes(kb[l] / S, N, S));
+    }
+    if (ok && ew_coresident(L * T * S, S, smem)) return S;
   }
   return 0;
 }

@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/onmt.h"
 #include "common.cuh"
 
@@ -172,6 +174,14 @@ struct Error {
   } while (0)
 
 static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// NVTX range for the host-side phases (C-ABI calls, and the enqueue of encode / decode /
+// finalize - inside a graph capture these mark when the graph was built, replays show as
+// the enclosing API range)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------------ TMA descriptors
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -340,8 +350,10 @@ struct GraphCache {
   cudaGraphExec_t exec = nullptr;
   std::vector<int64_t> key;
   int64_t kernels = 0;
+  uint64_t last_use = 0;
   std::vector<std::pair<std::string, EvPair>> ev_nodes;   // profiling events baked into the graph
 };
+constexpr int kGraphCacheEntries = 8;   // distinct (shape, pointer set) graphs kept instantiated
 
 }  // namespace onmt
 
@@ -406,16 +418,19 @@ struct onmt_model {
 
   std::map<std::string, EventPairs> evs;   // per kernel family ("gen", "step", "encode", ...)
   bool capturing = false;
-  GraphCache graph;
+  std::vector<GraphCache> graphs;            // LRU cache of instantiated whole-call graphs
+  uint64_t graph_clock = 0;
+  int64_t graph_captures = 0;                // captures since load (corpus runs: should stop growing)
   GraphCache* cap_graph = nullptr;           // the graph being captured (profiling event nodes)
-  GraphCache score_graph;
   // teacher-forced scoring workspace
   Act xs_all;                                // generator operand of every (step, sentence) row
   DevBuf s_tgt, s_gold, s_zgold, s_out, s_ms, s_tz, s_ti;
 
+  int64_t enqueue_variant() const { return 0; }   // bitmask of enqueue-shaping options (graph keys)
+
   ~onmt_model() {
-    if (graph.exec) cudaGraphExecDestroy(graph.exec);
-    if (score_graph.exec) cudaGraphExecDestroy(score_graph.exec);
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
@@ -776,6 +791,7 @@ static void prepare_encoder(onmt_model* m, int B, int S_max) {
 }
 
 static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max) {
+  Nvtx nv("onmt.encode");
   const bool bf = m->use_tc;
   const int rows = B * S_max, H = m->H, Hd = m->Hd, D = m->D;
   StepCtl none{nullptr, 0};
@@ -1130,6 +1146,7 @@ static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_ma
 
 static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int K, int max_len, float alpha,
                             bool trace, const DecodeOut& out, const DecodeOpts& op) {
+  Nvtx nv("onmt.decode");
   const bool bf = m->use_tc;
   const int R = B * K, H = m->H, E = m->E, L = m->L;
   const int rp = m->xg.rows_pad;
@@ -1227,9 +1244,66 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
     }
     prof_end(m, "step", ev);
   }
-  launch_finalize(bs, B, K, max_len, out.hyps, out.lens, out.scores, out.raw, out.tlogp, out.unk_pos, m->stream);
+  {
+    Nvtx nf("onmt.finalize");
+    launch_finalize(bs, B, K, max_len, out.hyps, out.lens, out.scores, out.raw, out.tlogp, out.unk_pos, m->stream);
+  }
   count(m);
   ONMT_CUDA(cudaGetLastError());
+}
+
+// Replay the whole call as one cached CUDA graph (LRU over kGraphCacheEntries shapes /
+// pointer sets): the first call of a key captures `enqueue` and instantiates it, later calls
+// are one cudaGraphLaunch.  A corpus whose batches differ in S_max reuses the graphs of its
+// (bucketed, translate_impl) S_max values instead of re-capturing every batch.
+template <typename F>
+static void replay_graph(onmt_model* m, const std::vector<int64_t>& key, F&& enqueue) {
+  GraphCache* gc = nullptr;
+  for (auto& g : m->graphs)
+    if (g.exec && g.key == key) gc = &g;
+  if (!gc) {
+    if ((int)m->graphs.size() < kGraphCacheEntries) {
+      m->graphs.emplace_back();
+      gc = &m->graphs.back();
+    } else {                                            // evict the least recently used graph
+      gc = &m->graphs[0];
+      for (auto& g : m->graphs)
+        if (g.last_use < gc->last_use) gc = &g;
+    }
+    if (gc->exec) {
+      ONMT_CUDA(cudaStreamSynchronize(m->stream));
+      ONMT_CUDA(cudaGraphExecDestroy(gc->exec));
+      gc->exec = nullptr;
+      for (auto& pe : gc->ev_nodes) m->evs[pe.first].release({pe.second});
+      gc->ev_nodes.clear();
+    }
+    cudaGraph_t graph;
+    const int64_t before = m->launches;
+    ONMT_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
+    m->capturing = true;
+    m->cap_graph = gc;
+    try {
+      enqueue();
+    } catch (...) {
+      m->capturing = false;
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(m->stream, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      throw;
+    }
+    m->capturing = false;
+    ONMT_CUDA(cudaStreamEndCapture(m->stream, &graph));
+    ONMT_CUDA(cudaGraphInstantiate(&gc->exec, graph, 0));
+    ONMT_CUDA(cudaGraphDestroy(graph));
+    gc->kernels = m->launches - before;
+    m->launches = before;
+    gc->key = key;
+    ++m->graph_captures;
+  }
+  gc->last_use = ++m->graph_clock;
+  ONMT_CUDA(cudaGraphLaunch(gc->exec, m->stream));
+  m->launches += gc->kernels;
+  for (auto& pe : gc->ev_nodes) m->evs[pe.first].pending.push_back({pe.second, false});
 }
 
 // Teacher-forced scoring: encoder, then T_max decoder steps fed with
@@ -1313,44 +1387,10 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
     enqueue_score(m, d_ids, d_lens, B, S_max, T_max);
     return;
   }
-  std::vector<int64_t> key = {B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->fold_cur,
-                              m->enc_persistent,
-                              (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
+  std::vector<int64_t> key = {-1, B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->fold_cur,
+                              m->enc_persistent, m->enc_wavefront, m->enqueue_variant(), (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
                               (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
-  GraphCache& gc = m->score_graph;
-  if (!gc.exec || gc.key != key) {
-    if (gc.exec) {
-      ONMT_CUDA(cudaStreamSynchronize(m->stream));
-      ONMT_CUDA(cudaGraphExecDestroy(gc.exec));
-      gc.exec = nullptr;
-      for (auto& pe : gc.ev_nodes) m->evs[pe.first].release({pe.second});
-      gc.ev_nodes.clear();
-    }
-    cudaGraph_t graph;
-    const int64_t before = m->launches;
-    ONMT_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
-    m->capturing = true;
-    m->cap_graph = &gc;
-    try {
-      enqueue_score(m, d_ids, d_lens, B, S_max, T_max);
-    } catch (...) {
-      m->capturing = false;
-      cudaGraph_t junk = nullptr;
-      cudaStreamEndCapture(m->stream, &junk);
-      if (junk) cudaGraphDestroy(junk);
-      throw;
-    }
-    m->capturing = false;
-    ONMT_CUDA(cudaStreamEndCapture(m->stream, &graph));
-    ONMT_CUDA(cudaGraphInstantiate(&gc.exec, graph, 0));
-    ONMT_CUDA(cudaGraphDestroy(graph));
-    gc.kernels = m->launches - before;
-    m->launches = before;
-    gc.key = key;
-  }
-  ONMT_CUDA(cudaGraphLaunch(gc.exec, m->stream));
-  m->launches += gc.kernels;
-  for (auto& pe : gc.ev_nodes) m->evs[pe.first].pending.push_back({pe.second, false});
+  replay_graph(m, key, [&]() { enqueue_score(m, d_ids, d_lens, B, S_max, T_max); });
 }
 
 // The whole translation (encoder, decoder init, every decode step, finalize) as one CUDA
@@ -1369,47 +1409,13 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     return;
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
-                              m->gen_step, m->fold_cur, m->enc_persistent,
-                              m->enc_wavefront,
+                              m->gen_step, m->fold_cur, m->enc_persistent, m->enc_wavefront, m->enqueue_variant(),
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
                               (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp,
                               (int64_t)(intptr_t)out.unk_pos, (int64_t)(op.beta * 1e9), op.nbest, op.unk,
                               (int64_t)(intptr_t)op.src_ext};
-  GraphCache& gc = m->graph;
-  if (!gc.exec || gc.key != key) {
-    if (gc.exec) {
-      ONMT_CUDA(cudaStreamSynchronize(m->stream));
-      ONMT_CUDA(cudaGraphExecDestroy(gc.exec));
-      gc.exec = nullptr;
-      for (auto& pe : gc.ev_nodes) m->evs[pe.first].release({pe.second});
-      gc.ev_nodes.clear();
-    }
-    cudaGraph_t graph;
-    const int64_t before = m->launches;
-    ONMT_CUDA(cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal));
-    m->capturing = true;
-    m->cap_graph = &gc;
-    try {
-      enqueue();
-    } catch (...) {
-      m->capturing = false;
-      cudaGraph_t junk = nullptr;
-      cudaStreamEndCapture(m->stream, &junk);
-      if (junk) cudaGraphDestroy(junk);
-      throw;
-    }
-    m->capturing = false;
-    ONMT_CUDA(cudaStreamEndCapture(m->stream, &graph));
-    ONMT_CUDA(cudaGraphInstantiate(&gc.exec, graph, 0));
-    ONMT_CUDA(cudaGraphDestroy(graph));
-    gc.kernels = m->launches - before;
-    m->launches = before;
-    gc.key = key;
-  }
-  ONMT_CUDA(cudaGraphLaunch(gc.exec, m->stream));
-  m->launches += gc.kernels;
-  for (auto& pe : gc.ev_nodes) m->evs[pe.first].pending.push_back({pe.second, false});
+  replay_graph(m, key, enqueue);
 }
 
 }  // namespace onmt
@@ -1538,13 +1544,20 @@ static onmt_status validate(onmt_model* m, const int32_t* ids, const int32_t* le
   return ONMT_OK;
 }
 
-static void upload_src(onmt_model* m, const int32_t* ids, const int32_t* lens, int B, int S_max) {
-  m->d_ids.ensure((size_t)B * S_max * 4);
+// Host-API calls pad the source to a bucket of 8 positions: padded positions are never read
+// (packed encoder, length-masked attention), so the result is the same up to the attention's
+// chunking of the source, and a corpus whose batches differ in S_max replays a handful of
+// cached graphs (replay_graph) instead of capturing one per batch.
+static int bucket_smax(int S_max) { return std::min(round_up(S_max, 8), 2048); }
+
+// ids [B x S_max] (host) -> device [B x S_dev] with pads zeroed (S_dev >= S_max)
+static void upload_src(onmt_model* m, const int32_t* ids, const int32_t* lens, int B, int S_max, int S_dev) {
+  m->d_ids.ensure((size_t)B * S_dev * 4);
   m->d_lens.ensure((size_t)B * 4);
   // ids at padded positions are ignored by contract; sanitize them so gathers stay in range
-  std::vector<int32_t> clean((size_t)B * S_max, 0);
+  std::vector<int32_t> clean((size_t)B * S_dev, 0);
   for (int b = 0; b < B; ++b)
-    for (int s = 0; s < lens[b]; ++s) clean[(size_t)b * S_max + s] = ids[(size_t)b * S_max + s];
+    for (int s = 0; s < lens[b]; ++s) clean[(size_t)b * S_dev + s] = ids[(size_t)b * S_max + s];
   ONMT_CUDA(cudaMemcpyAsync(m->d_ids.p, clean.data(), clean.size() * 4, cudaMemcpyHostToDevice, m->stream));
   ONMT_CUDA(cudaMemcpyAsync(m->d_lens.p, lens, (size_t)B * 4, cudaMemcpyHostToDevice, m->stream));
 }
@@ -1555,7 +1568,7 @@ onmt_status onmt_encode(onmt_model* m, const int32_t* ids, const int32_t* lens, 
   if (s != ONMT_OK || B == 0) return s;
   ONMT_API_BEGIN
   ONMT_CUDA(cudaSetDevice(m->device));
-  upload_src(m, ids, lens, B, S_max);
+  upload_src(m, ids, lens, B, S_max, S_max);
   m->fold_cur = false;
   prepare_encoder(m, B, S_max);
   enqueue_encoder(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max);
@@ -1598,12 +1611,14 @@ static onmt_status translate_impl(onmt_model* m, const int32_t* ids, const int32
   if (!hyps || !olens || !scores) return fail(ONMT_E_INVALID_ARG, "null output pointer");
   const bool trace = sel_parent || sel_token || sel_score;
   ONMT_API_BEGIN
+  Nvtx nv("onmt_translate");
   ONMT_CUDA(cudaSetDevice(m->device));
-  upload_src(m, ids, lens, B, S_max);
+  const int S_dev = bucket_smax(S_max);
+  upload_src(m, ids, lens, B, S_max, S_dev);
   if (src_ext) {                                     // pads -> 0 (never read)
-    std::vector<int32_t> e((size_t)B * S_max, 0);
+    std::vector<int32_t> e((size_t)B * S_dev, 0);
     for (int b = 0; b < B; ++b)
-      for (int t = 0; t < lens[b]; ++t) e[(size_t)b * S_max + t] = src_ext[(size_t)b * S_max + t];
+      for (int t = 0; t < lens[b]; ++t) e[(size_t)b * S_dev + t] = src_ext[(size_t)b * S_max + t];
     m->d_ext.ensure(e.size() * 4);
     ONMT_CUDA(cudaMemcpyAsync(m->d_ext.p, e.data(), e.size() * 4, cudaMemcpyHostToDevice, m->stream));
     ONMT_CUDA(cudaStreamSynchronize(m->stream));
@@ -1618,7 +1633,7 @@ static onmt_status translate_impl(onmt_model* m, const int32_t* ids, const int32
   if (unk_pos) m->o_unk.ensure((size_t)B * nb * max_len * 4);
   DecodeOut o{m->o_hyps.as<int>(), m->o_lens.as<int>(), m->o_scores.as<float>(), m->o_raw.as<float>(),
               m->o_tlogp.as<float>(), unk_pos ? m->o_unk.as<int>() : nullptr};
-  run_translate(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max, beam, max_len, alpha, trace, o, op);
+  run_translate(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_dev, beam, max_len, alpha, trace, o, op);
   ONMT_CUDA(cudaMemcpyAsync(hyps, o.hyps, (size_t)B * nb * max_len * 4, cudaMemcpyDeviceToHost, m->stream));
   ONMT_CUDA(cudaMemcpyAsync(olens, o.lens, (size_t)B * nb * 4, cudaMemcpyDeviceToHost, m->stream));
   ONMT_CUDA(cudaMemcpyAsync(scores, o.scores, (size_t)B * nb * 4, cudaMemcpyDeviceToHost, m->stream));
@@ -1697,7 +1712,8 @@ onmt_status onmt_score(onmt_model* m, const int32_t* ids, const int32_t* lens, i
   }
   ONMT_API_BEGIN
   ONMT_CUDA(cudaSetDevice(m->device));
-  upload_src(m, ids, lens, B, S_max);
+  const int S_dev = bucket_smax(S_max);
+  upload_src(m, ids, lens, B, S_max, S_dev);
   std::vector<int32_t> clean((size_t)B * T_max, 0), gold((size_t)T_max * B, -1);
   for (int b = 0; b < B; ++b)
     for (int t = 0; t < tgt_lens[b]; ++t) {
@@ -1709,7 +1725,7 @@ onmt_status onmt_score(onmt_model* m, const int32_t* ids, const int32_t* lens, i
   m->s_out.ensure((size_t)B * T_max * 4);
   ONMT_CUDA(cudaMemcpyAsync(m->s_tgt.p, clean.data(), clean.size() * 4, cudaMemcpyHostToDevice, m->stream));
   ONMT_CUDA(cudaMemcpyAsync(m->s_gold.p, gold.data(), gold.size() * 4, cudaMemcpyHostToDevice, m->stream));
-  run_score(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max, T_max);
+  run_score(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_dev, T_max);
   ONMT_CUDA(cudaMemcpyAsync(out_token_logp, m->s_out.p, (size_t)B * T_max * 4, cudaMemcpyDeviceToHost, m->stream));
   ONMT_CUDA(cudaStreamSynchronize(m->stream));
   if (out_nll)
@@ -1739,6 +1755,7 @@ onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_ids, const int32_
   if (!d_ids || !d_lens || !d_hyps || !d_olens || !d_scores) return fail(ONMT_E_INVALID_ARG, "null device pointer");
   if (m->copy) return fail(ONMT_E_UNSUPPORTED, "copy models decode through onmt_translate_copy");
   ONMT_API_BEGIN
+  Nvtx nv("onmt_translate_dev");
   ONMT_CUDA(cudaSetDevice(m->device));
   m->o_raw.ensure((size_t)B * 4);
   m->o_tlogp.ensure((size_t)B * max_len * 4);
@@ -1771,6 +1788,12 @@ onmt_status onmt_kernel_launches(onmt_model* m, int32_t reset, int64_t* launches
   if (!m || !launches) return fail(ONMT_E_INVALID_ARG, "null argument");
   *launches = m->launches;
   if (reset) m->launches = 0;
+  return ONMT_OK;
+}
+
+onmt_status onmt_graph_captures(onmt_model* m, int64_t* captures) {
+  if (!m || !captures) return fail(ONMT_E_INVALID_ARG, "null argument");
+  *captures = m->graph_captures;
   return ONMT_OK;
 }
 
