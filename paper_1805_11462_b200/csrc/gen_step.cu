@@ -142,7 +142,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   uint64_t* tempty = tfull + 1;
   uint64_t* sfull = tempty + 1;                                    // [2][kGsMaxCh] staged chunk filled (stagers)
   uint64_t* sempty = sfull + 2 * kGsMaxCh;                         // [2][kGsMaxCh] staged chunk scanned (scanners)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + 2 * kGsMaxCh);
+  uint64_t* sdone = sempty + 2 * kGsMaxCh;                         // every scanner warp finished a batch
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = blockIdx.x / a.C, ci = blockIdx.x % a.C;
@@ -166,6 +167,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     mbar_init(tempty, kGsStageWarps);
+    mbar_init(sdone, kGsScanWarps);
   }
   if (threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kGsMaxCh) {      // chunk barriers (warp 1)
     const int i = threadIdx.x - 32, k = i % kGsMaxCh;
@@ -224,7 +226,10 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       for (int bt = 0; bt < nbatch; ++bt) {
         const int t0 = bfirst(bt);
         const int nt = bsize(bt);
-        if (bt > 0 && !a.ovl) mbar_wait(tempty, (bt - 1) & 1);   // staging (ring overlay) finished
+        if (bt > 0 && !a.ovl) {                                   // the staging overlays the ring: the
+          mbar_wait(tempty, (bt - 1) & 1);                         // previous batch is staged AND scanned
+          mbar_wait(sdone, (bt - 1) & 1);                          // before its stages are reloaded
+        }
         for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
           const int s = it % a.stages;
           if (it >= a.stages) mbar_wait(&empty[s], ((it / a.stages) & 1) ^ 1);
@@ -521,6 +526,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         KTX(5, et == 0 && jj == 0);
         KTX(11, et == 0 && jj == 1);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(sdone);                     // (ring overlay: batch bt scanned)
     }
     KTX(8, et == 0);
     // ---- combine the P parts of a row (adjacent lanes, butterfly) and write the CTA's partial
@@ -572,7 +579,7 @@ static size_t gs_body_bytes(int n_group, int nt_max, int stages, int ovl, int nb
   const size_t stg = (size_t)nbuf * srows * kGsSLD * 4;
   return ovl ? ring + stg : (ring > stg ? ring : stg);
 }
-static size_t gs_smem_bytes(size_t body, int stages) { return 1024 + body + (2 * stages + 2 + 4 * kGsMaxCh) * 8 + 16; }
+static size_t gs_smem_bytes(size_t body, int stages) { return 1024 + body + (2 * stages + 3 + 4 * kGsMaxCh) * 8 + 16; }
 
 struct GsPlan {
   int C, nt_max, stages, P, ovl, nbuf, srows;

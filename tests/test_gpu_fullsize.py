@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 WORKERS = max(1, min(16, (os.cpu_count() or 2) // 2))
 
 
-def _full(workload, weight_cache, sentences):
+def _full(workload, weight_cache, sentences, derive=False):
     gm, om, prec = model_pair(workload, weight_cache)
     w = synth.WORKLOADS[workload]
     ids, lens = synth.make_corpus(workload)
@@ -30,8 +30,12 @@ def _full(workload, weight_cache, sentences):
     K, ML, alpha = w.decode.beam, w.decode.max_len, w.decode.alpha
     gpu = gm.translate(ids, lens, K, ML, alpha, trace=True)
     assert (gpu["lens"] == ML).all()                       # random weights: every sentence runs to max_len
-    res = compare_batch(om, ids, lens, gpu, K, ML, alpha, prec, sentences=sentences, workers=WORKERS)
+    res = compare_batch(om, ids, lens, gpu, K, ML, alpha, prec, sentences=sentences, workers=WORKERS, derive=derive)
     print(f"{workload} B={len(lens)} K={K} max_len={ML}: {summary(res)} over {len(sentences)} sentences")
+    if derive:
+        for st, d in res["details"]:
+            print(f"  {st}: logp_err {d['logp_err']:.2e}; north_star bar held over the first {d['strict_prefix']} "
+                  f"tokens; last-token bar {d['bar_last']:.2e}")
     fails = [d for s, d in res["details"] if s == "fail"]
     assert res["fail"] == 0, fails
     assert res["match"] + res["excused"] == len(sentences)
@@ -54,8 +58,12 @@ def test_c3_full_batch(weight_cache):
 
 def test_c4_full_batch(weight_cache):
     """configs[3]: B = 128 per GPU (R = 640: three row groups), 4 x 1000, alpha = 0.6,
-    max_len = 200 (unfused gate / W_out kernels, non-overlapped generator plan)."""
-    _full("c4", weight_cache, range(0, 128, 16))
+    max_len = 200 (unfused gate / W_out kernels, non-overlapped generator plan).
+    The 4 x 1000 random model is chaotic over 200 steps: a 2^-18 relative perturbation of its
+    weights moves the ORACLE's own token log-p by ~1 by step 200 (profiles/r02_sensitivity_c4.txt),
+    so no bf16 or fp32 implementation can hold 2e-3 there.  Per-token bars (reading R34): the
+    north_star bars over the well-conditioned prefix, 10x the oracle's sensitivity after it."""
+    _full("c4", weight_cache, range(0, 128, 16), derive=True)
 
 
 def test_c5_full_batch_all_sentences(weight_cache):
