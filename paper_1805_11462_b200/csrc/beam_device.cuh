@@ -136,6 +136,93 @@ __device__ __forceinline__ void select_gather_row(int r, int slice, int nslice, 
   }
 }
 
+__device__ __forceinline__ float rs_sigm(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+__device__ __forceinline__ float rs_tanh(float x) {
+  const float e = __expf(-2.f * fabsf(x));
+  return copysignf(__fdividef(1.f - e, 1.f + e), x);
+}
+
+// Recurrent-split step (GatherArgs::rsplit): layer 1's LSTM cell for the
+// sentence's new slots from the embedding-projection table and the generator's gate tiles,
+// plus the gate-bias / c_prev gathers of layers >= 2.  c_1[p] is read by every slot that
+// continues p, so the new states are computed into shared memory first (gbuf: 2 K H floats)
+// and written after a CTA barrier (a sentence's slots and parents are all in this CTA).
+template <int KMAX>
+__device__ __forceinline__ void rsplit_cell(int b, int K, const int* s_go, const int* s_prow, const int* s_y,
+                                            const GatherArgs& ga, float* gbuf) {
+  const int H = ga.H, G = ga.G, L = ga.L;
+  const size_t PQ = (size_t)ga.rows_pad * G;
+  float* cn = gbuf;
+  float* hn = gbuf + (size_t)K * H;
+  constexpr int U = KMAX < 4 ? KMAX : 4;                         // slots per batch of independent loads
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    const float4 bb = __ldg(ga.bias[0] + j);
+    for (int k0 = 0; k0 < K; k0 += U) {
+      float4 tv[U], pa[U], pb[U];
+      float cp[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {                              // every load of the batch in flight at once
+        const int kr = k0 + u;
+        if (kr < K && s_go[kr]) {
+          const int p = s_prow[kr];
+          tv[u] = __ldg(reinterpret_cast<const float4*>(ga.T + (size_t)s_y[kr] * G) + j);
+          pa[u] = __ldcg(reinterpret_cast<const float4*>(ga.P + (size_t)p * G) + j);
+          pb[u] = __ldcg(reinterpret_cast<const float4*>(ga.P + PQ + (size_t)p * G) + j);
+          cp[u] = __ldcg(ga.c + (size_t)p * H + j);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kr = k0 + u;
+        if (kr < K && s_go[kr]) {
+          // gates of unit j (rows 4j..4j+3 = i, f, g, o); same summation order for every slot
+          const float zi = ((tv[u].x + pa[u].x) + pb[u].x) + bb.x, zf = ((tv[u].y + pa[u].y) + pb[u].y) + bb.y;
+          const float zg = ((tv[u].z + pa[u].z) + pb[u].z) + bb.z, zo = ((tv[u].w + pa[u].w) + pb[u].w) + bb.w;
+          const float c = rs_sigm(zf) * cp[u] + rs_sigm(zi) * rs_tanh(zg);
+          cn[kr * H + j] = c;
+          hn[kr * H + j] = rs_sigm(zo) * rs_tanh(c);
+        }
+      }
+    }
+    for (int l = 1; l < L; ++l) {                                // layers >= 2: W_hh h_l[p] + c_prev gathers
+      for (int k0 = 0; k0 < K; k0 += U) {
+        float4 pl[U];
+        float cl[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int kr = k0 + u;
+          if (kr < K && s_go[kr]) {
+            const int p = s_prow[kr];
+            pl[u] = __ldcg(reinterpret_cast<const float4*>(ga.P + (size_t)(l + 1) * PQ + (size_t)p * G) + j);
+            cl[u] = __ldcg(ga.c + ((size_t)l * ga.rows_pad + p) * H + j);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int kr = k0 + u;
+          if (kr < K && s_go[kr]) {
+            const int r = b * K + kr;
+            reinterpret_cast<float4*>(ga.gb + (size_t)(l - 1) * PQ + (size_t)r * G)[j] = pl[u];
+            ga.cg[((size_t)l * ga.rows_pad + r) * H + j] = cl[u];
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();                                               // every c_1[p] read before any write
+  const int H4 = H >> 2;
+  for (int it = threadIdx.x; it < K * H4; it += blockDim.x) {
+    const int kr = it / H4, j4 = 4 * (it - kr * H4);
+    if (!s_go[kr]) continue;
+    const int r = b * K + kr;
+    const float4 c = *reinterpret_cast<const float4*>(cn + kr * H + j4);
+    const float4 h = *reinterpret_cast<const float4*>(hn + kr * H + j4);
+    *reinterpret_cast<float4*>(ga.c1_out + (size_t)r * H + j4) = c;
+    store_x4(ga.xh1[0], r, ga.col_h1[0] + j4, h);
+    store_x4(ga.xh1[1], r, ga.col_h1[1] + j4, h);
+  }
+}
+
 // A10 + A5 for one whole sentence b per CTA (512 threads): the generator partials of its K
 // hypothesis rows are combined (one warp per row: log-sum-exp and row top-K), thread 0
 // selects the K survivors (raw desc, slot asc, token asc; fp64 scores) with EOS / max_len
@@ -169,7 +256,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   // idle during the row reduce) and, as soon as a row's top-K is known, the embedding rows of
   // its K candidates (issued by that row's warp).  Each issuer raises the expected bytes of
   // s_bar before its copies; thread 0 arrives once all rows are reduced.
-  const bool pre = gbuf != nullptr && (E & 3) == 0 && (H & 3) == 0 &&
+  const bool pre = !ga.rsplit && gbuf != nullptr && (E & 3) == 0 && (H & 3) == 0 &&
                    (K * K * emb_f + K * st_f) <= gbuf_floats && !(dn != 0 && dn < t);
   __shared__ __align__(8) uint64_t s_bar;
   if (threadIdx.x == 0) { mbar_init(&s_bar, 1); fence_mbar_init(); }
@@ -456,6 +543,10 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   KT(4);
   if (!s_cont) {
     if (pre) mbar_wait(&s_bar, 0);                               // (no copy may land after exit)
+    return;
+  }
+  if (ga.rsplit) {                                               // layer 1's cell instead of a gather
+    rsplit_cell<KMAX>(b, K, s_go, s_prow, s_y, ga, gbuf);
     return;
   }
   // ---- gather the next step's inputs of the K rows (x1 = [E_tgt[y]; h~[p]; h_0[p]],

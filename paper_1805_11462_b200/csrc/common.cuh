@@ -179,6 +179,16 @@ __device__ __forceinline__ void write_gen_partial(const GenOut& g, int vt, int r
 }
 
 
+// Gate tiles of the generator step kernel: n_gt tiles of 128 rows of the
+// gate weight matrix (tensor map tmWg), tile g over K blocks [q * gkbh, (q + 1) * gkbh) of the
+// generator's activation operand, q = g / gt_per_q, written to gout[q][row][g % gt_per_q * 128 + m]
+// (row stride gld floats).  n_gt = 0: none.
+struct GateTiles {
+  const CUtensorMap* tmWg;
+  int n_gt, gt_per_q, gkbh, gld;
+  float* gout;
+};
+
 // Destinations of a decoder cell's h output (operand buffers and column offsets).
 struct CellDst {
   XOut x[2];
@@ -224,6 +234,21 @@ struct GatherArgs {
   int rows_pad;
   XOut x[8];           // x[0] = layer-0 operand; x[l] = layer-l operand
   int v_map;           // copy models: an emitted extended id >= v_map is fed back as <unk> (0: off)
+  // recurrent-split step: instead of gathering operands, the beam step runs
+  // layer 1's cell for every new slot r (parent p, token y):
+  //   gates = T[y] + P[0][p] + P[1][p] + bias[0]   (T = E_tgt W_emb^T, P[0] = W_feed h~, P[1] = W_hh h_1)
+  //   c_1 = f * c_1[p] + i * g, h_1 = o * tanh(c_1)  -> c1_out[r], xh1[0..1] (operand columns col_h1)
+  // and gathers layer l >= 2's recurrent gate term P[l][p] -> gb[l-2][r] and c_l[p] -> cg[l-1][r]
+  // (its cell kernel adds W_ih h_{l-1} and the bias)
+  int rsplit;
+  const float* T;      // [V][G]
+  const float* P;      // [L+1][rows_pad][G] gate tiles of the generator (row stride G)
+  int G;               // gate row stride (4H rounded to 128)
+  const float4* bias[8];
+  float* gb;           // [L-1][rows_pad][G]
+  float* c1_out;       // layer-1 cell state [rows_pad][H]
+  XOut xh1[2];
+  int col_h1[2];
 };
 // the embedding row fed back for an emitted (possibly extended) id
 __device__ __forceinline__ int feed_id(const GatherArgs& ga, int y) { return (ga.v_map && y >= ga.v_map) ? 1 : y; }

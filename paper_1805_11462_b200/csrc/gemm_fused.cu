@@ -49,6 +49,10 @@ struct FusedArgs {
   // units' share  W_out[:, units] h[units, cols]  to woh_part[m_tile][row][H] (fp32)
   const __nv_bfloat16* woh;
   float* woh_part;
+  // EPI_CELL, recurrent-split step: per-row gate pre-activations added to
+  // the GEMM result (gb[row * gb_ld + 4j .. 4j + 3] for unit j: W_hh h[parent] + bias), or null
+  const float* gb;
+  int gb_ld;
   StepCtl ctl;
   int dbg;                 // microbenchmark ablations (ONMT_KTRACE builds only)
 };
@@ -97,12 +101,15 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   uint64_t* done = full + a.stages;
   uint64_t* rbar = done + 1;
   uint64_t* wbar = rbar + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(wbar + 1);
+  uint64_t* empty = wbar + 1;                                      // [stages] (ring: stages < K blocks)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(empty + a.stages);
   const int ncp = (a.NC + 23) / 24 * 24;                           // s_hc row stride
   // (offsets from smem keep the shared address space visible to the compiler: LDS, not LD.E)
   const size_t woh_off = ((size_t)(reinterpret_cast<uint8_t*>(tslot) - smem) + 16 + 127) & ~(size_t)127;
   __nv_bfloat16* woh_s = reinterpret_cast<__nv_bfloat16*>(smem + woh_off);                          // [32][H]
   float* s_hc = reinterpret_cast<float*>(woh_s + (size_t)32 * fold_ld(a.H));                       // [32][ncp]
+  float4* s_gb = reinterpret_cast<float4*>(smem + woh_off + (a.woh ? (size_t)64 * fold_ld(a.H) + (size_t)128 * ncp : 0));
+                                                                  // [NC][32] (16-byte aligned offsets)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x / a.S;
@@ -122,12 +129,12 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
-    for (int s = 0; s < a.stages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(done, 1);
     mbar_init(rbar, 1);
     mbar_init(wbar, 1);
     fence_mbar_init();
-    for (int i = 0; i < nkb; ++i) {
+    for (int i = 0; i < nkb && i < a.stages; ++i) {                // the first ring stages' weights
       mbar_expect_tx(&full[i], a_bytes);
       tma_load_2d(smem + i * stage_bytes, &tmW, (kb0 + i) * kBK, m0, &full[i]);
     }
@@ -148,22 +155,31 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < nkb; ++i) {
-      uint8_t* st = smem + i * stage_bytes;
+      const int s = i % a.stages;
+      uint8_t* st = smem + s * stage_bytes;
       if (quit) {
-        mbar_arrive_local(&full[i]);
-      } else {
-        mbar_arrive_expect_tx(&full[i], 2 * b_bytes);
-        tma_load_2d(st + a_bytes, &tmX, (kb0 + i) * kBK, n0, &full[i]);
-        tma_load_2d(st + a_bytes + b_bytes, &tmX, (kb0 + i) * kBK, a.n_rows_pad + n0, &full[i]);
+        if (i < a.stages) mbar_arrive_local(&full[s]);
+        continue;
       }
+      if (i >= a.stages) {                                         // ring: slot s free again
+        mbar_wait(&empty[s], ((i / a.stages) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], a_bytes + 2 * b_bytes);
+        tma_load_2d(st, &tmW, (kb0 + i) * kBK, m0, &full[s]);
+      } else {
+        mbar_arrive_expect_tx(&full[s], 2 * b_bytes);
+      }
+      tma_load_2d(st + a_bytes, &tmX, (kb0 + i) * kBK, n0, &full[s]);
+      tma_load_2d(st + a_bytes + b_bytes, &tmX, (kb0 + i) * kBK, a.n_rows_pad + n0, &full[s]);
     }
   } else if (warp == 1 && lane == 0) {
     const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_group);
     for (int i = 0; i < nkb; ++i) {
-      mbar_wait(&full[i], 0);
+      const int s = i % a.stages;
+      if (quit && i >= a.stages) break;
+      mbar_wait(&full[s], (i / a.stages) & 1);
       tc_fence_after();
       if (quit) continue;
-      const uint32_t sa = smem_u32(smem + i * stage_bytes);
+      const uint32_t sa = smem_u32(smem + s * stage_bytes);
       const uint32_t sbh = sa + a_bytes, sbl = sa + a_bytes + b_bytes;
 #pragma unroll
       for (int kk = 0; kk < kBK / 16; ++kk) {
@@ -171,6 +187,7 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
         tc_mma_bf16(tmem, da, umma_desc_sw128(sbh + kk * 32), idesc, (i | kk) != 0);
         tc_mma_bf16(tmem, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
       }
+      tc_commit(&empty[s]);                      // slot s reusable once these MMAs retire
     }
     tc_commit(done);                             // also fires with no MMA issued
   } else if (warp >= 2 && EPI == EPI_CELL && !quit) {
@@ -180,6 +197,13 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
       const int j = m0 / 4 + t;
       s_bias[t] = j < a.H ? __ldg(&a.bias[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    if (a.gb)
+      for (int i = t; i < ncols * 32; i += 192) {
+        const int c = i / 32, ul = i % 32;
+        const int r = n0 + c_own + c, j = m0 / 4 + ul;
+        s_gb[i] = (r < a.n_valid && j < a.H) ? __ldcg(reinterpret_cast<const float4*>(a.gb + (size_t)r * a.gb_ld) + j)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     for (int i0 = t; i0 < ncols * 32; i0 += 192 * 8) {   // 8 loads in flight per thread
       float v[8];
 #pragma unroll
@@ -206,7 +230,29 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
     return;
   }
   float* red;
-  {
+  if (a.S == 1) {
+    // ---- (3') no split: the accumulator goes straight to red[c][128] in shared memory (the
+    //      ring is free: every MMA retired); a warp writes 128 contiguous bytes per column
+    red = recv;
+    const int q = warp & 3, half = warp >> 2;
+    const int m = q * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    for (int c0 = half * 16; c0 < a.n_group; c0 += 32) {
+      uint32_t r[16];
+      if (nkb > 0) {
+        tmem_ld16_nw(trow + c0, r);
+        tmem_wait_ld();
+        tmem_fence_regs(r);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) r[k] = 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (c0 + k < a.n_group) red[(size_t)(c0 + k) * kTileM + m] = __uint_as_float(r[k]);
+    }
+    tc_fence_before();
+  } else {
   // ---- (3) partial tile: TMEM -> registers -> global scratch [tile][split][n/4][128][4]
     //      (each thread stores float4 = 4 consecutive columns of its row: a warp writes 512
     //      contiguous bytes), then release the tile counter
@@ -301,6 +347,10 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
           const int ul = it % 32, c = it / 32;
           gz[u] = *reinterpret_cast<const float4*>(red + (size_t)c * kTileM + 4 * ul);
           bb[u] = s_bias[ul];
+          if (a.gb) {                                     // (GEMM + per-row gate bias) + unit bias
+            const float4 g2 = s_gb[it];
+            gz[u].x += g2.x; gz[u].y += g2.y; gz[u].z += g2.z; gz[u].w += g2.w;
+          }
           cp[u] = s_cg[it];
         }
 #pragma unroll
@@ -398,18 +448,19 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   KT(7);
 }
 
-static size_t fused_smem_bytes(int n_group, int stages, int S, int NC, int fold_H) {
+static size_t fused_smem_bytes(int n_group, int stages, int S, int NC, int fold_H, bool gb = false) {
   const size_t ring = (size_t)stages * (kTileM * 128 + 2 * (size_t)n_group * 128);
   const size_t recv = (size_t)(S + 1) * kTileM * NC * 4;
   const size_t fold = fold_H ? 128 + (size_t)32 * fold_ld(fold_H) * 2 + (size_t)32 * ((NC + 23) / 24 * 24) * 4 : 0;
-  return 1024 + (ring > recv ? ring : recv) + 32 * 16 + (size_t)NC * 32 * 4 + (stages + 3) * 8 + 16 + fold;
+  const size_t gbb = gb ? 128 + 16 + (size_t)NC * 32 * 16 : 0;
+  return 1024 + (ring > recv ? ring : recv) + 32 * 16 + (size_t)NC * 32 * 4 + (2 * stages + 3) * 8 + 16 + fold + gbb;
 }
 
 // Split S: the largest S <= 16 such that every split has >= 1 K block, the split's whole
 // K-slice fits the shared-memory ring, and tiles * S <= #SMs (one co-resident wave: the
 // tile counter wait needs every split resident).  1 CTA per SM (smem > half an SM).
 static bool fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, int k_blocks, int M, int m_tiles,
-                        int num_sms, int fold_H = 0) {
+                        int num_sms, int fold_H = 0, bool gb = false) {
   a.n_rows_pad = n_rows_pad;
   a.n_group = n_group;
   a.n_valid = n_valid;
@@ -424,12 +475,15 @@ static bool fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, 
     if (tiles * S > num_sms) continue;
     int NC = (n_group + S - 1) / S;
     NC = (NC + 3) / 4 * 4;
-    const size_t sm = fused_smem_bytes(n_group, kbps, S, NC, fold_H);
+    // the split's whole K-slice resident if it fits, else a ring of >= 2 stages
+    int stages = kbps;
+    while (stages > 2 && fused_smem_bytes(n_group, stages, S, NC, fold_H, gb) > limit) --stages;
+    const size_t sm = fused_smem_bytes(n_group, stages, S, NC, fold_H, gb);
     if (sm > limit) continue;
     a.S = S;
     a.NC = NC;
     a.kb_per_split = kbps;
-    a.stages = kbps;
+    a.stages = stages;
     int tc = 32;
     while (tc < n_group) tc <<= 1;
     a.tmem_cols = tc;
@@ -444,7 +498,7 @@ static cudaError_t launch_fused(const CUtensorMap& tmW, const CUtensorMap& tmX, 
                                 cudaStream_t st) {
   // at least 116 KB of shared memory: never two CTAs of this kernel on one SM (the tile wait
   // relies on one CTA per SM with grid <= #SMs)
-  size_t smem = fused_smem_bytes(a.n_group, a.stages, a.S, a.NC, a.woh ? a.H : 0);
+  size_t smem = fused_smem_bytes(a.n_group, a.stages, a.S, a.NC, a.woh ? a.H : 0, a.gb != nullptr);
   if (smem < 116 * 1024) smem = 116 * 1024;
   auto fn = tc_gemm_fused_kernel<EPI>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -465,11 +519,14 @@ int g_fused_dbg = 0;
 cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                          int n_valid, int k_blocks, const float* bias, const float* cg, float* c_out, float* h_out,
                          int H, CellDst dst, float* scratch, unsigned int* counters, int num_sms, StepCtl ctl,
-                         cudaStream_t st, const __nv_bfloat16* woh, float* woh_part) {
+                         cudaStream_t st, const __nv_bfloat16* woh, float* woh_part, const float* gb, int gb_ld) {
   FusedArgs a{};
   a.dbg = g_fused_dbg;
-  if (!fill_common(a, n_rows_pad, n_group, n_valid, k_blocks, 4 * H, m_pad / kTileM, num_sms, woh ? H : 0))
+  if (!fill_common(a, n_rows_pad, n_group, n_valid, k_blocks, 4 * H, m_pad / kTileM, num_sms, woh ? H : 0,
+                   gb != nullptr))
     return cudaErrorInvalidConfiguration;
+  a.gb = gb;
+  a.gb_ld = gb_ld;
   a.woh = woh;
   a.woh_part = woh_part;
   if (const char* e = std::getenv("ONMT_FUSED_DBG")) a.dbg = std::atoi(e);   // (ablations; wrong results)
@@ -501,9 +558,14 @@ cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_p
 }
 
 // does the top-layer cell kernel with the folded W_out share fit (shared memory, co-residency)?
-bool tc_cell_fold_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms) {
+bool tc_cell_fold_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms, bool gb) {
   FusedArgs a{};
-  return fill_common(a, n_rows_pad, n_group, n_group, k_blocks, 4 * H, m_pad / kTileM, num_sms, H);
+  return fill_common(a, n_rows_pad, n_group, n_group, k_blocks, 4 * H, m_pad / kTileM, num_sms, H, gb);
+}
+// does a (non-top) cell kernel with per-row gate biases fit?
+bool tc_cell_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms, bool gb) {
+  FusedArgs a{};
+  return fill_common(a, n_rows_pad, n_group, n_group, k_blocks, 4 * H, m_pad / kTileM, num_sms, 0, gb);
 }
 
 // split the fused kernels use for a shape (tests / DESIGN numbers; 0 = unfused)

@@ -15,6 +15,9 @@
 //            (max, sum exp, top-K) over the CTA's vocabulary; one partial per (CTA, row).
 #include <math_constants.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "beam_device.cuh"
 #include "common.cuh"
 #include "ptx.cuh"
@@ -51,6 +54,13 @@ struct GenStepArgs {
                                                 //    overlap batch b's epilogue (batches of nt_max)
   int nbuf;                                     // staging buffers (1 or 2)
   int srows_alloc;                              // staging rows per buffer (min(n_group, R))
+  // gate tiles (the recurrent halves of the NEXT step's LSTM gates): 128 rows
+  // of Wg (tensor map tmWg) over K blocks [q * gkbh, (q + 1) * gkbh) of the same activation
+  // operand, q = tile / gt_per_q; the accumulator goes to gout[q][row][tile % gt_per_q * 128 + m]
+  // (row stride gld floats).  One gate tile per CTA with the smaller vocabulary share (appended
+  // after its vocabulary tiles: no scan, a plain store).
+  int n_gt, gt_per_q, gkbh, gld;
+  float* gout;
 };
 
 __device__ __forceinline__ float gs_ex2(float x) {
@@ -125,7 +135,8 @@ __device__ __forceinline__ unsigned long long gs_fadd2(unsigned long long a, uns
 
 template <int KMAX>
 __global__ void __launch_bounds__(kGsThreads, 1)
-gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GenStepArgs a) {
+gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ CUtensorMap tmWg, GenStepArgs a) {
   KT(0);
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -147,14 +158,55 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = blockIdx.x / a.C, ci = blockIdx.x % a.C;
-  const int tb = (int)((long long)ci * a.n_vt / a.C), te = (int)((long long)(ci + 1) * a.n_vt / a.C);
+  const int tb = ci * a.n_vt / a.C, te = (ci + 1) * a.n_vt / a.C;   // (n_vt * C < 2^31)
   const int n0 = grp * a.n_group;
-  // batch bt = tiles [bfirst(bt), bfirst(bt) + bsize(bt)) of this CTA's run, staged from sequence
-  // number bfirst(bt) - tb.  ovl: two batches, the first one smaller (its epilogue starts early)
-  const int nbatch = (te - tb + a.nt_max - 1) / a.nt_max;
-  auto bfirst = [&](int bt) { return tb + bt * a.nt_max; };
-  auto bsize = [&](int bt) { return min(a.nt_max, te - bfirst(bt)); };
+  // local tiles i = 0 .. ntot-1: vocabulary tiles tb + i (i < nv), then the CTA's gate tile (if
+  // any).  Batch bt = local tiles [bt * nt_max, min(ntot, (bt + 1) * nt_max)), all accumulators of
+  // a batch in TMEM at once (K-outer over the union of its tiles' K-block ranges).  ovl: every
+  // tile its own TMEM columns, so batch bt + 1's MMAs overlap batch bt's epilogue.
+  const int nv = te - tb;
+  int gi = -1;                                                     // my gate tile
+  if (a.n_gt > 0 && nv == a.n_vt / a.C) {
+    // CTAs of my group before me with the smaller share: tb = ci * floor + (#larger shares before me)
+    const int idx = ci - (tb - ci * (a.n_vt / a.C));
+    if (idx < a.n_gt) gi = idx;
+  }
+  const int ntot = nv + (gi >= 0 ? 1 : 0);
+  const int nbatch = (ntot + a.nt_max - 1) / a.nt_max;
+  auto bfirst = [&](int bt) { return bt * a.nt_max; };
+  auto bsize = [&](int bt) { return min(a.nt_max, ntot - bfirst(bt)); };
   auto tcol = [&](int bt, int j) { return (uint32_t)((a.ovl ? bt * a.nt_max + j : j) * a.n_group); };
+  auto is_gate = [&](int i) { return i >= nv; };
+  const int g_lo = gi >= 0 ? (gi / a.gt_per_q) * a.gkbh : 0, g_hi = g_lo + a.gkbh;
+  // per-batch tile table, computed once per batch (the single producer / MMA threads must not
+  // redo index arithmetic per K block): K-block range, weight row and map of every tile slot
+  struct Bat {
+    int klo, khi;
+    int lo[4], hi[4], row[4];
+    bool gate[4];
+  };
+  auto make_bat = [&](int bt) {
+    Bat B;
+    B.klo = 1 << 30;
+    B.khi = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = bfirst(bt) + j;
+      const bool v = j < bsize(bt), g = is_gate(i);
+      B.gate[j] = g;
+      B.lo[j] = v ? (g ? g_lo : 0) : 0;
+      B.hi[j] = v ? (g ? g_hi : a.k_blocks) : 0;
+      B.row[j] = (g ? gi : tb + i) * kTileM;
+      if (v) { B.klo = min(B.klo, B.lo[j]); B.khi = max(B.khi, B.hi[j]); }
+    }
+    return B;
+  };
+  auto cover_mask = [](const Bat& B, int kb) {
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m |= (kb >= B.lo[j] && kb < B.hi[j]) ? (1u << j) : 0u;
+    return m;
+  };
   // staging is split into 32-hypothesis-row chunks with their own full/empty barriers: the
   // scanners of a chunk start as soon as it is staged and the stagers refill a chunk as soon
   // as its scanners are done (instead of whole-tile hand-offs)
@@ -164,6 +216,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
+    if (gi >= 0) tma_prefetch_desc(&tmWg);
     for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     mbar_init(tempty, kGsStageWarps);
@@ -182,21 +235,30 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   if (threadIdx.x == 0 || threadIdx.x == 32) fence_mbar_init();
   // the weight tiles of the first ring stages are constants of the translation: their TMA loads
   // are issued before griddepcontrol.wait (the activation halves follow after it)
-  int npre = nbatch > 0 ? min(a.stages, a.k_blocks) : 0;
-#ifdef ONMT_KTRACE
-  if (a.dbg == 11 || a.dbg == 12) npre = 0;
-#endif
   auto load_act = [&](int it, int kb) {
     uint8_t* st = smem + (size_t)(it % a.stages) * stage_bytes;
     tma_load_2d(st, &tmX, kb * kBK, n0, &full[it % a.stages]);
     tma_load_2d(st + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[it % a.stages]);
   };
-  if (threadIdx.x == 0) {
-    const int nt0 = bsize(0), t00 = bfirst(0);
-    for (int it = 0; it < npre; ++it) {
-      uint8_t* st = smem + (size_t)it * stage_bytes;
-      mbar_arrive_expect_tx(&full[it], 2 * b_bytes + nt0 * a_bytes);
-      for (int j = 0; j < nt0; ++j) tma_load_2d(st + 2 * b_bytes + j * a_bytes, &tmW, it * kBK, (t00 + j) * kTileM, &full[it]);
+  // weight tiles of batch B that cover kb (mask cov) -> stage slot j (their position); gate
+  // weights are stored compactly (K block kb - lo of the tile's block)
+  auto load_w = [&](const Bat& B, unsigned cov, int kb, uint8_t* st, uint64_t* bar) {
+    mbar_arrive_expect_tx(bar, 2 * b_bytes + (uint32_t)__popc(cov) * a_bytes);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((cov >> j) & 1u)
+        tma_load_2d(st + 2 * b_bytes + j * a_bytes, B.gate[j] ? &tmWg : &tmW, (kb - B.lo[j]) * kBK, B.row[j], bar);
+  };
+  // the weight tiles of the first ring stages are constants of the translation: their TMA loads
+  // are issued before griddepcontrol.wait (the activation halves follow after it)
+  int npre = 0;
+  if (threadIdx.x == 0 && nbatch > 0) {
+    const Bat B0 = make_bat(0);
+    for (int kb = B0.klo; kb < B0.khi && npre < a.stages; ++kb) {
+      const unsigned cov = cover_mask(B0, kb);
+      if (!cov) continue;
+      load_w(B0, cov, kb, smem + (size_t)npre * stage_bytes, &full[npre]);
+      ++npre;
     }
   }
   if (warp == 1) tmem_alloc<512>(tslot);
@@ -211,8 +273,12 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     for (int i = threadIdx.x; i < a.rows_pad * 4; i += blockDim.x) sl[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (all_done(a.ctl)) {                                           // uniform over the grid
-    if (threadIdx.x == 0)                                          // (no TMA may land after exit)
-      for (int it = 0; it < npre; ++it) { load_act(it, it); mbar_wait(&full[it], 0); }
+    if (threadIdx.x == 0 && npre > 0) {                              // (no TMA may land after exit)
+      const Bat B0 = make_bat(0);
+      int it = 0;
+      for (int kb = B0.klo; kb < B0.khi && it < npre; ++kb)
+        if (cover_mask(B0, kb)) { load_act(it, kb); mbar_wait(&full[it], 0); ++it; }
+    }
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
     return;
@@ -224,36 +290,19 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     if (lane == 0) {
       int it = 0;
       for (int bt = 0; bt < nbatch; ++bt) {
-        const int t0 = bfirst(bt);
-        const int nt = bsize(bt);
         if (bt > 0 && !a.ovl) {                                   // the staging overlays the ring: the
           mbar_wait(tempty, (bt - 1) & 1);                         // previous batch is staged AND scanned
           mbar_wait(sdone, (bt - 1) & 1);                          // before its stages are reloaded
         }
-        for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
+        const Bat B = make_bat(bt);
+        for (int kb = B.klo; kb < B.khi; ++kb) {
+          const unsigned cov = cover_mask(B, kb);
+          if (!cov) continue;
           const int s = it % a.stages;
           if (it >= a.stages) mbar_wait(&empty[s], ((it / a.stages) & 1) ^ 1);
-          uint8_t* st = smem + (size_t)s * stage_bytes;
-#ifdef ONMT_KTRACE
-          if (a.dbg == 11 || a.dbg == 12) {                        // ablations: activations / weights only
-            mbar_arrive_expect_tx(&full[s], a.dbg == 12 ? 2 * b_bytes : nt * a_bytes);
-            if (a.dbg == 12) {
-              tma_load_2d(st, &tmX, kb * kBK, n0, &full[s]);
-              tma_load_2d(st + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[s]);
-            } else {
-              for (int j = 0; j < nt; ++j) tma_load_2d(st + 2 * b_bytes + j * a_bytes, &tmW, kb * kBK, (t0 + j) * kTileM, &full[s]);
-            }
-            continue;
-          }
-#endif
-          if (it < npre) {                                         // weights already in flight
-            load_act(it, kb);
-            continue;
-          }
-          mbar_arrive_expect_tx(&full[s], 2 * b_bytes + nt * a_bytes);
-          tma_load_2d(st, &tmX, kb * kBK, n0, &full[s]);
-          tma_load_2d(st + b_bytes, &tmX, kb * kBK, a.n_rows_pad + n0, &full[s]);
-          for (int j = 0; j < nt; ++j) tma_load_2d(st + 2 * b_bytes + j * a_bytes, &tmW, kb * kBK, (t0 + j) * kTileM, &full[s]);
+          if (it >= npre) load_w(B, cov, kb, smem + (size_t)s * stage_bytes, &full[s]);   // (else: in flight)
+          load_act(it, kb);
+          ++it;
         }
       }
     }
@@ -263,24 +312,31 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_group);
       int it = 0;
       for (int bt = 0; bt < nbatch; ++bt) {
-        const int nt = bsize(bt);
-        for (int kb = 0; kb < a.k_blocks; ++kb, ++it) {
+        const Bat B = make_bat(bt);
+        const uint32_t tc0 = tmem + tcol(bt, 0);
+        for (int kb = B.klo; kb < B.khi; ++kb) {
+          const unsigned cov = cover_mask(B, kb);
+          if (!cov) continue;
           const int s = it % a.stages;
           mbar_wait(&full[s], (it / a.stages) & 1);
           tc_fence_after();
           KTX(7, it == 0);
           const uint32_t sb = smem_u32(smem + (size_t)s * stage_bytes);
-          for (int j = 0; j < nt; ++j) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (!((cov >> j) & 1u)) continue;
             const uint32_t sa = sb + 2 * b_bytes + j * a_bytes;
-            const uint32_t d = tmem + tcol(bt, j);
+            const uint32_t d = tc0 + (uint32_t)(j * a.n_group);
+            const uint32_t acc0 = kb == B.lo[j] ? 0u : 1u;
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {
               const uint64_t da = umma_desc_sw128(sa + kk * 32);
-              tc_mma_bf16(d, da, umma_desc_sw128(sb + kk * 32), idesc, (kb | kk) != 0);
+              tc_mma_bf16(d, da, umma_desc_sw128(sb + kk * 32), idesc, kk == 0 ? acc0 : 1u);
               tc_mma_bf16(d, da, umma_desc_sw128(sb + b_bytes + kk * 32), idesc, 1u);
             }
           }
           tc_commit(&empty[s]);
+          ++it;
         }
         tc_commit(tfull);
       }
@@ -296,14 +352,31 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       float bias_r[4];                                             // bias of my vocabulary row, loaded
 #pragma unroll                                                     // while the MMAs run
       for (int j = 0; j < 4; ++j) {
-        const int vid = (t0 + j) * kTileM + vr;
-        bias_r[j] = (j < nt && vid < a.V) ? __ldg(&a.bias[vid]) : -INFINITY;
+        const int vid = (tb + t0 + j) * kTileM + vr;
+        bias_r[j] = (j < nt && !is_gate(t0 + j) && vid < a.V) ? __ldg(&a.bias[vid]) : -INFINITY;
       }
       mbar_wait(tfull, bt & 1);
       tc_fence_after();
       KTX(2, threadIdx.x == 64 && bt == 0);
       for (int j = 0; j < nt; ++j) {
-        const int jj = t0 - tb + j;                                // staging sequence number
+        if (is_gate(t0 + j)) {
+          // gate tile: accumulator row vr (gate row of the tile) -> gout, 32 hypothesis rows per load
+          const uint32_t trow = tmem + tcol(bt, j) + ((uint32_t)(q * 32) << 16);
+          const int qb = gi / a.gt_per_q, col = (gi % a.gt_per_q) * kTileM + vr;
+          float* go = a.gout + ((size_t)qb * a.rows_pad + n0) * a.gld + col;
+          for (int c0 = 0; c0 < ncols; c0 += 32) {
+            uint32_t r[32];
+            if (c0 + 32 <= ncols) tmem_ld32_nw(trow + c0, r);
+            else tmem_ld16_nw(trow + c0, r);
+            tmem_wait_ld();
+            tmem_fence_regs(r);
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              if (c0 + k < srows) __stcg(go + (size_t)(c0 + k) * a.gld, __uint_as_float(r[k]));
+          }
+          continue;
+        }
+        const int jj = t0 + j;                                     // staging sequence number
         const int buf = jj % a.nbuf, use = jj / a.nbuf;
         KTX(6, threadIdx.x == 64 && jj == 2);
         {
@@ -352,6 +425,9 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         KTX(10, threadIdx.x == 64 && bt == 0 && j == 0);
       }
       tc_fence_before();                                           // batch's accumulators drained
+      // (ring overlay: the staging stores - generic proxy - must be ordered before the next
+      //  batch's TMA writes to the same bytes - async proxy - that this arrival releases)
+      if (!a.ovl) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive_local(tempty);
     }
@@ -377,9 +453,10 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     }
     int jj = 0;
     for (int bt = 0; bt < nbatch; ++bt) {
-      const int t0 = bfirst(bt);
+      const int t0 = tb + bfirst(bt);                              // (vocabulary tile of local index bfirst)
       const int nt = bsize(bt);
       for (int j = 0; j < nt; ++j, ++jj) {
+        if (is_gate(bfirst(bt) + j)) break;                        // (the gate tile comes last: no scan)
         const int buf = jj % a.nbuf, use = jj / a.nbuf;
         // the row's shared threshold: the largest list tail any scanner of any CTA published
         // so far - a K-th best of a subset of the row, so a lower bound of the row's K-th best
@@ -526,6 +603,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
         KTX(5, et == 0 && jj == 0);
         KTX(11, et == 0 && jj == 1);
       }
+      if (!a.ovl) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // (reads before the reload)
       __syncwarp();
       if (lane == 0) mbar_arrive_local(sdone);                     // (ring overlay: batch bt scanned)
     }
@@ -653,22 +731,31 @@ int gen_step_parts(int n_vt, int n_group, int groups, int num_sms) {
   return gs_plan(n_vt, n_group, groups, num_sms, n_group * groups, 16, p) ? p.C : 0;
 }
 
+// gate tiles the step kernel can take per row group without raising any CTA's tile count:
+// one each for the CTAs holding the smaller vocabulary share (0 if the split is even)
+int gen_step_gate_capacity(int n_vt, int n_group, int groups, int num_sms) {
+  GsPlan p;
+  if (!gs_plan(n_vt, n_group, groups, num_sms, n_group * groups, 16, p)) return 0;
+  return n_vt % p.C == 0 ? 0 : p.C - n_vt % p.C;
+}
+
 template <int KMAX>
-static cudaError_t launch_gs(const CUtensorMap& tmW, const CUtensorMap& tmX, const GenStepArgs& a, int grid,
-                             size_t smem, cudaStream_t st) {
+static cudaError_t launch_gs(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmWg,
+                             const GenStepArgs& a, int grid, size_t smem, cudaStream_t st) {
   auto fn = gen_step_kernel<KMAX>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(fn, dim3(grid), dim3(kGsThreads), smem, st, tmW, tmX, a);
+  return launch_pdl(fn, dim3(grid), dim3(kGsThreads), smem, st, tmW, tmX, tmWg, a);
 }
 
 // generator partials of decode step t (t selects the threshold buffers)
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i, int t,
-                     unsigned int* thr, StepCtl ctl, cudaStream_t st) {
+                     unsigned int* thr, StepCtl ctl, cudaStream_t st, const GateTiles& gt) {
   const int groups = n_rows_pad / n_group;
   GsPlan p;
   if (!gs_plan(n_vt, n_group, groups, num_sms, g.rows_valid, g.K, p)) return cudaErrorInvalidConfiguration;
+  if (gt.n_gt > 0 && (n_vt % p.C == 0 || gt.n_gt > p.C - n_vt % p.C)) return cudaErrorInvalidConfiguration;
   GenStepArgs a{};
   a.n_rows_pad = n_rows_pad;
   a.n_group = n_group;
@@ -696,16 +783,26 @@ cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, i
   a.dbg = g_gs_dbg;
   const int grid = p.C * groups;
   const size_t smem = gs_smem_bytes(p.body, p.stages);
+  if (getenv("ONMT_GEN_DEBUG") && t <= 1)
+    fprintf(stderr, "gen_step plan: C=%d groups=%d n_group=%d nt_max=%d stages=%d ovl=%d nbuf=%d srows=%d smem=%zu "
+            "static=%zu gates=%d\n", p.C, groups, n_group, p.nt_max, p.stages, p.ovl, p.nbuf, p.srows, smem,
+            gs_static_smem(g.K), gt.n_gt);
   a.ovl = p.ovl;
   a.nbuf = p.nbuf;
   a.srows_alloc = p.srows;
-  if (g.K <= 1) return launch_gs<1>(tmW, tmX, a, grid, smem, st);
-  if (g.K <= 2) return launch_gs<2>(tmW, tmX, a, grid, smem, st);
-  if (g.K <= 4) return launch_gs<4>(tmW, tmX, a, grid, smem, st);
-  if (g.K == 5) return launch_gs<5>(tmW, tmX, a, grid, smem, st);     // (the paper's beam size)
-  if (g.K <= 8) return launch_gs<8>(tmW, tmX, a, grid, smem, st);
-  if (g.K == 10) return launch_gs<10>(tmW, tmX, a, grid, smem, st);   // (BASELINE c5)
-  return launch_gs<16>(tmW, tmX, a, grid, smem, st);
+  a.n_gt = gt.n_gt;
+  a.gt_per_q = gt.gt_per_q > 0 ? gt.gt_per_q : 1;
+  a.gkbh = gt.gkbh;
+  a.gld = gt.gld;
+  a.gout = gt.gout;
+  const CUtensorMap& tmWg = gt.n_gt > 0 ? *gt.tmWg : tmW;
+  if (g.K <= 1) return launch_gs<1>(tmW, tmX, tmWg, a, grid, smem, st);
+  if (g.K <= 2) return launch_gs<2>(tmW, tmX, tmWg, a, grid, smem, st);
+  if (g.K <= 4) return launch_gs<4>(tmW, tmX, tmWg, a, grid, smem, st);
+  if (g.K == 5) return launch_gs<5>(tmW, tmX, tmWg, a, grid, smem, st);     // (the paper's beam size)
+  if (g.K <= 8) return launch_gs<8>(tmW, tmX, tmWg, a, grid, smem, st);
+  if (g.K == 10) return launch_gs<10>(tmW, tmX, tmWg, a, grid, smem, st);   // (BASELINE c5)
+  return launch_gs<16>(tmW, tmX, tmWg, a, grid, smem, st);
 }
 
 }  // namespace onmt

@@ -41,7 +41,8 @@ int gen_persistent_parts(int n_vt, int n_groups, int num_sms, int cs);
 int gen_step_parts(int n_vt, int n_group, int groups, int num_sms);
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i, int t,
-                     unsigned int* thr, StepCtl ctl, cudaStream_t st);
+                     unsigned int* thr, StepCtl ctl, cudaStream_t st, const GateTiles& gt);
+int gen_step_gate_capacity(int n_vt, int n_group, int groups, int num_sms);
 extern unsigned long long* g_gen_dbg;
 
 cudaError_t simt_gemm_partial(const void* W, bool w_bf16, int m_pad, int k_pad, const float* X, int n_rows_pad,
@@ -50,8 +51,10 @@ int simt_effective_splits(int k_pad, int splits);
 cudaError_t tc_gemm_cell(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                          int n_valid, int k_blocks, const float* bias, const float* cg, float* c_out, float* h_out,
                          int H, CellDst dst, float* scratch, unsigned int* counters, int num_sms, StepCtl ctl,
-                         cudaStream_t st, const __nv_bfloat16* woh = nullptr, float* woh_part = nullptr);
-bool tc_cell_fold_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms);
+                         cudaStream_t st, const __nv_bfloat16* woh = nullptr, float* woh_part = nullptr,
+                         const float* gb = nullptr, int gb_ld = 0);
+bool tc_cell_fold_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms, bool gb = false);
+bool tc_cell_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms, bool gb);
 struct EncRecDir {
   const float* Z;
   int z_ld;
@@ -373,6 +376,8 @@ struct onmt_model {
   bool enc_persistent = true;  // encoder recurrence of a layer as one persistent kernel (enc_rec.cu)
   bool fold_cur = false;       // ... for the call being enqueued (fold_on)
   bool use_graph = true;
+  bool rsplit = true;          // recurrent-split decode step where it applies
+  bool rs_cur = false;         // ... for the call being enqueued
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
   int64_t launches = 0;
@@ -392,6 +397,11 @@ struct onmt_model {
   DevBuf copy_w;                             // [H] fp32 (bf16-rounded in bf16 mode)
   float copy_b = 0.f;
   DevBuf woh_t;                              // W_out[:, H:2H]^T bf16 [top-layer tiles * 32][fold_ld(H)]
+  // recurrent-split step (bf16 models with L >= 2)
+  Mat wg;                                    // gate-tile weights [(L+1) blocks of 4H rows][H]: W_feed (dec.l0.w_ih
+                                             // input-feed columns), then W_hh of layers 1..L, gate-interleaved
+  std::vector<std::unique_ptr<Mat>> dec_wih; // [L]: layer l >= 1's W_ih alone (K = H); [0] unused
+  DevBuf emb_proj;                           // T = E_tgt W_emb^T  [V rows][4H rounded to 128] fp32
 
   // encoder workspace
   DevBuf d_ids, d_lens;
@@ -408,6 +418,8 @@ struct onmt_model {
   DevBuf f_scratch, f_count;                 // fused GEMM partial tiles + per-tile arrival counters
   DevBuf g_thr;                              // generator: shared per-row top-K thresholds [2][rows_pad] + slots [2][rows_pad][16]
   DevBuf woh_part;                           // folded W_out: top-layer shares W_out[:, units] h [tiles][rows_pad][H]
+  DevBuf pgate, gbias;                       // recurrent split: gate tiles [L+1][rows_pad][G], gate biases [L-1][rows_pad][G]
+  Act xr[8];                                 // recurrent split: layer l >= 1's operand [h_{l-1}] (K = H)
   DevBuf g_ms, g_tz, g_ti;
   DevBuf row_lse, row_z, row_i;
   DevBuf b_cum, b_live, b_y, b_prow, b_done, b_ndone, b_bt, b_br, b_braw, b_bnorm;
@@ -425,8 +437,6 @@ struct onmt_model {
   // teacher-forced scoring workspace
   Act xs_all;                                // generator operand of every (step, sentence) row
   DevBuf s_tgt, s_gold, s_zgold, s_out, s_ms, s_tz, s_ti;
-
-  int64_t enqueue_variant() const { return 0; }   // bitmask of enqueue-shaping options (graph keys)
 
   ~onmt_model() {
     for (auto& g : graphs)
@@ -448,7 +458,9 @@ static int auto_splits(onmt_model* m, const Mat& W, int n_groups) {
 
 // P[split][n][m] partial sums of W * X^T; returns the number of splits written.
 static int gemm(onmt_model* m, const Mat& W, const Act& X, int n_valid, int splits, float* out, StepCtl ctl) {
-  if (W.k_pad != X.k_pad) throw Error{ONMT_E_INVALID_ARG, "internal: K mismatch"};
+  if (W.k_pad != X.k_pad)
+    throw Error{ONMT_E_INVALID_ARG, "internal: K mismatch (W " + std::to_string(W.m) + "x" + std::to_string(W.k_pad) +
+                                        ", X " + std::to_string(X.rows) + "x" + std::to_string(X.k_pad) + ")"};
   if (splits <= 0) splits = auto_splits(m, W, X.rows_pad / X.n_group);
   if (m->use_tc) {
     int kb = W.k_pad / kBK;
@@ -597,6 +609,65 @@ static void upload_f32(DevBuf& d, const std::vector<float>& h) {
   ONMT_CUDA(cudaMemcpy(d.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
 }
 
+// Recurrent-split step weights.  The layer-1 gates of step t+1 are
+//   W_emb E_tgt[y] + W_feed h~_t[p] + W_hh1 h_1,t[p] + b_1
+// and (W x)[p] = W (x[p]): everything but the embedding term is computed for all step-t rows
+// BEFORE the beam step picks the parents p - by gate tiles of the generator kernel, whose
+// activation operand becomes [h~ | h_1 | ... | h_L] - and the embedding term is a row of the
+// table T = E_tgt W_emb^T (computed here once, one tcgen05 GEMM over the vocabulary).
+// Layers l >= 2 keep only W_ih h_{l-1} on the critical path; W_hh h_l comes from gate tiles.
+static int gemm(onmt_model* m, const Mat& W, const Act& X, int n_valid, int splits, float* out, StepCtl ctl);
+static void build_rsplit(onmt_model* m, std::map<std::string, HostTensor>& t) {
+  const int H = m->H, E = m->E, L = m->L;
+  const int G = round_up(4 * H, kTileM), kpH = round_up(H, kBK);
+  // gate-tile weights: block q = 0: W_feed = dec.l0.w_ih[:, E:E+H]; q = l (1..L): dec.l{l-1}.w_hh
+  std::vector<float> wg((size_t)(L + 1) * G * kpH, 0.f);
+  for (int q = 0; q <= L; ++q) {
+    const HostTensor& src = q == 0 ? t.at("dec.l0.w_ih") : t.at("dec.l" + std::to_string(q - 1) + ".w_hh");
+    const int ld = (int)src.dims[1], c0 = q == 0 ? E : 0;
+    for (int g = 0; g < 4; ++g)
+      for (int j = 0; j < H; ++j) {
+        const float* a = src.v.data() + (size_t)(g * H + j) * ld + c0;
+        std::copy(a, a + H, wg.data() + ((size_t)q * G + 4 * j + g) * kpH);
+      }
+  }
+  m->wg.upload(wg, (L + 1) * G, kpH, true);
+  // W_ih of layers >= 2 alone (K = H)
+  m->dec_wih.clear();
+  m->dec_wih.push_back(nullptr);
+  for (int l = 1; l < L; ++l) {
+    int K;
+    auto hw = gate_interleave(t.at("dec.l" + std::to_string(l) + ".w_ih"), nullptr, H, K);
+    auto w = std::make_unique<Mat>();
+    w->upload(hw, 4 * H, K, true);
+    m->dec_wih.push_back(std::move(w));
+  }
+  // T = E_tgt W_emb^T: W_emb = dec.l0.w_ih[:, 0:E] (gate-interleaved), E_tgt as a bf16 operand
+  // (the model's weights are bf16, so its lo plane is zero and the products are exact)
+  {
+    HostTensor we;
+    const HostTensor& w0 = t.at("dec.l0.w_ih");
+    we.dims = {(uint64_t)4 * H, (uint64_t)E};
+    we.v.resize((size_t)4 * H * E);
+    for (int r = 0; r < 4 * H; ++r)
+      std::copy(w0.v.data() + (size_t)r * (E + H), w0.v.data() + (size_t)r * (E + H) + E, we.v.data() + (size_t)r * E);
+    int K = 0;
+    const std::vector<float> hw = gate_interleave(we, nullptr, H, K);   // (sets K before upload reads it)
+    Mat W;
+    W.upload(hw, 4 * H, K, true);
+    Act X;
+    X.ensure(m->Vt, E, true);
+    const HostTensor& et = t.at("dec.emb");
+    std::vector<__nv_bfloat16> hl((size_t)2 * X.rows_pad * X.k_pad, __float2bfloat16_rn(0.f));
+    for (int v = 0; v < m->Vt; ++v)
+      for (int k = 0; k < E; ++k) hl[(size_t)v * X.k_pad + k] = __float2bfloat16_rn(et.v[(size_t)v * E + k]);
+    ONMT_CUDA(cudaMemcpy(X.hl.p, hl.data(), hl.size() * 2, cudaMemcpyHostToDevice));
+    m->emb_proj.ensure((size_t)X.rows_pad * G * 4);
+    gemm(m, W, X, m->Vt, 1, m->emb_proj.as<float>(), StepCtl{nullptr, 0});
+    ONMT_CUDA(cudaStreamSynchronize(m->stream));
+  }
+}
+
 static void load_model(onmt_model* m, const char* path) {
   auto t = read_mnmt(path);
   auto has = [&](const std::string& n) { return t.count(n) > 0; };
@@ -687,6 +758,7 @@ static void load_model(onmt_model* m, const char* path) {
     m->dec_w.push_back(std::move(w));
     m->dec_bias.push_back(std::move(bb));
   }
+  if (bf && m->L >= 2) build_rsplit(m, t);
   if (m->general) {
     const auto& wi = get(t, "attn.w_in", {H, H}, seen);
     m->attn_win.upload(plain_pad(wi), (int)H, (int)H, bf);
@@ -744,6 +816,42 @@ static bool fold_on(onmt_model* m, int rows) {
   const Mat& W = *m->dec_w[m->L - 1];
   const RowPlan rp = plan_rows(rows);
   return tc_cell_fold_fits(W.m_pad, rp.rows_pad, rp.n_group, W.k_pad / kBK, m->H, m->num_sms);
+}
+
+// recurrent split: layer l >= 2's GEMM (K = H) splits the hypothesis rows into groups of ns
+// instead of splitting K: every CTA owns a whole 128-row x ns-column output tile (no split-K
+// exchange through L2), m_tiles x rows_pad / ns <= #SMs
+static int rs_nsplit(onmt_model* m, int rows_pad) {
+  const int m_tiles = round_up(4 * m->H, kTileM) / kTileM;
+  for (int ns = 32; ns <= 256; ns += 16)
+    if (rows_pad % ns == 0 && m_tiles * (rows_pad / ns) <= m->num_sms) return ns;
+  return 0;
+}
+
+// recurrent-split step for a plain translation of R rows: bf16 models with
+// the folded W_out, L >= 2, whose gate tiles fit the generator's smaller-share CTAs and whose
+// layer kernels (with per-row gate biases) fit
+static bool rsplit_on(onmt_model* m, int B, int K, bool att) {
+  if (!(m->rsplit && m->use_tc && m->fused && m->gen_step && m->fold_cur && m->L >= 2 && m->wg.m > 0 && !att))
+    return false;
+  const int H = m->H, R = B * K;
+  if ((H & 3) != 0 || (size_t)2 * K * H * 4 > 120 * 1024) return false;       // beam step staging
+  const RowPlan rp = plan_rows(R);
+  const int groups = rp.rows_pad / rp.n_group;
+  const int n_vt = (m->Vt + kVTile - 1) / kVTile;
+  const int G = round_up(4 * H, kTileM);
+  const int n_gt = (m->L + 1) * (G / kTileM);
+  if (gen_step_gate_capacity(n_vt, rp.n_group, groups, m->num_sms) < n_gt) return false;
+  const int ns = rs_nsplit(m, rp.rows_pad);
+  if (ns == 0) return false;
+  for (int l = 1; l < m->L; ++l) {
+    const Mat& W = *m->dec_wih[l];
+    const bool ok = l + 1 == m->L
+                        ? tc_cell_fold_fits(W.m_pad, rp.rows_pad, ns, W.k_pad / kBK, H, m->num_sms, true)
+                        : tc_cell_fits(W.m_pad, rp.rows_pad, ns, W.k_pad / kBK, H, m->num_sms, true);
+    if (!ok) return false;
+  }
+  return true;
 }
 
 // ------------------------------------------------------------------ encoder
@@ -988,8 +1096,14 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
   m->xdec[0]->ensure(R, E + 2 * H, bfm);
   for (int l = 1; l < L; ++l) m->xdec[l]->ensure(R, 2 * H, bfm);
   m->xo.ensure(R, 2 * H, bfm);
-  m->xg.ensure(R, H, bfm);
+  const int kpH = round_up(H, kBK), G = round_up(4 * H, kTileM);
+  m->xg.ensure(R, m->rs_cur ? (L + 1) * kpH : H, bfm);          // recurrent split: [h~ | h_1 | .. | h_L]
   const int rp = m->xg.rows_pad;
+  if (m->rs_cur) {
+    m->pgate.ensure((size_t)(L + 1) * rp * G * 4);
+    m->gbias.ensure((size_t)std::max(L - 1, 1) * rp * G * 4);
+    for (int l = 1; l < L; ++l) m->xr[l].ensure(R, H, true);
+  }
   size_t pm = (size_t)m->dec_w[0]->m_pad;
   m->dec_p.ensure((size_t)16 * rp * pm * 4);
   m->st_h.ensure((size_t)L * rp * H * 4);
@@ -1038,6 +1152,10 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
     for (int l = 0; l < L; ++l)
       fs = std::max(fs, fused_scratch_floats(m->dec_w[l]->m_pad, m->xdec[l]->rows_pad, m->xdec[l]->n_group,
                                              m->dec_w[l]->k_pad / kBK, m->num_sms));
+    if (m->rs_cur)
+      for (int l = 1; l < L; ++l)
+        fs = std::max(fs, fused_scratch_floats(m->dec_wih[l]->m_pad, m->xr[l].rows_pad, rs_nsplit(m, m->xr[l].rows_pad),
+                                               m->dec_wih[l]->k_pad / kBK, m->num_sms));
     m->f_scratch.ensure(std::max<size_t>(fs, 1) * 4);
     if (m->g_thr.bytes < (size_t)2 * m->xg.rows_pad * 17 * 4) {
       m->g_thr.ensure((size_t)2 * m->xg.rows_pad * 17 * 4);
@@ -1051,54 +1169,14 @@ static void prepare_decoder(onmt_model* m, int B, int S_max, int K, int max_len,
   }
 }
 
-// One decoder step up to h~ (A5 inputs already gathered): the L LSTM layers, attention and
-// h~ = tanh(W_out [c; h]); h~ goes to m->htilde (input feed) and to the generator operand
-// xg_dst.  Used by translation (per-layer path) and by teacher-forced scoring.
-static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_max, int K, const int* done,
-                               XOut xg_dst, StepCtl ctl, float* att_out = nullptr) {
+// Attention (+ h~ = tanh(W_out [c; h]), folded or by the W_out kernel) on the top layer's h.
+static void enqueue_attention(onmt_model* m, const int* d_lens, int B, int S_max, int K, const int* done,
+                              XOut xg_dst, StepCtl ctl, float* att_out) {
   const bool bf = m->use_tc;
   const int R = B * K, H = m->H, L = m->L;
   const int rp = m->xg.rows_pad;
   float* hh = m->st_h.as<float>();
-  float* cc = m->st_c.as<float>();
-  float* cg = m->st_cg.as<float>();
   float* P = m->dec_p.as<float>();
-  for (int l = 0; l < L; ++l) {
-    const Mat& W = *m->dec_w[l];
-    CellDst dst{};
-    if (l + 1 < L) {
-      dst.x[0] = m->xdec[l + 1]->xo(bf); dst.col[0] = 0; dst.n = 1;
-    } else {
-      dst.x[0] = m->xo.xo(bf); dst.col[0] = H; dst.n = 1;
-    }
-    if (m->use_tc && m->fused) {
-      // gates GEMM + split-K cluster reduction + LSTM cell in one kernel
-      EvPair pg = prof_begin(m, "gemm");
-      const Act& X = *m->xdec[l];
-      const bool fold_l = m->fold_cur && l + 1 == L;        // top layer also leaves its W_out share
-      cudaError_t e = tc_gemm_cell(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, R, W.k_pad / kBK,
-                                   m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H, cc + (size_t)l * rp * H,
-                                   hh + (size_t)l * rp * H, H, dst, m->f_scratch.as<float>(),
-                                   m->f_count.as<unsigned int>() + (size_t)l * 2048, m->num_sms, ctl, m->stream,
-                                   fold_l ? m->woh_t.as<__nv_bfloat16>() : nullptr,
-                                   fold_l ? m->woh_part.as<float>() : nullptr);
-      if (fold_l && e == cudaErrorInvalidConfiguration) throw Error{ONMT_E_CUDA, "internal: folded W_out does not fit"};
-      prof_end(m, "gemm", pg);
-      if (e != cudaErrorInvalidConfiguration) {   // (no cluster shape fits: unfused path below)
-        ONMT_CUDA(e);
-        count(m);
-        continue;
-      }
-    }
-    EvPair pg = prof_begin(m, "gemm");
-    int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
-    prof_end(m, "gemm", pg);
-    EvPair pc = prof_begin(m, "cell");
-    launch_dec_cell(P, s, m->xdec[l]->rows_pad, W.m_pad, m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H,
-                    cc + (size_t)l * rp * H, hh + (size_t)l * rp * H, H, R, dst, ctl, m->stream);
-    count(m);
-    prof_end(m, "cell", pc);
-  }
   const float* htop = hh + (size_t)(L - 1) * rp * H;
   {
     EvPair pa = prof_begin(m, "attention");
@@ -1142,6 +1220,94 @@ static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_ma
     count(m);
     prof_end(m, "attn_out", po);
   }
+}
+
+// One decoder step up to h~ (A5 inputs already gathered): the L LSTM layers, attention and
+// h~ = tanh(W_out [c; h]); h~ goes to m->htilde (input feed) and to the generator operand
+// xg_dst.  Used by translation (per-layer path) and by teacher-forced scoring.
+static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_max, int K, const int* done,
+                               XOut xg_dst, StepCtl ctl, float* att_out = nullptr) {
+  const bool bf = m->use_tc;
+  const int R = B * K, H = m->H, L = m->L;
+  const int rp = m->xg.rows_pad;
+  float* hh = m->st_h.as<float>();
+  float* cc = m->st_c.as<float>();
+  float* cg = m->st_cg.as<float>();
+  float* P = m->dec_p.as<float>();
+  for (int l = 0; l < L; ++l) {
+    const Mat& W = *m->dec_w[l];
+    CellDst dst{};
+    if (l + 1 < L) {
+      dst.x[0] = m->xdec[l + 1]->xo(bf); dst.col[0] = 0; dst.n = 1;
+    } else {
+      dst.x[0] = m->xo.xo(bf); dst.col[0] = H; dst.n = 1;
+    }
+    if (m->rs_cur) {                    // recurrent split, step 1: h_l also feeds the gate tiles
+      dst.x[1] = m->xg.xo(bf); dst.col[1] = (l + 1) * round_up(H, kBK); dst.n = 2;
+    }
+    if (m->use_tc && m->fused) {
+      // gates GEMM + split-K cluster reduction + LSTM cell in one kernel
+      EvPair pg = prof_begin(m, "gemm");
+      const Act& X = *m->xdec[l];
+      const bool fold_l = m->fold_cur && l + 1 == L;        // top layer also leaves its W_out share
+      cudaError_t e = tc_gemm_cell(W.tmap, X.tmap, W.m_pad, X.rows_pad, X.n_group, R, W.k_pad / kBK,
+                                   m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H, cc + (size_t)l * rp * H,
+                                   hh + (size_t)l * rp * H, H, dst, m->f_scratch.as<float>(),
+                                   m->f_count.as<unsigned int>() + (size_t)l * 2048, m->num_sms, ctl, m->stream,
+                                   fold_l ? m->woh_t.as<__nv_bfloat16>() : nullptr,
+                                   fold_l ? m->woh_part.as<float>() : nullptr);
+      if (fold_l && e == cudaErrorInvalidConfiguration) throw Error{ONMT_E_CUDA, "internal: folded W_out does not fit"};
+      prof_end(m, "gemm", pg);
+      if (e != cudaErrorInvalidConfiguration) {   // (no cluster shape fits: unfused path below)
+        ONMT_CUDA(e);
+        count(m);
+        continue;
+      }
+    }
+    EvPair pg = prof_begin(m, "gemm");
+    int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
+    prof_end(m, "gemm", pg);
+    EvPair pc = prof_begin(m, "cell");
+    launch_dec_cell(P, s, m->xdec[l]->rows_pad, W.m_pad, m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H,
+                    cc + (size_t)l * rp * H, hh + (size_t)l * rp * H, H, R, dst, ctl, m->stream);
+    count(m);
+    prof_end(m, "cell", pc);
+  }
+  enqueue_attention(m, d_lens, B, S_max, K, done, xg_dst, ctl, att_out);
+}
+
+// Recurrent-split step, steps t >= 2: layer 1 already ran in the previous
+// beam step; layers l >= 2 reduce only W_ih h_{l-1} (K = H) and add the gathered recurrent term
+// (gb) in the cell epilogue; the top layer leaves its folded W_out share; then attention.
+static void enqueue_rs_layers(onmt_model* m, const int* d_lens, int B, int S_max, int K, const int* done, StepCtl ctl) {
+  const int R = B * K, H = m->H, L = m->L;
+  const int rp = m->xg.rows_pad, kpH = round_up(H, kBK), G = round_up(4 * H, kTileM);
+  float* hh = m->st_h.as<float>();
+  float* cc = m->st_c.as<float>();
+  float* cg = m->st_cg.as<float>();
+  const int ns = rs_nsplit(m, rp);
+  for (int l = 1; l < L; ++l) {
+    const Mat& W = *m->dec_wih[l];
+    const Act& X = m->xr[l];
+    const CUtensorMap tx = make_tmap(X.hl.p, X.k_pad, 2 * X.rows_pad, ns);   // box: ns hypothesis rows
+    CellDst dst{};
+    if (l + 1 < L) {
+      dst.x[0] = m->xr[l + 1].xo(true); dst.col[0] = 0;
+      dst.x[1] = m->xg.xo(true); dst.col[1] = (l + 1) * kpH; dst.n = 2;
+    } else {
+      dst.x[0] = m->xg.xo(true); dst.col[0] = L * kpH; dst.n = 1;
+    }
+    const bool top = l + 1 == L;
+    EvPair pg = prof_begin(m, "gemm");
+    ONMT_CUDA(tc_gemm_cell(W.tmap, tx, W.m_pad, X.rows_pad, ns, R, W.k_pad / kBK, m->dec_bias[l]->as<float>(),
+                           cg + (size_t)l * rp * H, cc + (size_t)l * rp * H, hh + (size_t)l * rp * H, H, dst,
+                           m->f_scratch.as<float>(), m->f_count.as<unsigned int>() + (size_t)l * 2048, m->num_sms, ctl,
+                           m->stream, top ? m->woh_t.as<__nv_bfloat16>() : nullptr,
+                           top ? m->woh_part.as<float>() : nullptr, m->gbias.as<float>() + (size_t)(l - 1) * rp * G, G));
+    prof_end(m, "gemm", pg);
+    count(m);
+  }
+  enqueue_attention(m, d_lens, B, S_max, K, done, m->xg.xo(true), ctl, nullptr);
 }
 
 static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, int K, int max_len, float alpha,
@@ -1208,24 +1374,45 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
                          m->row_i.as<int>(), ctl, m->stream);
     count(m, 3);
   };
-  float* P = m->dec_p.as<float>();
+  // recurrent split: the beam step runs layer 1's cell for the next step (GatherArgs::rsplit)
+  // and the generator computes the gate tiles; step 1 starts from the gathered initial state
+  GatherArgs gam = ga;
+  GateTiles gt{};
+  if (m->rs_cur) {
+    const int kpH = round_up(H, kBK), G = round_up(4 * H, kTileM);
+    gam.rsplit = 1;
+    gam.T = m->emb_proj.as<float>();
+    gam.P = m->pgate.as<float>();
+    gam.G = G;
+    for (int l = 0; l < L; ++l) gam.bias[l] = m->dec_bias[l]->as<float4>();
+    gam.gb = m->gbias.as<float>();
+    gam.c1_out = cc;
+    gam.xh1[0] = m->xr[1].xo(true); gam.col_h1[0] = 0;
+    gam.xh1[1] = m->xg.xo(true); gam.col_h1[1] = kpH;
+    gt = GateTiles{&m->wg.tmap, (L + 1) * (G / kTileM), G / kTileM, kpH / kBK, G, m->pgate.as<float>()};
+  }
   for (int t = 1; t <= max_len; ++t) {
     EvPair ev = prof_begin(m, "step");
-    enqueue_dec_layers(m, d_lens, B, S_max, K, bs.done, m->xg.xo(bf), ctl, op.att() ? m->b_att.as<float>() : nullptr);
+    if (m->rs_cur && t > 1)
+      enqueue_rs_layers(m, d_lens, B, S_max, K, bs.done, ctl);
+    else
+      enqueue_dec_layers(m, d_lens, B, S_max, K, bs.done, m->xg.xo(bf), ctl, op.att() ? m->b_att.as<float>() : nullptr);
     const double lp = std::pow((5.0 + t) / 6.0, (double)alpha);
     if (use_gen_step(m, m->xg)) {
       // K-outer generator (phase A of gen_step.cu), partials [row][C]; then row reduce + beam step
       EvPair pgs = prof_begin(m, "gen");
       ONMT_CUDA(gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
                            m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
-                           m->row_i.as<int>(), t, m->g_thr.as<unsigned int>(), ctl, m->stream));
+                           m->row_i.as<int>(), t, m->g_thr.as<unsigned int>(), ctl, m->stream,
+                           t < max_len ? gt : GateTiles{}));
       count(m);
       prof_end(m, "gen", pgs);
       EvPair pm = prof_begin(m, "merge");
       if (op.src_ext) {
         merge_copy(n_vt, 1, n_vt, t, lp);
       } else {
-        launch_beam_merge(g.ms, g.tz, g.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, ga, m->row_lse.as<float>(),
+        launch_beam_merge(g.ms, g.tz, g.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, m->rs_cur ? gam : ga,
+                          m->row_lse.as<float>(),
                           m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
         count(m, n_vt <= 256 ? 1 : 2);
       }
@@ -1372,6 +1559,7 @@ static void enqueue_score(onmt_model* m, const int* d_ids, const int* d_lens, in
 
 static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int T_max) {
   m->fold_cur = fold_on(m, B);
+  m->rs_cur = false;
   prepare_encoder(m, B, S_max);
   prepare_decoder(m, B, S_max, 1, T_max, false);
   const bool bf = m->use_tc;
@@ -1388,7 +1576,7 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
     return;
   }
   std::vector<int64_t> key = {-1, B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->fold_cur,
-                              m->enc_persistent, m->enc_wavefront, m->enqueue_variant(), (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
+                              m->enc_persistent, m->enc_wavefront, (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
                               (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
   replay_graph(m, key, [&]() { enqueue_score(m, d_ids, d_lens, B, S_max, T_max); });
 }
@@ -1398,6 +1586,7 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
 static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int K, int max_len,
                           float alpha, bool trace, const DecodeOut& out, const DecodeOpts& op = DecodeOpts{}) {
   m->fold_cur = fold_on(m, B * K);
+  m->rs_cur = rsplit_on(m, B, K, op.att() || op.src_ext);
   prepare_encoder(m, B, S_max);
   prepare_decoder(m, B, S_max, K, max_len, trace, op);
   auto enqueue = [&]() {
@@ -1409,7 +1598,7 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     return;
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
-                              m->gen_step, m->fold_cur, m->enc_persistent, m->enc_wavefront, m->enqueue_variant(),
+                              m->gen_step, m->fold_cur, m->enc_persistent, m->enc_wavefront, m->rs_cur,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
                               (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp,
@@ -1474,6 +1663,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   if (const char* ev = std::getenv("ONMT_FOLD_WOUT")) m->fold_wout = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_PERSISTENT")) m->enc_persistent = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_WAVE")) m->enc_wavefront = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_RSPLIT")) m->rsplit = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
   m->stream = m->own_stream;
@@ -1517,6 +1707,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->enc_wavefront = v != 0;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
+  } else if (n == "rsplit") {
+    m->rsplit = v != 0;
   } else {
     return fail(ONMT_E_INVALID_ARG, "unknown option " + n);
   }
@@ -1570,6 +1762,7 @@ onmt_status onmt_encode(onmt_model* m, const int32_t* ids, const int32_t* lens, 
   ONMT_CUDA(cudaSetDevice(m->device));
   upload_src(m, ids, lens, B, S_max, S_max);
   m->fold_cur = false;
+  m->rs_cur = false;
   prepare_encoder(m, B, S_max);
   enqueue_encoder(m, m->d_ids.as<int>(), m->d_lens.as<int>(), B, S_max);
   if (out_memory)
@@ -1892,7 +2085,7 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
     ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
     ONMT_CUDA(gen_step(m->gen_w.tmap, x.tmap, (m->Vt + kVTile - 1) / kVTile, x.rows_pad, x.n_group,
                        m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 0,
-                       m->g_thr.as<unsigned int>(), StepCtl{nullptr, 0}, m->stream));
+                       m->g_thr.as<unsigned int>(), StepCtl{nullptr, 0}, m->stream, GateTiles{}));
   } else {
     gen(m, x, g, StepCtl{nullptr, 0});
   }
