@@ -93,11 +93,17 @@ def dist_env():
     return ws, rank, local
 
 
-def gen_roofline_terms(w: synth.Workload, R: int):
+def gen_roofline_terms(w: synth.Workload, R: int, gate_tiles: int = 0):
     """Algorithmic bytes / flops of ONE generator launch:
-    bytes = 2*H*V (bf16 W_gen) + 4*V (fp32 bias); flops = 2*R*H*V."""
-    H, V = w.model.hidden, w.model.v_tgt
-    return 2.0 * H * V + 4.0 * V, 2.0 * R * H * V
+    bytes = 2*H*V (bf16 W_gen) + 4*V (fp32 bias); flops = 2*R*H*V.  With the recurrent-split
+    step the same launch also computes the next step's recurrent gate terms:
+    + 2*(L+1)*4H*H weight bytes and 2*R*(L+1)*4H*H flops (W_feed and every layer's W_hh)."""
+    H, V, L = w.model.hidden, w.model.v_tgt, w.model.layers
+    b, f = 2.0 * H * V + 4.0 * V, 2.0 * R * H * V
+    if gate_tiles:
+        b += 2.0 * (L + 1) * 4 * H * H
+        f += 2.0 * R * (L + 1) * 4 * H * H
+    return b, f
 
 
 # ---------------------------------------------------------------------------- ours
@@ -275,12 +281,14 @@ def run_ours(args):
         e2e_t, e2e_tokens = float(tm[0].item()), int(tt[1].item())
     h2d = ids.nbytes + lens.nbytes
     d2h = B * ML * 4 * 2 + B * 4 * 3
+    model_plan = model.last_plan()
     corpus = corpus_run(model, args, w, ws, rank, dev) if not args.no_corpus else None
 
     if rank == 0:
         pk = peaks()
         R = B * K
-        gbytes, gflops = gen_roofline_terms(w, R)
+        plan = model_plan
+        gbytes, gflops = gen_roofline_terms(w, R, plan.get("gate_tiles", 0))
         gen_avg_s = (gen_ms / gen_n) / 1e3 if gen_n else float("nan")
         achieved = gbytes / gen_avg_s / 1e9
         traffic = None
@@ -304,6 +312,7 @@ def run_ours(args):
             "e2e": {"value": round(e2e_tokens / (e2e_t / 1e3), 1), "unit": "target tok/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
+            "plan": model_plan,
             "roofline": {"kernel": "gen_step_kernel (K-outer tcgen05 generator + log-softmax + per-CTA top-K; logits never in HBM)",
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,

@@ -260,6 +260,18 @@ ONMT_API onmt_status onmt_kernel_launches(onmt_model* m, int32_t reset, int64_t*
  * reports this count).  INVALID_ARG on NULL. */
 ONMT_API onmt_status onmt_graph_captures(onmt_model* m, int64_t* captures);
 
+/*
+ * onmt_last_plan - how the last translate / score call of the handle was executed (for
+ * benchmarks and tests): rsplit = 1 if the recurrent-split decode step ran (DESIGN.md
+ * §6.4b), fold = 1 if W_out was folded into attention, gen_parts = generator partials per
+ * row, gate_tiles = gate tiles the generator computed per step (0 without rsplit), groups =
+ * hypothesis-row groups of the generator.  INVALID_ARG on NULL.
+ */
+typedef struct {
+  int32_t rsplit, fold, gen_parts, gate_tiles, groups;
+} onmt_plan_info;
+ONMT_API onmt_status onmt_last_plan(const onmt_model* m, onmt_plan_info* out);
+
 /* onmt_free - release every device/host resource of the handle (NULL is a no-op). */
 ONMT_API void onmt_free(onmt_model* m);
 

@@ -25,7 +25,7 @@ K_MAX = 16
 EXPORTS = ["onmt_load_weights", "onmt_model_get_info", "onmt_set_stream", "onmt_encode", "onmt_translate",
            "onmt_translate_trace", "onmt_translate_dev", "onmt_set_option", "onmt_get_kernel_time",
            "onmt_kernel_launches", "onmt_free", "onmt_last_error", "onmt_test_gemm", "onmt_test_gen", "onmt_score",
-           "onmt_translate_ex", "onmt_translate_copy", "onmt_graph_captures"]
+           "onmt_translate_ex", "onmt_translate_copy", "onmt_graph_captures", "onmt_last_plan"]
 
 
 class OnmtError(RuntimeError):
@@ -39,6 +39,11 @@ class _DecodeOpts(ctypes.Structure):
     """onmt_decode_opts (include/onmt.h)."""
     _fields_ = [("beam", ctypes.c_int32), ("max_len", ctypes.c_int32), ("length_penalty", ctypes.c_float),
                 ("coverage_penalty", ctypes.c_float), ("n_best", ctypes.c_int32), ("replace_unk", ctypes.c_int32)]
+
+
+class _Plan(ctypes.Structure):
+    """onmt_plan_info (include/onmt.h)."""
+    _fields_ = [(n, ctypes.c_int32) for n in ("rsplit", "fold", "gen_parts", "gate_tiles", "groups")]
 
 
 class _Info(ctypes.Structure):
@@ -69,6 +74,7 @@ def lib():
     L.onmt_get_kernel_time.argtypes = [VP, ctypes.c_char_p, I32, P(ctypes.c_double), P(I64)]
     L.onmt_kernel_launches.argtypes = [VP, I32, P(I64)]
     L.onmt_graph_captures.argtypes = [VP, P(I64)]
+    L.onmt_last_plan.argtypes = [VP, P(_Plan)]
     L.onmt_free.argtypes = [VP]
     L.onmt_free.restype = None
     L.onmt_last_error.restype = ctypes.c_char_p
@@ -142,6 +148,12 @@ class Model:
         n = ctypes.c_int64()
         _check(lib().onmt_kernel_launches(self._h, int(reset), ctypes.byref(n)))
         return n.value
+
+    def last_plan(self) -> Dict[str, int]:
+        """How the last translate call ran (onmt_last_plan)."""
+        p = _Plan()
+        _check(lib().onmt_last_plan(self._h, ctypes.byref(p)))
+        return {n: getattr(p, n) for n, _ in _Plan._fields_}
 
     def graph_captures(self) -> int:
         n = ctypes.c_int64()

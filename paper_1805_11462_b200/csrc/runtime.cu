@@ -433,6 +433,7 @@ struct onmt_model {
   std::vector<GraphCache> graphs;            // LRU cache of instantiated whole-call graphs
   uint64_t graph_clock = 0;
   int64_t graph_captures = 0;                // captures since load (corpus runs: should stop growing)
+  onmt_plan_info plan{};                     // how the last call ran (onmt_last_plan)
   GraphCache* cap_graph = nullptr;           // the graph being captured (profiling event nodes)
   // teacher-forced scoring workspace
   Act xs_all;                                // generator operand of every (step, sentence) row
@@ -1589,6 +1590,11 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
   m->rs_cur = rsplit_on(m, B, K, op.att() || op.src_ext);
   prepare_encoder(m, B, S_max);
   prepare_decoder(m, B, S_max, K, max_len, trace, op);
+  m->plan.rsplit = m->rs_cur;
+  m->plan.fold = m->fold_cur;
+  m->plan.gen_parts = gen_parts(m, m->xg);
+  m->plan.gate_tiles = m->rs_cur ? (m->L + 1) * (round_up(4 * m->H, kTileM) / kTileM) : 0;
+  m->plan.groups = m->xg.rows_pad / m->xg.n_group;
   auto enqueue = [&]() {
     enqueue_encoder(m, d_ids, d_lens, B, S_max);
     enqueue_decoder(m, d_lens, B, S_max, K, max_len, alpha, trace, out, op);
@@ -1981,6 +1987,12 @@ onmt_status onmt_kernel_launches(onmt_model* m, int32_t reset, int64_t* launches
   if (!m || !launches) return fail(ONMT_E_INVALID_ARG, "null argument");
   *launches = m->launches;
   if (reset) m->launches = 0;
+  return ONMT_OK;
+}
+
+onmt_status onmt_last_plan(const onmt_model* m, onmt_plan_info* out) {
+  if (!m || !out) return fail(ONMT_E_INVALID_ARG, "null argument");
+  *out = m->plan;
   return ONMT_OK;
 }
 

@@ -296,3 +296,37 @@ def test_repeated_calls_odd_max_len(weight_cache):
     again = gm.translate(ids, lens, 5, 7, 0.0)
     np.testing.assert_array_equal(first["hyps"], again["hyps"])
     np.testing.assert_array_equal(first["token_logp"], again["token_logp"])
+
+
+@pytest.mark.parametrize("workload,n", [("c2", 6), ("c5", 3)])
+def test_recurrent_split_step_plan_and_parity(workload, n, weight_cache):
+    """The recurrent-split decode step is the path the c2 / c5 shapes take
+    (onmt_last_plan), and both it and the per-layer step (option rsplit = 0) match the oracle;
+    they compute the same sums in a different order (token log p within 2e-5 of each other)."""
+    gm, om, prec = model_pair(workload, weight_cache)
+    w = synth.WORKLOADS[workload]
+    ids, lens = synth.make_corpus(workload, n)
+    outs = {}
+    for rs in (1, 0):
+        gm.set_option("rsplit", rs)
+        try:
+            res, outs[rs] = run_parity(gm, om, prec, ids, lens, w.decode.beam, 16, w.decode.alpha)
+            plan = gm.last_plan()
+        finally:
+            gm.set_option("rsplit", 1)
+        assert plan["rsplit"] == rs and plan["fold"] == 1
+        if rs:
+            assert plan["gate_tiles"] == (w.model.layers + 1) * ((4 * w.model.hidden + 127) // 128)
+    same = (outs[0]["hyps"] == outs[1]["hyps"]).all(axis=1)
+    np.testing.assert_allclose(outs[0]["token_logp"][same], outs[1]["token_logp"][same], atol=2e-5)
+
+
+def test_c4_takes_the_per_layer_step(weight_cache):
+    """c4 (4 x 1000, R = 640): the gate tiles do not fit the generator's smaller-share CTAs, so the
+    per-layer step runs (the plan reports it)."""
+    gm, om, prec = model_pair("c4", weight_cache)
+    ids, lens = synth.make_corpus("c4", 128)
+    S = int(lens.max())
+    gm.translate(np.ascontiguousarray(ids[:, :S]), lens, 5, 2, 0.6)
+    plan = gm.last_plan()
+    assert plan["rsplit"] == 0 and plan["groups"] == 3

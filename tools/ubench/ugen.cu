@@ -1,5 +1,6 @@
 // Microbenchmark of the persistent generator step kernel (gen_step.cu), c2 shape
-// (R = 150 rows, H = 500, V = 50000, K = 5), phases A (+B), with per-CTA phase stamps.
+// (R = 150 rows, H = 500, V = 50000, K = 5), with per-CTA phase stamps; argv[1] = 1 adds the
+// recurrent-split gate tiles (3 x 16 tiles of 128 x K 512 over an operand of 3 K blocks of 512).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DONMT_KTRACE -I../../paper_1805_11462_b200/csrc \
 //      -I../../include ugen.cu -lcuda -o ugen
 #include <cstdio>
@@ -26,25 +27,33 @@ static CUtensorMap make_tmap(const void* base, int k_pad, int rows, int box_rows
   return m;
 }
 int main(int argc, char** argv) {
-  const int phases = argc > 1 ? atoi(argv[1]) : 1;
+  const int gates = argc > 1 ? atoi(argv[1]) : 0;
   g_gs_dbg = argc > 2 ? atoi(argv[2]) : 0;
   cudaStream_t st; CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   const int R = 150, NP = 160, KP = 512, V = 50000, VP = 50048, K = 5, C = 148;
   __nv_bfloat16 *W, *X; float* bias;
-  CK(cudaMalloc(&W, (size_t)VP * KP * 2)); CK(cudaMalloc(&X, (size_t)2 * NP * KP * 2)); CK(cudaMalloc(&bias, VP * 4));
+  const int XK = gates ? 3 * KP : KP;                        // operand width (gate tiles: [h~ | h1 | h2])
+  CK(cudaMalloc(&W, (size_t)VP * KP * 2)); CK(cudaMalloc(&X, (size_t)2 * NP * XK * 2)); CK(cudaMalloc(&bias, VP * 4));
   {  // realistic values: W ~ U(-0.1, 0.1) bf16, activations tanh-like (hi plane; lo = 0), bias ~ U(-0.1, 0.1)
-    std::vector<__nv_bfloat16> hw((size_t)VP * KP), hx((size_t)2 * NP * KP);
+    std::vector<__nv_bfloat16> hw((size_t)VP * KP), hx((size_t)2 * NP * XK);
     std::vector<float> hb(VP);
     unsigned long long st_ = 88172645463325252ull;
     auto rnd = [&]() { st_ ^= st_ << 13; st_ ^= st_ >> 7; st_ ^= st_ << 17; return (st_ >> 11) * (1.0 / 9007199254740992.0); };
     for (size_t i = 0; i < hw.size(); ++i) hw[i] = __float2bfloat16((i % KP) < 500 ? (float)(0.2 * rnd() - 0.1) : 0.f);
-    for (size_t i = 0; i < hx.size(); ++i) hx[i] = __float2bfloat16(i < (size_t)NP * KP && (i % KP) < 500 ? (float)tanh(3 * rnd() - 1.5) : 0.f);
+    for (size_t i = 0; i < hx.size(); ++i) hx[i] = __float2bfloat16(i < (size_t)NP * XK && (i % KP) < 500 ? (float)tanh(3 * rnd() - 1.5) : 0.f);
     for (int i = 0; i < VP; ++i) hb[i] = i < V ? (float)(0.2 * rnd() - 0.1) : 0.f;
     CK(cudaMemcpy(W, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(X, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(bias, hb.data(), VP * 4, cudaMemcpyHostToDevice));
   }
-  CUtensorMap tmW = make_tmap(W, KP, VP, 128), tmX = make_tmap(X, KP, 2 * NP, NP);
+  CUtensorMap tmW = make_tmap(W, KP, VP, 128), tmX = make_tmap(X, XK, 2 * NP, NP);
+  const int G = 2048;
+  __nv_bfloat16* Wg; float* gout;
+  CK(cudaMalloc(&Wg, (size_t)3 * G * KP * 2)); CK(cudaMemset(Wg, 0, (size_t)3 * G * KP * 2));
+  CK(cudaMalloc(&gout, (size_t)3 * NP * G * 4));
+  CUtensorMap tmWg = make_tmap(Wg, KP, 3 * G, 128);
+  GateTiles gt{};
+  if (gates) gt = GateTiles{&tmWg, 3 * G / 128, G / 128, KP / 64, G, gout};
   float2* ms; float *tz, *rl, *rz; int *ti, *ri; unsigned int* gbar;
   CK(cudaMalloc(&ms, C * NP * 8)); CK(cudaMalloc(&tz, C * NP * K * 4)); CK(cudaMalloc(&ti, C * NP * K * 4));
   CK(cudaMalloc(&rl, R * 4)); CK(cudaMalloc(&rz, R * K * 4)); CK(cudaMalloc(&ri, R * K * 4));
@@ -52,28 +61,11 @@ int main(int argc, char** argv) {
   unsigned int* thr; CK(cudaMalloc(&thr, 2 * NP * 17 * 4)); CK(cudaMemset(thr, 0, 2 * NP * 17 * 4));
   unsigned long long* tr; CK(cudaMalloc(&tr, 4096 * 96)); CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
   GenOut g{ms, tz, ti, bias, V, K, R, NP};
-  // beam state / gather operands for phase C (zeroed; slot 0 of every sentence live)
-  const int B = R / K, H = 500, E = 500, L = 2, MAXLEN = 100;
-  auto zalloc = [&](size_t bytes) { void* p; CK(cudaMalloc(&p, bytes)); CK(cudaMemset(p, 0, bytes)); return p; };
-  BeamState bs{};
-  bs.cum = (double*)zalloc(2 * R * 8); bs.live = (int*)zalloc(2 * R * 4); bs.y = (int*)zalloc(R * 4);
-  bs.prow = (int*)zalloc(R * 4); bs.done = (int*)zalloc(B * 4); bs.n_done = (int*)zalloc(4);
-  bs.best_t = (int*)zalloc(B * 4); bs.best_r = (int*)zalloc(B * 4); bs.best_raw = (double*)zalloc(B * 8);
-  bs.best_norm = (double*)zalloc(B * 8); bs.hist_parent = (int*)zalloc(MAXLEN * R * 4);
-  bs.hist_token = (int*)zalloc(MAXLEN * R * 4); bs.hist_logp = (float*)zalloc(MAXLEN * R * 4);
-  { std::vector<int> lv(2 * R, 0); for (int b = 0; b < B; ++b) { lv[b * K] = 1; lv[R + b * K] = 1; }
-    CK(cudaMemcpy(bs.live, lv.data(), 2 * R * 4, cudaMemcpyHostToDevice)); }
-  GatherArgs ga{};
-  ga.emb_tgt = (float*)zalloc((size_t)V * E * 4); ga.E = E; ga.H = H; ga.L = L;
-  ga.htilde = (float*)zalloc(NP * H * 4); ga.h = (float*)zalloc(L * NP * H * 4); ga.c = (float*)zalloc(L * NP * H * 4);
-  ga.cg = (float*)zalloc(L * NP * H * 4); ga.rows_pad = NP;
-  ga.x[0] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1536 * 2), NP, 1536};
-  ga.x[1] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1024 * 2), NP, 1024};
+  const int MAXLEN = 100;
   int tstep = 2;  // alternate t: each launch clears the other threshold buffer, as in a decode
   auto launch = [&]() {
     tstep = tstep == 2 ? 3 : 2;
-    CK(gen_step(tmW, tmX, VP / 128, NP, NP, KP / 64, 148, g, rl, rz, ri, phases, tstep, MAXLEN, 1.0, bs, ga, gbar, thr,
-                StepCtl{nullptr, 0}, st, nullptr, B));
+    CK(gen_step(tmW, tmX, VP / 128, NP, NP, KP / 64, 148, g, rl, rz, ri, tstep, thr, StepCtl{nullptr, 0}, st, gt));
   };
   cudaGraph_t gr; cudaGraphExec_t ge;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -92,7 +84,8 @@ int main(int argc, char** argv) {
   double avg[12] = {0}, mx[12] = {0}; int cnt[12] = {0};
   for (int c = 0; c < grid; ++c) for (int i = 0; i < 12; ++i) if (h[c * 12 + i]) {
     double d = (h[c * 12 + i] - t0) / 1e3; avg[i] += d; cnt[i]++; mx[i] = std::max(mx[i], d); }
-  printf("gen_step phases=%d dbg=%d: %.2f us/launch (graph of 20)\n", phases, g_gs_dbg, ms_ * 1000 / 20);
+  printf("gen_step gates=%d dbg=%d: %.2f us/launch (graph of 20)\n", gates, g_gs_dbg, ms_ * 1000 / 20);
+  (void)MAXLEN;
   const char* nm[12] = {"entry", "pdl_wait", "mma done (epi)", "phase A end", "scan0 start (w6)", "scan0 end (w6)", "stager: tile2 buf free", "first data (mma)", "batch scanned", "partial write", "stager: tile0 staged", "scan1 end (w6)"};
   for (int i = 0; i < 12; ++i) if (cnt[i]) printf("   %-16s avg %7.2f  max %7.2f us (n=%d)\n", nm[i], avg[i] / cnt[i], mx[i], cnt[i]);
   return 0;
