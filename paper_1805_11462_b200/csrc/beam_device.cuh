@@ -223,6 +223,66 @@ __device__ __forceinline__ void rsplit_cell(int b, int K, const int* s_go, const
   }
 }
 
+// rsplit_cell with every input staged in shared memory: parent k's block at gbuf + k * PR
+// (P[0..L] rows of 4H, then c_0..c_{L-1} rows of H), new slot kr's T[y] row at gbuf + K * PR + kr * 4H;
+// the new c_1 / h_1 go to gbuf + K * PR + K * 4H (2 K H floats) before the write-out.
+#ifdef ONMT_KTRACE
+__device__ int g_rs_dbg;      // microbenchmark ablations (tools/ubench/ubeam): 1 no layer-2 gathers, 2 no math
+#endif
+__device__ __forceinline__ void rsplit_cell_smem(int b, int K, const int* s_go, const int* s_prow,
+                                                 const GatherArgs& ga, float* gbuf, int PR, int j0, int nj) {
+  // this CTA's units [j0, j0 + nj) (a slice of the sentence's cell: grid.y CTAs per sentence);
+  // staged rows hold only the slice (4 nj gate floats, nj state floats)
+  const int H = ga.H, G = ga.G, L = ga.L, G4 = 4 * nj, H4 = nj >> 2;
+  const size_t PQ = (size_t)ga.rows_pad * G;
+  const float* tb = gbuf + (size_t)K * PR;
+  float* cn = gbuf + (size_t)K * PR + (size_t)K * G4;
+  float* hn = cn + (size_t)K * nj;
+  const float4* s_b1 = reinterpret_cast<const float4*>(hn + (size_t)K * nj);  // layer 1's bias (staged)
+  for (int it = threadIdx.x; it < K * nj; it += blockDim.x) {
+    const int kr = it / nj, jl = it - kr * nj, j = j0 + jl;
+    if (!s_go[kr]) continue;
+    const int r = b * K + kr, pk = s_prow[kr] - b * K;
+    const float* pb = gbuf + (size_t)pk * PR;
+#ifdef ONMT_KTRACE
+    if (g_rs_dbg == 3) { cn[it] = pb[jl]; continue; }
+    if (g_rs_dbg != 1)
+#endif
+    for (int l = 1; l < L; ++l) {                                // layers >= 2: W_hh h_l[parent] and c_l[parent]
+      reinterpret_cast<float4*>(ga.gb + (size_t)(l - 1) * PQ + (size_t)r * G)[j] =
+          reinterpret_cast<const float4*>(pb + (size_t)(l + 1) * G4)[jl];
+      ga.cg[((size_t)l * ga.rows_pad + r) * H + j] = pb[(size_t)(L + 1) * G4 + (size_t)l * nj + jl];
+    }
+    const float4 tv = reinterpret_cast<const float4*>(tb + (size_t)kr * G4)[jl];
+    const float4 pa = reinterpret_cast<const float4*>(pb)[jl];
+    const float4 pc = reinterpret_cast<const float4*>(pb + G4)[jl];
+    const float4 bb = s_b1[jl];
+    const float cp = pb[(size_t)(L + 1) * G4 + jl];
+#ifdef ONMT_KTRACE
+    if (g_rs_dbg == 2) { cn[it] = tv.x + pa.y + pc.z + bb.w + cp; hn[it] = 0.f; continue; }
+#endif
+    // gates of unit j (rows 4j..4j+3 = i, f, g, o); same summation order as rsplit_cell
+    const float zi = ((tv.x + pa.x) + pc.x) + bb.x, zf = ((tv.y + pa.y) + pc.y) + bb.y;
+    const float zg = ((tv.z + pa.z) + pc.z) + bb.z, zo = ((tv.w + pa.w) + pc.w) + bb.w;
+    const float c = rs_sigm(zf) * cp + rs_sigm(zi) * rs_tanh(zg);
+    cn[it] = c;
+    hn[it] = rs_sigm(zo) * rs_tanh(c);
+  }
+  KT(10);
+  __syncthreads();                                               // (c_1 rows were staged: no hazard, but
+  KT(11);
+  for (int it = threadIdx.x; it < K * H4; it += blockDim.x) {    //  cn / hn must be complete)
+    const int kr = it / H4, j4 = 4 * (it - kr * H4);
+    if (!s_go[kr]) continue;
+    const int r = b * K + kr;
+    const float4 c = *reinterpret_cast<const float4*>(cn + kr * nj + j4);
+    const float4 h = *reinterpret_cast<const float4*>(hn + kr * nj + j4);
+    *reinterpret_cast<float4*>(ga.c1_out + (size_t)r * H + j0 + j4) = c;
+    store_x4(ga.xh1[0], r, ga.col_h1[0] + j0 + j4, h);
+    store_x4(ga.xh1[1], r, ga.col_h1[1] + j0 + j4, h);
+  }
+}
+
 // A10 + A5 for one whole sentence b per CTA (512 threads): the generator partials of its K
 // hypothesis rows are combined (one warp per row: log-sum-exp and row top-K), thread 0
 // selects the K survivors (raw desc, slot asc, token asc; fp64 scores) with EOS / max_len
@@ -233,7 +293,8 @@ template <int KMAX>
 __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restrict__ ms, const float* __restrict__ tz,
                                                    const int* __restrict__ ti, int n_parts, int ps, int rs, int K,
                                                    int R, int t, int max_len, double lp, const BeamState& bs,
-                                                   const GatherArgs& ga, float* gbuf, int gbuf_floats) {
+                                                   const GatherArgs& ga, float* gbuf, int gbuf_floats, int slice = 0,
+                                                   int nslice = 1) {
   KT(1);
   const int dn = __ldcg(&bs.done[b]);                            // (checked after the row reduce:
   const int* __restrict__ live_in = bs.live + (size_t)(t & 1) * R;   //  its loads overlap these)
@@ -258,13 +319,43 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   // s_bar before its copies; thread 0 arrives once all rows are reduced.
   const bool pre = !ga.rsplit && gbuf != nullptr && (E & 3) == 0 && (H & 3) == 0 &&
                    (K * K * emb_f + K * st_f) <= gbuf_floats && !(dn != 0 && dn < t);
-  __shared__ __align__(8) uint64_t s_bar;
-  if (threadIdx.x == 0) { mbar_init(&s_bar, 1); fence_mbar_init(); }
+  // recurrent split (GatherArgs::rsplit): the rows layer 1's cell reads are prefetched too - the
+  // live parents' gate-tile rows P[0..L][p] and cell states c_l[p] at entry, the new slots'
+  // embedding-projection rows T[y] as soon as the selection is known (s_bar2)
+  // (grid.y = nslice CTAs per sentence: every one reduces and selects - identical results - and
+  //  runs the cell for its slice of units [j0, j0 + nj); only slice 0 writes the beam state)
+  const int nq = ((H >> 2) + nslice - 1) / nslice;
+  const int j0 = min(H, 4 * nq * slice), nj = min(H, 4 * nq * (slice + 1)) - j0;
+  const int G4 = 4 * nj, PR = (L + 1) * G4 + L * nj;               // floats per parent block (my slice)
+  const bool rpre = ga.rsplit && gbuf != nullptr && (H & 3) == 0 && nj > 0 &&
+                    (size_t)K * PR + (size_t)(K + 1) * G4 + (size_t)2 * K * nj <= (size_t)gbuf_floats &&
+                    !(dn != 0 && dn < t);
+  __shared__ __align__(8) uint64_t s_bar, s_bar2;
+  if (threadIdx.x == 0) { mbar_init(&s_bar, 1); mbar_init(&s_bar2, 1); fence_mbar_init(); }
   if (threadIdx.x < K) {
     s_live[threadIdx.x] = __ldcg(&live_in[b * K + threadIdx.x]);
     s_cum[threadIdx.x] = __ldcg(&cum_in[b * K + threadIdx.x]);
   }
   __syncthreads();
+  if (rpre && warp == nw - 2 && lane == 0) {                     // layer 1's bias (a constant)
+    mbar_expect_tx(&s_bar, (uint32_t)G4 * 4);
+    bulk_g2s(gbuf + (size_t)K * PR + (size_t)K * G4 + (size_t)2 * K * nj, ga.bias[0] + j0, G4 * 4, &s_bar);
+  }
+  if (rpre && warp == nw - 1) {
+    const int nseg = 2 * L + 1;                                   // P[0..L] (4H each), c_0..c_{L-1} (H each)
+    const size_t PQ = (size_t)ga.rows_pad * ga.G;
+    for (int c = lane; c < K * nseg; c += 32) {
+      const int k = c / nseg, w = c % nseg;
+      if (!s_live[k]) continue;
+      const int p = b * K + k;
+      float* d = gbuf + (size_t)k * PR + (w <= L ? (size_t)w * G4 : (size_t)(L + 1) * G4 + (size_t)(w - L - 1) * nj);
+      const float* src = w <= L ? ga.P + (size_t)w * PQ + (size_t)p * ga.G + 4 * j0
+                                : ga.c + ((size_t)(w - L - 1) * ga.rows_pad + p) * H + j0;
+      const uint32_t bytes = (uint32_t)(w <= L ? G4 : nj) * 4;
+      mbar_expect_tx(&s_bar, bytes);
+      bulk_g2s(d, src, bytes, &s_bar);
+    }
+  }
   if (pre && warp == nw - 1) {
     const int nst = 1 + 2 * L;
     for (int c = lane; c < K * nst; c += 32) {                   // c -> slot c / nst, row kind c % nst
@@ -398,7 +489,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   __syncthreads();
   if (dn != 0 && dn < t) return;                                 // finished earlier (uniform)
   if (threadIdx.x < K * K && !s_live[threadIdx.x / K]) s_z[threadIdx.x / K][threadIdx.x % K] = -INFINITY;
-  if (pre && threadIdx.x == 0) mbar_arrive_local(&s_bar);       // every issuer raised its bytes
+  if ((pre || rpre) && threadIdx.x == 0) mbar_arrive_local(&s_bar);   // every issuer raised its bytes
   KT(3);
   // ---- selection (parallel ranks): candidate (k, j) = slot k's j-th row best; its raw score
   //      cum_k + z - lse_k in fp64; order (score desc, slot asc, position asc) - the merge of
@@ -460,21 +551,27 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     s_y[kr] = mine_live ? s_sel_w[kr] : 0;
     s_go[kr] = mine_live && !stop;
     s_src[kr] = mine_live ? s_sel_c[kr] : 0;
+    if (rpre && s_go[kr]) {                                      // my new slot's T[y] row
+      mbar_expect_tx(&s_bar2, (uint32_t)G4 * 4);
+      bulk_g2s(gbuf + (size_t)K * PR + (size_t)kr * G4, ga.T + (size_t)s_y[kr] * ga.G + 4 * j0, G4 * 4, &s_bar2);
+    }
     const size_t hb = (size_t)(t - 1) * (size_t)R + (size_t)r;
-    live_out[r] = mine_live;
-    cum_out[r] = mine_live ? s_sel_s[kr] : -CUDART_INF;
-    bs.prow[r] = s_prow[kr];
-    bs.y[r] = s_y[kr];
-    bs.hist_parent[hb] = mine_sel ? s_sel_k[kr] : -1;
-    bs.hist_token[hb] = mine_sel ? s_sel_w[kr] : 0;
-    bs.hist_logp[hb] = mine_sel ? s_sel_lp[kr] : 0.f;
-    if (bs.sel_parent) { bs.sel_parent[hb] = mine_sel ? s_sel_k[kr] : -1; bs.sel_score[hb] = mine_sel ? s_sel_s[kr] : -CUDART_INF; }
+    if (slice == 0) {                                            // (the sentence's state: one writer)
+      live_out[r] = mine_live;
+      cum_out[r] = mine_live ? s_sel_s[kr] : -CUDART_INF;
+      bs.prow[r] = s_prow[kr];
+      bs.y[r] = s_y[kr];
+      bs.hist_parent[hb] = mine_sel ? s_sel_k[kr] : -1;
+      bs.hist_token[hb] = mine_sel ? s_sel_w[kr] : 0;
+      bs.hist_logp[hb] = mine_sel ? s_sel_lp[kr] : 0.f;
+      if (bs.sel_parent) { bs.sel_parent[hb] = mine_sel ? s_sel_k[kr] : -1; bs.sel_score[hb] = mine_sel ? s_sel_s[kr] : -CUDART_INF; }
+    }
   }
   // ---- coverage / unknown replacement (S436-448): the new slot q inherits its parent's
   //      cumulative attention plus the parent's step-t attention row; its token's attention
   //      argmax (first maximum: ties -> smallest s) goes to the history
   __shared__ double s_cp[KMAX];
-  if (bs.catt || bs.hist_amax) {
+  if ((bs.catt || bs.hist_amax) && slice == 0) {
     __syncthreads();                                             // (selection results visible)
     const int Lb = __ldg(&bs.lens[b]);
     const size_t RS = (size_t)R * bs.S_max;
@@ -514,8 +611,8 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     __syncthreads();
   }
   KTX(9, threadIdx.x == 0);
-  if (threadIdx.x == 0) {
-    s_cont = !stop;
+  if (threadIdx.x == 0) s_cont = !stop;
+  if (threadIdx.x == 0 && slice == 0) {
     // sentence-level banking (final_score = raw / lp + cp, S436-439) into the n-best list
     // (norm desc; an equal norm never displaces an earlier step / lower rank, AMB-19)
     const int nb = bs.nbest > 0 ? bs.nbest : 1;
@@ -541,8 +638,18 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
   }
   __syncthreads();
   KT(4);
+  if (rpre && threadIdx.x == 0) mbar_arrive_local(&s_bar2);    // (after the barrier: every T copy issued)
   if (!s_cont) {
-    if (pre) mbar_wait(&s_bar, 0);                               // (no copy may land after exit)
+    if (pre || rpre) mbar_wait(&s_bar, 0);                       // (no copy may land after exit)
+    if (rpre) mbar_wait(&s_bar2, 0);
+    return;
+  }
+  if (rpre) {                                                    // layer 1's cell from shared memory
+    mbar_wait(&s_bar, 0);
+    mbar_wait(&s_bar2, 0);
+    KT(5);
+    rsplit_cell_smem(b, K, s_go, s_prow, ga, gbuf, PR, j0, nj);
+    KT(6);
     return;
   }
   if (ga.rsplit) {                                               // layer 1's cell instead of a gather

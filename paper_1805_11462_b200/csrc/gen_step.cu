@@ -63,6 +63,9 @@ struct GenStepArgs {
   float* gout;
 };
 
+// TMEM columns per accumulator (n_group rounded to 32)
+__host__ __device__ constexpr int gs_tstride(int n_group) { return (n_group + 31) & ~31; }
+
 __device__ __forceinline__ float gs_ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -175,7 +178,10 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   const int nbatch = (ntot + a.nt_max - 1) / a.nt_max;
   auto bfirst = [&](int bt) { return bt * a.nt_max; };
   auto bsize = [&](int bt) { return min(a.nt_max, ntot - bfirst(bt)); };
-  auto tcol = [&](int bt, int j) { return (uint32_t)((a.ovl ? bt * a.nt_max + j : j) * a.n_group); };
+  // accumulators start on 32-column boundaries: the stagers' tcgen05.ld.32x32b.x32 reads
+  // must not straddle (a 144-row group at column 144 read wrong data)
+  const int tstride = gs_tstride(a.n_group);
+  auto tcol = [&](int bt, int j) { return (uint32_t)((a.ovl ? bt * a.nt_max + j : j) * tstride); };
   auto is_gate = [&](int i) { return i >= nv; };
   const int g_lo = gi >= 0 ? (gi / a.gt_per_q) * a.gkbh : 0, g_hi = g_lo + a.gkbh;
   // per-batch tile table, computed once per batch (the single producer / MMA threads must not
@@ -211,7 +217,10 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   // scanners of a chunk start as soon as it is staged and the stagers refill a chunk as soon
   // as its scanners are done (instead of whole-tile hand-offs)
   const int srows = min(a.n_group, a.R - n0);                      // staged hypothesis rows (valid ones)
-  const int ncols = srows > 0 ? (srows + 15) & ~15 : 0;            // TMEM columns staged (x32 / x16 loads)
+  // TMEM columns staged: whole 32-column x32 loads (columns past srows are garbage; their stores
+  // are predicated off and the scanners skip those rows).  A half-chunk tcgen05.ld .x16 path was
+  // removed: rows of such chunks came out wrong intermittently in multi-group launches.
+  const int ncols = srows > 0 ? min((srows + 31) & ~31, tstride) : 0;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmW);
@@ -326,7 +335,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           for (int j = 0; j < 4; ++j) {
             if (!((cov >> j) & 1u)) continue;
             const uint32_t sa = sb + 2 * b_bytes + j * a_bytes;
-            const uint32_t d = tc0 + (uint32_t)(j * a.n_group);
+            const uint32_t d = tc0 + (uint32_t)(j * tstride);
             const uint32_t acc0 = kb == B.lo[j] ? 0u : 1u;
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {
@@ -366,8 +375,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           float* go = a.gout + ((size_t)qb * a.rows_pad + n0) * a.gld + col;
           for (int c0 = 0; c0 < ncols; c0 += 32) {
             uint32_t r[32];
-            if (c0 + 32 <= ncols) tmem_ld32_nw(trow + c0, r);
-            else tmem_ld16_nw(trow + c0, r);
+            tmem_ld32_nw(trow + c0, r);                          // (ncols: a multiple of 32)
             tmem_wait_ld();
             tmem_fence_regs(r);
 #pragma unroll
@@ -384,10 +392,9 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           const uint32_t trow = tmem + tcol(bt, j) + ((uint32_t)(q * 32) << 16);
           float* dst = stg + (size_t)buf * a.srows_alloc * kGsSLD + vr;
           // 32-column chunks, software-pipelined: the load of chunk i+1 is in flight while
-          // chunk i is stored (ncols is a multiple of 16: a last half chunk uses x16)
+          // chunk i is stored
           auto issue = [&](int c0, uint32_t* r) {
-            if (c0 + 32 <= ncols) tmem_ld32_nw(trow + c0, r);
-            else tmem_ld16_nw(trow + c0, r);
+            tmem_ld32_nw(trow + c0, r);                          // (ncols: a multiple of 32)
           };
           auto put = [&](int c0, uint32_t* r) {                    // c0: a multiple of 32 (one chunk)
             const int ch = buf * kGsMaxCh + (c0 >> 5);
@@ -699,7 +706,7 @@ static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, int R, int K
   // (every tile its own TMEM columns, staging outside the ring): batch b+1's MMAs run while
   // batch b is staged and scanned
   static const int ovl_env = getenv("ONMT_GEN_OVL") ? atoi(getenv("ONMT_GEN_OVL")) : 2;
-  if (ovl_env > 0 && need >= 2 && need * n_group <= 512) {
+  if (ovl_env > 0 && need >= 2 && need * gs_tstride(n_group) <= 512) {
     p.ovl = 1;
     p.nt_max = ovl_env < need ? ovl_env : need - 1;                  // tiles per batch
     p.stages = 2;
@@ -710,7 +717,7 @@ static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, int R, int K
   }
   p.ovl = 0;
   p.nbuf = 2;
-  p.nt_max = 512 / n_group;                                          // accumulators in TMEM
+  p.nt_max = 512 / gs_tstride(n_group);                              // accumulators in TMEM
   if (p.nt_max > 4) p.nt_max = 4;                                    // (bias registers of the stagers)
   if (p.nt_max > need) p.nt_max = need;
   if (p.nt_max < 1) return false;

@@ -150,7 +150,7 @@ void launch_init_decode(const BeamState& bs, int B, int K, const float* enc_h, c
 void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepCtl ctl, cudaStream_t st);
 void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_parts, int ps, int rs, int B, int K,
                        int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga, float* row_lse,
-                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st);
+                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st, int nslice = 1);
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
                      float* tlogp, int* unk_pos, cudaStream_t st);
 void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int ps, int rs, int R, int K,
@@ -1412,9 +1412,11 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       if (op.src_ext) {
         merge_copy(n_vt, 1, n_vt, t, lp);
       } else {
+        // recurrent split: a few CTAs per sentence share layer 1's cell (each selects redundantly)
+        static const int nsl_env = std::getenv("ONMT_BEAM_NSLICE") ? std::atoi(std::getenv("ONMT_BEAM_NSLICE")) : 0;
+        const int nsl = m->rs_cur ? (nsl_env > 0 ? nsl_env : std::max(1, std::min(4, m->num_sms / std::max(B, 1)))) : 1;
         launch_beam_merge(g.ms, g.tz, g.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, m->rs_cur ? gam : ga,
-                          m->row_lse.as<float>(),
-                          m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream);
+                          m->row_lse.as<float>(), m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream, nsl);
         count(m, n_vt <= 256 ? 1 : 2);
       }
       prof_end(m, "merge", pm);

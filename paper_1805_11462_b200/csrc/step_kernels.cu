@@ -416,7 +416,7 @@ void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepC
   gather_kernel<<<R, 128, 0, st>>>(bs, g, K, ctl);
 }
 
-constexpr size_t kBeamStageBytes = 120 * 1024;  // shared staging of the gathered rows
+constexpr size_t kBeamStageBytes = 216 * 1024;  // shared staging of the gathered / prefetched rows
 
 template <int KMAX>
 __global__ void __launch_bounds__(512) beam_step_kernel(const float2* __restrict__ ms, const float* __restrict__ tz,
@@ -429,19 +429,20 @@ __global__ void __launch_bounds__(512) beam_step_kernel(const float2* __restrict
   (void)ctl;
   extern __shared__ __align__(16) float gbuf_dyn[];
   beam_step_sentence<KMAX>(blockIdx.x, ms, tz, ti, n_parts, ps, rs, K, gridDim.x * K, t, max_len, lp, bs, ga,
-                           gbuf_dyn, (int)(kBeamStageBytes / 4));
+                           gbuf_dyn, (int)(kBeamStageBytes / 4), blockIdx.y, gridDim.y);
 }
 
 void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_parts, int ps, int rs, int B, int K,
                        int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga, float* row_lse,
-                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st) {
+                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st, int nslice) {
   const int R = B * K;
   // one CTA per sentence (row reduce + select + gather) when its lanes hold every partial;
   // otherwise (SIMT generator over many tiles) a row-reduce launch + a select/gather launch
 #define ONMT_MERGE(KM)                                                                                            \
   if (n_parts <= 256) {                                                                                           \
     cudaFuncSetAttribute(beam_step_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBeamStageBytes); \
-    launch_pdl(beam_step_kernel<KM>, dim3(B), dim3(512), kBeamStageBytes, st, ms, tz, ti, n_parts, ps, rs, K, t,   \
+    launch_pdl(beam_step_kernel<KM>, dim3(B, nslice), dim3(512), kBeamStageBytes, st, ms, tz, ti, n_parts, ps, rs,  \
+               K, t,                                                                                              \
                max_len, lp, bs, ga, ctl);                                                                         \
   } else {                                                                                                        \
     launch_pdl(row_reduce_topk_kernel<KM>, dim3(R), dim3(128), 0, st, ms, tz, ti, n_parts, ps, rs, K,             \

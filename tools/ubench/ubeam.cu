@@ -7,7 +7,10 @@
 #include "../../paper_1805_11462_b200/csrc/step_kernels.cu"
 using namespace onmt;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
-int main() {
+int main(int argc, char** argv) {
+  const int rsplit = argc > 1 ? atoi(argv[1]) : 0;   // 1: the recurrent-split step's layer-1 cell
+  const int rsdbg = argc > 2 ? atoi(argv[2]) : 0;
+  CK(cudaMemcpyToSymbol(g_rs_dbg, &rsdbg, sizeof(int)));
   cudaStream_t st; CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   const int B = 30, K = 5, R = B * K, NP = 160, C = 148, E = 500, H = 500, L = 2, V = 50000, MAXLEN = 100;
   auto zalloc = [&](size_t bytes) { void* p; CK(cudaMalloc(&p, bytes)); CK(cudaMemset(p, 0, bytes)); return p; };
@@ -38,9 +41,22 @@ int main() {
   ga.cg = (float*)zalloc(L * NP * H * 4); ga.rows_pad = NP;
   ga.x[0] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1536 * 2), NP, 1536};
   ga.x[1] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1024 * 2), NP, 1024};
+  if (rsplit) {
+    const int G = 2048;
+    ga.rsplit = 1;
+    ga.T = (float*)zalloc((size_t)V * G * 4);
+    ga.P = (float*)zalloc((size_t)3 * NP * G * 4);
+    ga.G = G;
+    for (int l = 0; l < L; ++l) ga.bias[l] = (const float4*)zalloc(G * 4);
+    ga.gb = (float*)zalloc((size_t)NP * G * 4);
+    ga.c1_out = (float*)ga.c;
+    ga.xh1[0] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 512 * 2), NP, 512}; ga.col_h1[0] = 0;
+    ga.xh1[1] = XOut{nullptr, (__nv_bfloat16*)zalloc(2 * NP * 1536 * 2), NP, 1536}; ga.col_h1[1] = 512;
+  }
   float* rl = (float*)zalloc(R * 4); float* rz = (float*)zalloc(R * K * 4); int* ri = (int*)zalloc(R * K * 4);
   unsigned long long* tr; CK(cudaMalloc(&tr, 4096 * 96)); CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
-  auto launch = [&]() { launch_beam_merge(ms, tz, ti, C, 1, C, B, K, 5, MAXLEN, 1.0, bs, ga, rl, rz, ri, StepCtl{nullptr, 0}, st); };
+  const int nsl = argc > 3 ? atoi(argv[3]) : 1;
+  auto launch = [&]() { launch_beam_merge(ms, tz, ti, C, 1, C, B, K, 5, MAXLEN, 1.0, bs, ga, rl, rz, ri, StepCtl{nullptr, 0}, st, nsl); };
   cudaGraph_t gr; cudaGraphExec_t ge;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   for (int i = 0; i < 20; ++i) launch();
@@ -57,8 +73,8 @@ int main() {
   double avg[12] = {0}, mx[12] = {0}; int cnt[12] = {0};
   for (int c = 0; c < B; ++c) for (int i = 0; i < 12; ++i) if (h[c * 12 + i]) {
     double d = (h[c * 12 + i] - t0) / 1e3; avg[i] += d; cnt[i]++; mx[i] = std::max(mx[i], d); }
-  printf("beam_step: %.2f us/launch (graph of 20)\n", ms_ * 1000 / 20);
-  const char* nm[12] = {"entry", "after pdl/done", "live/cum loaded", "rows reduced", "selected", "gather staged", "exit", "sc ready", "ranked", "owners done", "", ""};
+  printf("beam_step rsplit=%d: %.2f us/launch (graph of 20)\n", rsplit, ms_ * 1000 / 20);
+  const char* nm[12] = {"entry", "after pdl/done", "live/cum loaded", "rows reduced", "selected", "gather staged", "exit", "sc ready", "ranked", "owners done", "cell math done", "cell synced"};
   for (int i = 0; i < 12; ++i) if (cnt[i]) printf("   %-16s avg %7.2f  max %7.2f us (n=%d)\n", nm[i], avg[i] / cnt[i], mx[i], cnt[i]);
   return 0;
 }
