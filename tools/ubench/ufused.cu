@@ -39,9 +39,14 @@ int main() {
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   const int H = 500, R = 150, NP = 160;
-  struct Shape { const char* name; int M, K; bool tanh; };
-  Shape shapes[] = {{"L1 gates 2000x1500", 4 * H, 3 * H, false}, {"L2 gates 2000x1000", 4 * H, 2 * H, false},
-                    {"W_out 500x1000 tanh", H, 2 * H, true}};
+  struct Shape { const char* name; int M, K; bool tanh; int ns; bool fold; };
+  // ns < NP: the recurrent-split step's layer-2 kernel (N-split groups of ns rows, whole K, per-row
+  // gate bias gb); fold: the top layer's W_out[:, H:2H] h shares
+  Shape shapes[] = {{"L1 gates 2000x1500", 4 * H, 3 * H, false, NP, false},
+                    {"L2 gates 2000x1000", 4 * H, 2 * H, false, NP, false},
+                    {"rsplit L2 2000x500 ns32 +gb", 4 * H, H, false, 32, false},
+                    {"rsplit L2 2000x500 ns32 +gb +fold", 4 * H, H, false, 32, true},
+                    {"W_out 500x1000 tanh", H, 2 * H, true, NP, false}};
   unsigned long long* tr;
   CK(cudaMalloc(&tr, 4096 * 96));
   CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
@@ -58,6 +63,11 @@ int main() {
   CK(cudaMalloc(&xo, NP * 2048 * 4));
   CK(cudaMalloc(&xhl, 2 * NP * 2048 * 2));
   CK(cudaMemset(bias, 0, 4 * 4096 * 4));
+  float *gb, *woh_part;
+  __nv_bfloat16* woh;
+  CK(cudaMalloc(&gb, NP * 2048 * 4)); CK(cudaMemset(gb, 0, NP * 2048 * 4));
+  CK(cudaMalloc(&woh_part, 16 * NP * H * 4));
+  CK(cudaMalloc(&woh, 16 * 32 * fold_ld(H) * 2)); CK(cudaMemset(woh, 0, 16 * 32 * fold_ld(H) * 2));
   for (int dbg = 0; dbg < 4; ++dbg)
   for (auto& sh : shapes) {
     g_fused_dbg = dbg;
@@ -69,19 +79,21 @@ int main() {
     CK(cudaMalloc(&X, (size_t)2 * NP * kp * 2));
     CK(cudaMemset(W, 0, (size_t)mp * kp * 2));
     CK(cudaMemset(X, 0, (size_t)2 * NP * kp * 2));
-    CUtensorMap tmW = make_tmap(W, kp, mp, 128), tmX = make_tmap(X, kp, 2 * NP, NP);
+    CUtensorMap tmW = make_tmap(W, kp, mp, 128), tmX = make_tmap(X, kp, 2 * NP, sh.ns);
+    const bool rs = sh.ns < NP;
     XOut xd{nullptr, xhl, NP, 2048};
     CellDst dst{};
     dst.x[0] = xd; dst.col[0] = 0; dst.n = 1;
     auto launch = [&]() {
       cudaError_t e = sh.tanh ? tc_gemm_tanh(tmW, tmX, mp, NP, NP, R, kp / 64, H, hout, xd, scratch, counters, 148,
                                              StepCtl{nullptr, 0}, st)
-                              : tc_gemm_cell(tmW, tmX, mp, NP, NP, R, kp / 64, bias, cg, cout, hout, H, dst, scratch,
-                                             counters, 148, StepCtl{nullptr, 0}, st);
+                              : tc_gemm_cell(tmW, tmX, mp, NP, sh.ns, R, kp / 64, bias, cg, cout, hout, H, dst, scratch,
+                                             counters, 148, StepCtl{nullptr, 0}, st, sh.fold ? woh : nullptr,
+                                             sh.fold ? woh_part : nullptr, rs ? gb : nullptr, 2048);
       CK(e);
     };
-    const int S = fused_split(NP, NP, kp / 64, mp / 128, 148);
-    const int grid = mp / 128 * S;
+    const int S = fused_split(sh.ns, NP, kp / 64, mp / 128, 148);
+    const int grid = mp / 128 * (NP / sh.ns) * S;
     // graph of 50 launches
     cudaGraph_t g;
     cudaGraphExec_t ge;
