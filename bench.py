@@ -173,7 +173,12 @@ def run_ours(args):
         path = synth.weights_file(args.workload, cache)
     model = ob.Model(path, local, w.decode.precision)
     from paper_1805_11462_b200.parallel import gather_results, rank_slice
-    if args.scaling == "weak":
+    if args.vocab_parallel:
+        # vocabulary-parallel generator: every rank decodes the SAME batch and
+        # streams 1/world of W_gen; partials are exchanged through peer memory inside the graph
+        ids_all, lens_all = synth.make_corpus(args.workload)
+        b0, b1 = 0, B_wl
+    elif args.scaling == "weak":
         # weak scaling: rank r translates its own full batch, sentences [r*B, (r+1)*B) of one corpus
         ids_all, lens_all = synth.make_corpus(args.workload, B_wl * ws)
         b0, b1 = rank_slice(B_wl * ws, ws, rank)
@@ -186,6 +191,14 @@ def run_ours(args):
     lens = np.ascontiguousarray(lens_all[b0:b1])
     S = int(lens.max())
     ids = np.ascontiguousarray(ids[:, :S])
+    if args.vocab_parallel:
+        from paper_1805_11462_b200.parallel import open_vocab_parallel
+        model.set_option("rsplit", 0)
+        if ws > 1:
+            open_vocab_parallel(model, (b1 - b0) * K)
+        else:
+            model.vp_handle((b1 - b0) * K)
+            model.vp_open(1, 0, None)
     stream = torch.cuda.Stream(device=dev)
     model.set_stream(stream.cuda_stream)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -201,7 +214,7 @@ def run_ours(args):
 
     def step():
         model.translate_dev(ids_d, lens_d, K, ML, alpha, out, lens)
-        if ws > 1:
+        if ws > 1 and not args.vocab_parallel:
             gather_results(out, index_d)        # the path's only collective (NCCL all-gather)
 
     def timed_pass(profile):
@@ -255,8 +268,13 @@ def run_ours(args):
         tt = torch.tensor([t_ms, float(tokens)], dtype=torch.float64, device=dev)
         tmax = tt.clone()
         dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+        if not args.vocab_parallel:            # (vocabulary-parallel: every rank decodes the same batch)
+            dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
         t_ms, tokens = float(tmax[0].item()), int(tt[1].item())
+        if args.vocab_parallel:                 # every rank must hold the same translation
+            g = torch.empty((ws,) + tuple(out["hyps"].shape), dtype=out["hyps"].dtype, device=dev)
+            dist.all_gather_into_tensor(g, out["hyps"].contiguous())
+            assert bool((g == g[:1]).all().item()), "vocabulary-parallel ranks disagree"
     value = tokens / (t_ms / 1e3)
 
     # ---- e2e: host buffers through onmt_translate, H2D / D2H inside the timed region
@@ -282,7 +300,7 @@ def run_ours(args):
     h2d = ids.nbytes + lens.nbytes
     d2h = B * ML * 4 * 2 + B * 4 * 3
     model_plan = model.last_plan()
-    corpus = corpus_run(model, args, w, ws, rank, dev) if not args.no_corpus else None
+    corpus = corpus_run(model, args, w, ws, rank, dev) if not (args.no_corpus or args.vocab_parallel) else None
 
     if rank == 0:
         pk = peaks()
@@ -298,14 +316,17 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "target tok/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 4),
-            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "strong" if args.vocab_parallel else args.scaling,
+            "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded U(-0.1,0.1) weights, Zipf(1.1) ids; DESIGN.md §3)",
             "config": {"workload": args.workload, "model": "2x500 LSTM enc-dec, general attn, input feed, V=50k"
                        if args.workload == "c2" else args.workload,
                        "global_batch": B_wl * ws if args.scaling == "weak" else B_wl, "batch_per_gpu": B,
                        "beam": K, "max_len": ML,
                        "length_penalty": alpha, "src_len": [w.data.len_lo, w.data.len_hi],
-                       "parallelism": f"dp{ws} (sentence-sharded, NCCL all-gather of every output + indices)",
+                       "parallelism": (f"vocab-parallel generator over {ws} GPUs (peer-memory partial exchange)"
+                                       if args.vocab_parallel else
+                                       f"dp{ws} (sentence-sharded, NCCL all-gather of every output + indices)"),
                        "l2": "flushed (512 MB write) between timed steps; weights stay L2-resident "
                              "across the decode steps of one step",
                        "timed_graph": "uninstrumented (no CUDA-event nodes inside the call)"},
@@ -600,6 +621,8 @@ def main():
     ap.add_argument("--cpu-sample-sentences", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-corpus", action="store_true")
+    ap.add_argument("--vocab-parallel", action="store_true",
+                    help="split the generator's vocabulary over the ranks (SURVEY §8(f) rank 4)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: a full batch per GPU (c2, c4); strong: the workload's batch sharded (c3, c5)")
     ap.add_argument("--task", default="translate", choices=["translate", "score", "translate_ex", "copy"])

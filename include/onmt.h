@@ -261,6 +261,28 @@ ONMT_API onmt_status onmt_kernel_launches(onmt_model* m, int32_t reset, int64_t*
 ONMT_API onmt_status onmt_graph_captures(onmt_model* m, int64_t* captures);
 
 /*
+ * Vocabulary-parallel generator (PAPER.md P219-224 names
+ * multi-GPU parallelism).  `world` ranks (one process and one handle per GPU, the SAME model and
+ * the SAME translate calls on every rank) split the generator's vocabulary: each rank streams
+ * 1/world of W_gen per decode step and stores its per-CTA partials (max, sum exp, top-K) into
+ * every rank's exchange buffer over NVLink peer memory, then raises a per-step flag there; each
+ * rank's beam step waits for all flags and merges the same partials, so every rank selects the
+ * same hypotheses (outputs are identical on all ranks).  The encoder and decoder layers run on
+ * every rank.  Plain bf16 translation only (no copy / coverage / n-best customisations).
+ *
+ * onmt_vp_handle - allocate this handle's exchange buffer for up to max_rows = B x beam
+ *   hypothesis rows and write its cudaIpcMemHandle (64 bytes) to handle_out.
+ * onmt_vp_open   - map the other ranks' buffers: handles = world x 64 bytes in rank order (may be
+ *   NULL for world == 1).  Later translate calls of the handle run vocabulary-parallel; rows above
+ *   the capacity, beam > 16 or > 4 hypothesis-row groups return UNSUPPORTED.
+ * onmt_vp_close  - unmap the peers and return to single-GPU decoding.
+ * Errors: INVALID_ARG (bad world / rank, no handle yet), UNSUPPORTED (fp32 model), CUDA.
+ */
+ONMT_API onmt_status onmt_vp_handle(onmt_model* m, int32_t max_rows, void* handle_out);
+ONMT_API onmt_status onmt_vp_open(onmt_model* m, int32_t world, int32_t rank, const void* handles);
+ONMT_API onmt_status onmt_vp_close(onmt_model* m);
+
+/*
  * onmt_last_plan - how the last translate / score call of the handle was executed (for
  * benchmarks and tests): rsplit = 1 if the recurrent-split decode step ran (DESIGN.md
  * §6.4b), fold = 1 if W_out was folded into attention, gen_parts = generator partials per

@@ -25,7 +25,8 @@ K_MAX = 16
 EXPORTS = ["onmt_load_weights", "onmt_model_get_info", "onmt_set_stream", "onmt_encode", "onmt_translate",
            "onmt_translate_trace", "onmt_translate_dev", "onmt_set_option", "onmt_get_kernel_time",
            "onmt_kernel_launches", "onmt_free", "onmt_last_error", "onmt_test_gemm", "onmt_test_gen", "onmt_score",
-           "onmt_translate_ex", "onmt_translate_copy", "onmt_graph_captures", "onmt_last_plan"]
+           "onmt_translate_ex", "onmt_translate_copy", "onmt_graph_captures", "onmt_last_plan",
+           "onmt_vp_handle", "onmt_vp_open", "onmt_vp_close"]
 
 
 class OnmtError(RuntimeError):
@@ -75,6 +76,9 @@ def lib():
     L.onmt_kernel_launches.argtypes = [VP, I32, P(I64)]
     L.onmt_graph_captures.argtypes = [VP, P(I64)]
     L.onmt_last_plan.argtypes = [VP, P(_Plan)]
+    L.onmt_vp_handle.argtypes = [VP, I32, VP]
+    L.onmt_vp_open.argtypes = [VP, I32, I32, VP]
+    L.onmt_vp_close.argtypes = [VP]
     L.onmt_free.argtypes = [VP]
     L.onmt_free.restype = None
     L.onmt_last_error.restype = ctypes.c_char_p
@@ -154,6 +158,21 @@ class Model:
         p = _Plan()
         _check(lib().onmt_last_plan(self._h, ctypes.byref(p)))
         return {n: getattr(p, n) for n, _ in _Plan._fields_}
+
+    # ---------------------------------------------- vocabulary-parallel generator (multi-GPU)
+    def vp_handle(self, max_rows: int) -> bytes:
+        """Allocate the exchange buffer for up to max_rows hypothesis rows; its IPC handle."""
+        buf = ctypes.create_string_buffer(64)
+        _check(lib().onmt_vp_handle(self._h, int(max_rows), buf))
+        return buf.raw
+
+    def vp_open(self, world: int, rank: int, handles: bytes | None):
+        """Map every rank's exchange buffer (handles: world x 64 bytes in rank order)."""
+        hb = ctypes.create_string_buffer(handles, len(handles)) if handles else None
+        _check(lib().onmt_vp_open(self._h, int(world), int(rank), hb))
+
+    def vp_close(self):
+        _check(lib().onmt_vp_close(self._h))
 
     def graph_captures(self) -> int:
         n = ctypes.c_int64()

@@ -189,6 +189,29 @@ struct GateTiles {
   float* gout;
 };
 
+// Vocabulary-parallel generator: the generator of rank r
+// runs CTAs [ci0, ci0 + C) of a Ct-CTA vocabulary split and stores its partials into EVERY
+// rank's exchange buffer (peer pointers over NVLink), then raises its flag there with the step
+// epoch (*seq << 16 | t); each rank's beam step waits for all Ct x groups flags before it
+// merges the Ct partials of a row - the same partials everywhere, hence the same selection.
+struct VpOut {
+  int world;                       // exchange buffers written (0: off)
+  int ranks;                       // ranks of the vocabulary split (== world; tests emulate ranks with world 1)
+  float2* ms[8];                   // [rows_pad][Ct] of rank w (this step's parity)
+  float* tz[8];                    // [rows_pad][Ct][K]
+  int* ti[8];
+  unsigned long long* flag[8];     // [groups][Ct] of rank w (this step's parity)
+  const unsigned long long* seq;   // call sequence number (device; identical on every rank)
+};
+struct VpWait {
+  const unsigned long long* flags; // this rank's flags (this step's parity), nullptr: off
+  int n;                           // groups x Ct
+  const unsigned long long* seq;
+};
+__device__ __forceinline__ unsigned long long vp_epoch(const unsigned long long* seq, int t) {
+  return (*(volatile const unsigned long long*)seq << 16) | (unsigned long long)t;
+}
+
 // Destinations of a decoder cell's h output (operand buffers and column offsets).
 struct CellDst {
   XOut x[2];

@@ -61,6 +61,9 @@ struct GenStepArgs {
   // after its vocabulary tiles: no scan, a plain store).
   int n_gt, gt_per_q, gkbh, gld;
   float* gout;
+  // vocabulary-parallel ranks (VpOut): this launch runs CTAs [ci0, ci0 + C) of a Ct-CTA split
+  int ci0, Ct;
+  VpOut vp;
 };
 
 // TMEM columns per accumulator (n_group rounded to 32)
@@ -160,8 +163,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = blockIdx.x / a.C, ci = blockIdx.x % a.C;
-  const int tb = ci * a.n_vt / a.C, te = (ci + 1) * a.n_vt / a.C;   // (n_vt * C < 2^31)
+  const int grp = blockIdx.x / a.C, ci = a.ci0 + blockIdx.x % a.C;   // (global CTA index of the split)
+  const int tb = ci * a.n_vt / a.Ct, te = (ci + 1) * a.n_vt / a.Ct;  // (n_vt * Ct < 2^31)
   const int n0 = grp * a.n_group;
   // local tiles i = 0 .. ntot-1: vocabulary tiles tb + i (i < nv), then the CTA's gate tile (if
   // any).  Batch bt = local tiles [bt * nt_max, min(ntot, (bt + 1) * nt_max)), all accumulators of
@@ -169,9 +172,9 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
   // tile its own TMEM columns, so batch bt + 1's MMAs overlap batch bt's epilogue.
   const int nv = te - tb;
   int gi = -1;                                                     // my gate tile
-  if (a.n_gt > 0 && nv == a.n_vt / a.C) {
+  if (a.n_gt > 0 && nv == a.n_vt / a.Ct) {                         // (gate tiles: single rank, Ct == C)
     // CTAs of my group before me with the smaller share: tb = ci * floor + (#larger shares before me)
-    const int idx = ci - (tb - ci * (a.n_vt / a.C));
+    const int idx = ci - (tb - ci * (a.n_vt / a.Ct));
     if (idx < a.n_gt) gi = idx;
   }
   const int ntot = nv + (gi >= 0 ? 1 : 0);
@@ -643,19 +646,40 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
 #endif
     if (row_ok && part == 0) {
       const int r = n0 + c;
-      a.ms[(size_t)r * a.C + ci] = make_float2(run_m, run_s);
-      const size_t base = ((size_t)r * a.C + ci) * a.K;
+      const size_t base = ((size_t)r * a.Ct + ci) * a.K;
+      if (a.vp.world == 0) {
+        a.ms[(size_t)r * a.Ct + ci] = make_float2(run_m, run_s);
 #pragma unroll
-      for (int i = 0; i < KMAX; ++i)
-        if (i >= KMAX - a.K) {
-          a.tz[base + i - (KMAX - a.K)] = tz[i];
-          a.ti[base + i - (KMAX - a.K)] = ti[i];
+        for (int i = 0; i < KMAX; ++i)
+          if (i >= KMAX - a.K) {
+            a.tz[base + i - (KMAX - a.K)] = tz[i];
+            a.ti[base + i - (KMAX - a.K)] = ti[i];
+          }
+      } else {
+        for (int w = 0; w < a.vp.world; ++w) {                     // every rank's exchange buffer
+          __stcg(a.vp.ms[w] + (size_t)r * a.Ct + ci, make_float2(run_m, run_s));
+#pragma unroll
+          for (int i = 0; i < KMAX; ++i)
+            if (i >= KMAX - a.K) {
+              __stcg(a.vp.tz[w] + base + i - (KMAX - a.K), tz[i]);
+              __stcg(a.vp.ti[w] + base + i - (KMAX - a.K), ti[i]);
+            }
         }
+      }
     }
   }
   KT(3);
   tc_fence_before();
   __syncthreads();
+  if (a.vp.world > 0 && threadIdx.x == 0) {
+    // my partials are stored everywhere (the barrier orders every thread's stores before this
+    // thread's system-scope fence): raise my flag in every rank's buffer with the step epoch
+    __threadfence_system();
+    const unsigned long long ep = vp_epoch(a.vp.seq, a.t);
+    for (int w = 0; w < a.vp.world; ++w)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.vp.flag[w] + (size_t)grp * a.Ct + ci), "l"(ep)
+                   : "memory");
+  }
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -758,10 +782,15 @@ static cudaError_t launch_gs(const CUtensorMap& tmW, const CUtensorMap& tmX, con
 // generator partials of decode step t (t selects the threshold buffers)
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i, int t,
-                     unsigned int* thr, StepCtl ctl, cudaStream_t st, const GateTiles& gt) {
+                     unsigned int* thr, StepCtl ctl, cudaStream_t st, const GateTiles& gt, const VpOut* vp,
+                     int vp_rank, int vp_C) {
   const int groups = n_rows_pad / n_group;
   GsPlan p;
-  if (!gs_plan(n_vt, n_group, groups, num_sms, g.rows_valid, g.K, p)) return cudaErrorInvalidConfiguration;
+  // vocabulary-parallel: plan for this rank's CTA count (vp_C per group), split Ct = world x vp_C
+  if (!gs_plan(vp ? (n_vt + vp->ranks - 1) / vp->ranks : n_vt, n_group, groups, vp ? vp_C * groups : num_sms,
+               g.rows_valid, g.K, p))
+    return cudaErrorInvalidConfiguration;
+  if (vp) p.C = vp_C;
   if (gt.n_gt > 0 && (n_vt % p.C == 0 || gt.n_gt > p.C - n_vt % p.C)) return cudaErrorInvalidConfiguration;
   GenStepArgs a{};
   a.n_rows_pad = n_rows_pad;
@@ -790,6 +819,12 @@ cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, i
   a.dbg = g_gs_dbg;
   const int grid = p.C * groups;
   const size_t smem = gs_smem_bytes(p.body, p.stages);
+  a.ci0 = vp ? vp_rank * p.C : 0;
+  a.Ct = vp ? p.C * vp->ranks : p.C;
+  if (vp) {
+    if (gt.n_gt > 0 || p.C * vp->ranks > n_vt || vp->ranks < 1) return cudaErrorInvalidConfiguration;
+    a.vp = *vp;
+  }
   if (getenv("ONMT_GEN_DEBUG") && t <= 1)
     fprintf(stderr, "gen_step plan: C=%d groups=%d n_group=%d nt_max=%d stages=%d ovl=%d nbuf=%d srows=%d smem=%zu "
             "static=%zu gates=%d\n", p.C, groups, n_group, p.nt_max, p.stages, p.ovl, p.nbuf, p.srows, smem,

@@ -41,7 +41,9 @@ int gen_persistent_parts(int n_vt, int n_groups, int num_sms, int cs);
 int gen_step_parts(int n_vt, int n_group, int groups, int num_sms);
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i, int t,
-                     unsigned int* thr, StepCtl ctl, cudaStream_t st, const GateTiles& gt);
+                     unsigned int* thr, StepCtl ctl, cudaStream_t st, const GateTiles& gt,
+                     const VpOut* vp = nullptr, int vp_rank = 0, int vp_C = 0);
+void launch_vp_seq(unsigned long long* seq, cudaStream_t st);
 int gen_step_gate_capacity(int n_vt, int n_group, int groups, int num_sms);
 extern unsigned long long* g_gen_dbg;
 
@@ -150,7 +152,8 @@ void launch_init_decode(const BeamState& bs, int B, int K, const float* enc_h, c
 void launch_gather(const BeamState& bs, const GatherArgs& g, int R, int K, StepCtl ctl, cudaStream_t st);
 void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_parts, int ps, int rs, int B, int K,
                        int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga, float* row_lse,
-                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st, int nslice = 1);
+                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st, int nslice = 1,
+                       const VpWait* vw = nullptr);
 void launch_finalize(const BeamState& bs, int B, int K, int max_len, int* hyps, int* lens, float* scores, float* raw,
                      float* tlogp, int* unk_pos, cudaStream_t st);
 void launch_row_reduce(const float2* ms, const float* tz, const int* ti, int n_vt, int ps, int rs, int R, int K,
@@ -377,6 +380,7 @@ struct onmt_model {
   bool fold_cur = false;       // ... for the call being enqueued (fold_on)
   bool use_graph = true;
   bool rsplit = true;          // recurrent-split decode step where it applies
+  int test_gen_world = 0;      // onmt_test_gen: emulate this many vocabulary-parallel ranks (sequential launches)
   bool rs_cur = false;         // ... for the call being enqueued
   int num_sms = 148;
   cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -434,6 +438,17 @@ struct onmt_model {
   uint64_t graph_clock = 0;
   int64_t graph_captures = 0;                // captures since load (corpus runs: should stop growing)
   onmt_plan_info plan{};                     // how the last call ran (onmt_last_plan)
+  // vocabulary-parallel generator: this rank's exchange
+  // buffer (peers store partials + flags into it over NVLink) and the mapped buffers of every rank
+  struct Vp {
+    int world = 0, rank = 0;
+    DevBuf own, seq;
+    void* peer[8] = {};
+    bool ipc[8] = {};
+    int rows_cap = 0;
+    size_t parity_bytes = 0;
+  } vp;
+  static constexpr int kVpCt = 256, kVpK = 16, kVpG = 4;     // partials per row, beam, row groups (caps)
   GraphCache* cap_graph = nullptr;           // the graph being captured (profiling event nodes)
   // teacher-forced scoring workspace
   Act xs_all;                                // generator operand of every (step, sentence) row
@@ -442,6 +457,8 @@ struct onmt_model {
   ~onmt_model() {
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (int w = 0; w < 8; ++w)
+      if (vp.ipc[w] && vp.peer[w]) cudaIpcCloseMemHandle(vp.peer[w]);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 };
@@ -449,6 +466,29 @@ struct onmt_model {
 namespace onmt {
 
 static void count(onmt_model* m, int n = 1) { m->launches += n; }
+
+// vocabulary-parallel exchange buffer, per parity: ms [rows_cap][Ct] float2 | tz [rows_cap][Ct][K]
+// | ti [rows_cap][Ct][K] | flags [groups][Ct] u64 (strides of the call's Ct / K inside the caps)
+struct VpOffsets {
+  size_t ms, tz, ti, flag;
+};
+static VpOffsets vp_offsets(const onmt_model* m, int parity) {
+  const size_t rc = (size_t)m->vp.rows_cap, Ct = onmt_model::kVpCt, Kc = onmt_model::kVpK;
+  VpOffsets o;
+  o.ms = (size_t)parity * m->vp.parity_bytes;
+  o.tz = o.ms + rc * Ct * 8;
+  o.ti = o.tz + rc * Ct * Kc * 4;
+  o.flag = o.ti + rc * Ct * Kc * 4;
+  return o;
+}
+static size_t vp_parity_bytes(int rows_cap) {
+  const size_t rc = (size_t)rows_cap, Ct = onmt_model::kVpCt, Kc = onmt_model::kVpK;
+  return ((rc * Ct * 8 + 2 * rc * Ct * Kc * 4 + (size_t)onmt_model::kVpG * Ct * 8) + 255) / 256 * 256;
+}
+// generator CTAs per row group on each rank (partials per row = world x this <= kVpCt)
+static int vp_ctas(const onmt_model* m, int groups) {
+  return std::max(1, std::min(m->num_sms / std::max(groups, 1), onmt_model::kVpCt / std::max(m->vp.world, 1)));
+}
 
 static int auto_splits(onmt_model* m, const Mat& W, int n_groups) {
   int ctas = (W.m_pad / kTileM) * n_groups;
@@ -1317,7 +1357,9 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
   const bool bf = m->use_tc;
   const int R = B * K, H = m->H, E = m->E, L = m->L;
   const int rp = m->xg.rows_pad;
-  const int n_vt = gen_parts(m, m->xg);
+  const int groups = rp / m->xg.n_group;
+  const int vpC = m->vp.world > 0 ? vp_ctas(m, groups) : 0;        // vocabulary-parallel: CTAs per group here
+  const int n_vt = m->vp.world > 0 ? m->vp.world * vpC : gen_parts(m, m->xg);
   BeamState bs = beam_state(m, trace, op, d_lens, S_max);
   if ((op.beta != 0.0 || op.unk) && n_vt > 256)
     throw Error{ONMT_E_UNSUPPORTED, "coverage / unk replacement need the one-CTA-per-sentence beam step (<= 256 generator partials)"};
@@ -1392,8 +1434,34 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
     gam.xh1[1] = m->xg.xo(true); gam.col_h1[1] = kpH;
     gt = GateTiles{&m->wg.tmap, (L + 1) * (G / kTileM), G / kTileM, kpH / kBK, G, m->pgate.as<float>()};
   }
+  if (m->vp.world > 0) {                                        // this call's flag epochs
+    launch_vp_seq(m->vp.seq.as<unsigned long long>(), m->stream);
+    count(m);
+  }
   for (int t = 1; t <= max_len; ++t) {
     EvPair ev = prof_begin(m, "step");
+    // vocabulary-parallel: this step's parity of every rank's exchange buffer
+    VpOut vo{};
+    VpWait vw{};
+    GenOut gs = g;
+    if (m->vp.world > 0) {
+      const VpOffsets o = vp_offsets(m, t & 1);
+      vo.world = m->vp.world;
+      vo.ranks = m->vp.world;
+      for (int w = 0; w < m->vp.world; ++w) {
+        char* base = static_cast<char*>(m->vp.peer[w]);
+        vo.ms[w] = reinterpret_cast<float2*>(base + o.ms);
+        vo.tz[w] = reinterpret_cast<float*>(base + o.tz);
+        vo.ti[w] = reinterpret_cast<int*>(base + o.ti);
+        vo.flag[w] = reinterpret_cast<unsigned long long*>(base + o.flag);
+      }
+      vo.seq = m->vp.seq.as<unsigned long long>();
+      char* own = m->vp.own.as<char>();
+      gs.ms = reinterpret_cast<float2*>(own + o.ms);
+      gs.tz = reinterpret_cast<float*>(own + o.tz);
+      gs.ti = reinterpret_cast<int*>(own + o.ti);
+      vw = VpWait{reinterpret_cast<const unsigned long long*>(own + o.flag), groups * n_vt, vo.seq};
+    }
     if (m->rs_cur && t > 1)
       enqueue_rs_layers(m, d_lens, B, S_max, K, bs.done, ctl);
     else
@@ -1403,9 +1471,9 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
       // K-outer generator (phase A of gen_step.cu), partials [row][C]; then row reduce + beam step
       EvPair pgs = prof_begin(m, "gen");
       ONMT_CUDA(gen_step(m->gen_w.tmap, m->xg.tmap, (m->Vt + kVTile - 1) / kVTile, m->xg.rows_pad, m->xg.n_group,
-                           m->gen_w.k_pad / kBK, m->num_sms, g, m->row_lse.as<float>(), m->row_z.as<float>(),
+                           m->gen_w.k_pad / kBK, m->num_sms, gs, m->row_lse.as<float>(), m->row_z.as<float>(),
                            m->row_i.as<int>(), t, m->g_thr.as<unsigned int>(), ctl, m->stream,
-                           t < max_len ? gt : GateTiles{}));
+                           t < max_len ? gt : GateTiles{}, m->vp.world > 0 ? &vo : nullptr, m->vp.rank, vpC));
       count(m);
       prof_end(m, "gen", pgs);
       EvPair pm = prof_begin(m, "merge");
@@ -1415,8 +1483,9 @@ static void enqueue_decoder(onmt_model* m, const int* d_lens, int B, int S_max, 
         // recurrent split: a few CTAs per sentence share layer 1's cell (each selects redundantly)
         static const int nsl_env = std::getenv("ONMT_BEAM_NSLICE") ? std::atoi(std::getenv("ONMT_BEAM_NSLICE")) : 0;
         const int nsl = m->rs_cur ? (nsl_env > 0 ? nsl_env : std::max(1, std::min(4, m->num_sms / std::max(B, 1)))) : 1;
-        launch_beam_merge(g.ms, g.tz, g.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, m->rs_cur ? gam : ga,
-                          m->row_lse.as<float>(), m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream, nsl);
+        launch_beam_merge(gs.ms, gs.tz, gs.ti, n_vt, 1, n_vt, B, K, t, max_len, lp, bs, m->rs_cur ? gam : ga,
+                          m->row_lse.as<float>(), m->row_z.as<float>(), m->row_i.as<int>(), ctl, m->stream, nsl,
+                          m->vp.world > 0 ? &vw : nullptr);
         count(m, n_vt <= 256 ? 1 : 2);
       }
       prof_end(m, "merge", pm);
@@ -1589,12 +1658,19 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
 static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, int B, int S_max, int K, int max_len,
                           float alpha, bool trace, const DecodeOut& out, const DecodeOpts& op = DecodeOpts{}) {
   m->fold_cur = fold_on(m, B * K);
-  m->rs_cur = rsplit_on(m, B, K, op.att() || op.src_ext);
+  m->rs_cur = m->vp.world > 0 ? false : rsplit_on(m, B, K, op.att() || op.src_ext);
+  if (m->vp.world > 0) {
+    const RowPlan rp = plan_rows(B * K);
+    if (!m->use_tc || !m->gen_step || op.att() || op.src_ext || K > onmt_model::kVpK ||
+        rp.rows_pad > m->vp.rows_cap || rp.rows_pad / rp.n_group > onmt_model::kVpG)
+      throw Error{ONMT_E_UNSUPPORTED, "vocabulary-parallel decoding: bf16 plain translate with rows <= the exchange "
+                                      "capacity, beam <= 16 and <= 4 row groups"};
+  }
   prepare_encoder(m, B, S_max);
   prepare_decoder(m, B, S_max, K, max_len, trace, op);
   m->plan.rsplit = m->rs_cur;
   m->plan.fold = m->fold_cur;
-  m->plan.gen_parts = gen_parts(m, m->xg);
+  m->plan.gen_parts = m->vp.world > 0 ? m->vp.world * vp_ctas(m, m->xg.rows_pad / m->xg.n_group) : gen_parts(m, m->xg);
   m->plan.gate_tiles = m->rs_cur ? (m->L + 1) * (round_up(4 * m->H, kTileM) / kTileM) : 0;
   m->plan.groups = m->xg.rows_pad / m->xg.n_group;
   auto enqueue = [&]() {
@@ -1606,7 +1682,8 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     return;
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
-                              m->gen_step, m->fold_cur, m->enc_persistent, m->enc_wavefront, m->rs_cur,
+                              m->gen_step, m->fold_cur, m->enc_persistent, m->enc_wavefront, m->rs_cur, m->vp.world,
+                              m->vp.rank,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
                               (int64_t)(intptr_t)out.scores, (int64_t)(intptr_t)out.raw, (int64_t)(intptr_t)out.tlogp,
@@ -1717,6 +1794,9 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->use_graph = v != 0;
   } else if (n == "rsplit") {
     m->rsplit = v != 0;
+  } else if (n == "test_gen_world") {
+    if (v < 0 || v > 8) return fail(ONMT_E_INVALID_ARG, "test_gen_world must be in [0, 8]");
+    m->test_gen_world = (int)v;
   } else {
     return fail(ONMT_E_INVALID_ARG, "unknown option " + n);
   }
@@ -1992,6 +2072,66 @@ onmt_status onmt_kernel_launches(onmt_model* m, int32_t reset, int64_t* launches
   return ONMT_OK;
 }
 
+onmt_status onmt_vp_handle(onmt_model* m, int32_t max_rows, void* handle_out) {
+  if (!m || !handle_out || max_rows < 1) return fail(ONMT_E_INVALID_ARG, "bad argument");
+  ONMT_API_BEGIN
+  ONMT_CUDA(cudaSetDevice(m->device));
+  const int rc = plan_rows(max_rows).rows_pad;
+  if (m->vp.world > 0) return fail(ONMT_E_INVALID_ARG, "close the vocabulary-parallel group first");
+  m->vp.rows_cap = rc;
+  m->vp.parity_bytes = vp_parity_bytes(rc);
+  m->vp.own.ensure(2 * m->vp.parity_bytes);
+  ONMT_CUDA(cudaMemset(m->vp.own.p, 0, 2 * m->vp.parity_bytes));   // flags 0: no epoch is 0
+  m->vp.seq.ensure(8);
+  ONMT_CUDA(cudaMemset(m->vp.seq.p, 0, 8));
+  cudaIpcMemHandle_t h;
+  ONMT_CUDA(cudaIpcGetMemHandle(&h, m->vp.own.p));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return ONMT_OK;
+  ONMT_API_END
+}
+
+onmt_status onmt_vp_open(onmt_model* m, int32_t world, int32_t rank, const void* handles) {
+  if (!m || world < 1 || world > 8 || rank < 0 || rank >= world || (world > 1 && !handles))
+    return fail(ONMT_E_INVALID_ARG, "bad world / rank / handles");
+  if (!m->vp.own.p) return fail(ONMT_E_INVALID_ARG, "onmt_vp_handle first");
+  if (m->prec != ONMT_PREC_BF16) return fail(ONMT_E_UNSUPPORTED, "vocabulary-parallel decoding needs a bf16 model");
+  ONMT_API_BEGIN
+  ONMT_CUDA(cudaSetDevice(m->device));
+  for (int w = 0; w < world; ++w) {
+    if (w == rank) {
+      m->vp.peer[w] = m->vp.own.p;
+      m->vp.ipc[w] = false;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + (size_t)w * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    ONMT_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    m->vp.peer[w] = p;
+    m->vp.ipc[w] = true;
+  }
+  m->vp.world = world;
+  m->vp.rank = rank;
+  ++g_alloc_gen;                                    // (cached graphs hold the old pointers)
+  return ONMT_OK;
+  ONMT_API_END
+}
+
+onmt_status onmt_vp_close(onmt_model* m) {
+  if (!m) return fail(ONMT_E_INVALID_ARG, "null model");
+  ONMT_API_BEGIN
+  ONMT_CUDA(cudaSetDevice(m->device));
+  ONMT_CUDA(cudaStreamSynchronize(m->stream));
+  for (int w = 0; w < m->vp.world; ++w)
+    if (m->vp.ipc[w]) ONMT_CUDA(cudaIpcCloseMemHandle(m->vp.peer[w]));
+  for (int w = 0; w < 8; ++w) { m->vp.peer[w] = nullptr; m->vp.ipc[w] = false; }
+  m->vp.world = 0;
+  ++g_alloc_gen;
+  return ONMT_OK;
+  ONMT_API_END
+}
+
 onmt_status onmt_last_plan(const onmt_model* m, onmt_plan_info* out) {
   if (!m || !out) return fail(ONMT_E_INVALID_ARG, "null argument");
   *out = m->plan;
@@ -2097,9 +2237,36 @@ onmt_status onmt_test_gen(onmt_model* m, const float* htilde, int32_t R, int32_t
   if (gs) {
     if (m->g_thr.bytes < (size_t)2 * x.rows_pad * 17 * 4) m->g_thr.ensure((size_t)2 * x.rows_pad * 17 * 4);
     ONMT_CUDA(cudaMemset(m->g_thr.p, 0, m->g_thr.bytes));
-    ONMT_CUDA(gen_step(m->gen_w.tmap, x.tmap, (m->Vt + kVTile - 1) / kVTile, x.rows_pad, x.n_group,
-                       m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 0,
-                       m->g_thr.as<unsigned int>(), StepCtl{nullptr, 0}, m->stream, GateTiles{}));
+    const int W = m->test_gen_world;
+    if (W > 1) {
+      // the vocabulary-parallel split, its W ranks emulated by W launches one after another on this
+      // GPU (no launch waits on another): rank r runs CTAs [r C / W, (r + 1) C / W) of the C-CTA
+      // split and stores its partial columns through the exchange pointers (here: one buffer)
+      if (n_parts % W != 0 || W > 8) return fail(ONMT_E_INVALID_ARG, "test_gen_world must divide the partial count");
+      DevBuf flags, seq;
+      flags.ensure((size_t)(x.rows_pad / x.n_group) * n_parts * 8);
+      ONMT_CUDA(cudaMemset(flags.p, 0, flags.bytes));
+      seq.ensure(8);
+      ONMT_CUDA(cudaMemset(seq.p, 0, 8));
+      VpOut vo{};
+      vo.world = 1;
+      vo.ranks = W;
+      vo.ms[0] = g.ms; vo.tz[0] = g.tz; vo.ti[0] = g.ti;
+      vo.flag[0] = flags.as<unsigned long long>();
+      vo.seq = seq.as<unsigned long long>();
+      for (int r = 0; r < W; ++r) {
+        ONMT_CUDA(gen_step(m->gen_w.tmap, x.tmap, (m->Vt + kVTile - 1) / kVTile, x.rows_pad, x.n_group,
+                           m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 0,
+                           m->g_thr.as<unsigned int>(), StepCtl{nullptr, 0}, m->stream, GateTiles{}, &vo, r,
+                           n_parts / W));
+      }
+      // (emulation: every launch wrote column block r of the same Ct = C partials)
+      vo.world = 0;
+    } else {
+      ONMT_CUDA(gen_step(m->gen_w.tmap, x.tmap, (m->Vt + kVTile - 1) / kVTile, x.rows_pad, x.n_group,
+                         m->gen_w.k_pad / kBK, m->num_sms, g, dl.as<float>(), dz.as<float>(), di.as<int>(), 0,
+                         m->g_thr.as<unsigned int>(), StepCtl{nullptr, 0}, m->stream, GateTiles{}));
+    }
   } else {
     gen(m, x, g, StepCtl{nullptr, 0});
   }

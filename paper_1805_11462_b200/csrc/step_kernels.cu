@@ -422,11 +422,28 @@ template <int KMAX>
 __global__ void __launch_bounds__(512) beam_step_kernel(const float2* __restrict__ ms, const float* __restrict__ tz,
                                                         const int* __restrict__ ti, int n_parts, int ps, int rs, int K,
                                                         int t, int max_len, double lp, BeamState bs, GatherArgs ga,
-                                                        StepCtl ctl) {
+                                                        StepCtl ctl, VpWait vw) {
   KT(0);
   pdl_trigger();
   pdl_wait();
   (void)ctl;
+  if (vw.flags) {
+    // vocabulary-parallel: every rank's generator CTAs raised their flag for this step in my
+    // exchange buffer (their partials landed before it: release / acquire at system scope)
+    if (threadIdx.x < 32) {
+      const unsigned long long ep = vp_epoch(vw.seq, t);
+      const unsigned long long t0 = spin_clock();
+      unsigned int it = 0;
+      for (int i = threadIdx.x; i < vw.n; i += 32)
+        while (true) {
+          unsigned long long v;
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(vw.flags + i) : "memory");
+          if (v == ep) break;
+          spin_check(t0, it);
+        }
+    }
+    __syncthreads();
+  }
   extern __shared__ __align__(16) float gbuf_dyn[];
   beam_step_sentence<KMAX>(blockIdx.x, ms, tz, ti, n_parts, ps, rs, K, gridDim.x * K, t, max_len, lp, bs, ga,
                            gbuf_dyn, (int)(kBeamStageBytes / 4), blockIdx.y, gridDim.y);
@@ -434,7 +451,8 @@ __global__ void __launch_bounds__(512) beam_step_kernel(const float2* __restrict
 
 void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_parts, int ps, int rs, int B, int K,
                        int t, int max_len, double lp, const BeamState& bs, const GatherArgs& ga, float* row_lse,
-                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st, int nslice) {
+                       float* row_z, int* row_i, StepCtl ctl, cudaStream_t st, int nslice, const VpWait* vw) {
+  const VpWait vwv = vw ? *vw : VpWait{nullptr, 0, nullptr};
   const int R = B * K;
   // one CTA per sentence (row reduce + select + gather) when its lanes hold every partial;
   // otherwise (SIMT generator over many tiles) a row-reduce launch + a select/gather launch
@@ -443,7 +461,7 @@ void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_p
     cudaFuncSetAttribute(beam_step_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBeamStageBytes); \
     launch_pdl(beam_step_kernel<KM>, dim3(B, nslice), dim3(512), kBeamStageBytes, st, ms, tz, ti, n_parts, ps, rs,  \
                K, t,                                                                                              \
-               max_len, lp, bs, ga, ctl);                                                                         \
+               max_len, lp, bs, ga, ctl, vwv);                                                                    \
   } else {                                                                                                        \
     launch_pdl(row_reduce_topk_kernel<KM>, dim3(R), dim3(128), 0, st, ms, tz, ti, n_parts, ps, rs, K,             \
                bs.live + (size_t)(t & 1) * R, row_lse, row_z, row_i, ctl);                                        \
@@ -459,6 +477,12 @@ void launch_beam_merge(const float2* ms, const float* tz, const int* ti, int n_p
   else { ONMT_MERGE(16) }
 #undef ONMT_MERGE
 }
+
+// vocabulary-parallel: the call's sequence number (step epochs of the exchange flags)
+__global__ void vp_seq_kernel(unsigned long long* seq) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *seq += 1ull;
+}
+void launch_vp_seq(unsigned long long* seq, cudaStream_t st) { vp_seq_kernel<<<1, 32, 0, st>>>(seq); }
 
 // A11 with the sentence's history staged in shared memory: one CTA per sentence loads the
 // (token, parent, log p, attention argmax) entries of its K slots for every step (coalesced),

@@ -101,3 +101,21 @@ def translate_batches(model, ids, lens, batches: Sequence[Tuple[int, int]], mine
              "token_logp": np.zeros((0, max_len), np.float32)}
         return z, np.zeros(0, np.int64)
     return {k: np.concatenate([o[k] for o in outs]) for k in RESULT_KEYS}, np.concatenate(idx)
+
+
+def open_vocab_parallel(model, max_rows: int, group=None):
+    """Vocabulary-parallel generator: every rank allocates its exchange
+    buffer, the IPC handles are all-gathered (one object collective at set-up, not per step) and
+    every rank maps the others' buffers.  Afterwards each rank's translate calls stream 1/world of
+    W_gen and exchange the generator partials through peer memory inside the decode graph; every
+    rank returns the same translation."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = model.vp_handle(max_rows)
+    handles = [None] * world
+    dist.all_gather_object(handles, mine, group=group)
+    if any(h is None or len(h) != 64 for h in handles):
+        raise RuntimeError("bad exchange handle")
+    model.vp_open(world, rank, b"".join(handles))
+    return world, rank

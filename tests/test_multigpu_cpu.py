@@ -103,3 +103,45 @@ def test_gloo_world2_gather_restores_corpus_order(mode):
     for r in (0, 1):
         for k in RESULT_KEYS:
             np.testing.assert_array_equal(res[r][k], want[k])
+
+
+class FakeVpModel:
+    """Records the vocabulary-parallel set-up calls (the handle bytes identify the rank)."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.opened = None
+
+    def vp_handle(self, max_rows):
+        return bytes([self.rank]) * 32 + max_rows.to_bytes(32, "little")
+
+    def vp_open(self, world, rank, handles):
+        self.opened = (world, rank, handles)
+
+
+def _vp_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1805_11462_b200.parallel import open_vocab_parallel
+    m = FakeVpModel(rank)
+    open_vocab_parallel(m, 150)
+    q.put((rank, m.opened))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_vocab_parallel_handle_exchange():
+    """Every rank maps every rank's exchange buffer: the handles arrive in rank order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_vp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    want = b"".join(bytes([r]) * 32 + (150).to_bytes(32, "little") for r in range(2))
+    for r in (0, 1):
+        world, rank, handles = res[r]
+        assert (world, rank) == (2, r) and handles == want
