@@ -65,7 +65,7 @@ int main(int argc, char** argv) {
   int tstep = 2;  // alternate t: each launch clears the other threshold buffer, as in a decode
   auto launch = [&]() {
     tstep = tstep == 2 ? 3 : 2;
-    CK(gen_step(tmW, tmX, VP / 128, NP, NP, KP / 64, 148, g, rl, rz, ri, tstep, thr, StepCtl{nullptr, 0}, st, gt));
+    CK(gen_step(tmW, tmX, VP / 128, NP, NP, KP / 64, 148, g, rl, rz, ri, tstep, thr, StepCtl{nullptr, 0}, st, gt, nullptr, 0, 0));
   };
   cudaGraph_t gr; cudaGraphExec_t ge;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
