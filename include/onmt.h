@@ -236,6 +236,15 @@ ONMT_API onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_src_ids,
  *                   same kernel (L2 round trip + per-tile arrival counter) and apply the
  *                   LSTM cell / tanh there (default); 0 = separate partial GEMM + consumer
  *                   kernels.  Both give the same result up to fp32 summation order.
+ *   "enc_persistent" 1 = an encoder layer's recurrence as one persistent launch (default),
+ *                   0 = two launches per time step.
+ *   "enc_cluster"   1 = a direction's recurrence as one thread-block cluster with h_{t-1} in
+ *                   distributed shared memory where it fits (<= 16 gate tiles; default),
+ *                   0 = the split-K grid kernel with a step barrier through L2.
+ *   "enc_wavefront" 1 = unidirectional stacks as one layer-wavefront launch (default).
+ *   "gen_step", "fold_wout", "rsplit"  1 = the fused generator step / folded W_out /
+ *                   recurrent-split decode step where they apply (defaults), 0 = off.
+ *   All variants compute the same function up to fp32 summation order.
  * INVALID_ARG on an unknown name or value.
  */
 ONMT_API onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t value);

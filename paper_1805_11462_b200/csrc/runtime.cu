@@ -79,6 +79,27 @@ struct EncRecArgs {
   unsigned long long* trace;
 };
 int enc_rec_splits(int kb, int N, int D, int T, int num_sms);
+struct EncClDir {
+  const float* Z;
+  int z_ld;
+  const float4* bias;
+  float* h_st;
+  float* c_st;
+  int st_ld;
+  XOut xnext;
+  int next_col;
+  float* mem;
+  int mem_ld, mem_col;
+  int backward;
+};
+struct EncClArgs {
+  EncClDir dir[2];
+  int T, Hd, B, N, S_max, kb;
+  const int* lens;
+  unsigned long long* trace;
+};
+int enc_cl_fits(int T, int kb, int N, int D, int num_sms);
+cudaError_t launch_enc_cl(const CUtensorMap* tmW, const EncClArgs& a, int D, cudaStream_t st);
 struct EncWaveLayer {
   int T, S, kb, kb_in;
   int cta0;
@@ -377,6 +398,7 @@ struct onmt_model {
   bool gen_step = true;        // K-outer persistent generator (gen_step.cu)
   bool fold_wout = true;       // W_out folded into the top cell layer + attention (no W_out launch)
   bool enc_persistent = true;  // encoder recurrence of a layer as one persistent kernel (enc_rec.cu)
+  bool enc_cluster = true;     // ... as one cluster per direction with the state on chip (enc_cl.cu)
   bool fold_cur = false;       // ... for the call being enqueued (fold_on)
   bool use_graph = true;
   bool rsplit = true;          // recurrent-split decode step where it applies
@@ -999,6 +1021,50 @@ static void enqueue_encoder(onmt_model* m, const int* d_ids, const int* d_lens, 
       const Mat& w0 = *m->enc_whh[l * D];
       const Act& r0 = m->enc_rec[0];
       const int T = w0.m_pad / kTileM, kb = w0.k_pad / kBK;
+      if (m->use_tc && m->enc_persistent && m->enc_cluster && r0.n_group == r0.rows_pad &&
+          enc_cl_fits(T, kb, r0.rows_pad, D, m->num_sms)) {
+        // the whole recurrence of this layer, one cluster per direction, state on chip (enc_cl.cu)
+        EncClArgs ca{};
+        CUtensorMap tw[2];
+        for (int d = 0; d < D; ++d) {
+          EncClDir& dr = ca.dir[d];
+          dr.Z = m->enc_z[d].as<float>();
+          dr.z_ld = zld;
+          dr.bias = m->enc_bias[l * D + d]->as<float4>();
+          dr.h_st = m->enc_h.as<float>() + (size_t)l * B * H + d * Hd;
+          dr.c_st = m->enc_c.as<float>() + (size_t)l * B * H + d * Hd;
+          dr.st_ld = H;
+          if (xnext) dr.xnext = xnext->xo(bf);
+          else if (m->general || m->fold_cur) dr.xnext = m->mem_x.xo(bf);
+          dr.next_col = d * Hd;
+          dr.mem = l + 1 == m->L ? m->mem.as<float>() : nullptr;
+          dr.mem_ld = H;
+          dr.mem_col = d * Hd;
+          dr.backward = d == 1;
+          tw[d] = m->enc_whh[l * D + d]->tmap;
+        }
+        ca.T = T; ca.Hd = Hd; ca.B = B; ca.N = r0.rows_pad; ca.S_max = S_max; ca.kb = kb;
+        ca.lens = d_lens;
+        static unsigned long long* ec_trace = nullptr;            // (debug: ONMT_ENC_TRACE, no graph)
+        const bool trc = std::getenv("ONMT_ENC_TRACE") && !m->capturing;
+        if (trc && !ec_trace) cudaMalloc(&ec_trace, 64 * 8 * 8);
+        ca.trace = trc ? ec_trace : nullptr;
+        ONMT_CUDA(launch_enc_cl(tw, ca, D, m->stream));
+        count(m);
+        if (trc) {
+          std::vector<unsigned long long> h(64 * 8);
+          ONMT_CUDA(cudaStreamSynchronize(m->stream));
+          ONMT_CUDA(cudaMemcpy(h.data(), ec_trace, h.size() * 8, cudaMemcpyDeviceToHost));
+          for (int t = 8; t < 12; ++t)
+            std::fprintf(stderr, "enc_cl l%d t%d: h wait + mma issue %lld  mma done %lld  staged+z %lld  cell+sync %lld  "
+                         "to next step %lld ns\n", l, t,
+                         (long long)(h[t * 8 + 1] - h[t * 8 + 0]), (long long)(h[t * 8 + 2] - h[t * 8 + 0]),
+                         (long long)(h[t * 8 + 3] - h[t * 8 + 2]), (long long)(h[t * 8 + 5] - h[t * 8 + 3]),
+                         (long long)(h[(t + 1) * 8 + 0] - h[t * 8 + 5]));
+        }
+        xin = xnext;
+        continue;
+      }
       const int S = (m->use_tc && m->enc_persistent && r0.n_group == r0.rows_pad)
                         ? enc_rec_splits(kb, r0.rows_pad, D, T, m->num_sms) : 0;
       if (S > 0) {
@@ -1648,7 +1714,8 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
     return;
   }
   std::vector<int64_t> key = {-1, B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->fold_cur,
-                              m->enc_persistent, m->enc_wavefront, (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids,
+                              m->enc_persistent, m->enc_wavefront, m->enc_cluster, (int64_t)g_alloc_gen,
+                              (int64_t)(intptr_t)d_ids,
                               (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
   replay_graph(m, key, [&]() { enqueue_score(m, d_ids, d_lens, B, S_max, T_max); });
 }
@@ -1682,7 +1749,8 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     return;
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
-                              m->gen_step, m->fold_cur, m->enc_persistent, m->enc_wavefront, m->rs_cur, m->vp.world,
+                              m->gen_step, m->fold_cur, m->enc_persistent, m->enc_wavefront, m->enc_cluster, m->rs_cur,
+                              m->vp.world,
                               m->vp.rank,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
                               (int64_t)(intptr_t)m->stream, (int64_t)(intptr_t)out.hyps, (int64_t)(intptr_t)out.lens,
@@ -1748,6 +1816,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   if (const char* ev = std::getenv("ONMT_FOLD_WOUT")) m->fold_wout = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_PERSISTENT")) m->enc_persistent = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_WAVE")) m->enc_wavefront = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_ENC_CLUSTER")) m->enc_cluster = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_RSPLIT")) m->rsplit = std::atoi(ev) != 0;
 
   ONMT_CUDA(cudaStreamCreateWithFlags(&m->own_stream, cudaStreamNonBlocking));
@@ -1790,6 +1859,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->enc_persistent = v != 0;
   } else if (n == "enc_wavefront") {
     m->enc_wavefront = v != 0;
+  } else if (n == "enc_cluster") {
+    m->enc_cluster = v != 0;
   } else if (n == "use_graph") {
     m->use_graph = v != 0;
   } else if (n == "rsplit") {

@@ -142,6 +142,15 @@ def test_persistent_encoders_match_per_step_path(weight_cache, layers, bidir):
     np.testing.assert_allclose(mem1, mem0, atol=5e-6)
     np.testing.assert_allclose(h1, h0, atol=5e-6)
     np.testing.assert_allclose(c1, c0, atol=5e-6)
+    if bidir:                     # the cluster recurrence (enc_cl.cu) against the split-K grid kernel (enc_rec.cu)
+        gm.set_option("enc_cluster", 0)
+        try:
+            mem2, h2, c2 = gm.encode(ids, lens)
+        finally:
+            gm.set_option("enc_cluster", 1)
+        np.testing.assert_allclose(mem1, mem2, atol=5e-6)
+        np.testing.assert_allclose(h1, h2, atol=5e-6)
+        np.testing.assert_allclose(c1, c2, atol=5e-6)
     for b in range(len(lens)):
         ref_mem, finals = om.encode([int(v) for v in ids[b, :lens[b]]])
         np.testing.assert_allclose(mem1[b, :lens[b]], ref_mem, atol=2e-4)

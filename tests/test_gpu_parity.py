@@ -61,10 +61,12 @@ def run_parity(gm, om, prec, ids, lens, K, max_len, alpha):
 
 
 # ------------------------------------------------------------------ encoder
-@pytest.mark.parametrize("workload", ["c1", "c3"])
+@pytest.mark.parametrize("workload", ["c1", "c3", "c5"])
 def test_encoder_parity(workload, weight_cache):
+    """c3 / c5 (bidirectional, 4 and 2 sentences: N = 16) run the cluster recurrence (enc_cl.cu);
+    c5's 300-400-token sources are its longest recurrences."""
     gm, om, prec = model_pair(workload, weight_cache)
-    ids, lens = synth.make_corpus(workload, 4 if workload != "c1" else None)
+    ids, lens = synth.make_corpus(workload, {"c1": None, "c3": 4, "c5": 2}[workload])
     mem, h, c = gm.encode(ids, lens)
     tol = 1e-5 if prec == "fp32" else 2e-4
     for b in range(len(lens)):
