@@ -252,19 +252,19 @@ enc_cl_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ 
     if (send) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // staging stores -> bulk-copy reads
       __syncthreads();
-      if (threadIdx.x == 32) {
-        // push my block into K block `tile` of every CTA's buffer par ^ 1 (mine included)
+      if (warp == 1 && lane < T) {
+        // push my block into K block `tile` of every CTA's buffer par ^ 1 (mine included): lane
+        // p of warp 1 copies to CTA p
         const uint32_t dst0 = smem_u32(sX + (size_t)(par ^ 1) * xpar + (size_t)tile * 2 * nb);
         const uint32_t bar0 = smem_u32(&hbar[par ^ 1]);
-        for (int p = 0; p < T; ++p)
-          bulk_s2peer(mapa_peer(dst0, (uint32_t)p), hb, 2 * nb, mapa_peer(bar0, (uint32_t)p));
+        bulk_s2peer(mapa_peer(dst0, (uint32_t)lane), hb, 2 * nb, mapa_peer(bar0, (uint32_t)lane));
         bulk_commit();
         bulk_wait_read<1>();                                      // (step t-1's block may be rewritten)
       }
       if (tr && threadIdx.x == 0 && t < 64) a.trace[t * 8 + 5] = ec_now();
     }
   }
-  if (threadIdx.x == 32) bulk_wait_read<0>();
+  if (warp == 1 && lane < T) bulk_wait_read<0>();
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   if (threadIdx.x == 0 && a.S_max <= 1) mbar_wait(wbar, 0);       // (no MMA waited for the W load)
   tc_fence_before();
