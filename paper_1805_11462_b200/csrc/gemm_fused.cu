@@ -45,8 +45,9 @@ struct FusedArgs {
   float* htilde;
   XOut xg;
   // EPI_CELL of the top decoder layer with W_out folded into attention:
-  // woh = W_out[:, H:2H]^T in 32-unit tile slices (bf16 [m_tiles*32][H]); the CTA adds its
-  // units' share  W_out[:, units] h[units, cols]  to woh_part[m_tile][row][H] (fp32)
+  // woh = W_out[:, H:2H] per 32-unit tile: [fold_mo(H) outputs][32 units] bf16, K-major with the
+  // 64-byte swizzle already applied (the shared-memory image of the MMA A operand); the CTA
+  // writes its units' share  W_out[:, units] h[units, cols]  to woh_part[m_tile][row][H] (fp32)
   const __nv_bfloat16* woh;
   float* woh_part;
   // EPI_CELL, recurrent-split step: per-row gate pre-activations added to
@@ -70,7 +71,14 @@ __device__ __forceinline__ float tanhfast(float x) {
 
 // folded W_out slice: row stride (bf16 elements) of W_out[:, units]^T in shared memory -
 // 16-byte rows for ldmatrix, +8 so the 8 rows of an 8x8 matrix hit distinct banks
-__host__ __device__ __forceinline__ int fold_ld(int H) { return (H + 15) / 16 * 16 + 8; }
+__host__ __device__ __forceinline__ int fold_mo(int H) { return (H + 127) / 128 * 128; }   // outputs, padded
+__host__ __device__ __forceinline__ size_t fold_tile_bytes(int H) { return (size_t)fold_mo(H) * 64; }
+__host__ __device__ __forceinline__ int fold_chunks(int NC) { return (NC + 31) / 32; }      // 32-column chunks
+// byte offset of (row r, column c < 32) in a [rows][32] bf16 K-major tile with the 64-byte swizzle
+// (address bits 4-5 ^= bits 7-8): the layout the host packs woh in and the kernel writes h in
+__host__ __device__ __forceinline__ uint32_t fold_sw64(int r, int c) {
+  return (uint32_t)(r * 64 + ((((c >> 3) ^ (r >> 1)) & 3) << 4) + ((c & 7) << 1));
+}
 
 // D += A B, m16n8k16, bf16 inputs, fp32 accumulate (A: 4 regs, B: 2 regs, row.col)
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
@@ -102,13 +110,14 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   uint64_t* rbar = done + 1;
   uint64_t* wbar = rbar + 1;
   uint64_t* empty = wbar + 1;                                      // [stages] (ring: stages < K blocks)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(empty + a.stages);
-  const int ncp = (a.NC + 23) / 24 * 24;                           // s_hc row stride
+  uint64_t* fbar = empty + a.stages;                               // fold MMAs of a column chunk done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + 1);
   // (offsets from smem keep the shared address space visible to the compiler: LDS, not LD.E)
-  const size_t woh_off = ((size_t)(reinterpret_cast<uint8_t*>(tslot) - smem) + 16 + 127) & ~(size_t)127;
-  __nv_bfloat16* woh_s = reinterpret_cast<__nv_bfloat16*>(smem + woh_off);                          // [32][H]
-  float* s_hc = reinterpret_cast<float*>(woh_s + (size_t)32 * fold_ld(a.H));                       // [32][ncp]
-  float4* s_gb = reinterpret_cast<float4*>(smem + woh_off + (a.woh ? (size_t)64 * fold_ld(a.H) + (size_t)128 * ncp : 0));
+  const size_t woh_off = ((size_t)(reinterpret_cast<uint8_t*>(tslot) - smem) + 16 + 1023) & ~(size_t)1023;
+  uint8_t* woh_s = smem + woh_off;                                 // [fold_mo][32] bf16, SW64 (A operand)
+  uint8_t* s_hb = woh_s + fold_tile_bytes(a.H);                    // [chunk][hi, lo][32 cols][32 units] (B)
+  float4* s_gb = reinterpret_cast<float4*>(smem + woh_off +
+                                           (a.woh ? fold_tile_bytes(a.H) + (size_t)fold_chunks(a.NC) * 4096 : 0));
                                                                   // [NC][32] (16-byte aligned offsets)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -133,15 +142,16 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
     mbar_init(done, 1);
     mbar_init(rbar, 1);
     mbar_init(wbar, 1);
+    mbar_init(fbar, 1);
     fence_mbar_init();
     for (int i = 0; i < nkb && i < a.stages; ++i) {                // the first ring stages' weights
       mbar_expect_tx(&full[i], a_bytes);
       tma_load_2d(smem + i * stage_bytes, &tmW, (kb0 + i) * kBK, m0, &full[i]);
     }
-    if (EPI == EPI_CELL && a.woh) {                                // W_out[:, tile's units]^T (constant)
-      const uint32_t wb = (uint32_t)(32 * fold_ld(a.H) * 2);
+    if (EPI == EPI_CELL && a.woh) {                                // W_out[:, tile's units] (constant)
+      const uint32_t wb = (uint32_t)fold_tile_bytes(a.H);
       mbar_arrive_expect_tx(wbar, wb);
-      bulk_g2s(woh_s, a.woh + (size_t)mt * 32 * fold_ld(a.H), wb, wbar);
+      bulk_g2s(woh_s, reinterpret_cast<const uint8_t*>(a.woh) + (size_t)mt * wb, wb, wbar);
     }
   }
   if (warp == 0) tmem_alloc_dyn(tslot, a.tmem_cols);
@@ -362,7 +372,13 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
                       g_ = tanhfast(gz[u].z + bb[u].z), o_ = sigmf(gz[u].w + bb[u].w);
           const float cn = f_ * cp[u] + i_ * g_;
           const float h = o_ * tanhfast(cn);
-          if (a.woh && it < nit) s_hc[ul * ncp + c] = (r < a.n_valid && j < a.H) ? h : 0.f;
+          if (a.woh && it < nit) {                                 // h (bf16 hi / lo) -> fold B operand
+            const float hv = (r < a.n_valid && j < a.H) ? h : 0.f;
+            const __nv_bfloat16 hh = __float2bfloat16_rn(hv), hl = __float2bfloat16_rn(hv - __bfloat162float(hh));
+            uint8_t* cb = s_hb + (size_t)(c >> 5) * 4096 + fold_sw64(c & 31, ul);
+            *reinterpret_cast<__nv_bfloat16*>(cb) = hh;
+            *reinterpret_cast<__nv_bfloat16*>(cb + 2048) = hl;
+          }
           if (it >= nit || r >= a.n_valid || j >= a.H) continue;
 #ifdef ONMT_KTRACE
           if (a.dbg == 2) { if (h == 12345.f) a.c_out[0] = cn; continue; }
@@ -376,58 +392,58 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
           for (int d = 0; d < a.dst.n; ++d) store_x(a.dst.x[d], r, a.dst.col[d] + j, h);
         }
       }
-      if (a.woh && a.dbg != 11) {
-        // W_out[:, units] h[units, my columns] -> woh_part[mt][row][o] on the tensor cores
-        // (mma.sync m16n8k16: A = the bf16 weight slice via ldmatrix.trans, B = h split into
-        // bf16 hi + lo like every activation operand, fp32 accumulate; fixed order).
-        // Warp w: output tiles of 16 units o = 16 mi (mi = w, w + 8, ...), 24 columns per pass.
-        mbar_wait(wbar, 0);
+      if (a.woh) {
+        // W_out[:, units] h[units, my columns] -> woh_part[mt][row][o] with tcgen05: A = the
+        // tile's [outputs x 32 units] slice, B = a 32-column chunk of h as [hi rows ; lo rows]
+        // (N = 64: both planes in one MMA, the two column halves summed below); accumulators
+        // in TMEM columns 256.. (the GEMM's use < 256); fixed order, deterministic
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // h stores -> MMA operand reads
+        tc_fence_before();
         __syncthreads();
-        const int hs = fold_ld(a.H);
-        const int g = lane >> 2, tq = lane & 3;
-        for (int c0 = 0; c0 < ncols; c0 += 24) {
-          uint32_t bh[3][2][2], bl[3][2][2];                        // [n tile][k step][reg]
+        tc_fence_after();
+        const int mo_n = fold_mo(a.H) / kTileM;                    // output tiles (<= 4: H <= 512)
+        const uint32_t fcol = tmem + 256u;
+        for (int q = 0; q * 32 < ncols; ++q) {
+          if (threadIdx.x == 0) {
+            if (q == 0) mbar_wait(wbar, 0);
+            tc_fence_after();
+            const uint32_t idesc = umma_idesc_bf16(kTileM, 64);
+            const uint32_t sa = smem_u32(woh_s), sb = smem_u32(s_hb + (size_t)q * 4096);
+            for (int mo = 0; mo < mo_n; ++mo)
 #pragma unroll
-          for (int ni = 0; ni < 3; ++ni)
+              for (int ks = 0; ks < 2; ++ks)
+                tc_mma_bf16(fcol + (uint32_t)(mo * 64), umma_desc_sw64(sa + (uint32_t)mo * 8192u + (uint32_t)ks * 32u),
+                            umma_desc_sw64(sb + (uint32_t)ks * 32u), idesc, (uint32_t)ks);
+            tc_commit(fbar);
+          }
+          __syncwarp();
+          mbar_wait(fbar, (uint32_t)(q & 1));
+          tc_fence_after();
+          // warp w: TMEM lane quarter w & 3 (outputs), output tiles w / 4, w / 4 + 2
+          const int qd = warp & 3;
+          for (int mo = warp >> 2; mo < mo_n; mo += 2) {
+            const int o = mo * kTileM + qd * 32 + lane;
+            const uint32_t trow = fcol + (uint32_t)(mo * 64) + ((uint32_t)(qd * 32) << 16);
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks)
+            for (int cc = 0; cc < 32; cc += 8) {
+              uint32_t hv[8], lv[8];
+              tmem_ld8_nw(trow + cc, hv);
+              tmem_ld8_nw(trow + 32 + cc, lv);
+              tmem_wait_ld();
+              tmem_fence_regs(hv);
+              tmem_fence_regs(lv);
 #pragma unroll
-              for (int rr = 0; rr < 2; ++rr) {
-                const int k = ks * 16 + rr * 8 + tq * 2, c = c0 + ni * 8 + g;
-                const float x0 = s_hc[k * ncp + c], x1 = s_hc[(k + 1) * ncp + c];
-                const __nv_bfloat16 h0 = __float2bfloat16_rn(x0), h1 = __float2bfloat16_rn(x1);
-                const __nv_bfloat16 l0 = __float2bfloat16_rn(x0 - __bfloat162float(h0));
-                const __nv_bfloat16 l1 = __float2bfloat16_rn(x1 - __bfloat162float(h1));
-                bh[ni][ks][rr] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-                bl[ni][ks][rr] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
-              }
-          for (int mi = warp; mi * 16 < a.H; mi += 8) {
-            float acc[3][4];
-#pragma unroll
-            for (int ni = 0; ni < 3; ++ni) acc[ni][0] = acc[ni][1] = acc[ni][2] = acc[ni][3] = 0.f;
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              const int mat = lane >> 3, rw = lane & 7;
-              const __nv_bfloat16* ra = woh_s + (size_t)(ks * 16 + (mat >> 1) * 8 + rw) * hs + mi * 16 + (mat & 1) * 8;
-              uint32_t af[4];
-              asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
-                           : "r"(smem_u32(ra)));
-#pragma unroll
-              for (int ni = 0; ni < 3; ++ni) {
-                mma_bf16_16816(acc[ni], af, bh[ni][ks]);
-                mma_bf16_16816(acc[ni], af, bl[ni][ks]);
+              for (int k = 0; k < 8; ++k) {
+                const int c = q * 32 + cc + k;
+                if (o < a.H && c < ncols)
+                  __stcg(a.woh_part + ((size_t)mt * a.n_rows_pad + n0 + c_own + c) * a.H + o,
+                         __uint_as_float(hv[k]) + __uint_as_float(lv[k]));
               }
             }
-#pragma unroll
-            for (int ni = 0; ni < 3; ++ni)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int o = mi * 16 + g + (e >> 1) * 8, c = c0 + ni * 8 + tq * 2 + (e & 1);
-                if (o < a.H && c < ncols)
-                  __stcg(a.woh_part + ((size_t)mt * a.n_rows_pad + n0 + c_own + c) * a.H + o, acc[ni][e]);
-              }
           }
+          tc_fence_before();
+          __syncthreads();                                        // (the next chunk reuses the columns)
+          tc_fence_after();
         }
       }
     } else {
@@ -451,9 +467,9 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
 static size_t fused_smem_bytes(int n_group, int stages, int S, int NC, int fold_H, bool gb = false) {
   const size_t ring = (size_t)stages * (kTileM * 128 + 2 * (size_t)n_group * 128);
   const size_t recv = (size_t)(S + 1) * kTileM * NC * 4;
-  const size_t fold = fold_H ? 128 + (size_t)32 * fold_ld(fold_H) * 2 + (size_t)32 * ((NC + 23) / 24 * 24) * 4 : 0;
+  const size_t fold = fold_H ? 1024 + fold_tile_bytes(fold_H) + (size_t)fold_chunks(NC) * 4096 : 0;
   const size_t gbb = gb ? 128 + 16 + (size_t)NC * 32 * 16 : 0;
-  return 1024 + (ring > recv ? ring : recv) + 32 * 16 + (size_t)NC * 32 * 4 + (2 * stages + 3) * 8 + 16 + fold + gbb;
+  return 1024 + (ring > recv ? ring : recv) + 32 * 16 + (size_t)NC * 32 * 4 + (2 * stages + 4) * 8 + 16 + fold + gbb;
 }
 
 // Split S: the largest S <= 16 such that every split has >= 1 K block, the split's whole
@@ -486,6 +502,7 @@ static bool fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, 
     a.stages = stages;
     int tc = 32;
     while (tc < n_group) tc <<= 1;
+    if (fold_H) tc = 512;                                  // (fold accumulators at columns 256..)
     a.tmem_cols = tc;
     a.M = M;
     return true;
@@ -560,6 +577,7 @@ cudaError_t tc_gemm_tanh(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_p
 // does the top-layer cell kernel with the folded W_out share fit (shared memory, co-residency)?
 bool tc_cell_fold_fits(int m_pad, int n_rows_pad, int n_group, int k_blocks, int H, int num_sms, bool gb) {
   FusedArgs a{};
+  if (fold_mo(H) > 512 || n_group > 256) return false;   // (fold accumulators: TMEM columns 256..511)
   return fill_common(a, n_rows_pad, n_group, n_group, k_blocks, 4 * H, m_pad / kTileM, num_sms, H, gb);
 }
 // does a (non-top) cell kernel with per-row gate biases fit?

@@ -422,7 +422,7 @@ struct onmt_model {
   bool copy = false;                         // copy / pointer generator (copy.w, copy.b present)
   DevBuf copy_w;                             // [H] fp32 (bf16-rounded in bf16 mode)
   float copy_b = 0.f;
-  DevBuf woh_t;                              // W_out[:, H:2H]^T bf16 [top-layer tiles * 32][fold_ld(H)]
+  DevBuf woh_t;                              // W_out[:, H:2H] bf16 per 32-unit tile, swizzled (gemm_fused.cu)
   // recurrent-split step (bf16 models with L >= 2)
   Mat wg;                                    // gate-tile weights [(L+1) blocks of 4H rows][H]: W_feed (dec.l0.w_ih
                                              // input-feed columns), then W_hh of layers 1..L, gate-interleaved
@@ -843,11 +843,19 @@ static void load_model(onmt_model* m, const char* path) {
     for (uint64_t i = 0; i < H; ++i)
       for (uint64_t j = 0; j < H; ++j) woc.v[i * H + j] = wo.v[i * 2 * H + j];
     m->attn_woc.upload(plain_pad(woc), (int)H, (int)H, bf);
-    const size_t units = (size_t)m->dec_w[m->L - 1]->m_pad / 4;
-    const size_t hs = (H + 15) / 16 * 16 + 8;                      // (gemm_fused.cu fold_ld)
-    std::vector<__nv_bfloat16> wt(units * hs, __float2bfloat16_rn(0.f));
-    for (uint64_t j = 0; j < H; ++j)
-      for (uint64_t o = 0; o < H; ++o) wt[j * hs + o] = __float2bfloat16_rn(wo.v[o * 2 * H + H + j]);
+    // W_out[:, H:2H] per top-layer tile of 32 units: [fold_mo(H) outputs][32 units] bf16 with the
+    // 64-byte swizzle applied (gemm_fused.cu fold_sw64: the shared-memory image of the fold MMA's
+    // A operand, loaded by one bulk copy)
+    const size_t tiles = (size_t)m->dec_w[m->L - 1]->m_pad / 4 / 32;
+    const size_t mo = (H + 127) / 128 * 128, tb = mo * 64;
+    std::vector<__nv_bfloat16> wt(tiles * tb / 2, __float2bfloat16_rn(0.f));
+    for (size_t t = 0; t < tiles; ++t)
+      for (uint64_t o = 0; o < mo; ++o)
+        for (int ul = 0; ul < 32; ++ul) {
+          const uint64_t j = t * 32 + ul;
+          const size_t off = o * 64 + ((((ul >> 3) ^ (o >> 1)) & 3) << 4) + ((ul & 7) << 1);
+          wt[(t * tb + off) / 2] = __float2bfloat16_rn(o < H && j < H ? wo.v[o * 2 * H + H + j] : 0.f);
+        }
     m->woh_t.ensure(wt.size() * 2);
     ONMT_CUDA(cudaMemcpy(m->woh_t.p, wt.data(), wt.size() * 2, cudaMemcpyHostToDevice));
   }

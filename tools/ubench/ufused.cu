@@ -67,7 +67,7 @@ int main() {
   __nv_bfloat16* woh;
   CK(cudaMalloc(&gb, NP * 2048 * 4)); CK(cudaMemset(gb, 0, NP * 2048 * 4));
   CK(cudaMalloc(&woh_part, 16 * NP * H * 4));
-  CK(cudaMalloc(&woh, 16 * 32 * fold_ld(H) * 2)); CK(cudaMemset(woh, 0, 16 * 32 * fold_ld(H) * 2));
+  CK(cudaMalloc(&woh, 16 * fold_tile_bytes(H))); CK(cudaMemset(woh, 0, 16 * fold_tile_bytes(H)));
   for (int dbg = 0; dbg < 4; ++dbg)
   for (auto& sh : shapes) {
     g_fused_dbg = dbg;
@@ -85,12 +85,12 @@ int main() {
     CellDst dst{};
     dst.x[0] = xd; dst.col[0] = 0; dst.n = 1;
     auto launch = [&]() {
-      cudaError_t e = sh.tanh ? tc_gemm_tanh(tmW, tmX, mp, NP, NP, R, kp / 64, H, hout, xd, scratch, counters, 148,
+      cudaError_t err = sh.tanh ? tc_gemm_tanh(tmW, tmX, mp, NP, NP, R, kp / 64, H, hout, xd, scratch, counters, 148,
                                              StepCtl{nullptr, 0}, st)
                               : tc_gemm_cell(tmW, tmX, mp, NP, sh.ns, R, kp / 64, bias, cg, cout, hout, H, dst, scratch,
                                              counters, 148, StepCtl{nullptr, 0}, st, sh.fold ? woh : nullptr,
                                              sh.fold ? woh_part : nullptr, rs ? gb : nullptr, 2048);
-      CK(e);
+      CK(err);
     };
     const int S = fused_split(sh.ns, NP, kp / 64, mp / 128, 148);
     const int grid = mp / 128 * (NP / sh.ns) * S;
