@@ -56,7 +56,7 @@ int main(int argc, char** argv) {
   float* rl = (float*)zalloc(R * 4); float* rz = (float*)zalloc(R * K * 4); int* ri = (int*)zalloc(R * K * 4);
   unsigned long long* tr; CK(cudaMalloc(&tr, 4096 * 96)); CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
   const int nsl = argc > 3 ? atoi(argv[3]) : 1;
-  auto launch = [&]() { launch_beam_merge(ms, tz, ti, C, 1, C, B, K, 5, MAXLEN, 1.0, bs, ga, rl, rz, ri, StepCtl{nullptr, 0}, st, nsl); };
+  auto launch = [&]() { launch_beam_merge(ms, tz, ti, C, 1, C, B, K, 5, MAXLEN, 1.0, bs, ga, rl, rz, ri, StepCtl{nullptr, 0}, st, nsl, nullptr); };
   cudaGraph_t gr; cudaGraphExec_t ge;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   for (int i = 0; i < 20; ++i) launch();
