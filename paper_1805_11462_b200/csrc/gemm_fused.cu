@@ -89,7 +89,10 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
-template <int EPI>
+// RING = 0: the split's whole K-slice is resident (one stage per K block, loaded once);
+// RING = 1: fewer stages than K blocks, reloaded through empty barriers (separate instances:
+// the two loop shapes compiled into one kernel measured slower for both)
+template <int EPI, int RING>
 __global__ void __launch_bounds__(256, 1)
 tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                      FusedArgs a) {
@@ -164,29 +167,42 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
   KT(1);
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % a.stages;
-      uint8_t* st = smem + s * stage_bytes;
-      if (quit) {
-        if (i < a.stages) mbar_arrive_local(&full[s]);
-        continue;
+    if (!RING) {
+      for (int i = 0; i < nkb; ++i) {
+        uint8_t* st = smem + i * stage_bytes;
+        if (quit) {
+          mbar_arrive_local(&full[i]);
+        } else {
+          mbar_arrive_expect_tx(&full[i], 2 * b_bytes);
+          tma_load_2d(st + a_bytes, &tmX, (kb0 + i) * kBK, n0, &full[i]);
+          tma_load_2d(st + a_bytes + b_bytes, &tmX, (kb0 + i) * kBK, a.n_rows_pad + n0, &full[i]);
+        }
       }
-      if (i >= a.stages) {                                         // ring: slot s free again
-        mbar_wait(&empty[s], ((i / a.stages) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], a_bytes + 2 * b_bytes);
-        tma_load_2d(st, &tmW, (kb0 + i) * kBK, m0, &full[s]);
-      } else {
-        mbar_arrive_expect_tx(&full[s], 2 * b_bytes);
+    } else {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % a.stages;
+        uint8_t* st = smem + s * stage_bytes;
+        if (quit) {
+          if (i < a.stages) mbar_arrive_local(&full[s]);
+          continue;
+        }
+        if (i >= a.stages) {                                       // ring: slot s free again
+          mbar_wait(&empty[s], ((i / a.stages) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], a_bytes + 2 * b_bytes);
+          tma_load_2d(st, &tmW, (kb0 + i) * kBK, m0, &full[s]);
+        } else {
+          mbar_arrive_expect_tx(&full[s], 2 * b_bytes);
+        }
+        tma_load_2d(st + a_bytes, &tmX, (kb0 + i) * kBK, n0, &full[s]);
+        tma_load_2d(st + a_bytes + b_bytes, &tmX, (kb0 + i) * kBK, a.n_rows_pad + n0, &full[s]);
       }
-      tma_load_2d(st + a_bytes, &tmX, (kb0 + i) * kBK, n0, &full[s]);
-      tma_load_2d(st + a_bytes + b_bytes, &tmX, (kb0 + i) * kBK, a.n_rows_pad + n0, &full[s]);
     }
   } else if (warp == 1 && lane == 0) {
     const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_group);
     for (int i = 0; i < nkb; ++i) {
-      const int s = i % a.stages;
-      if (quit && i >= a.stages) break;
-      mbar_wait(&full[s], (i / a.stages) & 1);
+      const int s = RING ? i % a.stages : i;
+      if (RING && quit && i >= a.stages) break;
+      mbar_wait(&full[s], RING ? (i / a.stages) & 1 : 0);
       tc_fence_after();
       if (quit) continue;
       const uint32_t sa = smem_u32(smem + s * stage_bytes);
@@ -197,7 +213,7 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
         tc_mma_bf16(tmem, da, umma_desc_sw128(sbh + kk * 32), idesc, (i | kk) != 0);
         tc_mma_bf16(tmem, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
       }
-      tc_commit(&empty[s]);                      // slot s reusable once these MMAs retire
+      if (RING) tc_commit(&empty[s]);            // slot s reusable once these MMAs retire
     }
     tc_commit(done);                             // also fires with no MMA issued
   } else if (warp >= 2 && EPI == EPI_CELL && !quit) {
@@ -348,6 +364,9 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
     if (EPI == EPI_CELL) {
       // rows m = 4u + g (gate-interleaved): unit j = m0/4 + ul, 32 units per tile
       const int nit = 32 * ncols;
+      // fold B operand: chunk q of 32 columns holds nc8 hi rows then nc8 lo rows (nc8 = 32, or the
+      // last chunk's column count rounded to 8: a small chunk runs N = 2 nc8 MMAs)
+      const int qlast = (ncols - 1) >> 5, nc8_last = min(32, ((ncols - 32 * qlast) + 7) & ~7);
       for (int it0 = threadIdx.x; it0 < nit; it0 += 2 * blockDim.x) {
         float4 gz[2], bb[2];
         float cp[2];
@@ -375,9 +394,10 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
           if (a.woh && it < nit) {                                 // h (bf16 hi / lo) -> fold B operand
             const float hv = (r < a.n_valid && j < a.H) ? h : 0.f;
             const __nv_bfloat16 hh = __float2bfloat16_rn(hv), hl = __float2bfloat16_rn(hv - __bfloat162float(hh));
-            uint8_t* cb = s_hb + (size_t)(c >> 5) * 4096 + fold_sw64(c & 31, ul);
-            *reinterpret_cast<__nv_bfloat16*>(cb) = hh;
-            *reinterpret_cast<__nv_bfloat16*>(cb + 2048) = hl;
+            const int nc8 = (c >> 5) == qlast ? nc8_last : 32;
+            uint8_t* cb = s_hb + (size_t)(c >> 5) * 4096;
+            *reinterpret_cast<__nv_bfloat16*>(cb + fold_sw64(c & 31, ul)) = hh;
+            *reinterpret_cast<__nv_bfloat16*>(cb + fold_sw64(nc8 + (c & 31), ul)) = hl;
           }
           if (it >= nit || r >= a.n_valid || j >= a.H) continue;
 #ifdef ONMT_KTRACE
@@ -394,9 +414,9 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
       }
       if (a.woh) {
         // W_out[:, units] h[units, my columns] -> woh_part[mt][row][o] with tcgen05: A = the
-        // tile's [outputs x 32 units] slice, B = a 32-column chunk of h as [hi rows ; lo rows]
-        // (N = 64: both planes in one MMA, the two column halves summed below); accumulators
-        // in TMEM columns 256.. (the GEMM's use < 256); fixed order, deterministic
+        // tile's [outputs x 32 units] slice, B = a chunk of h as [hi rows ; lo rows] (N = 2 nc8:
+        // both planes in one MMA, the two column halves summed below); accumulators in TMEM
+        // columns 256.. (the GEMM's use < 256); fixed order, deterministic
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // h stores -> MMA operand reads
         tc_fence_before();
         __syncthreads();
@@ -404,10 +424,11 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
         const int mo_n = fold_mo(a.H) / kTileM;                    // output tiles (<= 4: H <= 512)
         const uint32_t fcol = tmem + 256u;
         for (int q = 0; q * 32 < ncols; ++q) {
+          const int nc8 = q == qlast ? nc8_last : 32;
           if (threadIdx.x == 0) {
             if (q == 0) mbar_wait(wbar, 0);
             tc_fence_after();
-            const uint32_t idesc = umma_idesc_bf16(kTileM, 64);
+            const uint32_t idesc = umma_idesc_bf16(kTileM, 2 * nc8);
             const uint32_t sa = smem_u32(woh_s), sb = smem_u32(s_hb + (size_t)q * 4096);
             for (int mo = 0; mo < mo_n; ++mo)
 #pragma unroll
@@ -426,9 +447,10 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
             const uint32_t trow = fcol + (uint32_t)(mo * 64) + ((uint32_t)(qd * 32) << 16);
 #pragma unroll
             for (int cc = 0; cc < 32; cc += 8) {
+              if (cc >= nc8) break;
               uint32_t hv[8], lv[8];
               tmem_ld8_nw(trow + cc, hv);
-              tmem_ld8_nw(trow + 32 + cc, lv);
+              tmem_ld8_nw(trow + nc8 + cc, lv);
               tmem_wait_ld();
               tmem_fence_regs(hv);
               tmem_fence_regs(lv);
@@ -517,7 +539,7 @@ static cudaError_t launch_fused(const CUtensorMap& tmW, const CUtensorMap& tmX, 
   // relies on one CTA per SM with grid <= #SMs)
   size_t smem = fused_smem_bytes(a.n_group, a.stages, a.S, a.NC, a.woh ? a.H : 0, a.gb != nullptr);
   if (smem < 116 * 1024) smem = 116 * 1024;
-  auto fn = tc_gemm_fused_kernel<EPI>;
+  auto fn = a.stages < a.kb_per_split ? tc_gemm_fused_kernel<EPI, 1> : tc_gemm_fused_kernel<EPI, 0>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(fn, dim3(tiles * a.S), dim3(256), smem, st, tmW, tmX, a);

@@ -821,7 +821,7 @@ static void load_model(onmt_model* m, const char* path) {
     m->dec_w.push_back(std::move(w));
     m->dec_bias.push_back(std::move(bb));
   }
-  if (bf && m->L >= 2) build_rsplit(m, t);
+  if (bf && m->L >= 2 && m->rsplit) build_rsplit(m, t);
   if (m->general) {
     const auto& wi = get(t, "attn.w_in", {H, H}, seen);
     m->attn_win.upload(plain_pad(wi), (int)H, (int)H, bf);

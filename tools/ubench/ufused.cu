@@ -38,11 +38,12 @@ static CUtensorMap make_tmap(const void* base, int k_pad, int rows, int box_rows
 int main() {
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  const int H = 500, R = 150, NP = 160;
+  const int H = 500, R = getenv("UF_R") ? atoi(getenv("UF_R")) : 150, NP = getenv("UF_NP") ? atoi(getenv("UF_NP")) : 160;
   struct Shape { const char* name; int M, K; bool tanh; int ns; bool fold; };
   // ns < NP: the recurrent-split step's layer-2 kernel (N-split groups of ns rows, whole K, per-row
   // gate bias gb); fold: the top layer's W_out[:, H:2H] h shares
   Shape shapes[] = {{"L1 gates 2000x1500", 4 * H, 3 * H, false, NP, false},
+                    {"L2 gates 2000x1000 +fold", 4 * H, 2 * H, false, NP, true},
                     {"L2 gates 2000x1000", 4 * H, 2 * H, false, NP, false},
                     {"rsplit L2 2000x500 ns32 +gb", 4 * H, H, false, 32, false},
                     {"rsplit L2 2000x500 ns32 +gb +fold", 4 * H, H, false, 32, true},
