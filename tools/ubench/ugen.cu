@@ -8,6 +8,9 @@
 #include <vector>
 #include <algorithm>
 #include "../../paper_1805_11462_b200/csrc/gen_step.cu"
+#ifndef ONMT_KTRACE
+__device__ unsigned long long* g_ktrace;   // (untraced build: the stamps below stay zero)
+#endif
 using namespace onmt;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
