@@ -594,7 +594,8 @@ static AttPlan att_plan(int B, int S_max, int H, int K, int key_ld, int val_ld, 
     size_t extra = 0;                              // folded W_out: prefetched tile shares
     if (fo.wpart) extra = (size_t)fo.n_wt * K * ((H / 4 + nch - 1) / nch) * 16;
     const size_t esave = fo.att_out ? r4((size_t)K * CH) * 4 : 0;   // attention output: raw scores
-    const int SC = bytes(16) + extra <= 200 * 1024 ? 16 : 8;
+    const int SC = bytes(16) + extra + esave <= 220 * 1024 ? 16 : 8;   // (16-position sub-chunks: half the
+                                                                     //  per-sub-chunk barriers of 8)
     // push combine (8 chunks or K >= 8) only when its receive buffer fits next to the rest;
     // otherwise the pull combine (no receive buffer)
     const bool vec = (H & 3) == 0 && (kl & 3) == 0 && (val_ld & 3) == 0;

@@ -58,9 +58,9 @@ int main() {
   const int grid = nch * B;
   std::vector<unsigned long long> h(grid * 12);
   CK(cudaMemcpy(h.data(), tr, grid * 96, cudaMemcpyDeviceToHost));
-  unsigned long long t0 = ~0ull; for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[c * 12]);
+  unsigned long long t0 = ~0ull; for (int c = 0; c < grid; ++c) if (h[c * 12]) t0 = std::min(t0, h[c * 12]);
   double avg[12] = {0}, mx[12] = {0}; int cnt[12] = {0};
-  for (int c = 0; c < grid; ++c) for (int i = 0; i < 9; ++i) if (h[c * 12 + i]) {
+  for (int c = 0; c < grid; ++c) for (int i = 0; i < 9; ++i) if (h[c * 12 + i] >= t0 && h[c * 12]) {
     double d = (h[c * 12 + i] - t0) / 1e3; avg[i] += d; cnt[i]++; mx[i] = std::max(mx[i], d); }
   {
     unsigned long long* o; float* sk; CK(cudaMalloc(&o, 16)); CK(cudaMalloc(&sk, 4));
