@@ -421,7 +421,10 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
         }
       }
     }
-    // (3) full lists of the qualifying partials (one more round trip), sorted insertion
+    // (3) full lists of the qualifying partials (one more round trip), sorted insertion.  The
+    //     qualifying partials are handed out one per lane in (u, lane) order, so every list is
+    //     loaded in the same round trip (a lane owning several used to load them one after the
+    //     other); beyond 32 of them the rest stay with their owner lanes.
     float lz[KMAX];
     int li[KMAX];
 #pragma unroll
@@ -429,10 +432,20 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     unsigned qual = 0;                                           // qualifying partials of this lane
 #pragma unroll
     for (int u = 0; u < PPL; ++u) qual |= (hz[u] >= theta && hz[u] != -INFINITY) ? (1u << u) : 0u;
-    while (qual) {
-      const int u = __ffs(qual) - 1;
-      qual &= qual - 1;
-      const size_t base = ((size_t)(lane + 32 * u) * ps + (size_t)r * rs) * K;
+    __shared__ int s_qp[kKMax][32];
+    int nq = 0;
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      const unsigned mk = __ballot_sync(0xffffffffu, (qual >> u) & 1u);
+      if ((qual >> u) & 1u) {
+        const int pos = nq + __popc(mk & ((1u << lane) - 1u));
+        if (pos < 32) { s_qp[k][pos] = lane + 32 * u; qual &= ~(1u << u); }
+      }
+      nq += __popc(mk);
+    }
+    __syncwarp();
+    auto merge_list = [&](int p) {
+      const size_t base = ((size_t)p * ps + (size_t)r * rs) * K;
       float cz[KMAX];
       int ci[KMAX];
 #pragma unroll
@@ -460,6 +473,12 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
         lz[0] = gt[0] ? z : lz[0];
         li[0] = gt[0] ? id : li[0];
       }
+    };
+    if (lane < nq) merge_list(s_qp[k][lane]);
+    while (qual) {                                               // (more than 32 qualified)
+      const int u = __ffs(qual) - 1;
+      qual &= qual - 1;
+      merge_list(lane + 32 * u);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);

@@ -12,7 +12,9 @@ int main(int argc, char** argv) {
   const int rsdbg = argc > 2 ? atoi(argv[2]) : 0;
   CK(cudaMemcpyToSymbol(g_rs_dbg, &rsdbg, sizeof(int)));
   cudaStream_t st; CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  const int B = 30, K = 5, R = B * K, NP = 160, C = 148, E = 500, H = 500, L = 2, V = 50000, MAXLEN = 100;
+  auto envi = [](const char* n, int d) { const char* v = getenv(n); return v ? atoi(v) : d; };
+  const int B = envi("UB_B", 30), K = envi("UB_K", 5), R = B * K, NP = (R + 31) / 32 * 32, C = 148, E = 500,
+            H = envi("UB_H", 500), L = 2, V = 50000, MAXLEN = 100;
   auto zalloc = [&](size_t bytes) { void* p; CK(cudaMalloc(&p, bytes)); CK(cudaMemset(p, 0, bytes)); return p; };
   // partials: random (m, s) and sorted random top-K lists, layout [r][C]
   std::vector<float2> hms((size_t)R * C); std::vector<float> htz((size_t)R * C * K); std::vector<int> hti((size_t)R * C * K);
