@@ -447,6 +447,9 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     const int P = a.P;
     const int c = et / P, part = et % P;                           // hypothesis row (column) and part
     const int nv = kTileM / P;                                     // vocabulary rows scanned per tile
+    // logits per register chunk: 64 (16 groups of 4); 32 for wide beams, whose longer top-K
+    // lists would otherwise spill the scan state to local memory
+    constexpr int ZC = KMAX <= 5 ? 64 : 32, NG = ZC / 4;
     const bool row_ok = c < a.n_group && n0 + c < a.R;
     const int wrow0 = 32 * (warp - 2 - kGsStageWarps) / P;         // first row of this warp
     const bool wact = wrow0 < ncols;                               // its chunk is staged at all
@@ -506,19 +509,19 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
           // increasing along the scan); chunk u0 / 64 covers 16 of them
           const float* col = stg + (size_t)buf * a.srows_alloc * kGsSLD + (size_t)c * kGsSLD + 4 * part;
           const int vbase = (t0 + j) * kTileM + 4 * part;
-          for (int u0 = 0; u0 < nv; u0 += 64) {                    // 64 logits per chunk, in registers
-            float z[64];
+          for (int u0 = 0; u0 < nv; u0 += ZC) {                    // ZC logits per chunk, in registers
+            float z[ZC];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < NG; ++k) {
               const float4 w = *reinterpret_cast<const float4*>(col + P * (u0 + 4 * k));
               z[4 * k] = w.x; z[4 * k + 1] = w.y; z[4 * k + 2] = w.z; z[4 * k + 3] = w.w;
             }
-            float g[16];                                           // group maxima (groups of 4)
+            float g[NG];                                           // group maxima (groups of 4)
 #pragma unroll
-            for (int k = 0; k < 16; ++k) g[k] = fmaxf(fmaxf(z[4 * k], z[4 * k + 1]), fmaxf(z[4 * k + 2], z[4 * k + 3]));
+            for (int k = 0; k < NG; ++k) g[k] = fmaxf(fmaxf(z[4 * k], z[4 * k + 1]), fmaxf(z[4 * k + 2], z[4 * k + 3]));
             float cmax = g[0];
 #pragma unroll
-            for (int k = 1; k < 16; ++k) cmax = fmaxf(cmax, g[k]);
+            for (int k = 1; k < NG; ++k) cmax = fmaxf(cmax, g[k]);
             const float mn = fmaxf(run_m, cmax);
 #ifdef ONMT_KTRACE
             if (a.dbg == 4) { run_m = mn; } else
@@ -529,7 +532,7 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
               const unsigned long long l2 = gs_pk(L2E, L2E), mo2 = gs_pk(-mo, -mo);
               unsigned long long s01 = gs_pk(0.f, 0.f), s23 = gs_pk(0.f, 0.f);
 #pragma unroll
-              for (int k = 0; k < 64; k += 4) {
+              for (int k = 0; k < ZC; k += 4) {
                 float e0, e1, e2, e3;
                 gs_upk(gs_ffma2(gs_pk(z[k], z[k + 1]), l2, mo2), e0, e1);
                 gs_upk(gs_ffma2(gs_pk(z[k + 2], z[k + 3]), l2, mo2), e2, e3);
@@ -556,20 +559,20 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
                 // cold list: extract the chunk's K best exactly - K rounds of (largest group
                 // maximum, its first element, the group's maximum without it) - uniform work
                 // instead of inserting every element of every group above the K-th group max
-                float gg[16];
+                float gg[NG];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) gg[k] = g[k];
+                for (int k = 0; k < NG; ++k) gg[k] = g[k];
                 unsigned long long rm = 0ull;                      // extracted: bit 4 * group + element
 #pragma unroll
                 for (int rnd = 0; rnd < KMAX; ++rnd) {
                   if (rnd < a.K) {
                     float mx = gg[0];
 #pragma unroll
-                    for (int k = 1; k < 16; ++k) mx = fmaxf(mx, gg[k]);
+                    for (int k = 1; k < NG; ++k) mx = fmaxf(mx, gg[k]);
                     if (mx != -INFINITY) {
-                      int sel = 15;
+                      int sel = NG - 1;
 #pragma unroll
-                      for (int k = 14; k >= 0; --k) sel = gg[k] == mx ? k : sel;
+                      for (int k = NG - 2; k >= 0; --k) sel = gg[k] == mx ? k : sel;
                       const float4 w = *reinterpret_cast<const float4*>(col + P * (u0 + 4 * sel));
                       const unsigned gone = (unsigned)(rm >> (4 * sel)) & 15u;
                       const float v0 = (gone & 1u) ? -INFINITY : w.x, v1 = (gone & 2u) ? -INFINITY : w.y;
@@ -580,14 +583,14 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
                       const float nm = fmaxf(fmaxf(e == 0 ? -INFINITY : v0, e == 1 ? -INFINITY : v1),
                                              fmaxf(e == 2 ? -INFINITY : v2, e == 3 ? -INFINITY : v3));
 #pragma unroll
-                      for (int k = 0; k < 16; ++k) gg[k] = k == sel ? nm : gg[k];
+                      for (int k = 0; k < NG; ++k) gg[k] = k == sel ? nm : gg[k];
                     }
                   }
                 }
               } else {
                 unsigned gm = 0;                                   // groups holding a candidate
 #pragma unroll
-                for (int k = 0; k < 16; ++k) gm |= (g[k] >= th) ? (1u << k) : 0u;
+                for (int k = 0; k < NG; ++k) gm |= (g[k] >= th) ? (1u << k) : 0u;
                 while (gm) {                                       // candidates in id order
                   const int gi = __ffs(gm) - 1;
                   gm &= gm - 1;

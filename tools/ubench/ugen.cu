@@ -33,7 +33,8 @@ int main(int argc, char** argv) {
   const int gates = argc > 1 ? atoi(argv[1]) : 0;
   g_gs_dbg = argc > 2 ? atoi(argv[2]) : 0;
   cudaStream_t st; CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  const int R = 150, NP = 160, KP = 512, V = 50000, VP = 50048, K = 5, C = 148;
+  const int R = getenv("UG_R") ? atoi(getenv("UG_R")) : 150, NP = 160, KP = 512, V = 50000, VP = 50048,
+            K = getenv("UG_K") ? atoi(getenv("UG_K")) : 5, C = 148;
   __nv_bfloat16 *W, *X; float* bias;
   const int XK = gates ? 3 * KP : KP;                        // operand width (gate tiles: [h~ | h1 | h2])
   CK(cudaMalloc(&W, (size_t)VP * KP * 2)); CK(cudaMalloc(&X, (size_t)2 * NP * XK * 2)); CK(cudaMalloc(&bias, VP * 4));
