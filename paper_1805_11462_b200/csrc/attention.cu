@@ -134,13 +134,33 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   const int s_beg = (int)r * CH;
   const int s_lim = min(S_max, s_beg + CH);
   const int nsub_max = s_lim > s_beg ? (s_lim - s_beg + SC - 1) / SC : 0;
+  // sub-chunk staging: one bulk copy per operand (the chunk's rows are contiguous) completing on
+  // the buffer's mbarrier - the TMA engine instead of 16-byte cp.async per thread, which bounded
+  // the loop at ~5 us per sub-chunk for 1000-wide rows; cp.async when the rows are not 16-byte
+  // aligned
+  const bool bulk = vec && ((reinterpret_cast<uintptr_t>(mem) | reinterpret_cast<uintptr_t>(keys)) & 15) == 0;
+  __shared__ __align__(8) uint64_t s_sbar[2];
+  if (bulk && threadIdx.x == 0) { mbar_init(&s_sbar[0], 1); mbar_init(&s_sbar[1], 1); fence_mbar_init(); }
+  if (bulk) __syncthreads();
+  int n_staged = 0;                                // bulk stages issued (waited before exit)
   auto stage = [&](int i) {
     const int s0 = s_beg + i * SC;
     const int ns = min(SC, s_lim - s0);
+    if (bulk) {
+      if (threadIdx.x == 0) {
+        const uint32_t mbytes = (uint32_t)ns * vl * 4, kbytes = same ? 0u : (uint32_t)ns * key_ld * 4;
+        mbar_arrive_expect_tx(&s_sbar[i & 1], mbytes + kbytes);
+        bulk_g2s(mbuf(i), mem + ((size_t)b * S_max + s0) * vl, mbytes, &s_sbar[i & 1]);
+        if (!same) bulk_g2s(kbuf(i), keys + ((size_t)b * S_max + s0) * key_ld, kbytes, &s_sbar[i & 1]);
+      }
+      n_staged = i + 1;
+      return;
+    }
     cp_async_rows(mbuf(i), mem + ((size_t)b * S_max + s0) * vl, ns * vl);
     if (!same) cp_async_rows(kbuf(i), keys + ((size_t)b * S_max + s0) * key_ld, ns * key_ld);
     cp_async_commit();
   };
+  auto stage_wait = [&](int i) { mbar_wait(&s_sbar[i & 1], (uint32_t)((i >> 1) & 1)); };
   if (nsub_max > 0) stage(0);
   if (nsub_max > 1) stage(1);
   KT(1);
@@ -149,6 +169,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   const bool quit = all_done(ctl) || (done && done[b]);   // uniform over the cluster
   if (quit) {
     cp_async_wait<0>();
+    if (bulk) for (int i = 0; i < n_staged; ++i) stage_wait(i);   // (no copy may land after exit)
     if (push) cluster_wait();                      // (complete the barrier phase opened above)
     return;
   }
@@ -202,7 +223,13 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
     for (int u = 0; u < JPT; ++u) acc[k][u] = 0.f;
 
   for (int i = 0; i < nsub; ++i) {
-    if (i + 1 >= nsub_max) cp_async_wait<0>();
+    if (bulk) {
+      if (i == 0) {                                          // q (the W_out shares may stay in flight)
+        if (hpref) cp_async_wait<1>();
+        else cp_async_wait<0>();
+      }
+      stage_wait(i);
+    } else if (i + 1 >= nsub_max) cp_async_wait<0>();
     else if (i == 0) {                                       // (iteration 0 also needs q; the
       if (hpref) cp_async_wait<1>();                         //  W_out shares may stay in flight)
       else cp_async_wait<0>();
@@ -369,6 +396,7 @@ attention_cluster_kernel(const float* __restrict__ htop, const float* __restrict
   }
   if (hpref) cp_async_wait<1>();                   // (q, and prefetches past S_b; the W_out shares
   else cp_async_wait<0>();                         //  are waited for only by the combine)
+  if (bulk) for (int i = nsub; i < n_staged; ++i) stage_wait(i);   // (stages past S_b)
   __syncthreads();
   if (push) {
     // ---- push my unnormalised partial context: column j goes to the chunk that owns it
@@ -594,8 +622,9 @@ static AttPlan att_plan(int B, int S_max, int H, int K, int key_ld, int val_ld, 
     size_t extra = 0;                              // folded W_out: prefetched tile shares
     if (fo.wpart) extra = (size_t)fo.n_wt * K * ((H / 4 + nch - 1) / nch) * 16;
     const size_t esave = fo.att_out ? r4((size_t)K * CH) * 4 : 0;   // attention output: raw scores
-    const int SC = bytes(16) + extra + esave <= 220 * 1024 ? 16 : 8;   // (16-position sub-chunks: half the
-                                                                     //  per-sub-chunk barriers of 8)
+    // positions per sub-chunk: the largest of 16 / 12 / 8 that fits (fewer sub-chunks = fewer
+    // barriers; c4's H = 1000 rows fit 12)
+    const int SC = bytes(16) + extra + esave <= 220 * 1024 ? 16 : bytes(12) + extra + esave <= 220 * 1024 ? 12 : 8;
     // push combine (8 chunks or K >= 8) only when its receive buffer fits next to the rest;
     // otherwise the pull combine (no receive buffer)
     const bool vec = (H & 3) == 0 && (kl & 3) == 0 && (val_ld & 3) == 0;

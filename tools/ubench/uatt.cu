@@ -23,7 +23,7 @@ int main() {
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   auto envi = [](const char* n, int d) { const char* v = getenv(n); return v ? atoi(v) : d; };
-  const int B = envi("UATT_B", 30), S = envi("UATT_S", 50), K = envi("UATT_K", 5), H = envi("UATT_H", 500), KL = 512;
+  const int B = envi("UATT_B", 30), S = envi("UATT_S", 50), K = envi("UATT_K", 5), H = envi("UATT_H", 500), KL = (H + 63) / 64 * 64;
   const int LO = envi("UATT_LO", 10), SPAN = envi("UATT_SPAN", 41);
   std::vector<int> lens(B);
   for (int b = 0; b < B; ++b) lens[b] = LO + (b * 37) % SPAN;
@@ -31,17 +31,18 @@ int main() {
   CK(cudaMalloc(&dl, B * 4)); CK(cudaMemcpy(dl, lens.data(), B * 4, cudaMemcpyHostToDevice));
   CK(cudaMalloc(&htop, B * K * H * 4)); CK(cudaMalloc(&keys, (size_t)B * S * KL * 4)); CK(cudaMalloc(&mem, (size_t)B * S * H * 4));
   CK(cudaMemset(htop, 0, B * K * H * 4)); CK(cudaMemset(keys, 0, (size_t)B * S * KL * 4)); CK(cudaMemset(mem, 0, (size_t)B * S * H * 4));
-  CK(cudaMalloc(&xhl, 2 * 256 * 1024 * 2));
+  const int RP = (B * K + 31) / 32 * 32, XW = ((2 * H + 63) / 64) * 64;
+  CK(cudaMalloc(&xhl, (size_t)2 * RP * XW * 2));
   unsigned long long* tr; CK(cudaMalloc(&tr, 8192 * 96)); CK(cudaMemcpyToSymbol(g_ktrace, &tr, sizeof(tr)));
-  XOut xo{nullptr, xhl, 256, 1024};
+  XOut xo{nullptr, xhl, RP, XW};
   // production configuration: folded W_out (values with ld 512, 16 top-layer tile shares)
   const bool fold = !getenv("UATT_PLAIN");
   float *wpart, *ht, *vals; __nv_bfloat16* xg;
-  CK(cudaMalloc(&wpart, (size_t)16 * 256 * H * 4)); CK(cudaMemset(wpart, 0, (size_t)16 * 256 * H * 4));
-  CK(cudaMalloc(&ht, 256 * H * 4)); CK(cudaMalloc(&xg, 2 * 256 * 512 * 2));
+  CK(cudaMalloc(&wpart, (size_t)16 * RP * H * 4)); CK(cudaMemset(wpart, 0, (size_t)16 * RP * H * 4));
+  CK(cudaMalloc(&ht, (size_t)RP * H * 4)); CK(cudaMalloc(&xg, (size_t)2 * RP * XW * 2));
   CK(cudaMalloc(&vals, (size_t)B * S * KL * 4)); CK(cudaMemset(vals, 0, (size_t)B * S * KL * 4));
   AttFold fo{};
-  if (fold) { fo.wpart = wpart; fo.n_wt = 16; fo.rows_pad = 256; fo.htilde = ht; fo.xg = XOut{nullptr, xg, 256, 512}; }
+  if (fold) { fo.wpart = wpart; fo.n_wt = 16; fo.rows_pad = RP; fo.htilde = ht; fo.xg = XOut{nullptr, xg, RP, XW}; }
   auto launch = [&]() { CK(launch_attention(htop, keys, KL, fold ? vals : mem, fold ? KL : H, dl, B, S, H, K, xo, nullptr, 148,
                                             StepCtl{nullptr, 0}, st, fo)); };
   cudaGraph_t g; cudaGraphExec_t ge;
