@@ -9,6 +9,11 @@
 namespace onmt {
 
 __device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+__device__ __forceinline__ float cell_sigm_fast(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+__device__ __forceinline__ float cell_tanh_fast(float x) {
+  const float e = __expf(-2.f * fabsf(x));
+  return copysignf(__fdividef(1.f - e, 1.f + e), x);
+}
 
 // Asynchronous global -> shared copy of n floats (cp.async, 16 B granules when aligned).
 __device__ __forceinline__ void stage_async(float* dst, const float* src, int n) {
@@ -117,12 +122,23 @@ __global__ void dec_cell_kernel(const float* __restrict__ P, int splits, int p_r
   float4 g = bias[j];
   const float4 p = sum_splits4(P, (size_t)p_rows_pad * p_ld, (size_t)r * p_ld + 4 * j, splits);
   g.x += p.x; g.y += p.y; g.z += p.z; g.w += p.w;
-  const float i = sigm(g.x), f = sigm(g.y), gg = tanhf(g.z), o = sigm(g.w);
-  const float c = f * cg[(size_t)r * H + j] + i * gg;
-  const float h = o * tanhf(c);
+  // bf16 models: the fused cell's fast exponentials (rel. error ~2^-21; IEEE expf / tanhf made
+  // this kernel instruction-bound: 570 instructions per thread at c4); fp32 models keep them
+  float i, f, gg, o, c, h;
+  if (dst.n > 0 && dst.x[0].hl) {
+    i = cell_sigm_fast(g.x); f = cell_sigm_fast(g.y); gg = cell_tanh_fast(g.z); o = cell_sigm_fast(g.w);
+    c = f * cg[(size_t)r * H + j] + i * gg;
+    h = o * cell_tanh_fast(c);
+  } else {
+    i = sigm(g.x); f = sigm(g.y); gg = tanhf(g.z); o = sigm(g.w);
+    c = f * cg[(size_t)r * H + j] + i * gg;
+    h = o * tanhf(c);
+  }
   c_out[(size_t)r * H + j] = c;
   h_out[(size_t)r * H + j] = h;
-  for (int d = 0; d < dst.n; ++d) store_x(dst.x[d], r, dst.col[d] + j, h);
+#pragma unroll
+  for (int d = 0; d < 2; ++d)                      // (static indices: no local-memory copy of dst)
+    if (d < dst.n) store_x(dst.x[d], r, dst.col[d] + j, h);
 }
 
 // A8: h~ = tanh(W_out [c ; h]) (P69; AMB-9) from split-K partials; writes h~ (fp32, for
@@ -136,7 +152,7 @@ __global__ void attn_out_kernel(const float* __restrict__ P, int splits, int p_r
   if (idx >= R * H) return;
   const int r = idx / H, j = idx % H;
   const float v = sum_splits(P, (size_t)p_rows_pad * p_ld, (size_t)r * p_ld + j, splits);
-  const float h = tanhf(v);
+  const float h = xg.hl ? cell_tanh_fast(v) : tanhf(v);       // (bf16 models: as the fused tanh epilogue)
   htilde[(size_t)r * H + j] = h;
   store_x(xg, r, j, h);
 }
