@@ -223,6 +223,28 @@ __device__ __forceinline__ void rsplit_cell(int b, int K, const int* s_go, const
   }
 }
 
+// warp-wide max / min of 32-bit unsigned values in one instruction (redux.sync), and the
+// order-preserving float <-> uint key (max of keys = max of floats; -inf is the smallest key
+// of any non-NaN value) - the row reduce's K-round selections use these instead of 5-step
+// shuffle trees
+__device__ __forceinline__ unsigned warp_max_u32(unsigned v) {
+  unsigned r;
+  asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned warp_min_u32(unsigned v) {
+  unsigned r;
+  asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned fkey(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
 // rsplit_cell with every input staged in shared memory: parent k's block at gbuf + k * PR
 // (P[0..L] rows of 4H, then c_0..c_{L-1} rows of H), new slot kr's T[y] row at gbuf + K * PR + kr * 4H;
 // the new c_1 / h_1 go to gbuf + K * PR + K * 4H (2 K H floats) before the write-out.
@@ -384,13 +406,17 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
       v[u] = p < n_parts ? __ldcg(&ms[ix]) : make_float2(-INFINITY, 0.f);
       hz[u] = p < n_parts ? __ldcg(&tz[ix * K]) : -INFINITY;
     }
+
+#ifdef ONMT_KTRACE
+    if (g_ktrace && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && k == 0) {
+      unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); g_ktrace[34000 + 0] = t_; }
+#endif
     // LSE: the row maximum first (warp), then every partial's sum rescaled to it - independent
     // terms instead of a running (max, sum) chain
     float m = -INFINITY;
 #pragma unroll
     for (int u = 0; u < PPL; ++u) m = fmaxf(m, v[u].x);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    m = fkey_inv(warp_max_u32(fkey(m)));
     float sm = 0.f;
 #pragma unroll
     for (int u = 0; u < PPL; ++u) sm += v[u].x == -INFINITY ? 0.f : v[u].y * __expf(v[u].x - m);
@@ -405,9 +431,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
         float lm = hh[0];
 #pragma unroll
         for (int u = 1; u < PPL; ++u) lm = fmaxf(lm, hh[u]);
-        float wm = lm;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        const float wm = fkey_inv(warp_max_u32(fkey(lm)));
         theta = wm;
         const unsigned own = __ballot_sync(0xffffffffu, lm == wm);
         if (lane == __ffs(own) - 1) {                            // the first owner drops one copy
@@ -421,6 +445,11 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
         }
       }
     }
+
+#ifdef ONMT_KTRACE
+    if (g_ktrace && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && k == 0) {
+      unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); g_ktrace[34000 + 1] = t_; }
+#endif
     // (3) full lists of the qualifying partials (one more round trip), sorted insertion.  The
     //     qualifying partials are handed out one per lane in (u, lane) order, so every list is
     //     loaded in the same round trip (a lane owning several used to load them one after the
@@ -480,18 +509,20 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
       qual &= qual - 1;
       merge_list(lane + 32 * u);
     }
+
+#ifdef ONMT_KTRACE
+    if (g_ktrace && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && k == 0) {
+      unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); g_ktrace[34000 + 2] = t_; }
+#endif
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
     if (lane == 0) s_lse[k] = m + logf(sm);
     for (int c = 0; c < K; ++c) {                                // K rounds of warp arg-max over list heads
-      float bz = lz[0];
-      int bi = li[0];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float z2 = __shfl_xor_sync(0xffffffffu, bz, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (better(z2, i2, bz, bi)) { bz = z2; bi = i2; }
-      }
+      // (z desc, id asc): the largest head value, then the smallest id among the lanes holding it
+      // (ids are >= 0, 0x7fffffff for an empty slot)
+      const unsigned kz = warp_max_u32(fkey(lz[0]));
+      const float bz = fkey_inv(kz);
+      const int bi = (int)warp_min_u32(fkey(lz[0]) == kz ? (unsigned)li[0] : 0xffffffffu);
       if (lane == 0) { s_z[k][c] = bz; s_id[k][c] = bi; }
       if (pre && lane == c && s_live[k] && bz != -INFINITY) {   // candidate (k, c): prefetch its embedding
         mbar_expect_tx(&s_bar, (uint32_t)E * 4);
@@ -504,6 +535,10 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
         li[KMAX - 1] = 0x7fffffff;
       }
     }
+#ifdef ONMT_KTRACE
+    if (g_ktrace && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && k == 0) {
+      unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); g_ktrace[34000 + 3] = t_; }
+#endif
   }
   __syncthreads();
   if (dn != 0 && dn < t) return;                                 // finished earlier (uniform)

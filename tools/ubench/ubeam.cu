@@ -78,5 +78,11 @@ int main(int argc, char** argv) {
   printf("beam_step rsplit=%d: %.2f us/launch (graph of 20)\n", rsplit, ms_ * 1000 / 20);
   const char* nm[12] = {"entry", "after pdl/done", "live/cum loaded", "rows reduced", "selected", "gather staged", "exit", "sc ready", "ranked", "owners done", "cell math done", "cell synced"};
   for (int i = 0; i < 12; ++i) if (cnt[i]) printf("   %-16s avg %7.2f  max %7.2f us (n=%d)\n", nm[i], avg[i] / cnt[i], mx[i], cnt[i]);
+  {
+    std::vector<unsigned long long> x(4);
+    CK(cudaMemcpy(x.data(), tr + 34000, 32, cudaMemcpyDeviceToHost));
+    const char* xn[4] = {"row0: partials loaded", "row0: theta done", "row0: lists merged", "row0: top-K out"};
+    for (int i = 0; i < 4; ++i) if (x[i] > t0) printf("   %-24s %7.2f us\n", xn[i], (x[i] - t0) / 1e3);
+  }
   return 0;
 }
