@@ -473,6 +473,7 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
       nq += __popc(mk);
     }
     __syncwarp();
+    bool empty_list = true;                                      // (lz / li hold no entry yet)
     auto merge_list = [&](int p) {
       const size_t base = ((size_t)p * ps + (size_t)r * rs) * K;
       float cz[KMAX];
@@ -481,6 +482,12 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
       for (int c = 0; c < KMAX; ++c) {
         cz[c] = c < K ? __ldcg(&tz[base + c]) : -INFINITY;
         ci[c] = c < K ? __ldcg(&ti[base + c]) : 0x7fffffff;
+      }
+      if (empty_list) {                                          // a partial's list is sorted: the
+#pragma unroll                                                   // lane's first one is its list as is
+        for (int c = 0; c < KMAX; ++c) { lz[c] = cz[c]; li[c] = ci[c]; }
+        empty_list = false;
+        return;
       }
 #pragma unroll 1
       for (int c = 0; c < K; ++c) {
