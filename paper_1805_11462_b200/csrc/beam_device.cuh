@@ -420,29 +420,21 @@ __device__ __forceinline__ void beam_step_sentence(int b, const float2* __restri
     float sm = 0.f;
 #pragma unroll
     for (int u = 0; u < PPL; ++u) sm += v[u].x == -INFINITY ? 0.f : v[u].y * __expf(v[u].x - m);
-    // (2) theta = K-th largest partial maximum: a partial whose best logit is below it holds
-    //     no row top-K entry (K other entries beat all of its entries)
+    // (2) theta = K-th largest of the LANES' partial maxima (one per lane): K distinct partials
+    //     have a best logit >= theta, so a partial whose best logit is below it holds no row
+    //     top-K entry.  (A lower bound of the K-th largest partial maximum; K rounds of one
+    //     warp max each - the exact value needed a lane maximum recomputed per round.)
     float theta = -INFINITY;
     {
-      float hh[PPL];
+      float lm = hz[0];
 #pragma unroll
-      for (int u = 0; u < PPL; ++u) hh[u] = hz[u];
+      for (int u = 1; u < PPL; ++u) lm = fmaxf(lm, hz[u]);
+      unsigned key = fkey(lm);
       for (int c = 0; c < K; ++c) {
-        float lm = hh[0];
-#pragma unroll
-        for (int u = 1; u < PPL; ++u) lm = fmaxf(lm, hh[u]);
-        const float wm = fkey_inv(warp_max_u32(fkey(lm)));
-        theta = wm;
-        const unsigned own = __ballot_sync(0xffffffffu, lm == wm);
-        if (lane == __ffs(own) - 1) {                            // the first owner drops one copy
-          bool hit = false;
-#pragma unroll
-          for (int u = 0; u < PPL; ++u) {
-            const bool h = !hit && hh[u] == wm;
-            hh[u] = h ? -INFINITY : hh[u];
-            hit |= h;
-          }
-        }
+        const unsigned wk = warp_max_u32(key);
+        theta = wk == 0u ? -INFINITY : fkey_inv(wk);             // (0: fewer than K lanes left)
+        const unsigned own = __ballot_sync(0xffffffffu, key == wk);
+        if (lane == __ffs(own) - 1) key = 0u;                    // (one lane per round)
       }
     }
 
