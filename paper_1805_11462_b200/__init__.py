@@ -14,7 +14,8 @@ from typing import Dict, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libonmt_b200.so")
+# ONMT_LIB_PATH: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("ONMT_LIB_PATH") or os.path.join(_HERE, "libonmt_b200.so")
 
 ONMT_OK = 0
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "IO", -3: "FORMAT", -4: "UNSUPPORTED", -5: "ID_RANGE",

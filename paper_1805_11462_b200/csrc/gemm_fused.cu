@@ -55,6 +55,10 @@ struct FusedArgs {
   const float* gb;
   int gb_ld;
   StepCtl ctl;
+  int stack;               // 2 n_group <= 256: the hi and lo B tiles (adjacent in shared memory) form
+                           // one N = 2 n_group operand, one MMA per K step instead of two; the hi /
+                           // lo sums land in TMEM columns [0, n) / [n, 2n) and are added in the
+                           // epilogue
   int dbg;                 // microbenchmark ablations (ONMT_KTRACE builds only)
 };
 
@@ -198,7 +202,7 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
       }
     }
   } else if (warp == 1 && lane == 0) {
-    const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_group);
+    const uint32_t idesc = umma_idesc_bf16(kTileM, a.stack ? 2 * a.n_group : a.n_group);
     for (int i = 0; i < nkb; ++i) {
       const int s = RING ? i % a.stages : i;
       if (RING && quit && i >= a.stages) break;
@@ -207,11 +211,17 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
       if (quit) continue;
       const uint32_t sa = smem_u32(smem + s * stage_bytes);
       const uint32_t sbh = sa + a_bytes, sbl = sa + a_bytes + b_bytes;
+      if (a.stack) {                             // (no branch between the MMAs)
 #pragma unroll
-      for (int kk = 0; kk < kBK / 16; ++kk) {
-        const uint64_t da = umma_desc_sw128(sa + kk * 32);
-        tc_mma_bf16(tmem, da, umma_desc_sw128(sbh + kk * 32), idesc, (i | kk) != 0);
-        tc_mma_bf16(tmem, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
+        for (int kk = 0; kk < kBK / 16; ++kk)
+          tc_mma_bf16(tmem, umma_desc_sw128(sa + kk * 32), umma_desc_sw128(sbh + kk * 32), idesc, (i | kk) != 0);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk) {
+          const uint64_t da = umma_desc_sw128(sa + kk * 32);
+          tc_mma_bf16(tmem, da, umma_desc_sw128(sbh + kk * 32), idesc, (i | kk) != 0);
+          tc_mma_bf16(tmem, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
+        }
       }
       if (RING) tc_commit(&empty[s]);            // slot s reusable once these MMAs retire
     }
@@ -265,7 +275,16 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     for (int c0 = half * 16; c0 < a.n_group; c0 += 32) {
       uint32_t r[16];
-      if (nkb > 0) {
+      if (nkb > 0 && a.stack) {
+        uint32_t r2[16];
+        tmem_ld16_nw(trow + c0, r);
+        tmem_ld16_nw(trow + a.n_group + c0, r2);
+        tmem_wait_ld();
+        tmem_fence_regs(r);
+        tmem_fence_regs(r2);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+      } else if (nkb > 0) {
         tmem_ld16_nw(trow + c0, r);
         tmem_wait_ld();
         tmem_fence_regs(r);
@@ -300,6 +319,20 @@ tc_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_const
         }
         tmem_wait_ld();
         tmem_fence_regs(r);
+        if (a.stack) {
+          uint32_t r2[32];
+  #pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (c0 + 4 * k < ce && nkb > 0)
+              tmem_ld4_nw(trow + a.n_group + c0 + 4 * k, r2[4 * k], r2[4 * k + 1], r2[4 * k + 2], r2[4 * k + 3]);
+            else
+              r2[4 * k] = r2[4 * k + 1] = r2[4 * k + 2] = r2[4 * k + 3] = 0u;
+          }
+          tmem_wait_ld();
+          tmem_fence_regs(r2);
+  #pragma unroll
+          for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+        }
   #pragma unroll
         for (int k = 0; k < 8; ++k)
           if (c0 + 4 * k < ce)
@@ -522,8 +555,10 @@ static bool fill_common(FusedArgs& a, int n_rows_pad, int n_group, int n_valid, 
     a.NC = NC;
     a.kb_per_split = kbps;
     a.stages = stages;
+    a.stack = 2 * n_group <= 256;
+    if (const char* e = std::getenv("ONMT_FUSED_NOSTACK")) a.stack = a.stack && !std::atoi(e);   // (A/B runs)
     int tc = 32;
-    while (tc < n_group) tc <<= 1;
+    while (tc < (a.stack ? 2 * n_group : n_group)) tc <<= 1;
     if (fold_H) tc = 512;                                  // (fold accumulators at columns 256..)
     a.tmem_cols = tc;
     a.M = M;

@@ -306,6 +306,39 @@ k_lat(const __grid_constant__ CUtensorMap tw, long long wspan, int mma_on, int n
   if (threadIdx.x >= 32) { tc_fence_after(); tmem_dealloc(tslot, 512); }
 }
 
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+// ---- 6. per-box cost: one thread pipelining 2D boxes {64, rows} (rows = 32 .. 256) and 3D
+// boxes {64, rows, 2} (two planes), depth 4, distinct rows per CTA over a 48 MB region
+__global__ void __launch_bounds__(32, 1)
+k_box(const __grid_constant__ CUtensorMap tm, int is3d, int box_bytes, long long nrows, int rows, int iters,
+      unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t tb[4];
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < 4; ++i) mbar_init(&tb[i], 1);
+  fence_mbar_init();
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (int it = 0; it < iters; ++it) {
+    const int s = it & 3;
+    if (it >= 4) mbar_wait(&tb[s], ((it >> 2) - 1) & 1);
+    mbar_arrive_expect_tx(&tb[s], box_bytes);
+    const long long row = ((long long)it * rows + (long long)blockIdx.x * 2621) % (nrows - rows);
+    if (is3d) tma_load_3d(smem + s * box_bytes, &tm, 0, (int)row, 0, &tb[s]);
+    else tma_load_2d(smem + s * box_bytes, &tm, 0, (int)row, &tb[s]);
+  }
+  for (int j = iters - 4; j < iters; ++j) mbar_wait(&tb[j & 3], (j >> 2) & 1);
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+  out[blockIdx.x] = t1 - t0;
+}
+
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -323,7 +356,42 @@ static CUtensorMap make_tmap(const void* base, int k, int rows, int box_rows) {
   return m;
 }
 
+static CUtensorMap make_tmap3p(const void* base, long long rows, int box_rows) {   // {64, rows, 2 planes}
+  typedef CUresult (*F)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                        const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                        CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* p = nullptr; cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+  CUtensorMap m;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, 2};
+  cuuint64_t strides[2] = {128, (cuuint64_t)rows * 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 2};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (((F)p)(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) { printf("tmap3\n"); exit(1); }
+  return m;
+}
 int main() {
+  if (getenv("UPAIR_BOX")) {                           // section 6 only
+    const long long NR = 48ll * 1024 * 1024 / 128;
+    __nv_bfloat16* S; CK(cudaMalloc(&S, (size_t)NR * 128)); CK(cudaMemset(S, 0, (size_t)NR * 128));
+    unsigned long long* o; CK(cudaMalloc(&o, 2048 * 8));
+    CK(cudaFuncSetAttribute(k_box, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (int is3d : {0, 1})
+      for (int rows : {32, 64, 128, 160, 256}) {
+        if (is3d && rows > 160) continue;
+        CUtensorMap tm = is3d ? make_tmap3p(S, NR / 2, rows) : make_tmap(S, 64, (int)NR, rows);
+        const int bytes = rows * 128 * (is3d ? 2 : 1), grid = 148, iters = 2000;
+        k_box<<<grid, 32, 200 * 1024>>>(tm, is3d, bytes, is3d ? NR / 2 : NR, rows, 100, o); CK(cudaDeviceSynchronize());
+        k_box<<<grid, 32, 200 * 1024>>>(tm, is3d, bytes, is3d ? NR / 2 : NR, rows, iters, o); CK(cudaDeviceSynchronize());
+        std::vector<unsigned long long> h(grid);
+        CK(cudaMemcpy(h.data(), o, grid * 8, cudaMemcpyDeviceToHost));
+        double ns = 0; for (int b = 0; b < grid; ++b) ns += h[b]; ns /= grid;
+        printf("%s box %3d rows (%6d B): %.0f ns per box, %.1f GB/s per SM\n", is3d ? "3D x2 planes" : "2D         ", rows,
+               bytes, ns / iters, (double)bytes * iters / ns);
+      }
+    return 0;
+  }
   // ---- 1. correctness
   for (int N : {32, 160, 256}) {
     std::vector<__nv_bfloat16> hA(256 * 64), hB((size_t)N * 64);
