@@ -108,8 +108,11 @@ enc_wave_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant__
   uint64_t* xfull = wbar + 2;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(xfull + kbs);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // hi and lo B tiles (adjacent) as one N = 2N operand when it fits: one MMA per K step; the lo
+  // sums land in TMEM columns [N, 2N)
+  const bool stk = 2 * N <= 256;
   uint32_t tcols = 32;
-  while ((int)tcols < N) tcols <<= 1;
+  while ((int)tcols < (stk ? 2 * N : N)) tcols <<= 1;
   const unsigned long long n_own = (unsigned long long)T * S;
   const unsigned long long n_prev = l > 0 ? (unsigned long long)a.layer[l - 1].T * a.layer[l - 1].S : 0;
   const unsigned long long n_next = l + 1 < a.L ? (unsigned long long)a.layer[l + 1].T * a.layer[l + 1].S : 0;
@@ -189,7 +192,7 @@ enc_wave_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant__
       if (mma) {
         if (warp == 1 && lane == 0) {
           if (n_mma == 0) mbar_wait(wbar, 0);
-          const uint32_t idesc = umma_idesc_bf16(kTileM, N);
+          const uint32_t idesc = umma_idesc_bf16(kTileM, stk ? 2 * N : N);
           for (int kg = first; kg < last; ++kg) {
             const int i = kg - kb0;
             // (slot i was loaded at every earlier step, the recurrent part from step 1 on)
@@ -197,11 +200,18 @@ enc_wave_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant__
             tc_fence_after();
             const uint32_t sa = smem_u32(sW + (size_t)i * 16384);
             const uint32_t sbh = smem_u32(sX + (size_t)i * 2 * nb), sbl = sbh + nb;
+            if (stk) {                                 // (no branch between the MMAs)
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-              const uint64_t da = umma_desc_sw128(sa + kk * 32);
-              tc_mma_bf16(tmem, da, umma_desc_sw128(sbh + kk * 32), idesc, (kg != first || kk != 0) ? 1u : 0u);
-              tc_mma_bf16(tmem, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
+              for (int kk = 0; kk < kBK / 16; ++kk)
+                tc_mma_bf16(tmem, umma_desc_sw128(sa + kk * 32), umma_desc_sw128(sbh + kk * 32), idesc,
+                            (kg != first || kk != 0) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                const uint64_t da = umma_desc_sw128(sa + kk * 32);
+                tc_mma_bf16(tmem, da, umma_desc_sw128(sbh + kk * 32), idesc, (kg != first || kk != 0) ? 1u : 0u);
+                tc_mma_bf16(tmem, da, umma_desc_sw128(sbl + kk * 32), idesc, 1u);
+              }
             }
           }
           tc_commit(mdone);
@@ -219,7 +229,16 @@ enc_wave_kernel(const __grid_constant__ CUtensorMap tw0, const __grid_constant__
         for (int p = warp >> 2; p < S; p += 2) {
           for (int c0 = 0; c0 < NS; c0 += 8) {
             uint32_t r[8];
-            if (mma) {
+            if (mma && stk) {
+              uint32_t r2[8];
+              tmem_ld8_nw(trow + p * NS + c0, r);
+              tmem_ld8_nw(trow + N + p * NS + c0, r2);
+              tmem_wait_ld();
+              tmem_fence_regs(r);
+              tmem_fence_regs(r2);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) + __uint_as_float(r2[k]));
+            } else if (mma) {
               tmem_ld8_nw(trow + p * NS + c0, r);
               tmem_wait_ld();
               tmem_fence_regs(r);
