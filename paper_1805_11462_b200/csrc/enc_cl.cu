@@ -23,6 +23,8 @@
 // produced after its step t-1 MMAs had completed.
 #include <math_constants.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -178,9 +180,30 @@ enc_cl_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ 
         tc_fence_after();
         const uint32_t idesc = umma_idesc_bf16(kTileM, 2 * N);
         const uint32_t xb = smem_u32(sX + (size_t)par * xpar), sw0 = smem_u32(sW);
-        for (int ks = 0; ks < 4 * kb; ++ks)
-          tc_mma_bf16(tmem, umma_desc_sw128(sw0 + (uint32_t)(ks >> 2) * 16384u + (uint32_t)(ks & 3) * 32u),
-                      umma_desc_sw64(xb + (uint32_t)(ks >> 1) * 2u * nb + (uint32_t)(ks & 1) * 32u), idesc, ks != 0);
+        // straight-line issue (the K-block count as a template argument): computing descriptors
+        // in a rolled loop makes each small MMA wait for the previous one
+        auto issue = [&](auto kbc) {
+          constexpr int KB = decltype(kbc)::value;
+#pragma unroll
+          for (int ks = 0; ks < 4 * KB; ++ks)
+            tc_mma_bf16(tmem, umma_desc_sw128(sw0 + (uint32_t)(ks >> 2) * 16384u + (uint32_t)(ks & 3) * 32u),
+                        umma_desc_sw64(xb + (uint32_t)(ks >> 1) * 2u * nb + (uint32_t)(ks & 1) * 32u), idesc, ks != 0);
+        };
+        switch (kb) {
+          case 1: issue(std::integral_constant<int, 1>{}); break;
+          case 2: issue(std::integral_constant<int, 2>{}); break;
+          case 3: issue(std::integral_constant<int, 3>{}); break;
+          case 4: issue(std::integral_constant<int, 4>{}); break;
+          case 5: issue(std::integral_constant<int, 5>{}); break;
+          case 6: issue(std::integral_constant<int, 6>{}); break;
+          case 7: issue(std::integral_constant<int, 7>{}); break;
+          case 8: issue(std::integral_constant<int, 8>{}); break;
+          default:
+            for (int ks = 0; ks < 4 * kb; ++ks)
+              tc_mma_bf16(tmem, umma_desc_sw128(sw0 + (uint32_t)(ks >> 2) * 16384u + (uint32_t)(ks & 3) * 32u),
+                          umma_desc_sw64(xb + (uint32_t)(ks >> 1) * 2u * nb + (uint32_t)(ks & 1) * 32u), idesc,
+                          ks != 0);
+        }
         tc_commit(mdone);
         if (tr && t < 64) a.trace[t * 8 + 1] = ec_now();
       }
