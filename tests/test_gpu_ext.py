@@ -154,3 +154,31 @@ def test_persistent_encoders_match_per_step_path(weight_cache, layers, bidir):
     for b in range(len(lens)):
         ref_mem, finals = om.encode([int(v) for v in ids[b, :lens[b]]])
         np.testing.assert_allclose(mem1[b, :lens[b]], ref_mem, atol=2e-4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("h_dir", [128, 192, 320, 384, 448])
+def test_cluster_encoder_widths(weight_cache, h_dir):
+    """The cluster recurrence (enc_cl.cu) issues each step's MMAs as straight-line code per
+    K-block count (h_dir / 64 = 2, 3, 5, 6, 7 here; 1 and 4 are covered above and by c3 / c5):
+    it matches the split-K grid kernel and the fp64 oracle at every width.  (The two kernels sum
+    the gate pre-activations in different fp32 orders - one accumulator per step against split-K
+    partials - so at h_dir up to 448 they agree to ~1e-5, not bitwise; both are held to the
+    oracle's 2e-4 bar.)"""
+    cfg = synth.ModelConfig(2, 64, 2 * h_dir, 300, 500, True, True)
+    gm, om, prec = toy_pair(cfg, 23, 0.2, weight_cache, "bf16", name=f"encw{h_dir}")
+    ids, lens = synth.make_corpus("c1")
+    ids = ids % 300
+    ids[ids < 4] += 4
+    mem1, h1, c1 = gm.encode(ids, lens)
+    gm.set_option("enc_cluster", 0)
+    try:
+        mem2, h2, c2 = gm.encode(ids, lens)
+    finally:
+        gm.set_option("enc_cluster", 1)
+    np.testing.assert_allclose(mem1, mem2, atol=2e-5)
+    np.testing.assert_allclose(h1, h2, atol=2e-5)
+    np.testing.assert_allclose(c1, c2, atol=2e-5)
+    for b in range(0, len(lens), 3):
+        ref_mem, finals = om.encode([int(v) for v in ids[b, :lens[b]]])
+        np.testing.assert_allclose(mem1[b, :lens[b]], ref_mem, atol=2e-4)
