@@ -232,7 +232,12 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
     for (int s = 0; s < a.stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     mbar_init(tempty, kGsStageWarps);
-    mbar_init(sdone, kGsScanWarps);
+    // only scanner warps with rows to scan arrive on sdone: an idle warp (rows past ncols: a
+    // ragged last row group, or P = 1) runs through every batch at once and its arrivals would
+    // complete later batches' phases before the active warps finished (the producer then
+    // reloaded the ring under the staged tile they were still scanning)
+    const int n_act = min(kGsScanWarps, (ncols * a.P + 31) >> 5);   // (warp sw scans rows from 32 sw / P; P | 32)
+    mbar_init(sdone, n_act > 0 ? n_act : 1);
   }
   if (threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kGsMaxCh) {      // chunk barriers (warp 1)
     const int i = threadIdx.x - 32, k = i % kGsMaxCh;
@@ -618,7 +623,8 @@ gen_step_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__
       }
       if (!a.ovl) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // (reads before the reload)
       __syncwarp();
-      if (lane == 0) mbar_arrive_local(sdone);                     // (ring overlay: batch bt scanned)
+      if (lane == 0 && (wact || (ncols == 0 && warp == 2 + kGsStageWarps)))
+        mbar_arrive_local(sdone);                                  // (ring overlay: batch bt scanned)
     }
     KTX(8, et == 0);
     // ---- combine the P parts of a row (adjacent lanes, butterfly) and write the CTA's partial
