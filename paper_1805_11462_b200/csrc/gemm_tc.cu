@@ -602,6 +602,9 @@ static size_t genp_smem_bytes(int n_group, int stages, int kmax) {
          (size_t)n_group * (2 + 2 * kmax) * 4 + (2 * stages + 4) * 8 + 16;
 }
 
+// does the tile-outer generator fit for this row group at any beam width (<= 16)?
+bool gen_persistent_fits(int n_group) { return genp_smem_bytes(n_group, 2, 16) <= 227 * 1024; }
+
 // number of partials per row the persistent generator writes (C = CTAs per N-group)
 int gen_persistent_parts(int n_vt, int n_groups, int num_sms, int cs) {
   int C = num_sms / n_groups;

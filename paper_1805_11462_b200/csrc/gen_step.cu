@@ -761,6 +761,15 @@ static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, int R, int K
     p.body = gs_body_bytes(n_group, p.nt_max, p.stages, 0, p.nbuf, p.srows);
     return gs_smem_bytes(p.body, p.stages) <= limit;
   };
+  const int nt0 = p.nt_max;
+  while (p.stages > 2 && !fits()) --p.stages;
+  while (p.nt_max > 1 && !fits()) --p.nt_max;
+  if (fits()) return true;
+  // wide row groups (> 160 rows: one scanner thread per row): one staging buffer - the stagers
+  // refill a chunk once its scanners are done with it (per-chunk barriers)
+  p.nbuf = 1;
+  p.nt_max = nt0;
+  p.stages = 4;
   while (p.stages > 2 && !fits()) --p.stages;
   while (p.nt_max > 1 && !fits()) --p.nt_max;
   return fits();
@@ -768,6 +777,11 @@ static bool gs_plan(int n_vt, int n_group, int groups, int num_sms, int R, int K
 
 // parts per row written by the step kernel's phase A (0 = not applicable)
 int g_gs_dbg = 0;
+// is the plan the non-overlapped one-buffer plan of wide row groups?
+bool gen_step_wide_plan(int n_vt, int n_group, int groups, int num_sms) {
+  GsPlan p;
+  return gs_plan(n_vt, n_group, groups, num_sms, n_group * groups, 16, p) && !p.ovl && p.nbuf == 1;
+}
 int gen_step_parts(int n_vt, int n_group, int groups, int num_sms) {
   GsPlan p;
   return gs_plan(n_vt, n_group, groups, num_sms, n_group * groups, 16, p) ? p.C : 0;

@@ -38,6 +38,8 @@ cudaError_t tc_gemm_gen(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pa
 cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                               int k_blocks, int num_sms, int cs, const GenOut& g, StepCtl ctl, cudaStream_t st);
 int gen_persistent_parts(int n_vt, int n_groups, int num_sms, int cs);
+bool gen_persistent_fits(int n_group);
+bool gen_step_wide_plan(int n_vt, int n_group, int groups, int num_sms);
 int gen_step_parts(int n_vt, int n_group, int groups, int num_sms);
 cudaError_t gen_step(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
                      int k_blocks, int num_sms, const GenOut& g, float* row_lse, float* row_z, int* row_i, int t,
@@ -559,10 +561,15 @@ static void prof_end(onmt_model* m, const char* name, const EvPair& ev) {
   else m->evs[name].pending.push_back({ev, true});
 }
 
-static bool use_gen_step(onmt_model* m, const Act& X) {
+// does the decode step run the K-outer generator (gen_step.cu) for row groups of n_group?
+static bool gen_step_chosen(onmt_model* m, int n_group, int groups) {
   const int n_vt = (m->Vt + kVTile - 1) / kVTile;
-  return m->use_tc && m->gen_step && gen_step_parts(n_vt, X.n_group, X.rows_pad / X.n_group, m->num_sms) > 0;
+  if (!(m->use_tc && m->gen_step && gen_step_parts(n_vt, n_group, groups, m->num_sms) > 0)) return false;
+  // the one-buffer plan of wide row groups measured slower than the tile-outer generator (c4:
+  // 123.6 vs 118 us per step): only where the latter does not fit (e.g. 256 rows)
+  return !(gen_step_wide_plan(n_vt, n_group, groups, m->num_sms) && gen_persistent_fits(n_group));
 }
+static bool use_gen_step(onmt_model* m, const Act& X) { return gen_step_chosen(m, X.n_group, X.rows_pad / X.n_group); }
 static int gen_parts(onmt_model* m, const Act& X) {
   const int n_vt = (m->Vt + kVTile - 1) / kVTile;
   if (use_gen_step(m, X)) return gen_step_parts(n_vt, X.n_group, X.rows_pad / X.n_group, m->num_sms);
@@ -909,6 +916,7 @@ static bool rsplit_on(onmt_model* m, int B, int K, bool att) {
   if ((H & 3) != 0 || (size_t)2 * K * H * 4 > 120 * 1024) return false;       // beam step staging
   const RowPlan rp = plan_rows(R);
   const int groups = rp.rows_pad / rp.n_group;
+  if (!gen_step_chosen(m, rp.n_group, groups)) return false;   // (the gate tiles run in gen_step)
   const int n_vt = (m->Vt + kVTile - 1) / kVTile;
   const int G = round_up(4 * H, kTileM);
   const int n_gt = (m->L + 1) * (G / kTileM);

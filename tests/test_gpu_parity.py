@@ -112,6 +112,20 @@ def test_multi_row_group_short(workload, B, weight_cache):
     assert res["fail"] == 0, res["details"]
 
 
+@pytest.mark.parametrize("B,K", [(1, 5), (7, 3), (33, 5), (40, 5), (50, 5), (61, 4), (70, 5), (20, 10), (16, 16), (40, 8)])
+def test_shape_sweep_c2_model(B, K, weight_cache):
+    """Batch / beam shapes off the configs (R = B*K from 5 to 350: one and two row groups, ragged
+    last groups, every scan width): the c2 model at a short max_len against the oracle on the
+    first, middle and last sentence - catches plan / barrier bugs that only odd shapes reach."""
+    gm, om, prec = model_pair("c2", weight_cache)
+    ids, lens = synth.make_corpus("c2", B)
+    S = int(lens.max())
+    gpu = gm.translate(np.ascontiguousarray(ids[:, :S]), lens, K, 6, 0.0, trace=True)
+    sents = sorted({0, B // 2, B - 1})
+    res = compare_batch(om, ids, lens, gpu, K, 6, 0.0, prec, sentences=sents)
+    assert res["fail"] == 0, res["details"]
+
+
 def test_fp32_mode_c2_model_subset(weight_cache):
     """fp32 mode on the c2 model (SIMT path): token log p within 1e-5."""
     gm, om, prec = model_pair("c2", weight_cache, precision="fp32")
