@@ -120,7 +120,7 @@ def corpus_run(model, args, w, ws, rank, dev):
     import torch.distributed as dist
     from paper_1805_11462_b200.parallel import deal_batches, gather_results, make_batches, translate_batches
     B, K, ML, alpha = w.data.batch, w.decode.beam, w.decode.max_len, w.decode.alpha
-    n = CORPUS[args.workload]
+    n = args.corpus_sentences or CORPUS[args.workload]
     ids, lens = synth.make_corpus(args.workload, n)
     batches = make_batches(n, B)
     mine = deal_batches(len(batches), ws, rank)
@@ -150,6 +150,8 @@ def corpus_run(model, args, w, ws, rank, dev):
             "(H2D/D2H per batch inside); batches dealt round-robin, one gather of every output + indices"}
 
 
+# default corpus sizes (bounded so a default run ends in minutes); SURVEY §8(d)'s full c4 corpus is
+# --corpus-sentences 16384
 CORPUS = {"c1": 2, "c2": 3840, "c3": 64 * 8, "c4": 128 * 8, "c5": 16 * 8}
 
 
@@ -621,6 +623,8 @@ def main():
     ap.add_argument("--cpu-sample-sentences", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-corpus", action="store_true")
+    ap.add_argument("--corpus-sentences", type=int, default=0,
+                    help="corpus-mode size (default: CORPUS[workload]; SURVEY §8(d) c4: 16384)")
     ap.add_argument("--vocab-parallel", action="store_true",
                     help="split the generator's vocabulary over the ranks (SURVEY §8(f) rank 4)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
