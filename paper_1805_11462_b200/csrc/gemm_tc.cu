@@ -702,7 +702,8 @@ static cudaError_t launch_tc(const CUtensorMap& tmW, const CUtensorMap& tmX, con
 }
 
 cudaError_t tc_gemm_partial(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
-                            int n_valid, int k_blocks, int splits, float* out, StepCtl ctl, cudaStream_t st) {
+                            int n_valid, int k_blocks, int splits, float* out, StepCtl ctl, cudaStream_t st,
+                            bool groups_from_valid) {
   TcGemmArgs a{};
   a.n_rows_pad = n_rows_pad;
   a.n_group = n_group;
@@ -717,7 +718,9 @@ cudaError_t tc_gemm_partial(const CUtensorMap& tmW, const CUtensorMap& tmX, int 
   a.out = out;
   a.ctl = ctl;
   GenOut g{};
-  dim3 grid(m_pad / kTileM, n_rows_pad / n_group, splits);
+  // groups_from_valid: row groups of a re-grouped box (tmX's box rows = n_group need not divide
+  // n_rows_pad); rows past n_valid are never stored
+  dim3 grid(m_pad / kTileM, groups_from_valid ? (n_valid + n_group - 1) / n_group : n_rows_pad / n_group, splits);
   return launch_tc<MODE_PARTIAL, 1>(tmW, tmX, a, g, grid, st);
 }
 

@@ -32,7 +32,8 @@
 namespace onmt {
 // kernels / launchers defined in the other translation units
 cudaError_t tc_gemm_partial(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
-                            int n_valid, int k_blocks, int splits, float* out, StepCtl ctl, cudaStream_t st);
+                            int n_valid, int k_blocks, int splits, float* out, StepCtl ctl, cudaStream_t st,
+                            bool groups_from_valid = false);
 cudaError_t tc_gemm_gen(const CUtensorMap& tmW, const CUtensorMap& tmX, int m_pad, int n_rows_pad, int n_group,
                         int k_blocks, const GenOut& g, StepCtl ctl, cudaStream_t st);
 cudaError_t tc_gen_persistent(const CUtensorMap& tmW, const CUtensorMap& tmX, int n_vt, int n_rows_pad, int n_group,
@@ -307,10 +308,13 @@ struct Act {
   bool bf16 = false;
   DevBuf f32, hl;
   CUtensorMap tmap;           // box {64, n_group}
+  int rg_ng = 0;              // box rows of rg_tmap (0: not built for the current buffers)
+  CUtensorMap rg_tmap;        // box {64, rg_ng}: single-split decoder gate GEMMs re-grouped (§6.4)
   void ensure(int rows_, int k_, bool bf) {
     RowPlan rp = plan_rows(rows_);
     int kp = round_up(k_, kBK);
     if (rp.rows_pad == rows_pad && kp == k_pad && bf == bf16 && f32.p) { rows = rows_; return; }
+    rg_ng = 0;
     rows = rows_; rows_pad = rp.rows_pad; n_group = rp.n_group; k = k_; k_pad = kp; bf16 = bf;
     f32.ensure((size_t)rows_pad * k_pad * 4);
     ONMT_CUDA(cudaMemset(f32.p, 0, (size_t)rows_pad * k_pad * 4));
@@ -398,6 +402,7 @@ struct onmt_model {
   bool fused = true;           // split-K GEMM with the reduction and the cell / tanh epilogue fused in
                                // (one launch per layer instead of GEMM + consumer kernel)
   bool gen_step = true;        // K-outer persistent generator (gen_step.cu)
+  bool regroup = true;         // unfused single-split gate GEMMs in smaller row groups (§6.4)
   bool fold_wout = true;       // W_out folded into the top cell layer + attention (no W_out launch)
   bool enc_persistent = true;  // encoder recurrence of a layer as one persistent kernel (enc_rec.cu)
   bool enc_cluster = true;     // ... as one cluster per direction with the state on chip (enc_cl.cu)
@@ -1388,7 +1393,22 @@ static void enqueue_dec_layers(onmt_model* m, const int* d_lens, int B, int S_ma
       }
     }
     EvPair pg = prof_begin(m, "gemm");
-    int s = gemm(m, W, *m->xdec[l], R, 0, P, ctl);
+    int s;
+    Act& X = *m->xdec[l];
+    const int per = std::max(1, m->num_sms / (W.m_pad / kTileM));
+    const int ng = std::min(X.n_group, std::max(16, round_up((R + per - 1) / per, 16)));
+    if (m->use_tc && m->regroup && W.k_pad == X.k_pad && ng < X.n_group &&
+        auto_splits(m, W, X.rows_pad / X.n_group) == 1) {
+      // one K split: row groups as small as the SM count allows (c4: 4 x 160 rows x 32 weight
+      // tiles = 128 CTAs instead of 3 x 224 = 96; the per-CTA work scales with the rows)
+      if (X.rg_ng != ng) { X.rg_tmap = make_tmap(X.hl.p, X.k_pad, 2 * X.rows_pad, ng); X.rg_ng = ng; }
+      ONMT_CUDA(tc_gemm_partial(W.tmap, X.rg_tmap, W.m_pad, X.rows_pad, ng, R, W.k_pad / kBK, 1, P, ctl, m->stream,
+                                true));
+      count(m);
+      s = 1;
+    } else {
+      s = gemm(m, W, X, R, 0, P, ctl);
+    }
     prof_end(m, "gemm", pg);
     EvPair pc = prof_begin(m, "cell");
     launch_dec_cell(P, s, m->xdec[l]->rows_pad, W.m_pad, m->dec_bias[l]->as<float>(), cg + (size_t)l * rp * H,
@@ -1729,7 +1749,7 @@ static void run_score(onmt_model* m, const int* d_ids, const int* d_lens, int B,
     enqueue_score(m, d_ids, d_lens, B, S_max, T_max);
     return;
   }
-  std::vector<int64_t> key = {-1, B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->fold_cur,
+  std::vector<int64_t> key = {-1, B, S_max, T_max, m->profile, m->use_tc, m->fused, m->gen_step, m->regroup, m->fold_cur,
                               m->enc_persistent, m->enc_wavefront, m->enc_cluster, (int64_t)g_alloc_gen,
                               (int64_t)(intptr_t)d_ids,
                               (int64_t)(intptr_t)d_lens, (int64_t)(intptr_t)m->stream};
@@ -1765,7 +1785,7 @@ static void run_translate(onmt_model* m, const int* d_ids, const int* d_lens, in
     return;
   }
   std::vector<int64_t> key = {B, S_max, K, max_len, (int64_t)(alpha * 1e6), trace, m->profile, m->use_tc, m->fused,
-                              m->gen_step, m->fold_cur, m->enc_persistent, m->enc_wavefront, m->enc_cluster, m->rs_cur,
+                              m->gen_step, m->regroup, m->fold_cur, m->enc_persistent, m->enc_wavefront, m->enc_cluster, m->rs_cur,
                               m->vp.world,
                               m->vp.rank,
                               (int64_t)g_alloc_gen, (int64_t)(intptr_t)d_ids, (int64_t)(intptr_t)d_lens,
@@ -1829,6 +1849,7 @@ onmt_status onmt_load_weights(const char* path, int32_t device, onmt_precision p
   if (const char* ev = std::getenv("ONMT_USE_GRAPH")) m->use_graph = std::atoi(ev) != 0;   // ncu runs use 0
   if (const char* ev = std::getenv("ONMT_FUSED_GEMM")) m->fused = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_GEN_STEP")) m->gen_step = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("ONMT_REGROUP")) m->regroup = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_FOLD_WOUT")) m->fold_wout = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_PERSISTENT")) m->enc_persistent = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("ONMT_ENC_WAVE")) m->enc_wavefront = std::atoi(ev) != 0;
@@ -1869,6 +1890,8 @@ onmt_status onmt_set_option(onmt_model* m, const char* name, int64_t v) {
     m->fused = v != 0;
   } else if (n == "gen_step") {
     m->gen_step = v != 0;
+  } else if (n == "regroup") {
+    m->regroup = v != 0;
   } else if (n == "fold_wout") {
     m->fold_wout = v != 0;
   } else if (n == "enc_persistent") {

@@ -40,6 +40,7 @@ __device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;"
 
 // Sum of `splits` split-K partials P[s*stride + off] with all loads in flight (up to 16).
 __device__ __forceinline__ float sum_splits(const float* __restrict__ P, size_t stride, size_t off, int splits) {
+  if (splits == 1) return __ldg(P + off);          // (one split: the sum is the partial itself)
   float v[16];
 #pragma unroll
   for (int s = 0; s < 16; ++s) v[s] = s < splits ? __ldg(P + s * stride + off) : 0.f;
@@ -49,6 +50,7 @@ __device__ __forceinline__ float sum_splits(const float* __restrict__ P, size_t 
   return a;
 }
 __device__ __forceinline__ float4 sum_splits4(const float* __restrict__ P, size_t stride, size_t off, int splits) {
+  if (splits == 1) return __ldg(reinterpret_cast<const float4*>(P + off));   // (c4's gate GEMMs: one split)
   float4 v[16];
 #pragma unroll
   for (int s = 0; s < 16; ++s)

@@ -42,3 +42,19 @@ def test_generator_modes_bit_identical(weight_cache, tmp_path):
     for mode in (0, 1):
         for key in ("hyps", "lens", "scores", "logp"):
             assert np.array_equal(outs[mode][key], ref[key]), (mode, key)
+
+
+def test_regrouped_gate_gemm_bit_identical(weight_cache):
+    """c4's single-split decoder gate GEMMs run in 160-row groups (128 CTAs) instead of the
+    operand's 224-row groups (96 CTAs) (option regroup): every output is the
+    same K-ordered tensor-core sum, so translations must be bit-identical."""
+    import paper_1805_11462_b200 as ob
+    path = synth.weights_file("c4", weight_cache)
+    ids, lens = synth.make_corpus("c4")
+    outs = {}
+    for v in (1, 0):
+        with ob.Model(path, 0, "bf16") as m:
+            m.set_option("regroup", v)
+            outs[v] = m.translate(ids, lens, 5, 16, 0.6)
+    for key in ("hyps", "lens", "scores", "token_logp"):
+        assert np.array_equal(outs[0][key], outs[1][key]), key
