@@ -112,35 +112,58 @@ __global__ void enc_cell_kernel(const float* __restrict__ Z, int z_ld, const flo
 // ------------------------------------------------------------------ decoder step
 // A6: LSTM cell of decoder layer l over all R rows; c_prev already gathered by parent.
 
+template <bool ONE>   // ONE: a single split (c4's gate GEMMs): no 16-way split-sum registers
 __global__ void dec_cell_kernel(const float* __restrict__ P, int splits, int p_rows_pad, int p_ld,
                                 const float4* __restrict__ bias, const float* __restrict__ cg, float* c_out,
                                 float* h_out, int H, int R, CellDst dst, StepCtl ctl) {
   pdl_trigger();
   pdl_wait();
   if (all_done(ctl)) return;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= R * H) return;
-  const int r = idx / H, j = idx % H;
-  float4 g = bias[j];
-  const float4 p = sum_splits4(P, (size_t)p_rows_pad * p_ld, (size_t)r * p_ld + 4 * j, splits);
-  g.x += p.x; g.y += p.y; g.z += p.z; g.w += p.w;
-  // bf16 models: the fused cell's fast exponentials (rel. error ~2^-21; IEEE expf / tanhf made
-  // this kernel instruction-bound: 570 instructions per thread at c4); fp32 models keep them
-  float i, f, gg, o, c, h;
-  if (dst.n > 0 && dst.x[0].hl) {
-    i = cell_sigm_fast(g.x); f = cell_sigm_fast(g.y); gg = cell_tanh_fast(g.z); o = cell_sigm_fast(g.w);
-    c = f * cg[(size_t)r * H + j] + i * gg;
-    h = o * cell_tanh_fast(c);
-  } else {
-    i = sigm(g.x); f = sigm(g.y); gg = tanhf(g.z); o = sigm(g.w);
-    c = f * cg[(size_t)r * H + j] + i * gg;
-    h = o * tanhf(c);
-  }
-  c_out[(size_t)r * H + j] = c;
-  h_out[(size_t)r * H + j] = h;
+  // two (row, unit) items per thread, idx and idx + half, with both items' loads issued before
+  // either's math (one wave at c4 instead of two, twice the loads in flight per thread)
+  const int n = R * H, half = (n + 1) / 2;
+  const int idx0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx0 >= half) return;
+  const bool fast = dst.n > 0 && dst.x[0].hl;
+  float4 g[2];
+  float cp[2];
+  int rr[2], jj[2];
+  bool ok[2];
 #pragma unroll
-  for (int d = 0; d < 2; ++d)                      // (static indices: no local-memory copy of dst)
-    if (d < dst.n) store_x(dst.x[d], r, dst.col[d] + j, h);
+  for (int e = 0; e < 2; ++e) {
+    const int idx = idx0 + e * half;
+    ok[e] = idx < n;
+    rr[e] = ok[e] ? idx / H : 0;
+    jj[e] = ok[e] ? idx % H : 0;
+    g[e] = bias[jj[e]];
+    const size_t off = (size_t)rr[e] * p_ld + 4 * jj[e];
+    const float4 p = ONE ? __ldg(reinterpret_cast<const float4*>(P + off))
+                         : sum_splits4(P, (size_t)p_rows_pad * p_ld, off, splits);
+    g[e].x += p.x; g[e].y += p.y; g[e].z += p.z; g[e].w += p.w;
+    cp[e] = cg[(size_t)rr[e] * H + jj[e]];
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    if (!ok[e]) continue;
+    const int r = rr[e], j = jj[e];
+    // bf16 models: the fused cell's fast exponentials (rel. error ~2^-21; IEEE expf / tanhf made
+    // this kernel instruction-bound: 570 instructions per thread at c4); fp32 models keep them
+    float i, f, gg, o, c, h;
+    if (fast) {
+      i = cell_sigm_fast(g[e].x); f = cell_sigm_fast(g[e].y); gg = cell_tanh_fast(g[e].z); o = cell_sigm_fast(g[e].w);
+      c = f * cp[e] + i * gg;
+      h = o * cell_tanh_fast(c);
+    } else {
+      i = sigm(g[e].x); f = sigm(g[e].y); gg = tanhf(g[e].z); o = sigm(g[e].w);
+      c = f * cp[e] + i * gg;
+      h = o * tanhf(c);
+    }
+    c_out[(size_t)r * H + j] = c;
+    h_out[(size_t)r * H + j] = h;
+#pragma unroll
+    for (int d = 0; d < 2; ++d)                    // (static indices: no local-memory copy of dst)
+      if (d < dst.n) store_x(dst.x[d], r, dst.col[d] + j, h);
+  }
 }
 
 // A8: h~ = tanh(W_out [c ; h]) (P69; AMB-9) from split-K partials; writes h~ (fp32, for
@@ -411,9 +434,9 @@ void launch_enc_cell(const float* Z, int z_ld, const float* P, int splits, int p
 
 void launch_dec_cell(const float* P, int splits, int p_rows_pad, int p_ld, const float* bias, const float* cg,
                      float* c_out, float* h_out, int H, int R, CellDst dst, StepCtl ctl, cudaStream_t st) {
-  const int n = R * H;
-  launch_pdl(dec_cell_kernel, dim3((n + 255) / 256), dim3(256), 0, st, P, splits, p_rows_pad, p_ld,
-             (const float4*)bias, cg, c_out, h_out, H, R, dst, ctl);
+  const int n = (R * H + 1) / 2;                    // (two items per thread)
+  launch_pdl(splits == 1 ? dec_cell_kernel<true> : dec_cell_kernel<false>, dim3((n + 255) / 256), dim3(256), 0, st, P,
+             splits, p_rows_pad, p_ld, (const float4*)bias, cg, c_out, h_out, H, R, dst, ctl);
 }
 
 
