@@ -10,7 +10,8 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
-        "l1tex__m_xbar2l1tex_read_bytes.sum", "sm__cycles_active.avg"]
+        "l1tex__m_xbar2l1tex_read_bytes.sum", "sm__cycles_active.avg",
+        "lts__t_sector_hit_rate.pct", "lts__t_sectors.sum"]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 out = []
 for vals in rows[2:]:
