@@ -244,6 +244,9 @@ ONMT_API onmt_status onmt_translate_dev(onmt_model* m, const int32_t* d_src_ids,
  *   "enc_wavefront" 1 = unidirectional stacks as one layer-wavefront launch (default).
  *   "gen_step", "fold_wout", "rsplit"  1 = the fused generator step / folded W_out /
  *                   recurrent-split decode step where they apply (defaults), 0 = off.
+ *   "regroup"       1 = single-split decoder gate GEMMs of the unfused per-layer step in row
+ *                   groups sized to the SM count (default; bit-identical), 0 = the operand's
+ *                   own row groups.
  *   All variants compute the same function up to fp32 summation order.
  * INVALID_ARG on an unknown name or value.
  */
